@@ -1,0 +1,269 @@
+"""oracle -- TEST INFRASTRUCTURE ONLY (never on the product path).
+
+The exact CPU oracle for arXiv 1903.03640 ("Analyzing GPU Tensor Core
+Potential for Fast Reductions").  Only ``tests/``, ``__graft_entry__.smoke()``
+and ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import
+this package.  It shares no code, header, table or constant with the CUDA
+path in ``paper_1903_03640_b200/`` and never imports it.
+
+Contents
+--------
+* :func:`exact_sum_fp16` -- R(X) = sum x_i exactly (§III Eq. 2,
+  lines 106-110), via the plain C loop in ``exact_sum.c`` (int128 in units of
+  2^-24).  Also returns A = sum |x_i| exactly.
+* :func:`exact_sum_fraction` -- the same definition in pure Python
+  ``fractions.Fraction`` arithmetic, for tiny inputs (an independent check of
+  the C code).
+* :func:`within_tolerance` -- the north-star acceptance test
+  |g - R| <= 2^-20 * sum|x_i|, evaluated in exact rational arithmetic
+  (reading G15).
+* :func:`round_to_f32` -- correctly rounded (RNE) binary32 of an exact value.
+* :mod:`oracle.model` -- the paper's structural algorithm R_tc (Eq. 9-14)
+  in exact arithmetic and its cost model (Eq. 15-17).
+
+Pins: every function here is pinned by ``tests/test_oracle_*.py`` against
+closed forms, invariants, brute force and the paper's printed values
+(see DESIGN.md §"Oracle and pins").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_SRC_PATH = os.path.join(_HERE, "exact_sum.c")
+
+UNIT = Fraction(1, 1 << 24)  # every finite binary16 value is a multiple of 2^-24
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [
+        ("t_lo", ctypes.c_uint64),
+        ("t_hi", ctypes.c_int64),
+        ("a_lo", ctypes.c_uint64),
+        ("a_hi", ctypes.c_uint64),
+        ("n_nan", ctypes.c_uint64),
+        ("n_pinf", ctypes.c_uint64),
+        ("n_ninf", ctypes.c_uint64),
+    ]
+
+
+def build(force: bool = False) -> str:
+    """Compile ``exact_sum.c`` into ``liboracle.so`` with gcc (plain -O2)."""
+    if force or not os.path.exists(_LIB_PATH) or (
+        os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC_PATH)
+    ):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.run(
+            ["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC_PATH],
+            check=True,
+        )
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        lib.oracle_exact_sum_fp16.argtypes = [
+            ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(_Result)]
+        lib.oracle_exact_sum_fp16.restype = ctypes.c_int
+        lib.oracle_exact_segment_sums_fp16.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(_Result)]
+        lib.oracle_exact_segment_sums_fp16.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+@dataclass(frozen=True)
+class ExactSum:
+    """Exact result of R(X): T = sum x_i * 2^24 and A = sum |x_i| * 2^24 (ints)."""
+
+    T: int
+    A: int
+    n_nan: int = 0
+    n_pinf: int = 0
+    n_ninf: int = 0
+
+    def __add__(self, other: "ExactSum") -> "ExactSum":
+        # Exact homomorphism R(X ++ Y) = R(X) + R(Y).
+        return ExactSum(self.T + other.T, self.A + other.A, self.n_nan + other.n_nan,
+                        self.n_pinf + other.n_pinf, self.n_ninf + other.n_ninf)
+
+    @property
+    def finite(self) -> bool:
+        return self.n_nan == 0 and self.n_pinf == 0 and self.n_ninf == 0
+
+    @property
+    def special(self) -> float | None:
+        """IEEE propagation for non-finite inputs (reading G13)."""
+        if self.n_nan or (self.n_pinf and self.n_ninf):
+            return float("nan")
+        if self.n_pinf:
+            return float("inf")
+        if self.n_ninf:
+            return float("-inf")
+        return None
+
+    @property
+    def value(self) -> Fraction:
+        """R(X) as an exact rational."""
+        return self.T * UNIT
+
+    @property
+    def abs_value(self) -> Fraction:
+        return self.A * UNIT
+
+    def f32(self) -> float:
+        """Correctly rounded (RNE) binary32 value of R(X), as a Python float."""
+        s = self.special
+        return s if s is not None else round_to_f32(self.value)
+
+    def f64(self) -> float:
+        """Correctly rounded binary64 value of R(X) (Fraction.__float__ is RNE)."""
+        s = self.special
+        return s if s is not None else float(self.value)
+
+
+def _from_struct(r: _Result) -> ExactSum:
+    t = (int(r.t_hi) << 64) | int(r.t_lo)
+    a = (int(r.a_hi) << 64) | int(r.a_lo)
+    return ExactSum(t, a, int(r.n_nan), int(r.n_pinf), int(r.n_ninf))
+
+
+def _as_bits(x) -> np.ndarray:
+    x = np.asarray(x)
+    if x.dtype == np.float16:
+        x = x.view(np.uint16)
+    if x.dtype != np.uint16:
+        raise TypeError(f"expected binary16 bit patterns (uint16/float16), got {x.dtype}")
+    return np.ascontiguousarray(x.reshape(-1))
+
+
+def exact_sum_fp16(x, threads: int = 1) -> ExactSum:
+    """Exact R(X) (Eq. 2) of binary16 inputs ``x`` (uint16 bits or float16).
+
+    ``threads`` > 1 splits X into contiguous chunks reduced concurrently and
+    adds the exact chunk results (homomorphism); the result is
+    identical for every thread count because integer addition is exact.
+    """
+    bits = _as_bits(x)
+    lib = _load()
+    n = bits.size
+    threads = max(1, min(int(threads), max(1, n)))
+
+    def run(lo: int, hi: int) -> ExactSum:
+        r = _Result()
+        lib.oracle_exact_sum_fp16(bits.ctypes.data + 2 * lo, hi - lo, ctypes.byref(r))
+        return _from_struct(r)
+
+    if threads == 1:
+        return run(0, n)
+    bounds = [n * k // threads for k in range(threads + 1)]
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        parts = list(ex.map(lambda k: run(bounds[k], bounds[k + 1]), range(threads)))
+    total = ExactSum(0, 0)
+    for p in parts:
+        total = total + p
+    return total
+
+
+def exact_segment_sums_fp16(x, offsets) -> list[ExactSum]:
+    """Exact per-segment R for CSR ``offsets`` (segment j = x[off[j]:off[j+1]])."""
+    bits = _as_bits(x)
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    s = off.size - 1
+    if s < 0:
+        raise ValueError("offsets must hold num_segments + 1 entries")
+    if s and (off[0] < 0 or off[-1] > bits.size):
+        raise ValueError("offsets out of range")
+    res = (_Result * max(s, 1))()
+    rc = _load().oracle_exact_segment_sums_fp16(bits.ctypes.data, off.ctypes.data, s, res)
+    if rc != 0:
+        raise ValueError("offsets must be non-decreasing")
+    return [_from_struct(res[j]) for j in range(s)]
+
+
+def exact_sum_fraction(values) -> Fraction:
+    """Pure-Python exact sum of binary16 inputs (brute force for tiny n).
+
+    Each element is converted by numpy to float64 (exact for binary16) and
+    then to ``Fraction`` (exact), and the Fractions are added left to right.
+    Independent of ``exact_sum.c``.
+    """
+    f = np.asarray(values)
+    if f.dtype == np.uint16:
+        f = f.view(np.float16)
+    total = Fraction(0)
+    for v in f.astype(np.float64).tolist():
+        total += Fraction(v)
+    return total
+
+
+def round_to_f32(q: Fraction) -> float:
+    """Round an exact rational to binary32, round-to-nearest-even.
+
+    Returns a Python float holding the binary32 value exactly (inf on
+    overflow).  Written from the IEEE-754 definition: quantum 2^(e-23) for
+    normal exponents e >= -126, 2^-149 below; ties to the even significand.
+    """
+    q = Fraction(q)
+    if q == 0:
+        return 0.0
+    sign = -1.0 if q < 0 else 1.0
+    a = abs(q)
+    # e = floor(log2(a)), exactly.
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fraction(2) ** e > a:
+        e -= 1
+    elif Fraction(2) ** (e + 1) <= a:
+        e += 1
+    quantum = Fraction(2) ** (max(e, -126) - 23)
+    m = a / quantum
+    mi = m.numerator // m.denominator
+    rem = m - mi
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and (mi & 1)):
+        mi += 1
+    r = mi * quantum
+    if r >= Fraction(2) ** 128:
+        return sign * float("inf")
+    return sign * float(r)
+
+
+def within_tolerance(g: float, es: ExactSum, rel: Fraction = Fraction(1, 1 << 20)) -> bool:
+    """North-star acceptance test, exact: |g - R(X)| <= rel * sum |x_i|.
+
+    ``g`` is the GPU's binary32 (or binary64) result.  Non-finite expected
+    values must match exactly (NaN matches NaN).  Evaluated in rationals, so
+    there is no rounding ambiguity at the boundary (reading G15).
+    """
+    s = es.special
+    if s is not None:
+        if s != s:
+            return g != g
+        return g == s
+    if not np.isfinite(g):
+        return False
+    return abs(Fraction(float(g)) - es.value) <= rel * es.abs_value
+
+
+def error_units(g: float, es: ExactSum) -> Fraction:
+    """|g - R(X)| in units of 2^-24 (exact)."""
+    return abs(Fraction(float(g)) - es.value) / UNIT
+
+
+__all__ = [
+    "ExactSum", "UNIT", "build", "exact_sum_fp16", "exact_segment_sums_fp16",
+    "exact_sum_fraction", "round_to_f32", "within_tolerance", "error_units",
+]

@@ -1,0 +1,171 @@
+"""tcr_inputs -- seeded synthetic input generators shared by the oracle side
+and the CUDA side.  Holds NONE of the method's arithmetic (no sums, no MMA).
+
+Each value depends only on (seed, global index i), through the splitmix64
+counter-based hash, so any shard or sample of a workload can be regenerated
+anywhere (DESIGN.md §"Input recipe").  Two implementations of the same
+definition exist: numpy here (host) and ``gen.cu`` (device, built into
+``libtcr_inputs.so``); ``tests/test_inputs.py`` checks them bit for bit.
+
+Distributions (``dist``):
+
+* ``UNIFORM_PM1`` (0) -- r = z >> 40 (24 bits), v = r * 2^-23 - 1 (exact in
+  binary32, range [-1, 1)), x = binary16 RNE(v).  BASELINE configs'
+  "fp16 uniform[-1,1]" (reading G14).
+* ``UNIFORM_01`` (1) -- v = r * 2^-24, x = RNE(v): all-positive stress.
+* ``ONES`` (2) -- x = 1.0 (0x3C00).
+* ``ALTERNATING`` (3) -- x_{2j} = UNIFORM_PM1(2j), x_{2j+1} = -x_{2j}.
+* ``WIDE`` (4) -- bits built from z: sign = bit 63, biased exponent =
+  (z >> 32) mod 31 (0..30, subnormals included), mantissa = z & 0x3ff.
+* ``SMALLINT`` (5) -- x = ((z >> 32) mod 5) - 2, integers in {-2..2}.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+UNIFORM_PM1 = 0
+UNIFORM_01 = 1
+ONES = 2
+ALTERNATING = 3
+WIDE = 4
+SMALLINT = 5
+
+DIST_NAMES = {
+    "uniform_pm1": UNIFORM_PM1,
+    "uniform01": UNIFORM_01,
+    "ones": ONES,
+    "alternating": ALTERNATING,
+    "wide": WIDE,
+    "smallint": SMALLINT,
+}
+
+# Workload seeds (DESIGN.md §"Input recipe"): C1..C5 of BASELINE.json configs.
+SEED_C1 = 1903036401
+SEED_C2 = 1903036402
+SEED_C3 = 1903036403
+SEED_C4 = 1903036404
+SEED_C5 = 1903036405
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_MIX1 = np.uint64(0xBF58476D1CE4E5B9)
+_MIX2 = np.uint64(0x94D049BB133111EB)
+
+
+def splitmix64(seed: int, idx: np.ndarray) -> np.ndarray:
+    """z = splitmix64 finaliser of seed + (i+1) * golden, all mod 2^64."""
+    idx = np.asarray(idx, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + (idx + np.uint64(1)) * _GOLDEN
+        z = (z ^ (z >> np.uint64(30))) * _MIX1
+        z = (z ^ (z >> np.uint64(27))) * _MIX2
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def _uniform_pm1_bits(seed: int, idx: np.ndarray) -> np.ndarray:
+    z = splitmix64(seed, idx)
+    r = (z >> np.uint64(40)).astype(np.float32)          # exact: r < 2^24
+    v = r * np.float32(2.0 ** -23) - np.float32(1.0)     # exact in binary32
+    return v.astype(np.float16).view(np.uint16)          # RNE
+
+
+def generate(seed: int, start: int, count: int, dist: int = UNIFORM_PM1) -> np.ndarray:
+    """Binary16 bit patterns x[start .. start+count) of the (seed, dist) stream."""
+    idx = np.arange(start, start + count, dtype=np.uint64)
+    if dist == UNIFORM_PM1:
+        return _uniform_pm1_bits(seed, idx)
+    if dist == UNIFORM_01:
+        z = splitmix64(seed, idx)
+        r = (z >> np.uint64(40)).astype(np.float32)
+        return (r * np.float32(2.0 ** -24)).astype(np.float16).view(np.uint16)
+    if dist == ONES:
+        return np.full(count, 0x3C00, dtype=np.uint16)
+    if dist == ALTERNATING:
+        even = idx & ~np.uint64(1)
+        b = _uniform_pm1_bits(seed, even)
+        odd = (idx & np.uint64(1)).astype(bool)
+        b = b.copy()
+        b[odd] ^= np.uint16(0x8000)
+        return b
+    if dist == WIDE:
+        z = splitmix64(seed, idx)
+        sign = (z >> np.uint64(63)).astype(np.uint16)
+        e = ((z >> np.uint64(32)) % np.uint64(31)).astype(np.uint16)
+        f = (z & np.uint64(0x3FF)).astype(np.uint16)
+        return (sign << np.uint16(15)) | (e << np.uint16(10)) | f
+    if dist == SMALLINT:
+        z = splitmix64(seed, idx)
+        v = ((z >> np.uint64(32)) % np.uint64(5)).astype(np.int64) - 2
+        return v.astype(np.float16).view(np.uint16)
+    raise ValueError(f"unknown dist {dist}")
+
+
+def loguniform_lengths(seed: int, num_segments: int, lo: int = 256, hi: int = 65536) -> np.ndarray:
+    """Segment lengths, log-uniform integers in [lo, hi] (reading G18).
+
+    u = (z >> 11) * 2^-53 in [0, 1); L = floor(exp2(log2(lo) + u * (log2(hi+1) - log2(lo)))),
+    clamped to [lo, hi].  Host-only (offsets are always generated here and uploaded).
+    """
+    z = splitmix64(seed ^ 0x5E6, np.arange(num_segments, dtype=np.uint64))
+    u = (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    ll = np.log2(float(lo)) + u * (np.log2(float(hi + 1)) - np.log2(float(lo)))
+    L = np.floor(np.exp2(ll)).astype(np.int64)
+    return np.clip(L, lo, hi)
+
+
+def offsets_from_lengths(lengths: np.ndarray, start: int = 0) -> np.ndarray:
+    """CSR offsets (num_segments + 1 entries, int64) from segment lengths."""
+    off = np.empty(len(lengths) + 1, dtype=np.int64)
+    off[0] = start
+    np.cumsum(np.asarray(lengths, dtype=np.int64), out=off[1:])
+    off[1:] += start
+    return off
+
+
+# ---------------------------------------------------------------------------
+# Device generator (gen.cu -> libtcr_inputs.so): same definition, on the GPU.
+# ---------------------------------------------------------------------------
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtcr_inputs.so")
+_dev = None
+
+
+def _device_lib():
+    global _dev
+    if _dev is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(LIB_PATH)
+        lib.tcr_inputs_generate.argtypes = [
+            ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+            ctypes.c_int, ctypes.c_void_p]
+        lib.tcr_inputs_generate.restype = ctypes.c_int
+        _dev = lib
+    return _dev
+
+
+def generate_device(out_ptr: int, seed: int, start: int, count: int, dist: int = UNIFORM_PM1,
+                    stream: int = 0) -> None:
+    """Fill device memory ``out_ptr`` (count binary16) with x[start .. start+count)."""
+    rc = _device_lib().tcr_inputs_generate(
+        ctypes.c_void_p(out_ptr), ctypes.c_uint64(seed), ctypes.c_uint64(start),
+        ctypes.c_uint64(count), int(dist), ctypes.c_void_p(stream))
+    if rc != 0:
+        raise RuntimeError(f"tcr_inputs_generate failed with code {rc}")
+
+
+def generate_tensor(seed: int, start: int, count: int, dist: int = UNIFORM_PM1, device="cuda"):
+    """torch.float16 tensor of the stream generated on ``device`` (CUDA)."""
+    import torch
+
+    t = torch.empty(count, dtype=torch.float16, device=device)
+    if count:
+        generate_device(t.data_ptr(), seed, start, count, dist,
+                        torch.cuda.current_stream(t.device).cuda_stream)
+    return t
