@@ -1,0 +1,200 @@
+/*
+ * tcr.h -- C ABI of libtcr: tensor-core (MMA-encoded) fp16 sum reduction on
+ * NVIDIA B200 (sm_100a).  From-scratch implementation of the hot path of
+ * arXiv 1903.03640, "Analyzing GPU Tensor Core Potential for Fast
+ * Reductions" (Carrasco, Vega, Navarro).
+ *
+ * Citations: "P:L" = line L of the paper text; section/equation
+ * numbers follow the paper's LaTeX auto-numbering.
+ *
+ * The operation (§III Eq. 2):  R(X) = sum_{i=1..n} x_i,
+ * with x_i IEEE-754 binary16.  The library encodes it as the paper does
+ * (§IV.A, Eq. 9-14): each 16x16 tile A of 256 inputs is
+ * multiplied by an all-ones matrix, D = A x 1 + C, which puts the tile's
+ * row sums in every column (Eq. 10); the accumulator C is carried
+ * across a bounded chain of tiles; a second MMA with the ones in the A
+ * position, D' = 1 x D (Eq. 11-12), collapses row sums to one
+ * scalar replicated in every entry; and the level recursion R_tc
+ * (Eq. 13-14) continues across warps, CTAs and the grid inside
+ * ONE launch (the inter-level barrier, which the paper gets from kernel
+ * termination, is a last-CTA completion ticket).
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ *  - x, offsets and out are DEVICE pointers (cudaMalloc / torch tensors)
+ *    owned by the caller, except in tcr_reduce_sum_host.  They must stay
+ *    valid until the enqueued work completes; the library never frees them.
+ *  - x holds binary16 bit patterns (tcr_half), 2-byte aligned; any 16-byte
+ *    misalignment is handled internally.  out must be 4-byte aligned
+ *    (8-byte for double).
+ *  - stream: a cudaStream_t (tcr_stream is layout-identical), NULL = the
+ *    legacy default stream.  Every call is stream-ordered and asynchronous
+ *    (no host synchronisation) except tcr_reduce_sum_host.
+ *  - Accuracy contract (north star, BASELINE.json): for finite inputs the
+ *    binary32 result g satisfies |g - R(X)| <= 2^-20 * sum |x_i|.  The
+ *    paper leaves the precision of the tensor-core reduction open;
+ *    this bound is the library's, not the paper's.  NaN/inf inputs
+ *    propagate as IEEE addition would.
+ *  - Results are bitwise deterministic for a given (device, n, x, algo,
+ *    configuration, library build): the order of every floating-point
+ *    operation is fixed, no floating-point atomics are used.
+ *  - n == 0 (or an empty segment) yields +0.0.
+ *  - Errors: a status is returned, nothing is thrown across the ABI.
+ *    TCR_ERR_INVALID_VALUE for NULL pointers with n > 0, misaligned
+ *    pointers, or an unknown algo/config key; TCR_ERR_UNSUPPORTED_DEVICE if
+ *    the current device is not compute capability 10.x (there is no
+ *    fallback of any kind); TCR_ERR_OUT_OF_MEMORY if the workspace cannot be
+ *    allocated; TCR_ERR_CUDA for a CUDA error (text in tcr_last_error()).
+ *    Asynchronous device faults surface at the caller's next synchronisation.
+ *  - Workspace: the library owns a small per-(device, stream) workspace
+ *    (fp64 partials of the CTAs, a completion ticket, scheduler counters),
+ *    allocated on the first call for that stream and reused.  The first
+ *    call on a stream must therefore not be made while that stream is being
+ *    captured into a CUDA graph.  tcr_release_workspaces() frees them.
+ *  - Threading: calls are reentrant; concurrent calls on distinct streams
+ *    are safe (separate workspaces); calls on one stream are serialised by
+ *    stream order.
+ */
+#ifndef TCR_H_
+#define TCR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TCR_VERSION 100 /* 1.0.0 */
+
+typedef uint16_t tcr_half;              /* IEEE-754 binary16 bit pattern */
+typedef struct CUstream_st *tcr_stream; /* == cudaStream_t / CUstream     */
+
+typedef enum {
+    TCR_OK = 0,
+    TCR_ERR_INVALID_VALUE = 1,
+    TCR_ERR_UNSUPPORTED_DEVICE = 2,
+    TCR_ERR_OUT_OF_MEMORY = 3,
+    TCR_ERR_CUDA = 4
+} tcr_status;
+
+/* Kernel selection for tcr_reduce_sum_algo / the _config default. */
+typedef enum {
+    TCR_ALGO_DEFAULT = 0, /* the library's fastest MMA-encoded kernel        */
+    TCR_ALGO_MMA_SYNC = 1, /* mma.sync m16n8k16 (A from 128-bit loads)       */
+    TCR_ALGO_TCGEN05 = 2, /* cp.async.bulk -> SMEM -> tcgen05.mma, D in TMEM */
+    TCR_ALGO_SHUFFLE = 3  /* classic comparison path (§II): fp32
+                             FADD chains + shfl_xor tree, no tensor cores    */
+} tcr_algo;
+
+/*
+ * tcr_reduce_sum -- R(X) of n binary16 values x[0..n) into *out (binary32).
+ * The north-star entry point: MMA-encoded, one kernel launch, writes *out
+ * on the device.  (Eq. 2; method P:169-236 Eq. 9-14.)
+ */
+tcr_status tcr_reduce_sum(const tcr_half *x, size_t n, float *out, tcr_stream stream);
+
+/*
+ * tcr_reduce_sum_shuffle -- same contract as tcr_reduce_sum, computed by the
+ * classic warp-shuffle tree reduction (the paper's comparison algorithm,
+ * P:83-85 and P:113-137) instead of MMAs.
+ */
+tcr_status tcr_reduce_sum_shuffle(const tcr_half *x, size_t n, float *out, tcr_stream stream);
+
+/*
+ * tcr_reduce_sum_f64 -- same reduction as tcr_reduce_sum, but writes the
+ * binary64 total *before* the final rounding to binary32.  Used as the
+ * per-GPU partial of a sharded reduction (the paper's "local reduction"
+ * of a distributed reduction), so the cross-GPU combine does not add
+ * binary32 roundings.
+ */
+tcr_status tcr_reduce_sum_f64(const tcr_half *x, size_t n, double *out, tcr_stream stream);
+
+/*
+ * tcr_reduce_sum_algo -- explicit kernel choice.  Writes the binary32
+ * result to out_f32 and/or the binary64 total to out_f64 (either may be
+ * NULL, not both).
+ */
+tcr_status tcr_reduce_sum_algo(const tcr_half *x, size_t n, float *out_f32, double *out_f64,
+                               tcr_algo algo, tcr_stream stream);
+
+/*
+ * tcr_reduce_sum_segmented -- per-segment R over CSR offsets:
+ * out[j] = R(x[offsets[j] .. offsets[j+1])) for j in [0, num_segments).
+ * offsets: device int64[num_segments + 1], non-decreasing, offsets[0] >= 0,
+ * all within the caller's x buffer (not checked on the device).  out:
+ * device float[num_segments].  Each segment is reduced by the MMA encoding
+ * with its unaligned head and tail zero-masked (the paper's zero padding of
+ * the trailing group, reading G5).  out[j] corresponds exactly to segment j.
+ * Segments may be read as whole aligned 16-byte vectors, i.e. up to 14 bytes
+ * outside [offsets[0], offsets[S]) but never outside the 16-byte-aligned
+ * chunks that contain segment data.
+ */
+tcr_status tcr_reduce_sum_segmented(const tcr_half *x, const int64_t *offsets,
+                                    size_t num_segments, float *out, tcr_stream stream);
+tcr_status tcr_reduce_sum_segmented_shuffle(const tcr_half *x, const int64_t *offsets,
+                                            size_t num_segments, float *out, tcr_stream stream);
+
+/*
+ * tcr_reduce_sum_batched -- num_segments contiguous segments of segment_len
+ * elements each: out[j] = R(x[j*segment_len .. (j+1)*segment_len)).
+ */
+tcr_status tcr_reduce_sum_batched(const tcr_half *x, size_t num_segments, size_t segment_len,
+                                  float *out, tcr_stream stream);
+tcr_status tcr_reduce_sum_batched_shuffle(const tcr_half *x, size_t num_segments,
+                                          size_t segment_len, float *out, tcr_stream stream);
+
+/*
+ * tcr_reduce_sum_host -- end-to-end form: x is a HOST pointer (pinned
+ * memory for full PCIe bandwidth; pageable works), *out is a HOST float.
+ * The library streams x to the device in chunks through its own staging
+ * buffers on `stream`, reduces each chunk with the default MMA kernel into
+ * a binary64 partial, combines the partials in chunk order on the device,
+ * copies the binary32 result back and synchronises `stream` before
+ * returning.  Same accuracy contract as tcr_reduce_sum.
+ */
+tcr_status tcr_reduce_sum_host(const tcr_half *x, size_t n, float *out, tcr_stream stream);
+
+/*
+ * tcr_round_f64_to_f32 -- out[0] = (float)in[0], round-to-nearest-even, on
+ * the device (finaliser of a sharded reduction after the allreduce of the
+ * binary64 partials).
+ */
+tcr_status tcr_round_f64_to_f32(const double *in, float *out, tcr_stream stream);
+
+/*
+ * tcr_probe_mma -- hardware characterisation (not part of the reduction):
+ * executes ONE MMA of the given algo (TCR_ALGO_MMA_SYNC: m16n8k16;
+ * TCR_ALGO_TCGEN05: M=128,N=16,K=16) with A = a (row-major 16x16 for
+ * mma.sync / 128x16 for tcgen05, binary16), B = all ones and C = c
+ * (binary32, one value per row of A), and writes D's first column to d.
+ * a: device tcr_half[16*16] or [128*16]; c, d: device float[16] or [128].
+ * Used by the tests to record whether the tensor-core fp32 accumulate
+ * rounds to nearest or truncates (reading G10).
+ */
+tcr_status tcr_probe_mma(const tcr_half *a, const float *c, float *d, tcr_algo algo,
+                         tcr_stream stream);
+
+/* Tuning knobs (process-wide; defaults are the measured best on B200). */
+typedef enum {
+    TCR_CFG_DEFAULT_ALGO = 0,     /* tcr_algo used by tcr_reduce_sum        */
+    TCR_CFG_BLOCKS_PER_SM = 1,    /* CTAs per SM of the streaming kernels   */
+    TCR_CFG_UNROLL = 2,           /* 16-byte loads in flight per lane (mma.sync/shuffle) */
+    TCR_CFG_TC05_STAGES = 3,      /* SMEM ring stages of the tcgen05 kernel */
+    TCR_CFG_TC05_STAGE_KB = 4,    /* KiB per stage of the tcgen05 kernel    */
+    TCR_CFG_CHAIN = 5             /* tiles per carried-accumulator chain (K) */
+} tcr_config_key;
+tcr_status tcr_set_config(tcr_config_key key, int value);
+int tcr_get_config(tcr_config_key key); /* -1 for an unknown key */
+
+const char *tcr_status_string(tcr_status s);
+const char *tcr_last_error(void);        /* thread-local detail of the last error */
+tcr_status tcr_release_workspaces(void); /* caller guarantees no in-flight work   */
+uint64_t tcr_launch_count(void);         /* kernels launched by this library so far */
+int tcr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCR_H_ */

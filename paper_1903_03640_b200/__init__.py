@@ -1,0 +1,270 @@
+"""paper_1903_03640_b200 -- B200-native tensor-core (MMA-encoded) fp16 sum
+reduction, from scratch, after arXiv 1903.03640 ("Analyzing GPU Tensor Core
+Potential for Fast Reductions").
+
+This module is the thin Python binding of ``libtcr.so`` (C ABI declared in
+``include/tcr.h``): argument marshalling only.  Every step of the reduction
+runs in the library's sm_100a kernels; there is no CPU or library fallback,
+and importing this module fails loudly if ``libtcr.so`` is missing.
+
+Functions take either torch CUDA tensors (dtype float16 / int64 / float32 /
+float64) or raw device pointers (ints), and a CUDA stream (torch.cuda.Stream,
+a raw handle int, or None for torch's current stream).
+
+Names follow the C ABI:
+
+* :func:`tcr_reduce_sum`, :func:`tcr_reduce_sum_shuffle`,
+  :func:`tcr_reduce_sum_f64`, :func:`tcr_reduce_sum_algo`
+* :func:`tcr_reduce_sum_segmented`, :func:`tcr_reduce_sum_segmented_shuffle`
+* :func:`tcr_reduce_sum_batched`, :func:`tcr_reduce_sum_batched_shuffle`
+* :func:`tcr_reduce_sum_host` (host buffers, end to end)
+* :func:`tcr_round_f64_to_f32`, :func:`tcr_probe_mma`
+* :func:`tcr_set_config` / :func:`tcr_get_config`, :func:`tcr_launch_count`,
+  :func:`tcr_release_workspaces`, :func:`tcr_version`
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtcr.so")
+
+TCR_OK = 0
+TCR_ERR_INVALID_VALUE = 1
+TCR_ERR_UNSUPPORTED_DEVICE = 2
+TCR_ERR_OUT_OF_MEMORY = 3
+TCR_ERR_CUDA = 4
+
+TCR_ALGO_DEFAULT = 0
+TCR_ALGO_MMA_SYNC = 1
+TCR_ALGO_TCGEN05 = 2
+TCR_ALGO_SHUFFLE = 3
+ALGOS = {"default": 0, "mma_sync": 1, "tcgen05": 2, "shuffle": 3}
+
+TCR_CFG_DEFAULT_ALGO = 0
+TCR_CFG_BLOCKS_PER_SM = 1
+TCR_CFG_UNROLL = 2
+TCR_CFG_TC05_STAGES = 3
+TCR_CFG_TC05_STAGE_KB = 4
+TCR_CFG_CHAIN = 5
+
+
+class TcrError(RuntimeError):
+    def __init__(self, status: int, fn: str, detail: str):
+        self.status = status
+        super().__init__(f"{fn} failed: {_status_name(status)}: {detail}")
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libtcr.so not found at {LIB_PATH}; build it with "
+        "`python -c 'import __graft_entry__ as g; g.build()'` (there is no fallback path)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+_P = ctypes.c_void_p
+_SZ = ctypes.c_size_t
+_I = ctypes.c_int
+
+_SIGS = {
+    "tcr_reduce_sum": [_P, _SZ, _P, _P],
+    "tcr_reduce_sum_shuffle": [_P, _SZ, _P, _P],
+    "tcr_reduce_sum_f64": [_P, _SZ, _P, _P],
+    "tcr_reduce_sum_algo": [_P, _SZ, _P, _P, _I, _P],
+    "tcr_reduce_sum_segmented": [_P, _P, _SZ, _P, _P],
+    "tcr_reduce_sum_segmented_shuffle": [_P, _P, _SZ, _P, _P],
+    "tcr_reduce_sum_batched": [_P, _SZ, _SZ, _P, _P],
+    "tcr_reduce_sum_batched_shuffle": [_P, _SZ, _SZ, _P, _P],
+    "tcr_reduce_sum_host": [_P, _SZ, _P, _P],
+    "tcr_round_f64_to_f32": [_P, _P, _P],
+    "tcr_probe_mma": [_P, _P, _P, _I, _P],
+    "tcr_set_config": [_I, _I],
+    "tcr_release_workspaces": [],
+}
+for _name, _args in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = ctypes.c_int
+_lib.tcr_get_config.argtypes = [_I]
+_lib.tcr_get_config.restype = ctypes.c_int
+_lib.tcr_status_string.argtypes = [_I]
+_lib.tcr_status_string.restype = ctypes.c_char_p
+_lib.tcr_last_error.argtypes = []
+_lib.tcr_last_error.restype = ctypes.c_char_p
+_lib.tcr_launch_count.argtypes = []
+_lib.tcr_launch_count.restype = ctypes.c_uint64
+_lib.tcr_version.argtypes = []
+_lib.tcr_version.restype = ctypes.c_int
+
+
+def _status_name(s: int) -> str:
+    return _lib.tcr_status_string(int(s)).decode()
+
+
+def _check(status: int, fn: str) -> None:
+    if status != TCR_OK:
+        raise TcrError(status, fn, _lib.tcr_last_error().decode())
+
+
+def _ptr(t) -> int | None:
+    """Device (or host) address of a tensor / int / None."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _numel(t, n):
+    if n is not None:
+        return int(n)
+    return int(t.numel())
+
+
+def _stream(stream, like=None) -> int | None:
+    if stream is None:
+        import torch
+
+        dev = like.device if like is not None and hasattr(like, "device") else None
+        return torch.cuda.current_stream(dev).cuda_stream or None
+    if isinstance(stream, int):
+        return stream or None
+    return stream.cuda_stream or None
+
+
+def tcr_reduce_sum(x, out, n=None, stream=None) -> None:
+    """out[0] (float32, device) = sum of the n binary16 values of x (MMA-encoded)."""
+    _check(_lib.tcr_reduce_sum(_ptr(x), _numel(x, n), _ptr(out), _stream(stream, x)),
+           "tcr_reduce_sum")
+
+
+def tcr_reduce_sum_shuffle(x, out, n=None, stream=None) -> None:
+    """Classic warp-shuffle tree reduction; same contract as tcr_reduce_sum."""
+    _check(_lib.tcr_reduce_sum_shuffle(_ptr(x), _numel(x, n), _ptr(out), _stream(stream, x)),
+           "tcr_reduce_sum_shuffle")
+
+
+def tcr_reduce_sum_f64(x, out, n=None, stream=None) -> None:
+    """out[0] (float64, device) = the binary64 total before the final rounding."""
+    _check(_lib.tcr_reduce_sum_f64(_ptr(x), _numel(x, n), _ptr(out), _stream(stream, x)),
+           "tcr_reduce_sum_f64")
+
+
+def tcr_reduce_sum_algo(x, out_f32=None, out_f64=None, algo=TCR_ALGO_DEFAULT, n=None,
+                        stream=None) -> None:
+    if isinstance(algo, str):
+        algo = ALGOS[algo]
+    _check(_lib.tcr_reduce_sum_algo(_ptr(x), _numel(x, n), _ptr(out_f32), _ptr(out_f64),
+                                    int(algo), _stream(stream, x)), "tcr_reduce_sum_algo")
+
+
+def tcr_reduce_sum_segmented(x, offsets, out, num_segments=None, stream=None) -> None:
+    """out[j] = sum of x[offsets[j]:offsets[j+1]] (CSR, int64 offsets on the device)."""
+    s = int(num_segments) if num_segments is not None else int(out.numel())
+    _check(_lib.tcr_reduce_sum_segmented(_ptr(x), _ptr(offsets), s, _ptr(out), _stream(stream, x)),
+           "tcr_reduce_sum_segmented")
+
+
+def tcr_reduce_sum_segmented_shuffle(x, offsets, out, num_segments=None, stream=None) -> None:
+    s = int(num_segments) if num_segments is not None else int(out.numel())
+    _check(_lib.tcr_reduce_sum_segmented_shuffle(_ptr(x), _ptr(offsets), s, _ptr(out),
+                                                 _stream(stream, x)),
+           "tcr_reduce_sum_segmented_shuffle")
+
+
+def tcr_reduce_sum_batched(x, segment_len, out, num_segments=None, stream=None) -> None:
+    """out[j] = sum of x[j*L:(j+1)*L]."""
+    s = int(num_segments) if num_segments is not None else int(out.numel())
+    _check(_lib.tcr_reduce_sum_batched(_ptr(x), s, int(segment_len), _ptr(out),
+                                       _stream(stream, x)), "tcr_reduce_sum_batched")
+
+
+def tcr_reduce_sum_batched_shuffle(x, segment_len, out, num_segments=None, stream=None) -> None:
+    s = int(num_segments) if num_segments is not None else int(out.numel())
+    _check(_lib.tcr_reduce_sum_batched_shuffle(_ptr(x), s, int(segment_len), _ptr(out),
+                                               _stream(stream, x)),
+           "tcr_reduce_sum_batched_shuffle")
+
+
+def tcr_reduce_sum_host(x, n=None, stream=None) -> float:
+    """End to end: x is a HOST buffer (pinned CPU tensor, numpy array or address).
+    Returns the binary32 sum as a Python float (the call synchronises `stream`)."""
+    res = ctypes.c_float(0.0)
+    if hasattr(x, "ctypes"):  # numpy
+        addr, cnt = x.ctypes.data, x.size
+    else:
+        addr, cnt = _ptr(x), (x.numel() if hasattr(x, "numel") else None)
+    cnt = int(n) if n is not None else int(cnt)
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream().cuda_stream
+    _check(_lib.tcr_reduce_sum_host(addr, cnt, ctypes.addressof(res), _stream(stream)),
+           "tcr_reduce_sum_host")
+    return float(res.value)
+
+
+def tcr_round_f64_to_f32(inp, out, stream=None) -> None:
+    _check(_lib.tcr_round_f64_to_f32(_ptr(inp), _ptr(out), _stream(stream, inp)),
+           "tcr_round_f64_to_f32")
+
+
+def tcr_probe_mma(a, c, d, algo=TCR_ALGO_MMA_SYNC, stream=None) -> None:
+    if isinstance(algo, str):
+        algo = ALGOS[algo]
+    _check(_lib.tcr_probe_mma(_ptr(a), _ptr(c), _ptr(d), int(algo), _stream(stream, a)),
+           "tcr_probe_mma")
+
+
+def tcr_set_config(key: int, value: int) -> None:
+    _check(_lib.tcr_set_config(int(key), int(value)), "tcr_set_config")
+
+
+def tcr_get_config(key: int) -> int:
+    return int(_lib.tcr_get_config(int(key)))
+
+
+def tcr_launch_count() -> int:
+    return int(_lib.tcr_launch_count())
+
+
+def tcr_release_workspaces() -> None:
+    _check(_lib.tcr_release_workspaces(), "tcr_release_workspaces")
+
+
+def tcr_version() -> int:
+    return int(_lib.tcr_version())
+
+
+def tcr_last_error() -> str:
+    return _lib.tcr_last_error().decode()
+
+
+def tcr_status_string(s: int) -> str:
+    return _status_name(s)
+
+
+# Convenience (allocating) wrappers --------------------------------------------------
+
+
+def reduce_sum(x, algo: str | int = "default", stream=None):
+    """Allocate a float32 device scalar and reduce x into it; returns the tensor."""
+    import torch
+
+    out = torch.empty(1, dtype=torch.float32, device=x.device)
+    tcr_reduce_sum_algo(x, out_f32=out, algo=algo, stream=stream)
+    return out
+
+
+def reduce_sum_segmented(x, offsets, mma: bool = True, stream=None):
+    import torch
+
+    out = torch.empty(offsets.numel() - 1, dtype=torch.float32, device=x.device)
+    f = tcr_reduce_sum_segmented if mma else tcr_reduce_sum_segmented_shuffle
+    f(x, offsets, out, stream=stream)
+    return out
+
+
+__all__ = [n for n in dir() if n.startswith("tcr_") or n.startswith("TCR_")] + [
+    "reduce_sum", "reduce_sum_segmented", "TcrError", "LIB_PATH", "ALGOS"]

@@ -1,0 +1,409 @@
+// tcr_api.cu -- the C ABI of libtcr (include/tcr.h): argument validation,
+// device check, per-(device, stream) workspace cache, kernel dispatch.
+// Every compute step runs in this library's kernels; there is no fallback.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/tcr.h"
+#include "tcr_internal.h"
+
+namespace tcr {
+cudaError_t launch_probe_mma_sync(const uint16_t* a, const float* c, float* d,
+                                  cudaStream_t stream);
+cudaError_t launch_probe_mma_tcgen05(const uint16_t* a, const float* c, float* d,
+                                     cudaStream_t stream);
+}  // namespace tcr
+
+namespace {
+
+using tcr::DevWorkspace;
+using tcr::LaunchCfg;
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+struct Config {
+    int default_algo = TCR_ALGO_MMA_SYNC;
+    int blocks_per_sm = 4;
+    int unroll = 8;
+    int flush_every = 1;  // chain K = flush_every * unroll / 2 tiles
+    int tc05_stages = 8;
+    int tc05_stage_kb = 16;
+};
+Config g_cfg;
+std::mutex g_cfg_mu;
+
+struct DeviceInfo {
+    int sms = 0;
+    int major = 0;
+    int minor = 0;
+};
+
+struct Workspace {
+    DevWorkspace dev{};
+    void* block = nullptr;           // one cudaMalloc for partials + counters
+    double* chunk_partials = nullptr;  // host-entry per-chunk fp64 partials
+    size_t chunk_cap = 0;
+    void* staging[2] = {nullptr, nullptr};
+    size_t staging_bytes = 0;
+    float* dev_out = nullptr;
+};
+
+std::mutex g_mu;
+std::map<int, DeviceInfo> g_devices;
+std::map<std::pair<int, cudaStream_t>, Workspace*> g_ws;
+
+tcr_status fail(tcr_status s, const char* what) {
+    g_last_error = what;
+    return s;
+}
+
+tcr_status cuda_fail(cudaError_t e, const char* where) {
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? TCR_ERR_OUT_OF_MEMORY : TCR_ERR_CUDA;
+}
+
+LaunchCfg make_cfg(const DeviceInfo& di) {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    LaunchCfg c;
+    c.sms = di.sms;
+    c.blocks_per_sm = g_cfg.blocks_per_sm;
+    c.unroll = g_cfg.unroll;
+    c.flush_every = g_cfg.flush_every;
+    c.tc05_stages = g_cfg.tc05_stages;
+    c.tc05_stage_kb = g_cfg.tc05_stage_kb;
+    return c;
+}
+
+// Current device, checked to be compute capability 10.x (B200 = sm_100).
+tcr_status current_device(int* dev, DeviceInfo* info) {
+    cudaError_t e = cudaGetDevice(dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_devices.find(*dev);
+    if (it == g_devices.end()) {
+        DeviceInfo di;
+        if ((e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, *dev)) ||
+            (e = cudaDeviceGetAttribute(&di.major, cudaDevAttrComputeCapabilityMajor, *dev)) ||
+            (e = cudaDeviceGetAttribute(&di.minor, cudaDevAttrComputeCapabilityMinor, *dev)))
+            return cuda_fail(e, "cudaDeviceGetAttribute");
+        it = g_devices.emplace(*dev, di).first;
+    }
+    *info = it->second;
+    if (info->major != 10) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "device %d is sm_%d%d; libtcr is built for sm_100a only",
+                 *dev, info->major, info->minor);
+        return fail(TCR_ERR_UNSUPPORTED_DEVICE, buf);
+    }
+    return TCR_OK;
+}
+
+// Workspace for (device, stream); partials sized for the largest grid any
+// kernel can use on this device (SMs x max CTAs/SM).
+tcr_status get_workspace(int dev, const DeviceInfo& di, cudaStream_t stream, Workspace** out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_pair(dev, stream);
+    auto it = g_ws.find(key);
+    if (it != g_ws.end()) {
+        *out = it->second;
+        return TCR_OK;
+    }
+    auto* ws = new Workspace();
+    const int capacity = di.sms * 32;  // 32 = max resident CTAs per SM
+    const size_t bytes = sizeof(double) * (size_t)capacity + 64;
+    cudaError_t e = cudaMalloc(&ws->block, bytes);
+    if (e != cudaSuccess) {
+        delete ws;
+        return cuda_fail(e, "cudaMalloc(workspace)");
+    }
+    char* p = static_cast<char*>(ws->block);
+    ws->dev.partials = reinterpret_cast<double*>(p);
+    char* ctr = p + sizeof(double) * (size_t)capacity;
+    ws->dev.seg_next = reinterpret_cast<unsigned long long*>(ctr);
+    ws->dev.ticket = reinterpret_cast<unsigned*>(ctr + 8);
+    ws->dev.seg_exit = reinterpret_cast<unsigned*>(ctr + 12);
+    ws->dev.capacity = capacity;
+    e = cudaMemsetAsync(ctr, 0, 64, stream);
+    if (e != cudaSuccess) {
+        cudaFree(ws->block);
+        delete ws;
+        return cuda_fail(e, "cudaMemsetAsync(workspace)");
+    }
+    g_ws.emplace(key, ws);
+    *out = ws;
+    return TCR_OK;
+}
+
+tcr_status prologue(cudaStream_t stream, DeviceInfo* di, Workspace** ws) {
+    int dev = 0;
+    tcr_status s = current_device(&dev, di);
+    if (s != TCR_OK) return s;
+    return get_workspace(dev, *di, stream, ws);
+}
+
+tcr_status after_launch(cudaError_t e, const char* where, int launches = 1) {
+    if (e != cudaSuccess) return cuda_fail(e, where);
+    g_launches.fetch_add(launches, std::memory_order_relaxed);
+    return TCR_OK;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_f64, int algo,
+                       cudaStream_t stream) {
+    if ((!x && n) || (!out_f32 && !out_f64)) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    if (!aligned(x, 2) || (out_f32 && !aligned(out_f32, 4)) || (out_f64 && !aligned(out_f64, 8)))
+        return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
+    if (algo == TCR_ALGO_DEFAULT) {
+        std::lock_guard<std::mutex> lk(g_cfg_mu);
+        algo = g_cfg.default_algo;
+    }
+    if (algo < TCR_ALGO_MMA_SYNC || algo > TCR_ALGO_SHUFFLE)
+        return fail(TCR_ERR_INVALID_VALUE, "unknown algo");
+    DeviceInfo di;
+    Workspace* ws = nullptr;
+    tcr_status s = prologue(stream, &di, &ws);
+    if (s != TCR_OK) return s;
+    const LaunchCfg cfg = make_cfg(di);
+    cudaError_t e;
+    if (algo == TCR_ALGO_TCGEN05)
+        e = tcr::launch_reduce_tcgen05(x, n, out_f32, out_f64, ws->dev, cfg, stream);
+    else
+        e = tcr::launch_reduce_stream(algo == TCR_ALGO_MMA_SYNC, x, n, out_f32, out_f64, ws->dev,
+                                      cfg, stream);
+    return after_launch(e, "reduce kernel launch");
+}
+
+tcr_status segmented_impl(bool mma, bool batched, const tcr_half* x, const int64_t* offsets,
+                          size_t S, size_t L, float* out, cudaStream_t stream) {
+    if (!out && S) return fail(TCR_ERR_INVALID_VALUE, "null out");
+    if (!batched && !offsets && S) return fail(TCR_ERR_INVALID_VALUE, "null offsets");
+    if (!x && S && (batched ? L != 0 : true)) return fail(TCR_ERR_INVALID_VALUE, "null x");
+    if (!aligned(x, 2) || !aligned(out, 4) || !aligned(offsets, 8))
+        return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
+    if (S == 0) return TCR_OK;
+    DeviceInfo di;
+    Workspace* ws = nullptr;
+    tcr_status s = prologue(stream, &di, &ws);
+    if (s != TCR_OK) return s;
+    const LaunchCfg cfg = make_cfg(di);
+    return after_launch(
+        tcr::launch_reduce_segmented(mma, batched, x, offsets, S, L, out, ws->dev, cfg, stream),
+        "segmented kernel launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+tcr_status tcr_reduce_sum(const tcr_half* x, size_t n, float* out, tcr_stream stream) {
+    return reduce_impl(x, n, out, nullptr, TCR_ALGO_DEFAULT, (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_shuffle(const tcr_half* x, size_t n, float* out, tcr_stream stream) {
+    return reduce_impl(x, n, out, nullptr, TCR_ALGO_SHUFFLE, (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_f64(const tcr_half* x, size_t n, double* out, tcr_stream stream) {
+    return reduce_impl(x, n, nullptr, out, TCR_ALGO_DEFAULT, (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_algo(const tcr_half* x, size_t n, float* out_f32, double* out_f64,
+                               tcr_algo algo, tcr_stream stream) {
+    return reduce_impl(x, n, out_f32, out_f64, (int)algo, (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_segmented(const tcr_half* x, const int64_t* offsets,
+                                    size_t num_segments, float* out, tcr_stream stream) {
+    return segmented_impl(true, false, x, offsets, num_segments, 0, out, (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_segmented_shuffle(const tcr_half* x, const int64_t* offsets,
+                                            size_t num_segments, float* out, tcr_stream stream) {
+    return segmented_impl(false, false, x, offsets, num_segments, 0, out, (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_batched(const tcr_half* x, size_t num_segments, size_t segment_len,
+                                  float* out, tcr_stream stream) {
+    return segmented_impl(true, true, x, nullptr, num_segments, segment_len, out,
+                          (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_batched_shuffle(const tcr_half* x, size_t num_segments,
+                                          size_t segment_len, float* out, tcr_stream stream) {
+    return segmented_impl(false, true, x, nullptr, num_segments, segment_len, out,
+                          (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_host(const tcr_half* x, size_t n, float* out, tcr_stream stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if ((!x && n) || !out) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    if (!aligned(x, 2)) return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
+    DeviceInfo di;
+    Workspace* ws = nullptr;
+    tcr_status s = prologue(stream, &di, &ws);
+    if (s != TCR_OK) return s;
+    const LaunchCfg cfg = make_cfg(di);
+    constexpr size_t kChunk = (size_t)1 << 26;  // elements per staged chunk (128 MiB)
+    const size_t chunks = n ? (n + kChunk - 1) / kChunk : 0;
+    cudaError_t e;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!ws->dev_out && (e = cudaMalloc(&ws->dev_out, sizeof(float))))
+            return cuda_fail(e, "cudaMalloc(out)");
+        if (ws->chunk_cap < chunks || !ws->chunk_partials) {
+            if (ws->chunk_partials) cudaFree(ws->chunk_partials);
+            ws->chunk_partials = nullptr;
+            const size_t cap = chunks < 64 ? 64 : chunks;
+            if ((e = cudaMalloc(&ws->chunk_partials, cap * sizeof(double))))
+                return cuda_fail(e, "cudaMalloc(chunk partials)");
+            ws->chunk_cap = cap;
+        }
+        const size_t need = (n < kChunk ? (n ? n : 1) : kChunk) * sizeof(uint16_t);
+        if (ws->staging_bytes < need) {
+            for (void*& b : ws->staging) {
+                if (b) cudaFree(b);
+                b = nullptr;
+            }
+            for (void*& b : ws->staging)
+                if ((e = cudaMalloc(&b, need))) return cuda_fail(e, "cudaMalloc(staging)");
+            ws->staging_bytes = need;
+        }
+    }
+    int launches = 0;
+    for (size_t c = 0; c < chunks; ++c) {
+        const size_t lo = c * kChunk, cnt = (n - lo < kChunk) ? n - lo : kChunk;
+        void* buf = ws->staging[c & 1];
+        if ((e = cudaMemcpyAsync(buf, x + lo, cnt * sizeof(uint16_t), cudaMemcpyHostToDevice,
+                                 stream)))
+            return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+        if ((e = tcr::launch_reduce_stream(true, static_cast<const uint16_t*>(buf), cnt, nullptr,
+                                           ws->chunk_partials + c, ws->dev, cfg, stream)))
+            return cuda_fail(e, "reduce kernel launch");
+        ++launches;
+    }
+    if ((e = tcr::launch_sum_partials(ws->chunk_partials, chunks, ws->dev_out, nullptr, stream)))
+        return cuda_fail(e, "sum_partials launch");
+    ++launches;
+    g_launches.fetch_add(launches, std::memory_order_relaxed);
+    if ((e = cudaMemcpyAsync(out, ws->dev_out, sizeof(float), cudaMemcpyDeviceToHost, stream)))
+        return cuda_fail(e, "cudaMemcpyAsync(D2H)");
+    if ((e = cudaStreamSynchronize(stream))) return cuda_fail(e, "cudaStreamSynchronize");
+    return TCR_OK;
+}
+
+tcr_status tcr_round_f64_to_f32(const double* in, float* out, tcr_stream stream) {
+    if (!in || !out) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    DeviceInfo di;
+    int dev;
+    tcr_status s = current_device(&dev, &di);
+    if (s != TCR_OK) return s;
+    return after_launch(tcr::launch_round_f64(in, out, (cudaStream_t)stream), "round launch");
+}
+
+tcr_status tcr_probe_mma(const tcr_half* a, const float* c, float* d, tcr_algo algo,
+                         tcr_stream stream) {
+    if (!a || !c || !d) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    DeviceInfo di;
+    int dev;
+    tcr_status s = current_device(&dev, &di);
+    if (s != TCR_OK) return s;
+    if (algo == TCR_ALGO_MMA_SYNC)
+        return after_launch(tcr::launch_probe_mma_sync(a, c, d, (cudaStream_t)stream), "probe");
+    if (algo == TCR_ALGO_TCGEN05)
+        return after_launch(tcr::launch_probe_mma_tcgen05(a, c, d, (cudaStream_t)stream),
+                            "probe");
+    return fail(TCR_ERR_INVALID_VALUE, "probe algo must be MMA_SYNC or TCGEN05");
+}
+
+tcr_status tcr_set_config(tcr_config_key key, int value) {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    switch (key) {
+        case TCR_CFG_DEFAULT_ALGO:
+            if (value < TCR_ALGO_MMA_SYNC || value > TCR_ALGO_SHUFFLE) break;
+            g_cfg.default_algo = value;
+            return TCR_OK;
+        case TCR_CFG_BLOCKS_PER_SM:
+            if (value < 1 || value > 32) break;
+            g_cfg.blocks_per_sm = value;
+            return TCR_OK;
+        case TCR_CFG_UNROLL:
+            if (value != 4 && value != 8 && value != 16) break;
+            g_cfg.unroll = value;
+            return TCR_OK;
+        case TCR_CFG_TC05_STAGES:
+            if (value < 2 || value > 16) break;
+            g_cfg.tc05_stages = value;
+            return TCR_OK;
+        case TCR_CFG_TC05_STAGE_KB:
+            if (value < 4 || value > 64 || value % 4) break;
+            g_cfg.tc05_stage_kb = value;
+            return TCR_OK;
+        case TCR_CFG_CHAIN:
+            if (value < 1 || value > 1024) break;
+            g_cfg.flush_every = value;
+            return TCR_OK;
+    }
+    g_last_error = "invalid config key or value";
+    return TCR_ERR_INVALID_VALUE;
+}
+
+int tcr_get_config(tcr_config_key key) {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    switch (key) {
+        case TCR_CFG_DEFAULT_ALGO: return g_cfg.default_algo;
+        case TCR_CFG_BLOCKS_PER_SM: return g_cfg.blocks_per_sm;
+        case TCR_CFG_UNROLL: return g_cfg.unroll;
+        case TCR_CFG_TC05_STAGES: return g_cfg.tc05_stages;
+        case TCR_CFG_TC05_STAGE_KB: return g_cfg.tc05_stage_kb;
+        case TCR_CFG_CHAIN: return g_cfg.flush_every;
+    }
+    return -1;
+}
+
+const char* tcr_status_string(tcr_status s) {
+    switch (s) {
+        case TCR_OK: return "TCR_OK";
+        case TCR_ERR_INVALID_VALUE: return "TCR_ERR_INVALID_VALUE";
+        case TCR_ERR_UNSUPPORTED_DEVICE: return "TCR_ERR_UNSUPPORTED_DEVICE";
+        case TCR_ERR_OUT_OF_MEMORY: return "TCR_ERR_OUT_OF_MEMORY";
+        case TCR_ERR_CUDA: return "TCR_ERR_CUDA";
+    }
+    return "TCR_ERR_UNKNOWN";
+}
+
+const char* tcr_last_error(void) { return g_last_error.c_str(); }
+
+tcr_status tcr_release_workspaces(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& kv : g_ws) {
+        Workspace* ws = kv.second;
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(kv.first.first);
+        cudaFree(ws->block);
+        if (ws->chunk_partials) cudaFree(ws->chunk_partials);
+        for (void* b : ws->staging)
+            if (b) cudaFree(b);
+        if (ws->dev_out) cudaFree(ws->dev_out);
+        cudaSetDevice(prev);
+        delete ws;
+    }
+    g_ws.clear();
+    return TCR_OK;
+}
+
+uint64_t tcr_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int tcr_version(void) { return TCR_VERSION; }
+
+}  // extern "C"

@@ -1,0 +1,52 @@
+// tcr_internal.h -- host-side declarations shared by the API and the kernel
+// translation units of libtcr (not part of the public ABI).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tcr {
+
+// Library-owned per-(device, stream) workspace, passed by value to kernels.
+struct DevWorkspace {
+    double* partials;               // [capacity] fp64 partial of every CTA (level >= 3)
+    unsigned* ticket;               // last-CTA completion ticket (self-resetting)
+    unsigned long long* seg_next;   // segmented: next segment index (self-resetting)
+    unsigned* seg_exit;             // segmented: warps that finished (self-resetting)
+    int capacity;                   // entries in partials
+};
+
+struct LaunchCfg {
+    int sms;            // SM count of the device
+    int blocks_per_sm;  // CTAs per SM for the streaming kernels
+    int unroll;         // 16-byte loads in flight per lane (4, 8 or 16)
+    int flush_every;    // iterations of `unroll` tiles per carried chain
+    int tc05_stages;    // tcgen05 kernel: SMEM ring stages
+    int tc05_stage_kb;  // tcgen05 kernel: KiB per stage (multiple of 4)
+};
+
+// Each launcher enqueues exactly one kernel on `stream` and returns the
+// cudaGetLastError() of the launch.
+cudaError_t launch_reduce_stream(bool mma, const uint16_t* x, size_t n, float* out_f32,
+                                 double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                 cudaStream_t stream);
+cudaError_t launch_reduce_tcgen05(const uint16_t* x, size_t n, float* out_f32, double* out_f64,
+                                  const DevWorkspace& ws, const LaunchCfg& cfg,
+                                  cudaStream_t stream);
+cudaError_t launch_reduce_segmented(bool mma, bool batched, const uint16_t* x,
+                                    const int64_t* offsets, size_t num_segments,
+                                    size_t segment_len, float* out, const DevWorkspace& ws,
+                                    const LaunchCfg& cfg, cudaStream_t stream);
+cudaError_t launch_sum_partials(const double* partials, size_t count, float* out_f32,
+                                double* out_f64, cudaStream_t stream);
+cudaError_t launch_round_f64(const double* in, float* out, cudaStream_t stream);
+cudaError_t launch_probe_mma(int algo, const uint16_t* a, const float* c, float* d,
+                             cudaStream_t stream);
+
+// Grid size of the streaming kernels for n elements (shared by the API's
+// workspace sizing and the launchers).
+int stream_grid(size_t n, const LaunchCfg& cfg);
+int tcgen05_grid(size_t n, const LaunchCfg& cfg);
+
+}  // namespace tcr

@@ -1,0 +1,231 @@
+// tcr_reduce.cu -- the streaming MMA-encoded reduction (mma.sync m16n8k16,
+// 128-bit loads) and its classic warp-shuffle twin, with last-CTA grid
+// completion.  One launch computes the whole hierarchy R_tc of the paper
+// (Eq. 13-14):
+//
+//   level 1  tile:  D = A x 1 + C, 256 inputs -> 16 row sums   (Eq. 9-10)
+//                   C carried over a bounded chain of K tiles,
+//                   then flushed into a per-lane fp64 accumulator
+//   level 2  warp:  D' = 1 x D via three fp64 DMMAs            (Eq. 11-12)
+//   level 3  CTA:   the same 1 x D collapse over the warp totals
+//   level 4  grid:  last CTA (completion ticket) collapses the CTA partials
+//                   in index order -- replaces the paper's relaunch per level
+//                   ("synchronization among blocks is not possible ... unless
+//                   the kernel is terminated").
+#include "tcr_device.cuh"
+#include "tcr_internal.h"
+
+namespace tcr {
+
+// Levels 2-4.  Every thread of the CTA calls this with its lane value; the
+// total lands in out_f32 / out_f64 (device pointers, either may be null).
+template <bool kMma, int WARPS>
+__device__ __forceinline__ void complete_block_and_grid(double lane_val, float* out_f32,
+                                                        double* out_f64, const DevWorkspace& ws) {
+    __shared__ double s_warp[WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double wt = warp_collapse<kMma>(lane_val);
+    if (lane == 0) s_warp[warp] = wt;
+    __syncthreads();
+    if (warp != 0) return;
+    const double bt = warp_collapse<kMma>(lane < WARPS ? s_warp[lane] : 0.0);
+    if (gridDim.x == 1) {
+        if (lane == 0) {
+            if (out_f32) *out_f32 = (float)bt;
+            if (out_f64) *out_f64 = bt;
+        }
+        return;
+    }
+    unsigned last = 0;
+    if (lane == 0) {
+        ws.partials[blockIdx.x] = bt;
+        __threadfence();  // release the partial before taking a ticket
+        last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();  // acquire: every other CTA's partial is visible
+    double v = 0.0;
+    for (int i = lane; i < (int)gridDim.x; i += 32) v += __ldcg(ws.partials + i);  // fixed order
+    const double tot = warp_collapse<kMma>(v);
+    if (lane == 0) {
+        if (out_f32) *out_f32 = (float)tot;
+        if (out_f64) *out_f64 = tot;
+        *ws.ticket = 0u;  // self-reset for the next launch on this stream
+    }
+}
+
+template <bool kMma>
+__device__ __forceinline__ void consume(const uint4& v, float (&c)[4], float& f) {
+    if constexpr (kMma) mma_rowsum(c, v);
+    else f += vec_sum_f32(v);
+}
+
+template <bool kMma>
+__device__ __forceinline__ void flush(float (&c)[4], float& f, double& acc, int lane) {
+    if constexpr (kMma) flush_rows(c, acc, lane);
+    else { acc += (double)f; f = 0.0f; }
+}
+
+// Grid-stride over 512-byte tiles: warp w handles tiles w, w+W, w+2W, ...,
+// U tiles (one 16-byte vector per lane each) in flight per iteration.
+// __launch_bounds__ minimum CTAs/SM: without it ptxas budgets registers for
+// full occupancy (32 regs at 256 threads) and sinks the U loads below their
+// consumers, which leaves ~2 loads in flight per warp.
+template <bool kMma, int U, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, (U <= 8 ? 4 : 2))
+reduce_stream_kernel(const uint16_t* __restrict__ x, size_t n, int flush_every, float* out_f32,
+                     double* out_f64, DevWorkspace ws) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // head: elements before the first 16-byte boundary (x is 2-byte aligned)
+    size_t head = ((16u - ((uintptr_t)x & 15u)) & 15u) >> 1;
+    if (head > n) head = n;
+    const uint16_t* xa = x + head;
+    const size_t nb = n - head;
+    const size_t T = nb / kTileElems;
+    const int tail = (int)(nb - T * kTileElems);
+    const size_t W = (size_t)gridDim.x * WARPS;
+    const size_t w = (size_t)blockIdx.x * WARPS + warp;
+    const uint4* base = reinterpret_cast<const uint4*>(xa) + lane;
+
+    double acc = 0.0;
+    float cA[4] = {0.f, 0.f, 0.f, 0.f}, cB[4] = {0.f, 0.f, 0.f, 0.f};
+    float fA = 0.f, fB = 0.f;
+    int it = 0;
+    size_t t = w;
+    for (; t + (size_t)(U - 1) * W < T; t += (size_t)U * W) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ldg_stream(base + (t + (size_t)u * W) * 32);
+        __syncwarp();  // scheduling fence: all U loads issue before the first consumer
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u & 1) consume<kMma>(v[u], cB, fB);
+            else consume<kMma>(v[u], cA, fA);
+        }
+        if (++it == flush_every) {
+            it = 0;
+            flush<kMma>(cA, fA, acc, lane);
+            flush<kMma>(cB, fB, acc, lane);
+        }
+    }
+    flush<kMma>(cA, fA, acc, lane);
+    flush<kMma>(cB, fB, acc, lane);
+    for (; t < T; t += W) {  // fewer than U tiles left for this warp
+        consume<kMma>(ldg_stream(base + t * 32), cA, fA);
+        flush<kMma>(cA, fA, acc, lane);
+    }
+    if (w == W - 1) {  // ragged head and tail: zero-padded tiles (reading G5)
+        if (head) {
+            consume<kMma>(load_ragged(x, (int)head, lane), cA, fA);
+            flush<kMma>(cA, fA, acc, lane);
+        }
+        if (tail) {
+            consume<kMma>(load_ragged(xa + T * kTileElems, tail, lane), cA, fA);
+            flush<kMma>(cA, fA, acc, lane);
+        }
+    }
+    complete_block_and_grid<kMma, WARPS>(acc, out_f32, out_f64, ws);
+}
+
+constexpr int kStreamWarps = 8;  // 256 threads per CTA
+
+int stream_grid(size_t n, const LaunchCfg& cfg) {
+    const size_t tiles = n / kTileElems;
+    const size_t per_cta = (size_t)kStreamWarps * cfg.unroll;  // tiles one CTA covers per iteration
+    size_t g = (tiles + per_cta - 1) / per_cta;
+    const size_t gmax = (size_t)cfg.sms * cfg.blocks_per_sm;
+    if (g > gmax) g = gmax;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+template <bool kMma>
+static cudaError_t launch_stream_t(const uint16_t* x, size_t n, float* out_f32, double* out_f64,
+                                   const DevWorkspace& ws, const LaunchCfg& cfg,
+                                   cudaStream_t stream) {
+    const int g = stream_grid(n, cfg);
+    const int fe = cfg.flush_every < 1 ? 1 : cfg.flush_every;
+    switch (cfg.unroll) {
+        case 4:
+            reduce_stream_kernel<kMma, 4, kStreamWarps>
+                <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
+            break;
+        case 16:
+            reduce_stream_kernel<kMma, 16, kStreamWarps>
+                <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
+            break;
+        default:
+            reduce_stream_kernel<kMma, 8, kStreamWarps>
+                <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
+            break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_stream(bool mma, const uint16_t* x, size_t n, float* out_f32,
+                                 double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                 cudaStream_t stream) {
+    return mma ? launch_stream_t<true>(x, n, out_f32, out_f64, ws, cfg, stream)
+               : launch_stream_t<false>(x, n, out_f32, out_f64, ws, cfg, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Small kernels: combine of chunk partials (host entry), f64 -> f32 rounding
+// (sharded finaliser), and the MMA rounding probe.
+// ---------------------------------------------------------------------------
+
+// One warp: lane l sums partials l, l+32, ... in order, then 1 x D collapse.
+__global__ void sum_partials_kernel(const double* __restrict__ p, size_t count, float* out_f32,
+                                    double* out_f64) {
+    const int lane = threadIdx.x & 31;
+    double v = 0.0;
+    for (size_t i = lane; i < count; i += 32) v += p[i];
+    const double tot = warp_collapse_mma(v);
+    if (lane == 0) {
+        if (out_f32) *out_f32 = (float)tot;
+        if (out_f64) *out_f64 = tot;
+    }
+}
+
+cudaError_t launch_sum_partials(const double* partials, size_t count, float* out_f32,
+                                double* out_f64, cudaStream_t stream) {
+    sum_partials_kernel<<<1, 32, 0, stream>>>(partials, count, out_f32, out_f64);
+    return cudaGetLastError();
+}
+
+__global__ void round_f64_kernel(const double* in, float* out) {
+    if (threadIdx.x == 0) *out = (float)*in;
+}
+
+cudaError_t launch_round_f64(const double* in, float* out, cudaStream_t stream) {
+    round_f64_kernel<<<1, 32, 0, stream>>>(in, out);
+    return cudaGetLastError();
+}
+
+// One m16n8k16 with A = a (row-major 16x16), B = ones, C[r][*] = c[r];
+// writes column 0 of D (d[r] = D[r][0]).  Lane 4g+t: a0 = A[g][2t..2t+1],
+// a1 = A[g+8][2t..], a2 = A[g][2t+8..], a3 = A[g+8][2t+8..] (PTX ISA
+// fragment layout of m16n8k16 .f16 A); c0 = C[g][2t], c2 = C[g+8][2t].
+__global__ void probe_mma_sync_kernel(const uint16_t* a, const float* c, float* d) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    auto pack = [&](int r, int k) {
+        return (uint32_t)a[r * 16 + k] | ((uint32_t)a[r * 16 + k + 1] << 16);
+    };
+    const uint4 av = make_uint4(pack(g, 2 * t), pack(g + 8, 2 * t), pack(g, 2 * t + 8),
+                                pack(g + 8, 2 * t + 8));
+    float acc[4] = {c[g], c[g], c[g + 8], c[g + 8]};
+    mma_rowsum(acc, av);
+    if (t == 0) {
+        d[g] = acc[0];
+        d[g + 8] = acc[2];
+    }
+}
+
+cudaError_t launch_probe_mma_sync(const uint16_t* a, const float* c, float* d,
+                                  cudaStream_t stream) {
+    probe_mma_sync_kernel<<<1, 32, 0, stream>>>(a, c, d);
+    return cudaGetLastError();
+}
+
+}  // namespace tcr

@@ -1,0 +1,307 @@
+// tcr_tcgen05.cu -- the Blackwell-native MMA-encoded reduction:
+//
+//   HBM --(bulk async copy, TMA engine)--> SMEM ring --(tcgen05.mma, A from
+//   SMEM, B = all-ones in SMEM)--> fp32 accumulator in TMEM --(tcgen05.ld of
+//   one column, every kSlots chunks)--> fp64 registers -> 1 x D collapse.
+//
+// The input never passes through registers: the tensor core reads each
+// 4 KiB chunk of X straight from shared memory as a 128x16 A tile.  Any
+// bijection of the chunk onto the tile is a valid placement of the group
+// (permutation invariance, reading G1); the no-swizzle K-major descriptor
+// below (LBO = 128 B, SBO = 256 B) tiles the 4 KiB contiguously.
+//
+// Paper mapping (arXiv 1903.03640):
+//   D = A x 1 + C (Eq. 9-10): tcgen05.mma M=128, N=16, K=16,
+//     B = ones.  Every column of D holds the 128 row sums (Eq. 10);
+//     C is carried over the K = stage_bytes / 4 KiB tiles of one chunk
+//     (enable_input_d), then the chunk's accumulator slot is read out.
+//   D' = 1 x D (Eq. 11-12): fp64 DMMA collapse of the row sums
+//     (warp), of the warps (CTA) and of the CTAs (grid, last-CTA ticket).
+//
+// Warp roles (192 threads, 1 CTA per SM):
+//   warp 0   lane 0: producer -- bulk copies into the SMEM ring
+//   warp 1   lane 0: MMA issuer; the whole warp allocates TMEM
+//   warps 2-5      : epilogue -- drain TMEM slots into fp64, ragged edges
+#include <map>
+#include <mutex>
+
+#include "tcr_device.cuh"
+#include "tcr_internal.h"
+#include "tcr_sm100.cuh"
+
+namespace tcr {
+
+namespace {
+
+constexpr int kTcWarps = 6;
+constexpr int kSlots = 8;                            // accumulator slots per TMEM buffer
+constexpr uint32_t kSlotCols = 16;                   // N = 16 fp32 columns per slot
+constexpr uint32_t kBufCols = kSlots * kSlotCols;    // 128
+constexpr uint32_t kTmemCols = 2 * kBufCols;         // double-buffered: 256 columns
+constexpr uint32_t kTileBytes = 128 * 16 * 2;        // one 128x16 fp16 A tile = 4 KiB
+constexpr uint32_t kHeaderBytes = 1024;              // ones tile + barriers + TMEM address
+constexpr uint32_t kIdesc = sm100::idesc_f16_f32(128, 16);
+
+}  // namespace
+
+// Levels 2-4 (identical to the streaming kernel's, instantiated for 6 warps).
+template <int WARPS>
+__device__ __forceinline__ void tc_complete(double lane_val, float* out_f32, double* out_f64,
+                                            const DevWorkspace& ws) {
+    __shared__ double s_warp[WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double wt = warp_collapse_mma(lane_val);
+    if (lane == 0) s_warp[warp] = wt;
+    __syncthreads();
+    if (warp != 0) return;
+    const double bt = warp_collapse_mma(lane < WARPS ? s_warp[lane] : 0.0);
+    if (gridDim.x == 1) {
+        if (lane == 0) {
+            if (out_f32) *out_f32 = (float)bt;
+            if (out_f64) *out_f64 = bt;
+        }
+        return;
+    }
+    unsigned last = 0;
+    if (lane == 0) {
+        ws.partials[blockIdx.x] = bt;
+        __threadfence();
+        last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();
+    double v = 0.0;
+    for (int i = lane; i < (int)gridDim.x; i += 32) v += __ldcg(ws.partials + i);
+    const double tot = warp_collapse_mma(v);
+    if (lane == 0) {
+        if (out_f32) *out_f32 = (float)tot;
+        if (out_f64) *out_f64 = tot;
+        *ws.ticket = 0u;
+    }
+}
+
+__global__ void __launch_bounds__(kTcWarps * 32, 1)
+reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, int stages, uint32_t stage_bytes,
+                      float* out_f32, double* out_f64, DevWorkspace ws) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint16_t* ones = reinterpret_cast<uint16_t*>(smem);             // 512 B: 16x16 fp16 ones
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 512);       // [stages]
+    uint64_t* empty = full + stages;                                // [stages]
+    uint64_t* tfull = empty + stages;                               // [2]
+    uint64_t* tempty = tfull + 2;                                   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kHeaderBytes - 8);
+    uint8_t* ring = smem + kHeaderBytes;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    size_t head = ((16u - ((uintptr_t)x & 15u)) & 15u) >> 1;
+    if (head > n) head = n;
+    const uint16_t* xa = x + head;
+    const size_t nb = n - head;
+    const size_t chunk_elems = stage_bytes / 2;
+    const size_t C = nb / chunk_elems;
+    const size_t c_begin = (size_t)blockIdx.x * C / gridDim.x;
+    const size_t c_end = (size_t)(blockIdx.x + 1) * C / gridDim.x;
+    const int nchunks = (int)(c_end - c_begin);
+
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) ones[i] = 0x3C00;
+    sm100::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            sm100::mbar_init(&full[s], 1);
+            sm100::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            sm100::mbar_init(&tfull[b], 1);
+            sm100::mbar_init(&tempty[b], 4);
+        }
+        sm100::fence_mbar_init();
+    }
+    if (warp == 1) sm100::tmem_alloc(tmem_slot, kTmemCols);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    double acc = 0.0;
+    if (warp == 0) {
+        if (lane == 0 && nchunks > 0) {  // producer
+            const uint64_t pol = sm100::policy_evict_first();
+            for (int i = 0; i < nchunks; ++i) {
+                const int s = i % stages;
+                const uint32_t ph = (uint32_t)(i / stages) & 1u;
+                sm100::mbar_wait(&empty[s], ph ^ 1u);
+                sm100::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                sm100::bulk_g2s(ring + (size_t)s * stage_bytes, xa + (c_begin + i) * chunk_elems,
+                                stage_bytes, &full[s], pol);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0 && nchunks > 0) {  // MMA issuer
+            const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
+            const uint64_t adesc0 = sm100::smem_desc_kmajor(sm100::smem_addr(ring), 128, 256);
+            const int kmma = (int)(stage_bytes / kTileBytes);
+            for (int i = 0; i < nchunks; ++i) {
+                const int s = i % stages;
+                const uint32_t ph = (uint32_t)(i / stages) & 1u;
+                const int round = i / kSlots, slot = i % kSlots, buf = round & 1;
+                if (slot == 0) sm100::mbar_wait(&tempty[buf], ((uint32_t)(round >> 1) & 1u) ^ 1u);
+                sm100::mbar_wait(&full[s], ph);
+                sm100::tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)buf * kBufCols + (uint32_t)slot * kSlotCols;
+                for (int k = 0; k < kmma; ++k) {
+                    const uint64_t adesc =
+                        adesc0 + (uint64_t)(((size_t)s * stage_bytes + (size_t)k * kTileBytes) >> 4);
+                    sm100::mma_f16_ss(d, adesc, bdesc, kIdesc, k > 0 ? 1u : 0u);
+                }
+                sm100::mma_commit(&empty[s]);  // SMEM stage free once these MMAs complete
+                if (slot == kSlots - 1 || i == nchunks - 1) sm100::mma_commit(&tfull[buf]);
+            }
+        }
+        __syncwarp();
+    } else {  // epilogue warps 2..5: TMEM lane quarter (warp % 4)
+        const uint32_t quarter = (uint32_t)(warp & 3) * 32u;
+        const int rounds = (nchunks + kSlots - 1) / kSlots;
+        for (int r = 0; r < rounds; ++r) {
+            const int buf = r & 1;
+            const int valid = min(kSlots, nchunks - r * kSlots);
+            sm100::mbar_wait(&tfull[buf], (uint32_t)(r >> 1) & 1u);
+            sm100::tc_fence_after();
+            uint32_t v[kSlots];
+#pragma unroll
+            for (int s = 0; s < kSlots; ++s)
+                if (s < valid)
+                    v[s] = sm100::tmem_ld_32x32b_x1(tmem + (quarter << 16) +
+                                                    (uint32_t)buf * kBufCols +
+                                                    (uint32_t)s * kSlotCols);
+            sm100::tmem_wait_ld();
+#pragma unroll
+            for (int s = 0; s < kSlots; ++s)
+                if (s < valid) acc += (double)__uint_as_float(v[s]);
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&tempty[buf]);
+        }
+        if (blockIdx.x == gridDim.x - 1) {
+            // Ragged work (< one chunk past the last full chunk, and the
+            // unaligned head): 256-element mma.sync tiles, zero padded.
+            const int e = warp - 2;
+            const uint16_t* xr = xa + C * chunk_elems;
+            const size_t rem = nb - C * chunk_elems;
+            const size_t Tr = rem / kTileElems;
+            const int tail = (int)(rem - Tr * kTileElems);
+            float c[4] = {0.f, 0.f, 0.f, 0.f};
+            const uint4* base = reinterpret_cast<const uint4*>(xr) + lane;
+            for (size_t t = e; t < Tr; t += 4) {
+                mma_rowsum(c, ldg_stream(base + t * 32));
+                flush_rows(c, acc, lane);
+            }
+            if (e == 0 && head) {
+                mma_rowsum(c, load_ragged(x, (int)head, lane));
+                flush_rows(c, acc, lane);
+            }
+            if (e == 1 && tail) {
+                mma_rowsum(c, load_ragged(xr + Tr * kTileElems, tail, lane));
+                flush_rows(c, acc, lane);
+            }
+        }
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
+    tc_complete<kTcWarps>(acc, out_f32, out_f64, ws);
+}
+
+int tcgen05_grid(size_t n, const LaunchCfg& cfg) {
+    const size_t chunk_elems = (size_t)cfg.tc05_stage_kb * 512;
+    const size_t C = n / chunk_elems;
+    size_t g = C < (size_t)cfg.sms ? C : (size_t)cfg.sms;
+    return g < 1 ? 1 : (int)g;
+}
+
+cudaError_t launch_reduce_tcgen05(const uint16_t* x, size_t n, float* out_f32, double* out_f64,
+                                  const DevWorkspace& ws, const LaunchCfg& cfg,
+                                  cudaStream_t stream) {
+    const int stages = cfg.tc05_stages;
+    const uint32_t stage_bytes = (uint32_t)cfg.tc05_stage_kb * 1024u;
+    const size_t smem = kHeaderBytes + (size_t)stages * stage_bytes;
+    if (kHeaderBytes - 8 < 512 + (size_t)(2 * stages + 4) * 8) return cudaErrorInvalidValue;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    {
+        // largest dynamic shared memory size configured so far, per device
+        static std::mutex mu;
+        static std::map<int, size_t> configured;
+        std::lock_guard<std::mutex> lk(mu);
+        if (smem > configured[dev]) {
+            if ((e = cudaFuncSetAttribute(reduce_tcgen05_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+                return e;
+            configured[dev] = smem;
+        }
+    }
+    const int g = tcgen05_grid(n, cfg);
+    reduce_tcgen05_kernel<<<g, kTcWarps * 32, smem, stream>>>(x, n, stages, stage_bytes, out_f32,
+                                                              out_f64, ws);
+    return cudaGetLastError();
+}
+
+// One tcgen05.mma (M=128, N=16, K=16) with A = a (row-major 128x16 fp16),
+// B = ones, C[r][*] = c[r] written into TMEM with tcgen05.st; d[r] = D[r][0].
+// Element (r, k) of A is placed at byte (r/8)*256 + (k/8)*128 + (r%8)*16 +
+// (k%8)*2 -- the layout the reduction's descriptor (LBO=128, SBO=256) names.
+__global__ void __launch_bounds__(128) probe_tcgen05_kernel(const uint16_t* a, const float* c,
+                                                            float* d) {
+    __shared__ __align__(1024) uint16_t sa[128 * 16];
+    __shared__ __align__(1024) uint16_t sb[256];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 128 * 16; i += 128) {
+        const int r = i / 16, k = i % 16;
+        sa[((r / 8) * 256 + (k / 8) * 128 + (r % 8) * 16 + (k % 8) * 2) / 2] = a[i];
+    }
+    for (int i = tid; i < 256; i += 128) sb[i] = 0x3C00;
+    sm100::fence_proxy_async_smem();
+    if (tid == 0) {
+        sm100::mbar_init(&bar, 1);
+        sm100::fence_mbar_init();
+    }
+    if (warp == 0) sm100::tmem_alloc(&tbase, 32);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = tbase;
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+    uint32_t cv[16];
+    for (int j = 0; j < 16; ++j) cv[j] = __float_as_uint(c[tid]);
+    sm100::tmem_st_32x32b_x16(lane_addr, cv);
+    sm100::tmem_wait_st();
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    if (tid == 0) {
+        sm100::mma_f16_ss(tmem, sm100::smem_desc_kmajor(sm100::smem_addr(sa), 128, 256),
+                          sm100::smem_desc_kmajor(sm100::smem_addr(sb), 128, 256), kIdesc, 1u);
+        sm100::mma_commit(&bar);
+    }
+    sm100::mbar_wait(&bar, 0);
+    sm100::tc_fence_after();
+    const uint32_t r = sm100::tmem_ld_32x32b_x1(lane_addr);
+    sm100::tmem_wait_ld();
+    d[tid] = __uint_as_float(r);
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) sm100::tmem_dealloc(tmem, 32);
+}
+
+cudaError_t launch_probe_mma_tcgen05(const uint16_t* a, const float* c, float* d,
+                                     cudaStream_t stream) {
+    probe_tcgen05_kernel<<<1, 128, 0, stream>>>(a, c, d);
+    return cudaGetLastError();
+}
+
+}  // namespace tcr

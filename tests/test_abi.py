@@ -1,0 +1,103 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol that
+include/tcr.h declares, and its host-side validation answers without touching
+a device.  (No compute calls: there is no GPU in this container.)"""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "tcr.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = set(re.findall(r"\b(tcr_[a-z0-9_]+)\s*\(", src))
+    assert len(names) >= 15
+    return sorted(names)
+
+
+def test_header_symbols_exported():
+    import paper_1903_03640_b200 as tcr
+
+    lib = ctypes.CDLL(tcr.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(lib, name), f"{name} declared in tcr.h but not exported"
+
+
+def test_binding_names_match_abi():
+    import paper_1903_03640_b200 as tcr
+
+    for name in declared_symbols():
+        if name in ("tcr_status_string", "tcr_last_error"):
+            continue
+        assert hasattr(tcr, name), f"python binding lacks {name}"
+
+
+def test_version_and_status_strings():
+    import paper_1903_03640_b200 as tcr
+
+    assert tcr.tcr_version() == 100
+    assert tcr.tcr_status_string(0) == "TCR_OK"
+    assert tcr.tcr_status_string(2) == "TCR_ERR_UNSUPPORTED_DEVICE"
+    assert tcr.tcr_launch_count() >= 0
+
+
+def test_invalid_arguments_rejected_before_device():
+    import paper_1903_03640_b200 as tcr
+
+    with pytest.raises(tcr.TcrError) as e:
+        tcr.tcr_reduce_sum(0, 0, n=16, stream=0)  # x NULL with n > 0
+    assert e.value.status == tcr.TCR_ERR_INVALID_VALUE
+    with pytest.raises(tcr.TcrError) as e:
+        tcr.tcr_reduce_sum(0x1001, 0x2000, n=16, stream=0)  # x not 2-byte aligned
+    assert e.value.status == tcr.TCR_ERR_INVALID_VALUE
+    with pytest.raises(tcr.TcrError) as e:
+        tcr.tcr_reduce_sum_algo(0x1000, 0x2000, None, algo=99, n=16, stream=0)
+    assert e.value.status == tcr.TCR_ERR_INVALID_VALUE
+    with pytest.raises(tcr.TcrError) as e:
+        tcr.tcr_reduce_sum_segmented(0x1000, 0, 0x2000, num_segments=4, stream=0)
+    assert e.value.status == tcr.TCR_ERR_INVALID_VALUE
+
+
+def test_config_validation():
+    import paper_1903_03640_b200 as tcr
+
+    old = tcr.tcr_get_config(tcr.TCR_CFG_UNROLL)
+    with pytest.raises(tcr.TcrError):
+        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 5)
+    tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 16)
+    assert tcr.tcr_get_config(tcr.TCR_CFG_UNROLL) == 16
+    tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, old)
+    with pytest.raises(tcr.TcrError):
+        tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGE_KB, 6)
+    assert tcr.tcr_get_config(99) == -1
+
+
+def test_product_path_does_not_import_oracle():
+    # The product package must not reference the test oracle (independence rule).
+    pkg = os.path.join(ROOT, "paper_1903_03640_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in src.replace("oracle/", ""), f
+
+
+def test_sass_is_sm100a_with_tensor_core_instructions():
+    # cuobjdump runs on the host: the library carries sm_100a SASS with the
+    # legacy tensor path (HMMA/DMMA) and the tcgen05 path (UTCHMMA, LDTM, UBLKCP).
+    import shutil
+    import subprocess
+
+    import paper_1903_03640_b200 as tcr
+
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run(["cuobjdump", "-sass", tcr.LIB_PATH], capture_output=True,
+                          text=True, check=True).stdout
+    assert "sm_100a" in sass
+    for mnemonic in ("HMMA.16816.F32", "DMMA.8x8x4", "UTCHMMA", "LDTM", "UBLKCP"):
+        assert mnemonic in sass, mnemonic

@@ -1,0 +1,298 @@
+"""GPU parity: the CUDA path through the C ABI vs the exact CPU oracle.
+
+Bar (north star, BASELINE.json): |g - R(X)| <= 2^-20 * sum|x_i| for every
+finite input (oracle.within_tolerance, exact rational test); bitwise equality
+wherever the exact sum is reachable without rounding (integer-valued inputs
+whose partial sums stay below 2^24); bitwise segment indexing; bitwise
+run-to-run determinism.  Inputs come from tcr_inputs (seeded, shared by both
+sides); expected values only from oracle/.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import tcr_inputs as gen
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = ["mma_sync", "tcgen05", "shuffle"]
+DISTS = [gen.UNIFORM_PM1, gen.UNIFORM_01, gen.ONES, gen.ALTERNATING, gen.WIDE]
+
+
+@pytest.fixture(scope="module")
+def tcr():
+    import torch
+
+    torch.cuda.set_device(0)
+    import paper_1903_03640_b200 as m
+
+    return m
+
+
+def _dev(bits, offset=0):
+    """Upload binary16 bits so that x starts `offset` elements past a 256-B boundary."""
+    import torch
+
+    buf = torch.empty(bits.size + offset + 8, dtype=torch.int16, device="cuda")
+    x = buf[offset:offset + bits.size]
+    if bits.size:
+        x.copy_(torch.from_numpy(bits.view(np.int16)))
+    return x.view(torch.float16)
+
+
+def _reduce(tcr, x, algo, f64=False):
+    import torch
+
+    o32 = torch.full((1,), float("nan"), dtype=torch.float32, device="cuda")
+    o64 = torch.full((1,), float("nan"), dtype=torch.float64, device="cuda") if f64 else None
+    tcr.tcr_reduce_sum_algo(x, out_f32=o32, out_f64=o64, algo=algo)
+    torch.cuda.synchronize()
+    return (float(o32.item()), float(o64.item())) if f64 else float(o32.item())
+
+
+SIZES = [0, 1, 2, 7, 8, 9, 255, 256, 257, 4095, 8191, 8192, 8193, 65536, 65536 + 37,
+         (1 << 20) + 5, 3 * (1 << 20) + 4099]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("n", SIZES)
+def test_sizes_uniform_pm1(tcr, algo, n):
+    bits = gen.generate(gen.SEED_C1, 0, n, gen.UNIFORM_PM1)
+    es = oracle.exact_sum_fp16(bits)
+    for off in (0, 3):
+        g = _reduce(tcr, _dev(bits, off), algo)
+        assert oracle.within_tolerance(g, es), (algo, n, off, g, es.f64())
+    if n == 0:
+        assert g == 0.0 and not np.signbit(g)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("dist", DISTS)
+def test_distributions(tcr, algo, dist):
+    n = (1 << 22) + 123
+    bits = gen.generate(1903 + dist, 0, n, dist)
+    es = oracle.exact_sum_fp16(bits, threads=4)
+    for off in (0, 1, 7):
+        g, g64 = _reduce(tcr, _dev(bits, off), algo, f64=True)
+        assert oracle.within_tolerance(g, es), (algo, dist, off, g, es.f64(), float(oracle.error_units(g, es)))
+        assert oracle.within_tolerance(g64, es)
+        assert np.float32(g64) == np.float32(g)  # out_f32 is RNE(out_f64)
+    if dist == gen.ONES:
+        assert g == float(n)
+    if dist == gen.ALTERNATING and n % 2 == 0:
+        assert g == 0.0
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_integer_inputs_bitwise(tcr, algo):
+    # SMALLINT values in {-2..2}: every partial sum is an integer below 2^24 in
+    # magnitude, so each fp32 / fp64 step is exact and g must equal R(X) exactly.
+    for n in (17, 256 * 33 + 5, (1 << 21) + 11):
+        bits = gen.generate(77, 0, n, gen.SMALLINT)
+        es = oracle.exact_sum_fp16(bits)
+        g = _reduce(tcr, _dev(bits, 5), algo)
+        assert g == float(es.value), (algo, n, g, es.value)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_deterministic(tcr, algo):
+    bits = gen.generate(5, 0, (1 << 24) + 3, gen.WIDE)
+    x = _dev(bits, 2)
+    a = [_reduce(tcr, x, algo) for _ in range(3)]
+    assert a[0] == a[1] == a[2]
+
+
+def test_wide_range_overflow_and_specials(tcr):
+    import torch
+
+    # sum beyond binary32 range is impossible for n < 2^90 fp16 inputs; test inf/nan propagation
+    for algo in ALGOS:
+        bits = gen.generate(9, 0, 100_000, gen.UNIFORM_PM1)
+        bits[12345] = 0x7C00  # +inf
+        es = oracle.exact_sum_fp16(bits)
+        g = _reduce(tcr, _dev(bits), algo)
+        assert oracle.within_tolerance(g, es), (algo, g)
+        bits[99] = 0xFC00  # -inf -> NaN
+        g = _reduce(tcr, _dev(bits), algo)
+        assert g != g, algo
+    del torch
+
+
+def test_full_size_c3_bench_config(tcr):
+    """n = 2^30 (BASELINE config 3) in the launch configuration bench.py times."""
+    import torch
+
+    n = 1 << 30
+    x = gen.generate_tensor(gen.SEED_C3, 0, n, gen.UNIFORM_PM1)
+    # the shared generator on the device matches the host definition (sampled)
+    idx = np.random.default_rng(0).integers(0, n, 4096)
+    xs = x.view(torch.int16)[torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint16)
+    host = np.array([gen.generate(gen.SEED_C3, int(i), 1, gen.UNIFORM_PM1)[0] for i in idx])
+    assert np.array_equal(xs, host)
+    bits = x.view(torch.int16).cpu().numpy().view(np.uint16)
+    es = oracle.exact_sum_fp16(bits, threads=os.cpu_count() or 8)
+    for algo in ["default"] + ALGOS:
+        g = _reduce(tcr, x, algo)
+        assert oracle.within_tolerance(g, es), (algo, g, es.f64())
+
+
+def test_f64_entry_and_round(tcr):
+    import torch
+
+    bits = gen.generate(21, 0, 1_000_003, gen.UNIFORM_PM1)
+    es = oracle.exact_sum_fp16(bits)
+    x = _dev(bits)
+    o64 = torch.empty(1, dtype=torch.float64, device="cuda")
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    tcr.tcr_reduce_sum_f64(x, o64)
+    tcr.tcr_round_f64_to_f32(o64, o32)
+    torch.cuda.synchronize()
+    assert oracle.within_tolerance(float(o64.item()), es)
+    assert float(o32.item()) == float(np.float32(o64.item()))
+
+
+def test_host_entry_end_to_end(tcr):
+    import torch
+
+    n = (1 << 27) + 5  # three 2^26-element chunks
+    bits = gen.generate(gen.SEED_C2, 0, n, gen.UNIFORM_PM1)
+    es = oracle.exact_sum_fp16(bits, threads=8)
+    pinned = torch.from_numpy(bits.view(np.int16)).pin_memory()
+    g = tcr.tcr_reduce_sum_host(pinned, n=n)
+    assert oracle.within_tolerance(g, es), (g, es.f64())
+    g2 = tcr.tcr_reduce_sum_host(bits[:1000])  # pageable numpy
+    assert oracle.within_tolerance(g2, oracle.exact_sum_fp16(bits[:1000]))
+
+
+def test_config_knobs(tcr):
+    bits = gen.generate(31, 0, (1 << 23) + 77, gen.UNIFORM_01)
+    es = oracle.exact_sum_fp16(bits, threads=4)
+    x = _dev(bits, 1)
+    try:
+        for unroll in (4, 8, 16):
+            for bps in (1, 2, 4, 8):
+                for chain in (1, 4):
+                    tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, unroll)
+                    tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, bps)
+                    tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, chain)
+                    for algo in ("mma_sync", "shuffle"):
+                        g = _reduce(tcr, x, algo)
+                        assert oracle.within_tolerance(g, es), (unroll, bps, chain, algo)
+        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 8)
+        tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 4)
+        tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 1)
+        for stages, kb in ((2, 4), (4, 8), (8, 16), (6, 32), (3, 64)):
+            tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGES, stages)
+            tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGE_KB, kb)
+            g = _reduce(tcr, x, "tcgen05")
+            assert oracle.within_tolerance(g, es), (stages, kb, g, es.f64())
+    finally:
+        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 8)
+        tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 4)
+        tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 1)
+        tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGES, 8)
+        tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGE_KB, 16)
+
+
+def test_two_streams_concurrently(tcr):
+    import torch
+
+    b1 = gen.generate(1, 0, 1 << 24, gen.UNIFORM_PM1)
+    b2 = gen.generate(2, 0, (1 << 24) + 9, gen.WIDE)
+    x1, x2 = _dev(b1), _dev(b2)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    o1 = torch.empty(8, dtype=torch.float32, device="cuda")
+    o2 = torch.empty(8, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    for k in range(8):
+        tcr.tcr_reduce_sum(x1, o1[k:k + 1], stream=s1)
+        tcr.tcr_reduce_sum(x2, o2[k:k + 1], stream=s2)
+    torch.cuda.synchronize()
+    e1, e2 = oracle.exact_sum_fp16(b1), oracle.exact_sum_fp16(b2)
+    r1, r2 = o1.cpu().tolist(), o2.cpu().tolist()
+    assert len(set(r1)) == 1 and len(set(r2)) == 1
+    assert oracle.within_tolerance(r1[0], e1) and oracle.within_tolerance(r2[0], e2)
+
+
+def test_cuda_graph_capture(tcr):
+    import torch
+
+    bits = gen.generate(3, 0, 1 << 22, gen.UNIFORM_PM1)
+    x = _dev(bits)
+    out = torch.empty(1, dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        tcr.tcr_reduce_sum(x, out)  # first call on this stream: allocates the workspace
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        tcr.tcr_reduce_sum(x, out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert oracle.within_tolerance(float(out.item()), oracle.exact_sum_fp16(bits))
+
+
+def test_invalid_device_pointer_status(tcr):
+    with pytest.raises(tcr.TcrError):
+        tcr.tcr_reduce_sum(0, 0, n=5)
+
+
+# ------------------------------------------------------------------ probes
+
+def test_probe_mma_sync_layout_and_rounding(tcr):
+    import torch
+
+    rng = np.random.default_rng(4)
+    a = rng.integers(-8, 9, (16, 16)).astype(np.float16)
+    c = rng.integers(-100, 100, 16).astype(np.float32)
+    d = torch.empty(16, dtype=torch.float32, device="cuda")
+    ta = torch.from_numpy(a.view(np.int16)).cuda()
+    tcr.tcr_probe_mma(ta, torch.from_numpy(c).cuda(), d, algo="mma_sync")
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), c + a.astype(np.float32).sum(axis=1))
+    _rounding_probe(tcr, "mma_sync", 16)
+
+
+def test_probe_tcgen05_layout_and_rounding(tcr):
+    import torch
+
+    rng = np.random.default_rng(5)
+    a = rng.integers(-8, 9, (128, 16)).astype(np.float16)
+    c = rng.integers(-100, 100, 128).astype(np.float32)
+    d = torch.empty(128, dtype=torch.float32, device="cuda")
+    tcr.tcr_probe_mma(torch.from_numpy(a.view(np.int16)).cuda(), torch.from_numpy(c).cuda(), d,
+                      algo="tcgen05")
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), c + a.astype(np.float32).sum(axis=1))
+    _rounding_probe(tcr, "tcgen05", 128)
+
+
+def _rounding_probe(tcr, algo, rows):
+    """C = 2.0, A row = [3*2^-24, 0, ...]: RN gives 2 + 2^-22, truncation gives 2.0
+    (reading G10).  Recorded, not asserted; written to gpurun_out/ for DESIGN.md."""
+    import json
+
+    import torch
+
+    a = np.zeros((rows, 16), dtype=np.float16)
+    a[:, 0] = np.float16(3 * 2.0 ** -24)
+    a[1, :] = np.float16(3 * 2.0 ** -24)          # 16 small terms: 48 * 2^-24
+    a[2, 0], a[2, 1] = np.float16(1.0), np.float16(2.0 ** -24)   # alignment inside the dot product
+    c = np.full(rows, 2.0, dtype=np.float32)
+    c[3] = -2.0
+    d = torch.empty(rows, dtype=torch.float32, device="cuda")
+    tcr.tcr_probe_mma(torch.from_numpy(a.view(np.int16)).cuda(), torch.from_numpy(c).cuda(), d,
+                      algo=algo)
+    torch.cuda.synchronize()
+    r = d.cpu().numpy()
+    rec = {"algo": algo, "row0_c2_plus_3u": float(r[0]), "RN_expect": 2 + 2.0 ** -22,
+           "RZ_expect": 2.0, "row1_c2_plus_48u": float(r[1]), "row2_c2_plus_1_plus_u": float(r[2]),
+           "row3_cm2_plus_3u": float(r[3]),
+           "mode_guess": "RN" if r[0] == 2 + 2.0 ** -22 else ("RZ" if r[0] == 2.0 else "other")}
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(f"gpurun_out/probe_{algo}.json", "w") as f:
+        json.dump(rec, f, indent=1)
+    print(rec)

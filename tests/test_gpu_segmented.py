@@ -1,0 +1,149 @@
+"""GPU parity of the segmented / batched entry points (BASELINE config 5),
+and of the device input generator against its host definition."""
+import numpy as np
+import pytest
+
+import oracle
+import tcr_inputs as gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tcr():
+    import torch
+
+    torch.cuda.set_device(0)
+    import paper_1903_03640_b200 as m
+
+    return m
+
+
+def _dev(bits, offset=0):
+    import torch
+
+    buf = torch.empty(bits.size + offset + 8, dtype=torch.int16, device="cuda")
+    x = buf[offset:offset + bits.size]
+    x.copy_(torch.from_numpy(bits.view(np.int16)))
+    return x.view(torch.float16)
+
+
+def _seg(tcr, x, off, mma=True):
+    import torch
+
+    out = torch.full((len(off) - 1,), float("nan"), dtype=torch.float32, device="cuda")
+    f = tcr.tcr_reduce_sum_segmented if mma else tcr.tcr_reduce_sum_segmented_shuffle
+    f(x, torch.from_numpy(np.asarray(off, dtype=np.int64)).cuda(), out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("mma", [True, False])
+def test_generator_device_matches_host(tcr, mma):
+    import torch
+
+    for dist in range(6):
+        for start, n in ((0, 1), (5, 1000), (1 << 33, 100_003)):
+            d = gen.generate_tensor(17 + dist, start, n, dist).view(torch.int16).cpu().numpy()
+            assert np.array_equal(d.view(np.uint16), gen.generate(17 + dist, start, n, dist)), dist
+
+
+@pytest.mark.parametrize("mma", [True, False])
+def test_edge_segments(tcr, mma):
+    n = 300_000
+    bits = gen.generate(12, 0, n, gen.UNIFORM_PM1)
+    lens = [0, 1, 2, 7, 8, 9, 15, 16, 17, 255, 256, 257, 0, 4095, 4096, 4097, 65536, 0, 1, 33333]
+    starts = [0, 3, 11, 100, 1001]
+    for s0 in starts:
+        off = gen.offsets_from_lengths(np.array(lens), start=s0)
+        assert off[-1] <= n
+        for xoff in (0, 3):
+            g = _seg(tcr, _dev(bits, xoff), off, mma)
+            ref = oracle.exact_segment_sums_fp16(bits, off)
+            for j, (gj, rj) in enumerate(zip(g.tolist(), ref)):
+                assert oracle.within_tolerance(gj, rj), (mma, s0, xoff, j, gj, rj.f64())
+                if lens[j] == 0:
+                    assert gj == 0.0
+
+
+@pytest.mark.parametrize("mma", [True, False])
+def test_segment_index_bit_exact(tcr, mma):
+    # All-ones data and pairwise-distinct lengths: out[j] must equal len(j)
+    # exactly, so any permutation or off-by-one of the output index fails.
+    rng = np.random.default_rng(0)
+    lens = rng.permutation(np.arange(0, 6000, 3))
+    off = gen.offsets_from_lengths(lens, start=5)
+    bits = np.full(int(off[-1]) + 8, 0x3C00, dtype=np.uint16)
+    g = _seg(tcr, _dev(bits, 1), off, mma)
+    assert np.array_equal(g, lens.astype(np.float32))
+
+
+@pytest.mark.parametrize("mma", [True, False])
+def test_loguniform_mix(tcr, mma):
+    S = 4096
+    lens = gen.loguniform_lengths(gen.SEED_C5, S)
+    off = gen.offsets_from_lengths(lens)
+    n = int(off[-1])
+    for dist in (gen.UNIFORM_PM1, gen.UNIFORM_01, gen.WIDE):
+        bits = gen.generate(gen.SEED_C5, 0, n, dist)
+        g = _seg(tcr, _dev(bits), off, mma)
+        ref = oracle.exact_segment_sums_fp16(bits, off)
+        bad = [j for j in range(S) if not oracle.within_tolerance(float(g[j]), ref[j])]
+        assert not bad, (dist, bad[:5])
+        # deterministic across runs
+        assert np.array_equal(g, _seg(tcr, _dev(bits), off, mma))
+
+
+@pytest.mark.parametrize("mma", [True, False])
+def test_batched(tcr, mma):
+    import torch
+
+    for L, S in ((1, 1000), (7, 333), (256, 4096), (1000, 777), (4096, 1024), (65536, 17)):
+        bits = gen.generate(L, 0, L * S, gen.UNIFORM_PM1)
+        x = _dev(bits, 2)
+        out = torch.empty(S, dtype=torch.float32, device="cuda")
+        f = tcr.tcr_reduce_sum_batched if mma else tcr.tcr_reduce_sum_batched_shuffle
+        f(x, L, out)
+        torch.cuda.synchronize()
+        ref = oracle.exact_segment_sums_fp16(bits, np.arange(S + 1, dtype=np.int64) * L)
+        g = out.cpu().numpy()
+        assert all(oracle.within_tolerance(float(g[j]), ref[j]) for j in range(S)), (L, S)
+
+
+def test_empty_and_zero_segments(tcr):
+    import torch
+
+    out = torch.empty(0, dtype=torch.float32, device="cuda")
+    off = torch.zeros(1, dtype=torch.int64, device="cuda")
+    x = torch.empty(0, dtype=torch.float16, device="cuda")
+    tcr.tcr_reduce_sum_segmented(x, off, out, num_segments=0)
+    torch.cuda.synchronize()
+
+
+def test_full_size_c5_sampled(tcr):
+    """BASELINE config 5: 2^20 log-uniform segments (~1.2e10 elements), in the
+    launch configuration bench.py times; 256 sampled segments vs the oracle
+    (values regenerated on the host from (seed, index))."""
+    import torch
+
+    S = 1 << 20
+    lens = gen.loguniform_lengths(gen.SEED_C5, S)
+    off = gen.offsets_from_lengths(lens)
+    n = int(off[-1])
+    x = gen.generate_tensor(gen.SEED_C5, 0, n, gen.UNIFORM_PM1)
+    toff = torch.from_numpy(off).cuda()
+    out = torch.empty(S, dtype=torch.float32, device="cuda")
+    tcr.tcr_reduce_sum_segmented(x, toff, out)
+    torch.cuda.synchronize()
+    g = out.cpu().numpy()
+    rng = np.random.default_rng(1)
+    sample = np.concatenate([[0, S - 1], rng.integers(0, S, 254)])
+    for j in sample.tolist():
+        bits = gen.generate(gen.SEED_C5, int(off[j]), int(lens[j]), gen.UNIFORM_PM1)
+        es = oracle.exact_sum_fp16(bits)
+        assert oracle.within_tolerance(float(g[j]), es), (j, g[j], es.f64())
+    out2 = torch.empty(S, dtype=torch.float32, device="cuda")
+    tcr.tcr_reduce_sum_segmented(x, toff, out2)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)
+    del x
