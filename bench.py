@@ -168,6 +168,16 @@ def main():
     ap.add_argument("--n-per-rank", type=int, default=N_PER_RANK)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--unroll", type=int, help="TCR_CFG_UNROLL (mma_sync/shuffle)")
+    ap.add_argument("--bps", type=int, help="TCR_CFG_BLOCKS_PER_SM")
+    ap.add_argument("--chain", type=int, help="TCR_CFG_CHAIN (flush every N iterations)")
+    ap.add_argument("--stages", type=int, help="TCR_CFG_TC05_STAGES")
+    ap.add_argument("--stage-kb", type=int, help="TCR_CFG_TC05_STAGE_KB")
+    ap.add_argument("--slots", type=int, help="TCR_CFG_TC05_SLOTS")
+    ap.add_argument("--tc-chain", type=int, help="TCR_CFG_TC05_CHAIN")
+    ap.add_argument("--ctas", type=int, help="TCR_CFG_TC05_CTAS_PER_SM")
+    ap.add_argument("--prefetch", type=int, help="TCR_CFG_TC05_PREFETCH")
+    ap.add_argument("--split", type=int, help="TCR_CFG_TC05_SPLIT")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -179,6 +189,13 @@ def main():
     import paper_1903_03640_b200 as tcr
     import tcr_inputs as gen
 
+    for key, val in ((tcr.TCR_CFG_UNROLL, args.unroll), (tcr.TCR_CFG_BLOCKS_PER_SM, args.bps),
+                     (tcr.TCR_CFG_CHAIN, args.chain), (tcr.TCR_CFG_TC05_STAGES, args.stages),
+                     (tcr.TCR_CFG_TC05_STAGE_KB, args.stage_kb), (tcr.TCR_CFG_TC05_SLOTS, args.slots),
+                     (tcr.TCR_CFG_TC05_CHAIN, args.tc_chain), (tcr.TCR_CFG_TC05_CTAS_PER_SM, args.ctas),
+                     (tcr.TCR_CFG_TC05_PREFETCH, args.prefetch), (tcr.TCR_CFG_TC05_SPLIT, args.split)):
+        if val is not None:
+            tcr.tcr_set_config(key, val)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -315,6 +332,12 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f16",
             "data": "synthetic (splitmix64-seeded, generated on the device)",
             "config": {"workload": workload, "algo": algo_name, "n_per_rank": n,
+                       "knobs": {k: tcr.tcr_get_config(v) for k, v in (
+                           ("unroll", tcr.TCR_CFG_UNROLL), ("blocks_per_sm", tcr.TCR_CFG_BLOCKS_PER_SM),
+                           ("chain", tcr.TCR_CFG_CHAIN), ("tc05_stages", tcr.TCR_CFG_TC05_STAGES),
+                           ("tc05_stage_kb", tcr.TCR_CFG_TC05_STAGE_KB), ("tc05_slots", tcr.TCR_CFG_TC05_SLOTS),
+                           ("tc05_chain", tcr.TCR_CFG_TC05_CHAIN), ("tc05_ctas", tcr.TCR_CFG_TC05_CTAS_PER_SM),
+                           ("tc05_prefetch", tcr.TCR_CFG_TC05_PREFETCH), ("tc05_split", tcr.TCR_CFG_TC05_SPLIT))},
                        "n_total": n * world, "l2": "inputs larger than L2 (no flush needed)",
                        "parallelism": f"dp{world}" if world > 1 else "single"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

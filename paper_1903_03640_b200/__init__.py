@@ -48,6 +48,11 @@ TCR_CFG_UNROLL = 2
 TCR_CFG_TC05_STAGES = 3
 TCR_CFG_TC05_STAGE_KB = 4
 TCR_CFG_CHAIN = 5
+TCR_CFG_TC05_SLOTS = 6
+TCR_CFG_TC05_CHAIN = 7
+TCR_CFG_TC05_CTAS_PER_SM = 8
+TCR_CFG_TC05_PREFETCH = 9
+TCR_CFG_TC05_SPLIT = 10
 
 
 class TcrError(RuntimeError):

@@ -37,6 +37,11 @@ struct Config {
     int flush_every = 1;  // chain K = flush_every * unroll / 2 tiles
     int tc05_stages = 8;
     int tc05_stage_kb = 16;
+    int tc05_slots = 16;
+    int tc05_chain = 4;
+    int tc05_ctas = 1;
+    int tc05_prefetch = 0;
+    int tc05_split = 1;
 };
 Config g_cfg;
 std::mutex g_cfg_mu;
@@ -80,6 +85,11 @@ LaunchCfg make_cfg(const DeviceInfo& di) {
     c.flush_every = g_cfg.flush_every;
     c.tc05_stages = g_cfg.tc05_stages;
     c.tc05_stage_kb = g_cfg.tc05_stage_kb;
+    c.tc05_slots = g_cfg.tc05_slots;
+    c.tc05_chain = g_cfg.tc05_chain;
+    c.tc05_ctas = g_cfg.tc05_ctas;
+    c.tc05_prefetch = g_cfg.tc05_prefetch;
+    c.tc05_split = g_cfg.tc05_split;
     return c;
 }
 
@@ -352,6 +362,26 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             if (value < 1 || value > 1024) break;
             g_cfg.flush_every = value;
             return TCR_OK;
+        case TCR_CFG_TC05_SLOTS:
+            if (value < 1 || value > 16 || (value & (value - 1))) break;
+            g_cfg.tc05_slots = value;
+            return TCR_OK;
+        case TCR_CFG_TC05_CHAIN:
+            if (value < 1 || value > 256) break;
+            g_cfg.tc05_chain = value;
+            return TCR_OK;
+        case TCR_CFG_TC05_CTAS_PER_SM:
+            if (value < 1 || value > 2) break;
+            g_cfg.tc05_ctas = value;
+            return TCR_OK;
+        case TCR_CFG_TC05_PREFETCH:
+            if (value < 0 || value > 64) break;
+            g_cfg.tc05_prefetch = value;
+            return TCR_OK;
+        case TCR_CFG_TC05_SPLIT:
+            if (value != 1 && value != 2 && value != 4 && value != 8) break;
+            g_cfg.tc05_split = value;
+            return TCR_OK;
     }
     g_last_error = "invalid config key or value";
     return TCR_ERR_INVALID_VALUE;
@@ -366,6 +396,11 @@ int tcr_get_config(tcr_config_key key) {
         case TCR_CFG_TC05_STAGES: return g_cfg.tc05_stages;
         case TCR_CFG_TC05_STAGE_KB: return g_cfg.tc05_stage_kb;
         case TCR_CFG_CHAIN: return g_cfg.flush_every;
+        case TCR_CFG_TC05_SLOTS: return g_cfg.tc05_slots;
+        case TCR_CFG_TC05_CHAIN: return g_cfg.tc05_chain;
+        case TCR_CFG_TC05_CTAS_PER_SM: return g_cfg.tc05_ctas;
+        case TCR_CFG_TC05_PREFETCH: return g_cfg.tc05_prefetch;
+        case TCR_CFG_TC05_SPLIT: return g_cfg.tc05_split;
     }
     return -1;
 }

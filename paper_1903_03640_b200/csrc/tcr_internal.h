@@ -24,6 +24,11 @@ struct LaunchCfg {
     int flush_every;    // iterations of `unroll` tiles per carried chain
     int tc05_stages;    // tcgen05 kernel: SMEM ring stages
     int tc05_stage_kb;  // tcgen05 kernel: KiB per stage (multiple of 4)
+    int tc05_slots;     // tcgen05 kernel: independent accumulators per TMEM buffer
+    int tc05_chain;     // tcgen05 kernel: MMAs carried per accumulator before a flush
+    int tc05_ctas;      // tcgen05 kernel: CTAs per SM
+    int tc05_prefetch;  // tcgen05 kernel: L2 prefetch distance in chunks
+    int tc05_split;     // tcgen05 kernel: bulk copies per stage
 };
 
 // Each launcher enqueues exactly one kernel on `stream` and returns the

@@ -2,7 +2,7 @@
 //
 //   HBM --(bulk async copy, TMA engine)--> SMEM ring --(tcgen05.mma, A from
 //   SMEM, B = all-ones in SMEM)--> fp32 accumulator in TMEM --(tcgen05.ld of
-//   one column, every kSlots chunks)--> fp64 registers -> 1 x D collapse.
+//   one column per accumulator, once per round)--> fp64 registers -> 1 x D.
 //
 // The input never passes through registers: the tensor core reads each
 // 4 KiB chunk of X straight from shared memory as a 128x16 A tile.  Any
@@ -34,10 +34,7 @@ namespace tcr {
 namespace {
 
 constexpr int kTcWarps = 6;
-constexpr int kSlots = 8;                            // accumulator slots per TMEM buffer
-constexpr uint32_t kSlotCols = 16;                   // N = 16 fp32 columns per slot
-constexpr uint32_t kBufCols = kSlots * kSlotCols;    // 128
-constexpr uint32_t kTmemCols = 2 * kBufCols;         // double-buffered: 256 columns
+constexpr uint32_t kSlotCols = 16;                   // N = 16 fp32 columns per accumulator
 constexpr uint32_t kTileBytes = 128 * 16 * 2;        // one 128x16 fp16 A tile = 4 KiB
 constexpr uint32_t kHeaderBytes = 1024;              // ones tile + barriers + TMEM address
 constexpr uint32_t kIdesc = sm100::idesc_f16_f32(128, 16);
@@ -81,10 +78,29 @@ __device__ __forceinline__ void tc_complete(double lane_val, float* out_f32, dou
     }
 }
 
+struct Tc05Params {
+    int stages;            // SMEM ring stages
+    uint32_t stage_bytes;  // bytes per stage (multiple of 4 KiB)
+    int slots;             // independent accumulators per TMEM buffer (power of 2, <= 16)
+    int chain;             // MMAs carried per accumulator before its flush (K)
+    int prefetch;          // L2 prefetch distance in chunks (0 = off)
+    int split;             // bulk copies per stage
+};
+
+// Accumulator schedule: MMA number j of this CTA (j = 0, 1, ...) goes to
+// round r = j / (slots*chain), slot j % slots of TMEM buffer r & 1, and
+// accumulates unless it is the slot's first MMA of the round.  Consecutive
+// MMAs therefore target different accumulators (no read-after-write chain
+// between neighbours), each accumulator carries `chain` tiles (bounded
+// truncation, reading G10), and the epilogue drains one buffer per round
+// while the tensor core fills the other.
 __global__ void __launch_bounds__(kTcWarps * 32, 1)
-reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, int stages, uint32_t stage_bytes,
-                      float* out_f32, double* out_f64, DevWorkspace ws) {
+reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, float* out_f32,
+                      double* out_f64, DevWorkspace ws) {
     extern __shared__ __align__(1024) uint8_t smem[];
+    const int stages = prm.stages;
+    const uint32_t stage_bytes = prm.stage_bytes;
+    const uint32_t buf_cols = (uint32_t)prm.slots * kSlotCols;
     uint16_t* ones = reinterpret_cast<uint16_t*>(smem);             // 512 B: 16x16 fp16 ones
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + 512);       // [stages]
     uint64_t* empty = full + stages;                                // [stages]
@@ -104,6 +120,9 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, int stages, uint
     const size_t c_begin = (size_t)blockIdx.x * C / gridDim.x;
     const size_t c_end = (size_t)(blockIdx.x + 1) * C / gridDim.x;
     const int nchunks = (int)(c_end - c_begin);
+    const int kmma = (int)(stage_bytes / kTileBytes);
+    const int per_round = prm.slots * prm.chain;
+    const long long total_mma = (long long)nchunks * kmma;
 
     for (int i = threadIdx.x; i < 256; i += blockDim.x) ones[i] = 0x3C00;
     sm100::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
@@ -118,7 +137,8 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, int stages, uint
         }
         sm100::fence_mbar_init();
     }
-    if (warp == 1) sm100::tmem_alloc(tmem_slot, kTmemCols);
+    const uint32_t tmem_cols = 2u * buf_cols < 32u ? 32u : 2u * buf_cols;
+    if (warp == 1) sm100::tmem_alloc(tmem_slot, tmem_cols);
     sm100::tc_fence_before();
     __syncthreads();
     sm100::tc_fence_after();
@@ -128,13 +148,22 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, int stages, uint
     if (warp == 0) {
         if (lane == 0 && nchunks > 0) {  // producer
             const uint64_t pol = sm100::policy_evict_first();
+            const uint32_t piece = stage_bytes / (uint32_t)prm.split;
+            for (int i = 0; i < prm.prefetch && i < nchunks; ++i)
+                sm100::prefetch_l2(xa + (c_begin + i) * chunk_elems, stage_bytes);
             for (int i = 0; i < nchunks; ++i) {
                 const int s = i % stages;
                 const uint32_t ph = (uint32_t)(i / stages) & 1u;
+                if (prm.prefetch && i + prm.prefetch < nchunks)
+                    sm100::prefetch_l2(xa + (c_begin + i + prm.prefetch) * chunk_elems,
+                                       stage_bytes);
                 sm100::mbar_wait(&empty[s], ph ^ 1u);
                 sm100::mbar_arrive_expect_tx(&full[s], stage_bytes);
-                sm100::bulk_g2s(ring + (size_t)s * stage_bytes, xa + (c_begin + i) * chunk_elems,
-                                stage_bytes, &full[s], pol);
+                const uint8_t* src =
+                    reinterpret_cast<const uint8_t*>(xa + (c_begin + i) * chunk_elems);
+                for (int q = 0; q < prm.split; ++q)
+                    sm100::bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)q * piece,
+                                    src + (size_t)q * piece, piece, &full[s], pol);
             }
         }
         __syncwarp();
@@ -142,44 +171,52 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, int stages, uint
         if (lane == 0 && nchunks > 0) {  // MMA issuer
             const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
             const uint64_t adesc0 = sm100::smem_desc_kmajor(sm100::smem_addr(ring), 128, 256);
-            const int kmma = (int)(stage_bytes / kTileBytes);
+            long long j = 0;
             for (int i = 0; i < nchunks; ++i) {
                 const int s = i % stages;
                 const uint32_t ph = (uint32_t)(i / stages) & 1u;
-                const int round = i / kSlots, slot = i % kSlots, buf = round & 1;
-                if (slot == 0) sm100::mbar_wait(&tempty[buf], ((uint32_t)(round >> 1) & 1u) ^ 1u);
                 sm100::mbar_wait(&full[s], ph);
                 sm100::tc_fence_after();
-                const uint32_t d = tmem + (uint32_t)buf * kBufCols + (uint32_t)slot * kSlotCols;
-                for (int k = 0; k < kmma; ++k) {
+                for (int k = 0; k < kmma; ++k, ++j) {
+                    const long long r = j / per_round;
+                    const int pos = (int)(j - r * per_round);
+                    const int buf = (int)(r & 1);
+                    if (pos == 0) {  // buffer drained by the epilogue two rounds ago?
+                        sm100::mbar_wait(&tempty[buf], ((uint32_t)(r >> 1) & 1u) ^ 1u);
+                        sm100::tc_fence_after();
+                    }
+                    const uint32_t d = tmem + (uint32_t)buf * buf_cols +
+                                       (uint32_t)(pos & (prm.slots - 1)) * kSlotCols;
                     const uint64_t adesc =
                         adesc0 + (uint64_t)(((size_t)s * stage_bytes + (size_t)k * kTileBytes) >> 4);
-                    sm100::mma_f16_ss(d, adesc, bdesc, kIdesc, k > 0 ? 1u : 0u);
+                    sm100::mma_f16_ss(d, adesc, bdesc, kIdesc, pos >= prm.slots ? 1u : 0u);
+                    if (pos == per_round - 1 || j == total_mma - 1) sm100::mma_commit(&tfull[buf]);
                 }
                 sm100::mma_commit(&empty[s]);  // SMEM stage free once these MMAs complete
-                if (slot == kSlots - 1 || i == nchunks - 1) sm100::mma_commit(&tfull[buf]);
             }
         }
         __syncwarp();
     } else {  // epilogue warps 2..5: TMEM lane quarter (warp % 4)
         const uint32_t quarter = (uint32_t)(warp & 3) * 32u;
-        const int rounds = (nchunks + kSlots - 1) / kSlots;
-        for (int r = 0; r < rounds; ++r) {
-            const int buf = r & 1;
-            const int valid = min(kSlots, nchunks - r * kSlots);
+        const long long rounds = (total_mma + per_round - 1) / per_round;
+        for (long long r = 0; r < rounds; ++r) {
+            const int buf = (int)(r & 1);
+            const long long cnt = total_mma - r * per_round;
+            const int valid = cnt < prm.slots ? (int)cnt : prm.slots;
             sm100::mbar_wait(&tfull[buf], (uint32_t)(r >> 1) & 1u);
             sm100::tc_fence_after();
-            uint32_t v[kSlots];
+            const uint32_t base = tmem + (quarter << 16) + (uint32_t)buf * buf_cols;
+            for (int s0 = 0; s0 < valid; s0 += 4) {
+                uint32_t v[4];
 #pragma unroll
-            for (int s = 0; s < kSlots; ++s)
-                if (s < valid)
-                    v[s] = sm100::tmem_ld_32x32b_x1(tmem + (quarter << 16) +
-                                                    (uint32_t)buf * kBufCols +
-                                                    (uint32_t)s * kSlotCols);
-            sm100::tmem_wait_ld();
+                for (int q = 0; q < 4; ++q)
+                    if (s0 + q < valid)
+                        v[q] = sm100::tmem_ld_32x32b_x1(base + (uint32_t)(s0 + q) * kSlotCols);
+                sm100::tmem_wait_ld();
 #pragma unroll
-            for (int s = 0; s < kSlots; ++s)
-                if (s < valid) acc += (double)__uint_as_float(v[s]);
+                for (int q = 0; q < 4; ++q)
+                    if (s0 + q < valid) acc += (double)__uint_as_float(v[q]);
+            }
             sm100::tc_fence_before();
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(&tempty[buf]);
@@ -210,24 +247,35 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, int stages, uint
     }
     sm100::tc_fence_before();
     __syncthreads();
-    if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
+    if (warp == 1) sm100::tmem_dealloc(tmem, tmem_cols);
     tc_complete<kTcWarps>(acc, out_f32, out_f64, ws);
 }
 
 int tcgen05_grid(size_t n, const LaunchCfg& cfg) {
     const size_t chunk_elems = (size_t)cfg.tc05_stage_kb * 512;
     const size_t C = n / chunk_elems;
-    size_t g = C < (size_t)cfg.sms ? C : (size_t)cfg.sms;
+    const size_t gmax = (size_t)cfg.sms * (size_t)(cfg.tc05_ctas < 1 ? 1 : cfg.tc05_ctas);
+    size_t g = C < gmax ? C : gmax;
     return g < 1 ? 1 : (int)g;
 }
 
 cudaError_t launch_reduce_tcgen05(const uint16_t* x, size_t n, float* out_f32, double* out_f64,
                                   const DevWorkspace& ws, const LaunchCfg& cfg,
                                   cudaStream_t stream) {
-    const int stages = cfg.tc05_stages;
-    const uint32_t stage_bytes = (uint32_t)cfg.tc05_stage_kb * 1024u;
-    const size_t smem = kHeaderBytes + (size_t)stages * stage_bytes;
-    if (kHeaderBytes - 8 < 512 + (size_t)(2 * stages + 4) * 8) return cudaErrorInvalidValue;
+    Tc05Params prm;
+    prm.stages = cfg.tc05_stages;
+    prm.stage_bytes = (uint32_t)cfg.tc05_stage_kb * 1024u;
+    prm.slots = cfg.tc05_slots;
+    prm.chain = cfg.tc05_chain;
+    prm.prefetch = cfg.tc05_prefetch;
+    prm.split = cfg.tc05_split;
+    if (prm.slots < 1 || prm.slots > 16 || (prm.slots & (prm.slots - 1)) || prm.chain < 1 ||
+        prm.stage_bytes % kTileBytes || prm.stage_bytes % (16u * (uint32_t)prm.split))
+        return cudaErrorInvalidValue;
+    if (cfg.tc05_ctas > 1 && 2 * prm.slots * (int)kSlotCols * cfg.tc05_ctas > 512)
+        return cudaErrorInvalidValue;  // TMEM columns of co-resident CTAs
+    const size_t smem = kHeaderBytes + (size_t)prm.stages * prm.stage_bytes;
+    if (kHeaderBytes - 8 < 512 + (size_t)(2 * prm.stages + 4) * 8) return cudaErrorInvalidValue;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -244,8 +292,7 @@ cudaError_t launch_reduce_tcgen05(const uint16_t* x, size_t n, float* out_f32, d
         }
     }
     const int g = tcgen05_grid(n, cfg);
-    reduce_tcgen05_kernel<<<g, kTcWarps * 32, smem, stream>>>(x, n, stages, stage_bytes, out_f32,
-                                                              out_f64, ws);
+    reduce_tcgen05_kernel<<<g, kTcWarps * 32, smem, stream>>>(x, n, prm, out_f32, out_f64, ws);
     return cudaGetLastError();
 }
 

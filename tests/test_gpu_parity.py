@@ -188,12 +188,27 @@ def test_config_knobs(tcr):
             tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGE_KB, kb)
             g = _reduce(tcr, x, "tcgen05")
             assert oracle.within_tolerance(g, es), (stages, kb, g, es.f64())
+        tc_knobs = [  # (stages, kb, slots, chain, ctas, prefetch, split)
+            (8, 16, 1, 4, 1, 0, 1), (8, 16, 2, 1, 1, 0, 2), (8, 16, 16, 4, 1, 8, 4),
+            (6, 16, 8, 4, 2, 0, 1), (3, 64, 16, 2, 1, 4, 8), (4, 32, 4, 3, 2, 2, 1)]
+        for st, kb, sl, ch, ct, pf, sp in tc_knobs:
+            for key, val in ((tcr.TCR_CFG_TC05_STAGES, st), (tcr.TCR_CFG_TC05_STAGE_KB, kb),
+                             (tcr.TCR_CFG_TC05_SLOTS, sl), (tcr.TCR_CFG_TC05_CHAIN, ch),
+                             (tcr.TCR_CFG_TC05_CTAS_PER_SM, ct), (tcr.TCR_CFG_TC05_PREFETCH, pf),
+                             (tcr.TCR_CFG_TC05_SPLIT, sp)):
+                tcr.tcr_set_config(key, val)
+            g = _reduce(tcr, x, "tcgen05")
+            assert oracle.within_tolerance(g, es), (st, kb, sl, ch, ct, pf, sp, g, es.f64())
+            assert g == _reduce(tcr, x, "tcgen05")
     finally:
         tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 8)
         tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 4)
         tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 1)
-        tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGES, 8)
-        tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGE_KB, 16)
+        for key, val in ((tcr.TCR_CFG_TC05_STAGES, 8), (tcr.TCR_CFG_TC05_STAGE_KB, 16),
+                         (tcr.TCR_CFG_TC05_SLOTS, 16), (tcr.TCR_CFG_TC05_CHAIN, 4),
+                         (tcr.TCR_CFG_TC05_CTAS_PER_SM, 1), (tcr.TCR_CFG_TC05_PREFETCH, 0),
+                         (tcr.TCR_CFG_TC05_SPLIT, 1)):
+            tcr.tcr_set_config(key, val)
 
 
 def test_two_streams_concurrently(tcr):
