@@ -170,7 +170,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unroll", type=int, help="TCR_CFG_UNROLL (mma_sync/shuffle)")
     ap.add_argument("--bps", type=int, help="TCR_CFG_BLOCKS_PER_SM")
-    ap.add_argument("--chain", type=int, help="TCR_CFG_CHAIN (flush every N iterations)")
+    ap.add_argument("--chain", type=int, help="TCR_CFG_CHAIN (carried chain K, tiles)")
     ap.add_argument("--stages", type=int, help="TCR_CFG_TC05_STAGES")
     ap.add_argument("--stage-kb", type=int, help="TCR_CFG_TC05_STAGE_KB")
     ap.add_argument("--slots", type=int, help="TCR_CFG_TC05_SLOTS")

@@ -182,12 +182,13 @@ typedef enum {
     TCR_CFG_UNROLL = 2,           /* 16-byte loads in flight per lane (mma.sync/shuffle) */
     TCR_CFG_TC05_STAGES = 3,      /* SMEM ring stages of the tcgen05 kernel */
     TCR_CFG_TC05_STAGE_KB = 4,    /* KiB per stage of the tcgen05 kernel    */
-    TCR_CFG_CHAIN = 5,            /* mma_sync/shuffle: flush every N iterations
-                                     (carried chain K = N * unroll / 2 tiles)  */
+    TCR_CFG_CHAIN = 5,            /* mma_sync/shuffle: carried chain K, tiles per
+                                     fp32 accumulator before its fp64 flush
+                                     (rounded to a multiple of unroll/2)       */
     TCR_CFG_TC05_SLOTS = 6,       /* tcgen05: independent TMEM accumulators per
                                      buffer (1, 2, 4, 8, 16)                    */
     TCR_CFG_TC05_CHAIN = 7,       /* tcgen05: MMAs carried per accumulator (K) */
-    TCR_CFG_TC05_CTAS_PER_SM = 8, /* tcgen05: CTAs per SM (1 or 2)             */
+    TCR_CFG_TC05_CTAS_PER_SM = 8, /* tcgen05: CTAs per SM (1..4)              */
     TCR_CFG_TC05_PREFETCH = 9,    /* tcgen05: L2 prefetch distance in chunks (0 = off) */
     TCR_CFG_TC05_SPLIT = 10       /* tcgen05: bulk copies per stage (1, 2, 4, 8) */
 } tcr_config_key;

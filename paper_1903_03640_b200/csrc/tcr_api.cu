@@ -31,15 +31,16 @@ thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
 
 struct Config {
+    // Defaults = the measured best on B200 at n = 2^30 (profiles/r01/tuning.md).
     int default_algo = TCR_ALGO_MMA_SYNC;
-    int blocks_per_sm = 4;
-    int unroll = 8;
-    int flush_every = 1;  // chain K = flush_every * unroll / 2 tiles
-    int tc05_stages = 8;
+    int blocks_per_sm = 8;
+    int unroll = 4;
+    int chain = 4;        // carried chain K (tiles per fp32 accumulator before a flush)
+    int tc05_stages = 4;
     int tc05_stage_kb = 16;
-    int tc05_slots = 16;
+    int tc05_slots = 4;
     int tc05_chain = 4;
-    int tc05_ctas = 1;
+    int tc05_ctas = 3;
     int tc05_prefetch = 0;
     int tc05_split = 1;
 };
@@ -82,7 +83,7 @@ LaunchCfg make_cfg(const DeviceInfo& di) {
     c.sms = di.sms;
     c.blocks_per_sm = g_cfg.blocks_per_sm;
     c.unroll = g_cfg.unroll;
-    c.flush_every = g_cfg.flush_every;
+    c.chain = g_cfg.chain;
     c.tc05_stages = g_cfg.tc05_stages;
     c.tc05_stage_kb = g_cfg.tc05_stage_kb;
     c.tc05_slots = g_cfg.tc05_slots;
@@ -360,7 +361,7 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             return TCR_OK;
         case TCR_CFG_CHAIN:
             if (value < 1 || value > 1024) break;
-            g_cfg.flush_every = value;
+            g_cfg.chain = value;
             return TCR_OK;
         case TCR_CFG_TC05_SLOTS:
             if (value < 1 || value > 16 || (value & (value - 1))) break;
@@ -371,7 +372,7 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             g_cfg.tc05_chain = value;
             return TCR_OK;
         case TCR_CFG_TC05_CTAS_PER_SM:
-            if (value < 1 || value > 2) break;
+            if (value < 1 || value > 4) break;
             g_cfg.tc05_ctas = value;
             return TCR_OK;
         case TCR_CFG_TC05_PREFETCH:
@@ -395,7 +396,7 @@ int tcr_get_config(tcr_config_key key) {
         case TCR_CFG_UNROLL: return g_cfg.unroll;
         case TCR_CFG_TC05_STAGES: return g_cfg.tc05_stages;
         case TCR_CFG_TC05_STAGE_KB: return g_cfg.tc05_stage_kb;
-        case TCR_CFG_CHAIN: return g_cfg.flush_every;
+        case TCR_CFG_CHAIN: return g_cfg.chain;
         case TCR_CFG_TC05_SLOTS: return g_cfg.tc05_slots;
         case TCR_CFG_TC05_CHAIN: return g_cfg.tc05_chain;
         case TCR_CFG_TC05_CTAS_PER_SM: return g_cfg.tc05_ctas;

@@ -21,7 +21,8 @@ struct LaunchCfg {
     int sms;            // SM count of the device
     int blocks_per_sm;  // CTAs per SM for the streaming kernels
     int unroll;         // 16-byte loads in flight per lane (4, 8 or 16)
-    int flush_every;    // iterations of `unroll` tiles per carried chain
+    int chain;          // carried chain K in tiles (mma_sync / shuffle); the kernel
+                        // flushes every max(1, 2K/unroll) iterations of `unroll` tiles
     int tc05_stages;    // tcgen05 kernel: SMEM ring stages
     int tc05_stage_kb;  // tcgen05 kernel: KiB per stage (multiple of 4)
     int tc05_slots;     // tcgen05 kernel: independent accumulators per TMEM buffer

@@ -145,7 +145,8 @@ static cudaError_t launch_stream_t(const uint16_t* x, size_t n, float* out_f32, 
                                    const DevWorkspace& ws, const LaunchCfg& cfg,
                                    cudaStream_t stream) {
     const int g = stream_grid(n, cfg);
-    const int fe = cfg.flush_every < 1 ? 1 : cfg.flush_every;
+    // two interleaved accumulators take unroll/2 tiles each per iteration
+    const int fe = 2 * cfg.chain / cfg.unroll < 1 ? 1 : 2 * cfg.chain / cfg.unroll;
     switch (cfg.unroll) {
         case 4:
             reduce_stream_kernel<kMma, 4, kStreamWarps>

@@ -110,13 +110,14 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
 
 constexpr int kSegWarps = 8;
 constexpr int kSegUnroll = 8;
+constexpr int kSegCtasPerSm = 4;  // resident CTAs per SM at <= 64 registers (launch bounds)
 
 cudaError_t launch_reduce_segmented(bool mma, bool batched, const uint16_t* x,
                                     const int64_t* offsets, size_t num_segments,
                                     size_t segment_len, float* out, const DevWorkspace& ws,
                                     const LaunchCfg& cfg, cudaStream_t stream) {
     size_t g = (num_segments + kSegWarps - 1) / kSegWarps;
-    const size_t gmax = (size_t)cfg.sms * cfg.blocks_per_sm;
+    const size_t gmax = (size_t)cfg.sms * kSegCtasPerSm;
     if (g > gmax) g = gmax;
     if (g < 1) g = 1;
     const dim3 grid((unsigned)g), block(kSegWarps * 32);

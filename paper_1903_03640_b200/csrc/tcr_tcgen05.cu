@@ -31,6 +31,26 @@
 
 namespace tcr {
 
+#ifdef TCR_TC05_TRACE
+// Diagnostic timeline of CTA 0 (scripts/tc05_trace.cu compiles this file with
+// -DTCR_TC05_TRACE): [0] producer issues chunk i, [1] MMA thread sees chunk i
+// full, [2] MMA thread committed chunk i, [3] epilogue sees round r full.
+__device__ unsigned long long g_tc05_trace[4][4096];
+__device__ __forceinline__ unsigned long long tc05_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TC05_TRACE(role, idx)                                                    \
+    do {                                                                         \
+        if (blockIdx.x == 0 && (idx) < 4096) g_tc05_trace[role][idx] = tc05_now(); \
+    } while (0)
+#else
+#define TC05_TRACE(role, idx) \
+    do {                      \
+    } while (0)
+#endif
+
 namespace {
 
 constexpr int kTcWarps = 6;
@@ -94,7 +114,7 @@ struct Tc05Params {
 // between neighbours), each accumulator carries `chain` tiles (bounded
 // truncation, reading G10), and the epilogue drains one buffer per round
 // while the tensor core fills the other.
-__global__ void __launch_bounds__(kTcWarps * 32, 1)
+__global__ void __launch_bounds__(kTcWarps * 32)
 reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, float* out_f32,
                       double* out_f64, DevWorkspace ws) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -149,21 +169,25 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
         if (lane == 0 && nchunks > 0) {  // producer
             const uint64_t pol = sm100::policy_evict_first();
             const uint32_t piece = stage_bytes / (uint32_t)prm.split;
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(xa + c_begin * chunk_elems);
             for (int i = 0; i < prm.prefetch && i < nchunks; ++i)
-                sm100::prefetch_l2(xa + (c_begin + i) * chunk_elems, stage_bytes);
-            for (int i = 0; i < nchunks; ++i) {
-                const int s = i % stages;
-                const uint32_t ph = (uint32_t)(i / stages) & 1u;
+                sm100::prefetch_l2(src + (size_t)i * stage_bytes, stage_bytes);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int i = 0; i < nchunks; ++i, src += stage_bytes) {
                 if (prm.prefetch && i + prm.prefetch < nchunks)
-                    sm100::prefetch_l2(xa + (c_begin + i + prm.prefetch) * chunk_elems,
-                                       stage_bytes);
+                    sm100::prefetch_l2(src + (size_t)prm.prefetch * stage_bytes, stage_bytes);
                 sm100::mbar_wait(&empty[s], ph ^ 1u);
+                TC05_TRACE(0, i);
                 sm100::mbar_arrive_expect_tx(&full[s], stage_bytes);
-                const uint8_t* src =
-                    reinterpret_cast<const uint8_t*>(xa + (c_begin + i) * chunk_elems);
+                uint8_t* dst = ring + (size_t)s * stage_bytes;
                 for (int q = 0; q < prm.split; ++q)
-                    sm100::bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)q * piece,
-                                    src + (size_t)q * piece, piece, &full[s], pol);
+                    sm100::bulk_g2s(dst + (size_t)q * piece, src + (size_t)q * piece, piece, &full[s],
+                                    pol);
+                if (++s == stages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
         }
         __syncwarp();
@@ -171,39 +195,55 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
         if (lane == 0 && nchunks > 0) {  // MMA issuer
             const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
             const uint64_t adesc0 = sm100::smem_desc_kmajor(sm100::smem_addr(ring), 128, 256);
-            long long j = 0;
+            const uint64_t stage_step = stage_bytes >> 4, tile_step = kTileBytes >> 4;
+            const uint32_t last_slot = (uint32_t)prm.slots - 1;
+            int s = 0;
+            uint32_t ph = 0;
+            int pos = 0;          // MMA index within the current round
+            int buf = 0;          // TMEM buffer of the current round
+            uint32_t use = 0;     // how many times `buf` was filled before (parity)
+            long long left = total_mma;
             for (int i = 0; i < nchunks; ++i) {
-                const int s = i % stages;
-                const uint32_t ph = (uint32_t)(i / stages) & 1u;
                 sm100::mbar_wait(&full[s], ph);
+                TC05_TRACE(1, i);
                 sm100::tc_fence_after();
-                for (int k = 0; k < kmma; ++k, ++j) {
-                    const long long r = j / per_round;
-                    const int pos = (int)(j - r * per_round);
-                    const int buf = (int)(r & 1);
+                uint64_t adesc = adesc0 + (uint64_t)s * stage_step;
+                for (int k = 0; k < kmma; ++k, adesc += tile_step) {
                     if (pos == 0) {  // buffer drained by the epilogue two rounds ago?
-                        sm100::mbar_wait(&tempty[buf], ((uint32_t)(r >> 1) & 1u) ^ 1u);
+                        sm100::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
                         sm100::tc_fence_after();
                     }
                     const uint32_t d = tmem + (uint32_t)buf * buf_cols +
-                                       (uint32_t)(pos & (prm.slots - 1)) * kSlotCols;
-                    const uint64_t adesc =
-                        adesc0 + (uint64_t)(((size_t)s * stage_bytes + (size_t)k * kTileBytes) >> 4);
+                                       ((uint32_t)pos & last_slot) * kSlotCols;
                     sm100::mma_f16_ss(d, adesc, bdesc, kIdesc, pos >= prm.slots ? 1u : 0u);
-                    if (pos == per_round - 1 || j == total_mma - 1) sm100::mma_commit(&tfull[buf]);
+                    --left;
+                    if (++pos == per_round || left == 0) {
+                        sm100::mma_commit(&tfull[buf]);
+                        pos = 0;
+                        if (buf) ++use;
+                        buf ^= 1;
+                    }
                 }
                 sm100::mma_commit(&empty[s]);  // SMEM stage free once these MMAs complete
+                TC05_TRACE(2, i);
+                if (++s == stages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
         }
         __syncwarp();
     } else {  // epilogue warps 2..5: TMEM lane quarter (warp % 4)
         const uint32_t quarter = (uint32_t)(warp & 3) * 32u;
         const long long rounds = (total_mma + per_round - 1) / per_round;
+        long long left = total_mma;
+        int buf = 0;
+        uint32_t use = 0;
         for (long long r = 0; r < rounds; ++r) {
-            const int buf = (int)(r & 1);
-            const long long cnt = total_mma - r * per_round;
-            const int valid = cnt < prm.slots ? (int)cnt : prm.slots;
-            sm100::mbar_wait(&tfull[buf], (uint32_t)(r >> 1) & 1u);
+            const int valid = left < prm.slots ? (int)left : prm.slots;
+            left -= per_round;
+            sm100::mbar_wait(&tfull[buf], use & 1u);
+            if (lane == 0 && warp == 2) TC05_TRACE(3, (int)r);
             sm100::tc_fence_after();
             const uint32_t base = tmem + (quarter << 16) + (uint32_t)buf * buf_cols;
             for (int s0 = 0; s0 < valid; s0 += 4) {
@@ -220,6 +260,8 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
             sm100::tc_fence_before();
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(&tempty[buf]);
+            if (buf) ++use;
+            buf ^= 1;
         }
         if (blockIdx.x == gridDim.x - 1) {
             // Ragged work (< one chunk past the last full chunk, and the
@@ -274,6 +316,8 @@ cudaError_t launch_reduce_tcgen05(const uint16_t* x, size_t n, float* out_f32, d
         return cudaErrorInvalidValue;
     if (cfg.tc05_ctas > 1 && 2 * prm.slots * (int)kSlotCols * cfg.tc05_ctas > 512)
         return cudaErrorInvalidValue;  // TMEM columns of co-resident CTAs
+    if ((kHeaderBytes + (size_t)prm.stages * prm.stage_bytes) * (size_t)cfg.tc05_ctas > 227u * 1024u)
+        return cudaErrorInvalidValue;  // shared memory of co-resident CTAs
     const size_t smem = kHeaderBytes + (size_t)prm.stages * prm.stage_bytes;
     if (kHeaderBytes - 8 < 512 + (size_t)(2 * prm.stages + 4) * 8) return cudaErrorInvalidValue;
     int dev = 0;

@@ -1,0 +1,80 @@
+// tc05_trace.cu -- diagnostic (not part of libtcr): timeline of CTA 0 of the
+// tcgen05 reduction kernel, compiled from the library's own source with
+// -DTCR_TC05_TRACE.  Usage: tc05_trace [stages] [stage_kb] [slots] [chain] [ctas]
+// Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a
+//        -DTCR_TC05_TRACE -o scripts/tc05_trace scripts/tc05_trace.cu
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1903_03640_b200/csrc/tcr_tcgen05.cu"
+
+int main(int argc, char** argv) {
+    tcr::LaunchCfg cfg{};
+    cudaDeviceGetAttribute(&cfg.sms, cudaDevAttrMultiProcessorCount, 0);
+    cfg.tc05_stages = argc > 1 ? atoi(argv[1]) : 8;
+    cfg.tc05_stage_kb = argc > 2 ? atoi(argv[2]) : 16;
+    cfg.tc05_slots = argc > 3 ? atoi(argv[3]) : 16;
+    cfg.tc05_chain = argc > 4 ? atoi(argv[4]) : 4;
+    cfg.tc05_ctas = argc > 5 ? atoi(argv[5]) : 1;
+    cfg.tc05_prefetch = 0;
+    cfg.tc05_split = 1;
+    const size_t n = (size_t)1 << 30;
+    uint16_t* x;
+    cudaMalloc(&x, n * 2);
+    cudaMemset(x, 0x3C, n * 2);
+    tcr::DevWorkspace ws{};
+    cudaMalloc(&ws.partials, 8 * 4096);
+    cudaMalloc(&ws.ticket, 64);
+    cudaMemset(ws.ticket, 0, 64);
+    ws.capacity = 4096;
+    float* out;
+    cudaMalloc(&out, 4);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float ms = 0;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(a);
+        cudaError_t e = tcr::launch_reduce_tcgen05(x, n, out, nullptr, ws, cfg, 0);
+        cudaEventRecord(b);
+        if (e || (e = cudaDeviceSynchronize())) {
+            printf("error %s\n", cudaGetErrorString(e));
+            return 1;
+        }
+        cudaEventElapsedTime(&ms, a, b);
+    }
+    printf("cfg stages=%d kb=%d slots=%d chain=%d ctas=%d: %.1f us, %.1f GB/s\n", cfg.tc05_stages,
+           cfg.tc05_stage_kb, cfg.tc05_slots, cfg.tc05_chain, cfg.tc05_ctas, ms * 1e3,
+           n * 2 / (ms * 1e-3) / 1e9);
+    static unsigned long long tr[4][4096];
+    cudaMemcpyFromSymbol(tr, tcr::g_tc05_trace, sizeof(tr));
+    const int nch = (int)((n * 2 / (cfg.tc05_stage_kb * 1024)) / (cfg.sms * cfg.tc05_ctas));
+    const int m = std::min(nch, 4096);
+    const unsigned long long t0 = tr[0][0];
+    auto pct = [](std::vector<double> v, double p) {
+        std::sort(v.begin(), v.end());
+        return v.empty() ? 0.0 : v[(size_t)(p * (v.size() - 1))];
+    };
+    std::vector<double> issue_gap, tma_lat, mma_time, full_gap;
+    for (int i = 1; i < m; ++i) {
+        issue_gap.push_back((double)(tr[0][i] - tr[0][i - 1]));
+        full_gap.push_back((double)(tr[1][i] - tr[1][i - 1]));
+    }
+    for (int i = 0; i < m; ++i) {
+        tma_lat.push_back((double)(tr[1][i] - tr[0][i]));
+        mma_time.push_back((double)(tr[2][i] - tr[1][i]));
+    }
+    printf("chunks/CTA %d; ns: producer issue gap p50 %.0f p90 %.0f | issue->full p50 %.0f p90 %.0f | "
+           "full->committed p50 %.0f p90 %.0f | full gap p50 %.0f p90 %.0f\n",
+           nch, pct(issue_gap, .5), pct(issue_gap, .9), pct(tma_lat, .5), pct(tma_lat, .9),
+           pct(mma_time, .5), pct(mma_time, .9), pct(full_gap, .5), pct(full_gap, .9));
+    printf("first 24 chunks (ns from first issue): i issue full committed\n");
+    for (int i = 0; i < std::min(m, 24); ++i)
+        printf("  %3d %8llu %8llu %8llu\n", i, tr[0][i] - t0, tr[1][i] - t0, tr[2][i] - t0);
+    printf("epilogue rounds (ns): ");
+    for (int r = 0; r < 12; ++r) printf("%llu ", tr[3][r] - t0);
+    printf("\nlast chunk committed at %llu ns\n", tr[2][m - 1] - t0);
+    return 0;
+}

@@ -173,16 +173,16 @@ def test_config_knobs(tcr):
     try:
         for unroll in (4, 8, 16):
             for bps in (1, 2, 4, 8):
-                for chain in (1, 4):
+                for chain in (2, 4, 16):
                     tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, unroll)
                     tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, bps)
                     tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, chain)
                     for algo in ("mma_sync", "shuffle"):
                         g = _reduce(tcr, x, algo)
                         assert oracle.within_tolerance(g, es), (unroll, bps, chain, algo)
-        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 8)
-        tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 4)
-        tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 1)
+        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
+        tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 8)
+        tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
         for stages, kb in ((2, 4), (4, 8), (8, 16), (6, 32), (3, 64)):
             tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGES, stages)
             tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGE_KB, kb)
@@ -201,12 +201,12 @@ def test_config_knobs(tcr):
             assert oracle.within_tolerance(g, es), (st, kb, sl, ch, ct, pf, sp, g, es.f64())
             assert g == _reduce(tcr, x, "tcgen05")
     finally:
-        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 8)
-        tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 4)
-        tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 1)
-        for key, val in ((tcr.TCR_CFG_TC05_STAGES, 8), (tcr.TCR_CFG_TC05_STAGE_KB, 16),
-                         (tcr.TCR_CFG_TC05_SLOTS, 16), (tcr.TCR_CFG_TC05_CHAIN, 4),
-                         (tcr.TCR_CFG_TC05_CTAS_PER_SM, 1), (tcr.TCR_CFG_TC05_PREFETCH, 0),
+        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
+        tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 8)
+        tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
+        for key, val in ((tcr.TCR_CFG_TC05_STAGES, 4), (tcr.TCR_CFG_TC05_STAGE_KB, 16),
+                         (tcr.TCR_CFG_TC05_SLOTS, 4), (tcr.TCR_CFG_TC05_CHAIN, 4),
+                         (tcr.TCR_CFG_TC05_CTAS_PER_SM, 3), (tcr.TCR_CFG_TC05_PREFETCH, 0),
                          (tcr.TCR_CFG_TC05_SPLIT, 1)):
             tcr.tcr_set_config(key, val)
 

@@ -1,0 +1,79 @@
+"""NEXT-1 precision study (the paper's open question: "it remains
+unknown what is the level of precision loss by performing reductions in
+FP16"): error of each GPU path against the exact oracle, as a function of
+the carried-chain length K and the input distribution.
+
+Errors are reported in units of 2^-24 * sum|x_i| (the north-star tolerance
+is 16 such units).  The table is written to gpurun_out/precision.json; the
+assertions are the tolerance at the library's default K, and the expected
+monotone growth of the worst error with K for all-positive data under the
+truncating accumulator measured by the probes (reading G10).
+"""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import tcr_inputs as gen
+
+pytestmark = pytest.mark.gpu
+
+
+def _err_units(g, es):
+    return float(abs(Fraction(g) - es.value) / (es.abs_value * Fraction(1, 1 << 24)))
+
+
+def test_precision_vs_chain_length():
+    import torch
+
+    import paper_1903_03640_b200 as tcr
+
+    n = 1 << 24
+    dists = {"uniform_pm1": gen.UNIFORM_PM1, "uniform01": gen.UNIFORM_01, "wide": gen.WIDE,
+             "alternating": gen.ALTERNATING}
+    rows = []
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    o64 = torch.empty(1, dtype=torch.float64, device="cuda")
+    try:
+        for dname, d in dists.items():
+            bits = gen.generate(gen.SEED_C2, 0, n, d)
+            es = oracle.exact_sum_fp16(bits, threads=8)
+            x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.float16)
+            # mma.sync / shuffle: carried chain K tiles per accumulator (unroll 4)
+            for algo in ("mma_sync", "shuffle"):
+                for K in (2, 4, 8, 32, 128, 1024):
+                    tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
+                    tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, K)
+                    tcr.tcr_reduce_sum_algo(x, out_f32=o32, out_f64=o64, algo=algo)
+                    torch.cuda.synchronize()
+                    rows.append({"dist": dname, "algo": algo, "K": K,
+                                 "err_f64_units": _err_units(float(o64.item()), es),
+                                 "err_f32_units": _err_units(float(o32.item()), es)})
+            tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
+            for K in (1, 4, 16, 64, 256):
+                tcr.tcr_set_config(tcr.TCR_CFG_TC05_CHAIN, K)
+                tcr.tcr_reduce_sum_algo(x, out_f32=o32, out_f64=o64, algo="tcgen05")
+                torch.cuda.synchronize()
+                rows.append({"dist": dname, "algo": "tcgen05", "K": K,
+                             "err_f64_units": _err_units(float(o64.item()), es),
+                             "err_f32_units": _err_units(float(o32.item()), es)})
+            tcr.tcr_set_config(tcr.TCR_CFG_TC05_CHAIN, 4)
+    finally:
+        tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
+        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
+        tcr.tcr_set_config(tcr.TCR_CFG_TC05_CHAIN, 4)
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/precision.json", "w") as f:
+        json.dump({"n": n, "unit": "2^-24 * sum|x|", "rows": rows}, f, indent=1)
+    for r in rows:
+        print(r)
+    # default chain length (K = 4) is within the north-star tolerance everywhere
+    for r in rows:
+        if r["K"] == 4:
+            assert r["err_f32_units"] <= 16, r
+    # truncating accumulator: the all-positive error grows with the chain
+    u01 = {r["K"]: r["err_f64_units"] for r in rows if r["dist"] == "uniform01" and r["algo"] == "tcgen05"}
+    assert u01[256] > u01[4]
