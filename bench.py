@@ -178,6 +178,7 @@ def main():
     ap.add_argument("--ctas", type=int, help="TCR_CFG_TC05_CTAS_PER_SM")
     ap.add_argument("--prefetch", type=int, help="TCR_CFG_TC05_PREFETCH")
     ap.add_argument("--split", type=int, help="TCR_CFG_TC05_SPLIT")
+    ap.add_argument("--interleave", type=int, help="TCR_CFG_TC05_INTERLEAVE")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -193,7 +194,8 @@ def main():
                      (tcr.TCR_CFG_CHAIN, args.chain), (tcr.TCR_CFG_TC05_STAGES, args.stages),
                      (tcr.TCR_CFG_TC05_STAGE_KB, args.stage_kb), (tcr.TCR_CFG_TC05_SLOTS, args.slots),
                      (tcr.TCR_CFG_TC05_CHAIN, args.tc_chain), (tcr.TCR_CFG_TC05_CTAS_PER_SM, args.ctas),
-                     (tcr.TCR_CFG_TC05_PREFETCH, args.prefetch), (tcr.TCR_CFG_TC05_SPLIT, args.split)):
+                     (tcr.TCR_CFG_TC05_PREFETCH, args.prefetch), (tcr.TCR_CFG_TC05_SPLIT, args.split),
+                     (tcr.TCR_CFG_TC05_INTERLEAVE, args.interleave)):
         if val is not None:
             tcr.tcr_set_config(key, val)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -337,7 +339,8 @@ def main():
                            ("chain", tcr.TCR_CFG_CHAIN), ("tc05_stages", tcr.TCR_CFG_TC05_STAGES),
                            ("tc05_stage_kb", tcr.TCR_CFG_TC05_STAGE_KB), ("tc05_slots", tcr.TCR_CFG_TC05_SLOTS),
                            ("tc05_chain", tcr.TCR_CFG_TC05_CHAIN), ("tc05_ctas", tcr.TCR_CFG_TC05_CTAS_PER_SM),
-                           ("tc05_prefetch", tcr.TCR_CFG_TC05_PREFETCH), ("tc05_split", tcr.TCR_CFG_TC05_SPLIT))},
+                           ("tc05_prefetch", tcr.TCR_CFG_TC05_PREFETCH), ("tc05_split", tcr.TCR_CFG_TC05_SPLIT),
+                           ("tc05_interleave", tcr.TCR_CFG_TC05_INTERLEAVE))},
                        "n_total": n * world, "l2": "inputs larger than L2 (no flush needed)",
                        "parallelism": f"dp{world}" if world > 1 else "single"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

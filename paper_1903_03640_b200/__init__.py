@@ -53,6 +53,7 @@ TCR_CFG_TC05_CHAIN = 7
 TCR_CFG_TC05_CTAS_PER_SM = 8
 TCR_CFG_TC05_PREFETCH = 9
 TCR_CFG_TC05_SPLIT = 10
+TCR_CFG_TC05_INTERLEAVE = 11
 
 
 class TcrError(RuntimeError):

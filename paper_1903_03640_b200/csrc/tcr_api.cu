@@ -43,6 +43,7 @@ struct Config {
     int tc05_ctas = 3;
     int tc05_prefetch = 0;
     int tc05_split = 1;
+    int tc05_interleave = 0;
 };
 Config g_cfg;
 std::mutex g_cfg_mu;
@@ -91,6 +92,7 @@ LaunchCfg make_cfg(const DeviceInfo& di) {
     c.tc05_ctas = g_cfg.tc05_ctas;
     c.tc05_prefetch = g_cfg.tc05_prefetch;
     c.tc05_split = g_cfg.tc05_split;
+    c.tc05_interleave = g_cfg.tc05_interleave;
     return c;
 }
 
@@ -383,6 +385,10 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             if (value != 1 && value != 2 && value != 4 && value != 8) break;
             g_cfg.tc05_split = value;
             return TCR_OK;
+        case TCR_CFG_TC05_INTERLEAVE:
+            if (value != 0 && value != 1) break;
+            g_cfg.tc05_interleave = value;
+            return TCR_OK;
     }
     g_last_error = "invalid config key or value";
     return TCR_ERR_INVALID_VALUE;
@@ -402,6 +408,7 @@ int tcr_get_config(tcr_config_key key) {
         case TCR_CFG_TC05_CTAS_PER_SM: return g_cfg.tc05_ctas;
         case TCR_CFG_TC05_PREFETCH: return g_cfg.tc05_prefetch;
         case TCR_CFG_TC05_SPLIT: return g_cfg.tc05_split;
+        case TCR_CFG_TC05_INTERLEAVE: return g_cfg.tc05_interleave;
     }
     return -1;
 }

@@ -30,6 +30,7 @@ struct LaunchCfg {
     int tc05_ctas;      // tcgen05 kernel: CTAs per SM
     int tc05_prefetch;  // tcgen05 kernel: L2 prefetch distance in chunks
     int tc05_split;     // tcgen05 kernel: bulk copies per stage
+    int tc05_interleave;  // tcgen05 kernel: chunk-to-CTA mapping (0 contiguous, 1 interleaved)
 };
 
 // Each launcher enqueues exactly one kernel on `stream` and returns the

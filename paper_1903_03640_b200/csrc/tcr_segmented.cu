@@ -23,8 +23,10 @@ __device__ __forceinline__ double seg_reduce(const uint4* __restrict__ xb, int64
     float fA = 0.f, fB = 0.f;
     const int64_t v0 = s >> 3, v1 = (e + 7) >> 3;  // vectors touching [s, e)
     const int64_t f0 = (s + 7) >> 3, f1 = e >> 3;  // vectors entirely inside
-    int64_t vb = v0;
-    for (; vb + 32 * U <= v1; vb += 32 * U) {
+    // Every group of U tiles (32*U vectors) is one memory round trip: interior
+    // groups load unmasked; the first and last groups load only the vectors
+    // that touch the segment (predicated) and zero the halves outside it.
+    for (int64_t vb = v0; vb < v1; vb += 32 * U) {
         uint4 v[U];
         if (vb >= f0 && vb + 32 * U <= f1) {
 #pragma unroll
@@ -33,7 +35,8 @@ __device__ __forceinline__ double seg_reduce(const uint4* __restrict__ xb, int64
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t vi = vb + u * 32 + lane;
-                v[u] = mask_vec(ldg_stream(xb + vi), vi * 8, s, e);
+                v[u] = make_uint4(0u, 0u, 0u, 0u);
+                if (vi < v1) v[u] = mask_vec(ldg_stream(xb + vi), vi * 8, s, e);
             }
         }
         __syncwarp();  // scheduling fence: all U loads issue before the first consumer
@@ -55,17 +58,6 @@ __device__ __forceinline__ double seg_reduce(const uint4* __restrict__ xb, int64
             fA = fB = 0.f;
         }
     }
-    for (; vb < v1; vb += 32) {  // last < 32*U vectors, one masked tile at a time
-        const int64_t vi = vb + lane;
-        uint4 t = make_uint4(0u, 0u, 0u, 0u);
-        if (vi < v1) t = mask_vec(ldg_stream(xb + vi), vi * 8, s, e);
-        if constexpr (kMma) {
-            mma_rowsum(cA, t);
-            flush_rows(cA, acc, lane);
-        } else {
-            acc += (double)vec_sum_f32(t);
-        }
-    }
     return acc;
 }
 
@@ -82,10 +74,8 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
     unsigned long long j = 0;
     if (lane == 0) j = atomicAdd(ws.seg_next, 1ull);
     j = __shfl_sync(0xffffffffu, j, 0);
-    while (j < S) {
-        unsigned long long jn = 0;
-        if (lane == 0) jn = atomicAdd(ws.seg_next, 1ull);  // prefetch the next segment index
-        int64_t s, e;
+    int64_t s = 0, e = 0;
+    if (j < S) {
         if constexpr (kBatched) {
             s = (int64_t)(j * L);
             e = s + (int64_t)L;
@@ -93,10 +83,29 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
             s = __ldg(offsets + j);
             e = __ldg(offsets + j + 1);
         }
+    }
+    while (j < S) {
+        unsigned long long jn = 0;
+        if (lane == 0) jn = atomicAdd(ws.seg_next, 1ull);  // next segment index, in flight
         const double acc = seg_reduce<kMma, U>(xb, s + shift, e + shift, lane);
+        // the next index has arrived by now; start loading its offsets before
+        // the collapse so that their latency overlaps it
+        jn = __shfl_sync(0xffffffffu, jn, 0);
+        int64_t sn = 0, en = 0;
+        if (jn < S) {
+            if constexpr (kBatched) {
+                sn = (int64_t)(jn * L);
+                en = sn + (int64_t)L;
+            } else {
+                sn = __ldg(offsets + jn);
+                en = __ldg(offsets + jn + 1);
+            }
+        }
         const double tot = warp_collapse<kMma>(acc);
         if (lane == 0) out[j] = (float)tot;
-        j = __shfl_sync(0xffffffffu, jn, 0);
+        j = jn;
+        s = sn;
+        e = en;
     }
     if (lane == 0) {
         __threadfence();

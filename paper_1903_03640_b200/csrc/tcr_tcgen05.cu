@@ -105,6 +105,7 @@ struct Tc05Params {
     int chain;             // MMAs carried per accumulator before its flush (K)
     int prefetch;          // L2 prefetch distance in chunks (0 = off)
     int split;             // bulk copies per stage
+    int interleave;        // 0: CTA b owns a contiguous run of chunks; 1: chunks b, b+G, b+2G, ...
 };
 
 // Accumulator schedule: MMA number j of this CTA (j = 0, 1, ...) goes to
@@ -137,9 +138,11 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
     const size_t nb = n - head;
     const size_t chunk_elems = stage_bytes / 2;
     const size_t C = nb / chunk_elems;
-    const size_t c_begin = (size_t)blockIdx.x * C / gridDim.x;
-    const size_t c_end = (size_t)(blockIdx.x + 1) * C / gridDim.x;
-    const int nchunks = (int)(c_end - c_begin);
+    const size_t G = gridDim.x, b = blockIdx.x;
+    const size_t c_begin = prm.interleave ? b : b * C / G;
+    const int nchunks = prm.interleave ? (int)(C > b ? (C - b + G - 1) / G : 0)
+                                       : (int)((b + 1) * C / G - b * C / G);
+    const size_t chunk_step = prm.interleave ? G * (size_t)stage_bytes : (size_t)stage_bytes;
     const int kmma = (int)(stage_bytes / kTileBytes);
     const int per_round = prm.slots * prm.chain;
     const long long total_mma = (long long)nchunks * kmma;
@@ -171,12 +174,12 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
             const uint32_t piece = stage_bytes / (uint32_t)prm.split;
             const uint8_t* src = reinterpret_cast<const uint8_t*>(xa + c_begin * chunk_elems);
             for (int i = 0; i < prm.prefetch && i < nchunks; ++i)
-                sm100::prefetch_l2(src + (size_t)i * stage_bytes, stage_bytes);
+                sm100::prefetch_l2(src + (size_t)i * chunk_step, stage_bytes);
             int s = 0;
             uint32_t ph = 0;
-            for (int i = 0; i < nchunks; ++i, src += stage_bytes) {
+            for (int i = 0; i < nchunks; ++i, src += chunk_step) {
                 if (prm.prefetch && i + prm.prefetch < nchunks)
-                    sm100::prefetch_l2(src + (size_t)prm.prefetch * stage_bytes, stage_bytes);
+                    sm100::prefetch_l2(src + (size_t)prm.prefetch * chunk_step, stage_bytes);
                 sm100::mbar_wait(&empty[s], ph ^ 1u);
                 TC05_TRACE(0, i);
                 sm100::mbar_arrive_expect_tx(&full[s], stage_bytes);
@@ -293,10 +296,24 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
     tc_complete<kTcWarps>(acc, out_f32, out_f64, ws);
 }
 
+// CTAs of this kernel that can be co-resident on one SM for `cfg`: the
+// requested count, clamped by shared memory (227 KiB per SM) and by TMEM
+// (512 columns per SM; each CTA allocates 2 buffers x slots x 16 columns).
+static int tc05_resident(const LaunchCfg& cfg) {
+    const size_t smem = kHeaderBytes + (size_t)cfg.tc05_stages * (size_t)cfg.tc05_stage_kb * 1024u;
+    const int tmem_cols = 2 * cfg.tc05_slots * (int)kSlotCols < 32 ? 32 : 2 * cfg.tc05_slots * (int)kSlotCols;
+    int r = cfg.tc05_ctas < 1 ? 1 : cfg.tc05_ctas;
+    const int by_smem = (int)((227u * 1024u) / smem);
+    const int by_tmem = 512 / tmem_cols;
+    if (r > by_smem) r = by_smem;
+    if (r > by_tmem) r = by_tmem;
+    return r < 1 ? 1 : r;
+}
+
 int tcgen05_grid(size_t n, const LaunchCfg& cfg) {
     const size_t chunk_elems = (size_t)cfg.tc05_stage_kb * 512;
     const size_t C = n / chunk_elems;
-    const size_t gmax = (size_t)cfg.sms * (size_t)(cfg.tc05_ctas < 1 ? 1 : cfg.tc05_ctas);
+    const size_t gmax = (size_t)cfg.sms * (size_t)tc05_resident(cfg);
     size_t g = C < gmax ? C : gmax;
     return g < 1 ? 1 : (int)g;
 }
@@ -311,13 +328,10 @@ cudaError_t launch_reduce_tcgen05(const uint16_t* x, size_t n, float* out_f32, d
     prm.chain = cfg.tc05_chain;
     prm.prefetch = cfg.tc05_prefetch;
     prm.split = cfg.tc05_split;
+    prm.interleave = cfg.tc05_interleave;
     if (prm.slots < 1 || prm.slots > 16 || (prm.slots & (prm.slots - 1)) || prm.chain < 1 ||
         prm.stage_bytes % kTileBytes || prm.stage_bytes % (16u * (uint32_t)prm.split))
         return cudaErrorInvalidValue;
-    if (cfg.tc05_ctas > 1 && 2 * prm.slots * (int)kSlotCols * cfg.tc05_ctas > 512)
-        return cudaErrorInvalidValue;  // TMEM columns of co-resident CTAs
-    if ((kHeaderBytes + (size_t)prm.stages * prm.stage_bytes) * (size_t)cfg.tc05_ctas > 227u * 1024u)
-        return cudaErrorInvalidValue;  // shared memory of co-resident CTAs
     const size_t smem = kHeaderBytes + (size_t)prm.stages * prm.stage_bytes;
     if (kHeaderBytes - 8 < 512 + (size_t)(2 * prm.stages + 4) * 8) return cudaErrorInvalidValue;
     int dev = 0;

@@ -197,9 +197,12 @@ def test_config_knobs(tcr):
                              (tcr.TCR_CFG_TC05_CTAS_PER_SM, ct), (tcr.TCR_CFG_TC05_PREFETCH, pf),
                              (tcr.TCR_CFG_TC05_SPLIT, sp)):
                 tcr.tcr_set_config(key, val)
-            g = _reduce(tcr, x, "tcgen05")
-            assert oracle.within_tolerance(g, es), (st, kb, sl, ch, ct, pf, sp, g, es.f64())
-            assert g == _reduce(tcr, x, "tcgen05")
+            for il in (0, 1):
+                tcr.tcr_set_config(tcr.TCR_CFG_TC05_INTERLEAVE, il)
+                g = _reduce(tcr, x, "tcgen05")
+                assert oracle.within_tolerance(g, es), (st, kb, sl, ch, ct, pf, sp, il, g, es.f64())
+                assert g == _reduce(tcr, x, "tcgen05")
+            tcr.tcr_set_config(tcr.TCR_CFG_TC05_INTERLEAVE, 0)
     finally:
         tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
         tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 8)
