@@ -11,6 +11,8 @@
 
 namespace tcr {
 
+constexpr unsigned long long kBatchSeg = 8;  // segments per scheduler atomic (guided)
+
 // Reduce elements [s, e) of the 16-byte-aligned array xb (element indices
 // relative to xb).  Returns the lane's fp64 share; the sum over lanes is the
 // segment total.
@@ -71,36 +73,46 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
     const uint4* xb = reinterpret_cast<const uint4*>(addr & ~(uintptr_t)15u);
     const unsigned total_warps = gridDim.x * WARPS;
 
-    unsigned long long j = 0;
-    if (lane == 0) j = atomicAdd(ws.seg_next, 1ull);
-    j = __shfl_sync(0xffffffffu, j, 0);
-    int64_t s = 0, e = 0;
-    if (j < S) {
+    // Guided self-scheduling: a warp takes a batch of kBatchSeg consecutive
+    // segments per atomic while plenty remain, single segments near the end
+    // (one global atomic per segment saturates the L2 atomic unit at ~4 ns
+    // per segment -- the whole C5 kernel time).
+    const unsigned long long tail_zone = 2ull * total_warps * kBatchSeg;
+    auto grab = [&](unsigned long long hint) -> unsigned long long {
+        unsigned long long got = 0;
+        const unsigned long long b = (S > hint + tail_zone) ? kBatchSeg : 1ull;
+        if (lane == 0) got = atomicAdd(ws.seg_next, b) | (b << 56);
+        return got;  // start index in bits 0..55, batch size in 56..63 (lane 0)
+    };
+    auto bounds = [&](unsigned long long jj, int64_t& ss, int64_t& ee) {
         if constexpr (kBatched) {
-            s = (int64_t)(j * L);
-            e = s + (int64_t)L;
+            ss = (int64_t)(jj * L);
+            ee = ss + (int64_t)L;
         } else {
-            s = __ldg(offsets + j);
-            e = __ldg(offsets + j + 1);
+            ss = __ldg(offsets + jj);
+            ee = __ldg(offsets + jj + 1);
         }
-    }
+    };
+    const unsigned long long kIdx = (1ull << 56) - 1;
+    unsigned long long g = __shfl_sync(0xffffffffu, grab(0), 0);
+    unsigned long long j = g & kIdx, batch_end = j + (g >> 56);
+    int64_t s = 0, e = 0;
+    if (j < S) bounds(j, s, e);
     while (j < S) {
-        unsigned long long jn = 0;
-        if (lane == 0) jn = atomicAdd(ws.seg_next, 1ull);  // next segment index, in flight
+        const bool last = (j + 1 == batch_end);
+        unsigned long long gn = 0;
+        if (last) gn = grab(j);  // next batch start, in flight during this segment
         const double acc = seg_reduce<kMma, U>(xb, s + shift, e + shift, lane);
-        // the next index has arrived by now; start loading its offsets before
-        // the collapse so that their latency overlaps it
-        jn = __shfl_sync(0xffffffffu, jn, 0);
-        int64_t sn = 0, en = 0;
-        if (jn < S) {
-            if constexpr (kBatched) {
-                sn = (int64_t)(jn * L);
-                en = sn + (int64_t)L;
-            } else {
-                sn = __ldg(offsets + jn);
-                en = __ldg(offsets + jn + 1);
-            }
+        unsigned long long jn;
+        if (last) {
+            gn = __shfl_sync(0xffffffffu, gn, 0);
+            jn = gn & kIdx;
+            batch_end = jn + (gn >> 56);
+        } else {
+            jn = j + 1;
         }
+        int64_t sn = 0, en = 0;  // next bounds: their latency overlaps the collapse
+        if (jn < S) bounds(jn, sn, en);
         const double tot = warp_collapse<kMma>(acc);
         if (lane == 0) out[j] = (float)tot;
         j = jn;
