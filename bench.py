@@ -162,7 +162,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--algo", default="default", choices=["default", "mma_sync", "tcgen05", "shuffle"])
+    ap.add_argument("--algo", default="default",
+                    choices=["default", "mma_sync", "tcgen05", "shuffle", "exact"])
     ap.add_argument("--workload", default="c3", choices=["c3", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n-per-rank", type=int, default=N_PER_RANK)
@@ -206,7 +207,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(dev)
-    algo = tcr.ALGOS[args.algo]
+    exact = args.algo == "exact"
+    algo = tcr.ALGOS["default" if exact else args.algo]
     peak, peak_src = _peaks()
 
     # ---------------- inputs (untimed), resident in HBM ----------------
@@ -232,6 +234,7 @@ def main():
         workload = "c5: 2^20 segments, log-uniform lengths in [256, 65536], fp16 uniform[-1,1]"
     out32 = torch.empty(1, dtype=torch.float32, device=dev)
     out64 = torch.empty(1, dtype=torch.float64, device=dev)
+    acc6 = torch.empty(6, dtype=torch.int64, device=dev)
     torch.cuda.synchronize()
 
     def step(ev_k0=None, ev_k1=None):
@@ -240,6 +243,9 @@ def main():
                 ev_k0.record(stream)
             if args.workload == "c5":
                 tcr.tcr_reduce_sum_segmented(x, toff, seg_out, stream=stream)
+            elif exact:
+                tcr.tcr_reduce_sum_exact(x, acc=acc6, out_f32=out32 if world == 1 else None,
+                                         stream=stream)
             elif world == 1:
                 tcr.tcr_reduce_sum_algo(x, out_f32=out32, algo=algo, stream=stream)
             else:
@@ -247,8 +253,12 @@ def main():
             if ev_k1 is not None:
                 ev_k1.record(stream)
             if args.workload == "c3" and world > 1:
-                dist.all_reduce(out64)  # the paper's distributed merge, over NVLink
-                tcr.tcr_round_f64_to_f32(out64, out32, stream=stream)
+                if exact:  # integer limbs: the allreduce is exact, result independent of N
+                    dist.all_reduce(acc6)
+                    tcr.tcr_exact_finalize(acc6, out_f32=out32, stream=stream)
+                else:
+                    dist.all_reduce(out64)  # the paper's distributed merge, over NVLink
+                    tcr.tcr_round_f64_to_f32(out64, out32, stream=stream)
 
     for _ in range(args.warmup):
         step()

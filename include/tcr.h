@@ -156,6 +156,29 @@ tcr_status tcr_reduce_sum_batched_shuffle(const tcr_half *x, size_t num_segments
 tcr_status tcr_reduce_sum_host(const tcr_half *x, size_t n, float *out, tcr_stream stream);
 
 /*
+ * tcr_reduce_sum_exact -- NEXT-3: the EXACT sum (no rounding before the
+ * final conversion).  Each binary16 is placed bit-exactly into a scaled
+ * binary64 (x * 2^-1008, subnormals included); <= 1024 of them are added
+ * exactly per accumulator, flushed into 128-bit integers in units of 2^-24,
+ * and combined exactly across warps, CTAs and the grid (one launch).
+ * Outputs (each may be NULL, not all):
+ *   acc[6]  (device int64): {l0, l1, l2, n_nan, n_pinf, n_ninf} with the
+ *           exact sum T = (l0 + l1*2^40 + l2*2^80) * 2^-24, l0, l1 in
+ *           [0, 2^40).  Integer-summing acc[] of several shards (e.g. an
+ *           NCCL int64 SUM allreduce) is exact; see tcr_exact_finalize.
+ *   out_f32 / out_f64: the correctly rounded (RNE) value of T, or the IEEE
+ *           special value if any input was NaN / inf.
+ * Bitwise identical to the exact oracle for every input; independent of
+ * grid size, thread count and (for sharded use) the number of GPUs.
+ */
+tcr_status tcr_reduce_sum_exact(const tcr_half *x, size_t n, int64_t *acc, float *out_f32,
+                                double *out_f64, tcr_stream stream);
+
+/* tcr_exact_finalize -- RNE binary32 / binary64 of an (allreduced) acc[6]. */
+tcr_status tcr_exact_finalize(const int64_t *acc, float *out_f32, double *out_f64,
+                              tcr_stream stream);
+
+/*
  * tcr_round_f64_to_f32 -- out[0] = (float)in[0], round-to-nearest-even, on
  * the device (finaliser of a sharded reduction after the allreduce of the
  * binary64 partials).

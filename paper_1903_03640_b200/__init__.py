@@ -84,6 +84,8 @@ _SIGS = {
     "tcr_reduce_sum_batched_shuffle": [_P, _SZ, _SZ, _P, _P],
     "tcr_reduce_sum_host": [_P, _SZ, _P, _P],
     "tcr_round_f64_to_f32": [_P, _P, _P],
+    "tcr_reduce_sum_exact": [_P, _SZ, _P, _P, _P, _P],
+    "tcr_exact_finalize": [_P, _P, _P, _P],
     "tcr_probe_mma": [_P, _P, _P, _I, _P],
     "tcr_set_config": [_I, _I],
     "tcr_release_workspaces": [],
@@ -211,6 +213,25 @@ def tcr_reduce_sum_host(x, n=None, stream=None) -> float:
     return float(res.value)
 
 
+def tcr_reduce_sum_exact(x, acc=None, out_f32=None, out_f64=None, n=None, stream=None) -> None:
+    """Exact sum: acc (int64[6] device: limbs l0,l1,l2 of T*2^24 in base 2^40,
+    NaN/+inf/-inf counts) and/or the correctly rounded float32 / float64."""
+    _check(_lib.tcr_reduce_sum_exact(_ptr(x), _numel(x, n), _ptr(acc), _ptr(out_f32),
+                                     _ptr(out_f64), _stream(stream, x)), "tcr_reduce_sum_exact")
+
+
+def tcr_exact_finalize(acc, out_f32=None, out_f64=None, stream=None) -> None:
+    """RNE float32 / float64 of an (allreduced) exact accumulator acc[6]."""
+    _check(_lib.tcr_exact_finalize(_ptr(acc), _ptr(out_f32), _ptr(out_f64), _stream(stream, acc)),
+           "tcr_exact_finalize")
+
+
+def exact_limbs_to_int(acc) -> int:
+    """Python int T (units of 2^-24) from the limbs of acc[6] (host-side decode)."""
+    a = [int(v) for v in acc]
+    return a[0] + (a[1] << 40) + (a[2] << 80)
+
+
 def tcr_round_f64_to_f32(inp, out, stream=None) -> None:
     _check(_lib.tcr_round_f64_to_f32(_ptr(inp), _ptr(out), _stream(stream, inp)),
            "tcr_round_f64_to_f32")
@@ -273,4 +294,4 @@ def reduce_sum_segmented(x, offsets, mma: bool = True, stream=None):
 
 
 __all__ = [n for n in dir() if n.startswith("tcr_") or n.startswith("TCR_")] + [
-    "reduce_sum", "reduce_sum_segmented", "TcrError", "LIB_PATH", "ALGOS"]
+    "reduce_sum", "reduce_sum_segmented", "exact_limbs_to_int", "TcrError", "LIB_PATH", "ALGOS"]

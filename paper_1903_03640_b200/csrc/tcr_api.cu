@@ -314,6 +314,34 @@ tcr_status tcr_reduce_sum_host(const tcr_half* x, size_t n, float* out, tcr_stre
     return TCR_OK;
 }
 
+tcr_status tcr_reduce_sum_exact(const tcr_half* x, size_t n, int64_t* acc, float* out_f32,
+                                double* out_f64, tcr_stream stream) {
+    if ((!x && n) || (!acc && !out_f32 && !out_f64))
+        return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    if (!aligned(x, 2) || !aligned(acc, 8) || !aligned(out_f32, 4) || !aligned(out_f64, 8))
+        return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
+    DeviceInfo di;
+    Workspace* ws = nullptr;
+    tcr_status s = prologue((cudaStream_t)stream, &di, &ws);
+    if (s != TCR_OK) return s;
+    const LaunchCfg cfg = make_cfg(di);
+    return after_launch(tcr::launch_reduce_exact(x, n, reinterpret_cast<long long*>(acc), out_f32,
+                                                 out_f64, ws->dev, cfg, (cudaStream_t)stream),
+                        "exact kernel launch");
+}
+
+tcr_status tcr_exact_finalize(const int64_t* acc, float* out_f32, double* out_f64,
+                              tcr_stream stream) {
+    if (!acc || (!out_f32 && !out_f64)) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    DeviceInfo di;
+    int dev;
+    tcr_status s = current_device(&dev, &di);
+    if (s != TCR_OK) return s;
+    return after_launch(tcr::launch_exact_finalize(reinterpret_cast<const long long*>(acc),
+                                                   out_f32, out_f64, (cudaStream_t)stream),
+                        "exact finalize launch");
+}
+
 tcr_status tcr_round_f64_to_f32(const double* in, float* out, tcr_stream stream) {
     if (!in || !out) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
     DeviceInfo di;

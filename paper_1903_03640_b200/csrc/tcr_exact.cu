@@ -1,0 +1,310 @@
+// tcr_exact.cu -- NEXT-3: bitwise-exact sum of binary16 (R(X) of Eq. 2,
+// P:106-110, with no rounding at all until the final conversion).
+//
+// Every finite binary16 value is an integer multiple of 2^-24 below 2^16.
+// Placing its 15 magnitude bits at bit 42 of a binary64 (and its sign at
+// bit 63) gives a binary64 equal to the value times 2^-1008 -- exact for
+// normal AND subnormal inputs (the subnormal binary16 f*2^-24 lands on the
+// binary64 subnormal f*2^-1032).  All such numbers are multiples of 2^-1032,
+// so binary64 additions of up to 8192 of them (|sum| < 2^-979, i.e. fewer
+// than 53 significant bits) are exact.  Each lane therefore adds scaled
+// binary64 values in two accumulators, flushes them every kFlushIter
+// iterations (<= 1024 elements per accumulator) into a signed 128-bit
+// integer in units of 2^-24, and the warp / CTA / grid levels add int128
+// exactly (the same last-CTA completion as the MMA kernels).  The result is
+// independent of thread count and order: it equals the exact integer
+// T = sum x_i * 2^24 of Eq. 2 bit for bit, and the binary32 / binary64 outputs are the correctly
+// rounded (RNE) values of T * 2^-24.
+//
+// Accumulator state for sharded use: int64 acc[6] = {l0, l1, l2, n_nan,
+// n_pinf, n_ninf} with T = l0 + l1*2^40 + l2*2^80 (l0, l1 in [0, 2^40)); an
+// integer SUM-allreduce of acc[] over GPUs is exact, and
+// tcr_exact_finalize() rounds it.
+#include "tcr_device.cuh"
+#include "tcr_internal.h"
+
+namespace tcr {
+
+namespace {
+
+constexpr int kExactWarps = 8;
+constexpr int kExactUnroll = 4;
+constexpr int kFlushIter = 64;  // 64 iterations x 4 vectors x 4 halves = 1024 per accumulator
+
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+// Scaled binary64 of the low / high binary16 of a 32-bit word (x 2^-1008).
+__device__ __forceinline__ double scaled_lo(uint32_t w) {
+    const uint32_t hi = ((w << 10) & 0x01FFFC00u) | ((w << 16) & 0x80000000u);
+    return __hiloint2double((int)hi, 0);
+}
+__device__ __forceinline__ double scaled_hi(uint32_t w) {
+    const uint32_t hi = ((w >> 6) & 0x01FFFC00u) | (w & 0x80000000u);
+    return __hiloint2double((int)hi, 0);
+}
+
+// Count and zero the non-finite halves of v (exponent field all ones).
+__device__ __forceinline__ void strip_specials(uint32_t (&w)[4], uint32_t (&cnt)[3]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t half = (w[k] >> (16 * h)) & 0xFFFFu;
+            if ((half & 0x7C00u) == 0x7C00u) {
+                if (half & 0x3FFu) ++cnt[0];            // NaN
+                else if (half & 0x8000u) ++cnt[2];      // -inf
+                else ++cnt[1];                          // +inf
+                w[k] &= ~(0xFFFFu << (16 * h));
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void exact_vec(const uint4& v, double& a0, double& a1,
+                                          uint32_t (&cnt)[3]) {
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t sp = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sp |= ((w[k] & 0x7C007C00u) + 0x04000400u) & 0x80008000u;
+    if (sp) strip_specials(w, cnt);  // rare
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        a0 += scaled_lo(w[k]);
+        a1 += scaled_hi(w[k]);
+    }
+}
+
+// Exact conversion of a flushed accumulator to integer units of 2^-24.
+__device__ __forceinline__ long long to_units(double a) {
+    return __double2ll_rn((a * 0x1p1008) * 0x1p24);  // both scalings exact; result < 2^53
+}
+
+__device__ __forceinline__ i128 shfl_xor_i128(i128 v, int o) {
+    const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+    const unsigned long long lo2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const unsigned long long hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    return (i128)(((u128)hi2 << 64) | (u128)lo2);
+}
+
+__device__ __forceinline__ i128 warp_sum_i128(i128 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += shfl_xor_i128(v, o);
+    return v;
+}
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Split an int128 into limbs l0 + l1*2^40 + l2*2^80 (l0, l1 in [0, 2^40)).
+__device__ __forceinline__ void to_limbs(i128 t, long long* acc) {
+    const u128 m = ((u128)1 << 40) - 1;
+    acc[0] = (long long)((u128)t & m);
+    acc[1] = (long long)(((u128)t >> 40) & m);
+    acc[2] = (long long)(t >> 80);
+}
+
+__device__ __forceinline__ i128 from_limbs(const long long* acc) {
+    return (i128)acc[0] + ((i128)acc[1] << 40) + ((i128)acc[2] << 80);
+}
+
+// Correctly rounded (RNE) value of T * 2^-24 with `bits` significand bits,
+// returned as mantissa (<= 2^bits) and binary exponent: value = mant * 2^exp.
+__device__ __forceinline__ void round_units(u128 U, int bits, unsigned long long& mant, int& exp) {
+    if (U == 0) {
+        mant = 0;
+        exp = 0;
+        return;
+    }
+    const unsigned long long hi = (unsigned long long)(U >> 64), lo = (unsigned long long)U;
+    const int msb = hi ? 127 - __clzll((long long)hi) : 63 - __clzll((long long)lo);
+    if (msb < bits) {  // exact
+        mant = lo;
+        exp = -24;
+        return;
+    }
+    const int shift = msb - (bits - 1);
+    u128 q = U >> shift;
+    const u128 rem = U - (q << shift);
+    const u128 halfway = (u128)1 << (shift - 1);
+    if (rem > halfway || (rem == halfway && (q & 1))) ++q;
+    mant = (unsigned long long)q;  // may equal 2^bits after rounding up: still exact below
+    exp = shift - 24;
+}
+
+__device__ void finalize(const long long* acc, float* out_f32, double* out_f64) {
+    float f;
+    double d;
+    const long long n_nan = acc[3], n_pinf = acc[4], n_ninf = acc[5];
+    if (n_nan || (n_pinf && n_ninf)) {
+        f = __int_as_float(0x7FC00000);
+        d = __longlong_as_double(0x7FF8000000000000ll);
+    } else if (n_pinf) {
+        f = __int_as_float(0x7F800000);
+        d = __longlong_as_double(0x7FF0000000000000ll);
+    } else if (n_ninf) {
+        f = __int_as_float(0xFF800000);
+        d = __longlong_as_double((long long)0xFFF0000000000000ull);
+    } else {
+        const i128 T = from_limbs(acc);
+        const bool neg = T < 0;
+        const u128 U = neg ? (u128)(-T) : (u128)T;
+        unsigned long long m;
+        int e;
+        round_units(U, 24, m, e);
+        f = ldexpf((float)m, e);  // m <= 2^24: exact; scaling by 2^e exact (no overflow below 2^104)
+        round_units(U, 53, m, e);
+        d = ldexp((double)m, e);
+        if (neg) {
+            f = -f;
+            d = -d;
+        }
+    }
+    if (out_f32) *out_f32 = f;
+    if (out_f64) *out_f64 = d;
+}
+
+__global__ void __launch_bounds__(kExactWarps * 32, 4)
+reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc, float* out_f32,
+                    double* out_f64, DevWorkspace ws) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    size_t head = ((16u - ((uintptr_t)x & 15u)) & 15u) >> 1;
+    if (head > n) head = n;
+    const uint16_t* xa = x + head;
+    const size_t nb = n - head;
+    const size_t T = nb / kTileElems;
+    const int tail = (int)(nb - T * kTileElems);
+    const size_t W = (size_t)gridDim.x * kExactWarps;
+    const size_t w = (size_t)blockIdx.x * kExactWarps + warp;
+    const uint4* base = reinterpret_cast<const uint4*>(xa) + lane;
+    constexpr int U = kExactUnroll;
+
+    double a0 = 0.0, a1 = 0.0;
+    i128 acc = 0;
+    uint32_t cnt[3] = {0u, 0u, 0u};
+    int it = 0;
+    size_t t = w;
+    for (; t + (size_t)(U - 1) * W < T; t += (size_t)U * W) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ldg_stream(base + (t + (size_t)u * W) * 32);
+        __syncwarp();  // scheduling fence: all U loads issue before the first consumer
+#pragma unroll
+        for (int u = 0; u < U; ++u) exact_vec(v[u], a0, a1, cnt);
+        if (++it == kFlushIter) {
+            it = 0;
+            acc += (i128)to_units(a0) + (i128)to_units(a1);
+            a0 = a1 = 0.0;
+        }
+    }
+    for (; t < T; t += W) exact_vec(ldg_stream(base + t * 32), a0, a1, cnt);
+    if (w == W - 1) {  // ragged head and tail
+        if (head) exact_vec(load_ragged(x, (int)head, lane), a0, a1, cnt);
+        if (tail) exact_vec(load_ragged(xa + T * kTileElems, tail, lane), a0, a1, cnt);
+    }
+    acc += (i128)to_units(a0) + (i128)to_units(a1);
+
+    // warp, CTA and grid levels: exact integer adds (order-free)
+    __shared__ long long s_part[kExactWarps][5];
+    __shared__ unsigned s_last;
+    acc = warp_sum_i128(acc);
+    for (int k = 0; k < 3; ++k) cnt[k] = warp_sum_u32(cnt[k]);
+    if (lane == 0) {
+        s_part[warp][0] = (long long)(unsigned long long)acc;
+        s_part[warp][1] = (long long)(acc >> 64);
+        for (int k = 0; k < 3; ++k) s_part[warp][2 + k] = cnt[k];
+    }
+    __syncthreads();
+    if (warp != 0) return;
+    i128 b = 0;
+    long long c[3] = {0, 0, 0};
+    if (lane < kExactWarps) {
+        b = (i128)(((u128)(unsigned long long)s_part[lane][1] << 64) |
+                   (u128)(unsigned long long)s_part[lane][0]);
+        for (int k = 0; k < 3; ++k) c[k] = s_part[lane][2 + k];
+    }
+    b = warp_sum_i128(b);
+    for (int k = 0; k < 3; ++k)
+        for (int o = 16; o > 0; o >>= 1) c[k] += __shfl_xor_sync(0xffffffffu, c[k], o);
+    long long res[6];
+    if (gridDim.x > 1) {
+        // CTA partial: 5 int64 words per CTA in the workspace (reinterpreted doubles)
+        long long* parts = reinterpret_cast<long long*>(ws.partials);
+        if (lane == 0) {
+            long long* p = parts + 5 * (size_t)blockIdx.x;
+            p[0] = (long long)(unsigned long long)b;
+            p[1] = (long long)(b >> 64);
+            p[2] = c[0];
+            p[3] = c[1];
+            p[4] = c[2];
+            __threadfence();
+            s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+        }
+        __syncwarp();
+        if (!__shfl_sync(0xffffffffu, s_last, 0)) return;
+        __threadfence();
+        b = 0;
+        c[0] = c[1] = c[2] = 0;
+        for (int i = lane; i < (int)gridDim.x; i += 32) {
+            const long long* p = parts + 5 * (size_t)i;
+            b += (i128)(((u128)(unsigned long long)__ldcg(p + 1) << 64) |
+                        (u128)(unsigned long long)__ldcg(p));
+            c[0] += __ldcg(p + 2);
+            c[1] += __ldcg(p + 3);
+            c[2] += __ldcg(p + 4);
+        }
+        b = warp_sum_i128(b);
+        for (int k = 0; k < 3; ++k)
+            for (int o = 16; o > 0; o >>= 1) c[k] += __shfl_xor_sync(0xffffffffu, c[k], o);
+        if (lane == 0) *ws.ticket = 0u;
+    }
+    if (lane == 0) {
+        to_limbs(b, res);
+        res[3] = c[0];
+        res[4] = c[1];
+        res[5] = c[2];
+        if (out_acc)
+            for (int k = 0; k < 6; ++k) out_acc[k] = res[k];
+        finalize(res, out_f32, out_f64);
+    }
+}
+
+__global__ void exact_finalize_kernel(const long long* acc, float* out_f32, double* out_f64) {
+    if (threadIdx.x == 0) {
+        long long a[6];
+        for (int k = 0; k < 6; ++k) a[k] = acc[k];
+        finalize(a, out_f32, out_f64);
+    }
+}
+
+}  // namespace
+
+int exact_grid(size_t n, const LaunchCfg& cfg, int capacity_words) {
+    const size_t tiles = n / kTileElems;
+    const size_t per_cta = (size_t)kExactWarps * kExactUnroll;
+    size_t g = (tiles + per_cta - 1) / per_cta;
+    size_t gmax = (size_t)cfg.sms * 4;  // 4 resident CTAs per SM (launch bounds)
+    const size_t cap = (size_t)capacity_words / 5;  // 5 int64 words per CTA partial
+    if (gmax > cap) gmax = cap;
+    if (g > gmax) g = gmax;
+    return g < 1 ? 1 : (int)g;
+}
+
+cudaError_t launch_reduce_exact(const uint16_t* x, size_t n, long long* out_acc, float* out_f32,
+                                double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                cudaStream_t stream) {
+    const int g = exact_grid(n, cfg, ws.capacity);
+    reduce_exact_kernel<<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32, out_f64, ws);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_exact_finalize(const long long* acc, float* out_f32, double* out_f64,
+                                  cudaStream_t stream) {
+    exact_finalize_kernel<<<1, 32, 0, stream>>>(acc, out_f32, out_f64);
+    return cudaGetLastError();
+}
+
+}  // namespace tcr

@@ -45,6 +45,11 @@ cudaError_t launch_reduce_segmented(bool mma, bool batched, const uint16_t* x,
                                     const int64_t* offsets, size_t num_segments,
                                     size_t segment_len, float* out, const DevWorkspace& ws,
                                     const LaunchCfg& cfg, cudaStream_t stream);
+cudaError_t launch_reduce_exact(const uint16_t* x, size_t n, long long* out_acc, float* out_f32,
+                                double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                cudaStream_t stream);
+cudaError_t launch_exact_finalize(const long long* acc, float* out_f32, double* out_f64,
+                                  cudaStream_t stream);
 cudaError_t launch_sum_partials(const double* partials, size_t count, float* out_f32,
                                 double* out_f64, cudaStream_t stream);
 cudaError_t launch_round_f64(const double* in, float* out, cudaStream_t stream);

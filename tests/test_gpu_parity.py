@@ -314,3 +314,36 @@ def _rounding_probe(tcr, algo, rows):
     with open(f"gpurun_out/probe_{algo}.json", "w") as f:
         json.dump(rec, f, indent=1)
     print(rec)
+
+
+def test_full_size_c4_on_one_gpu(tcr):
+    """n = 2^33 (BASELINE config 4's global array, 16 GiB) on one GPU: more
+    than 2^32 elements (64-bit indexing everywhere), and the sharded numeric
+    path of §8(e) emulated on one device -- 8 contiguous shards reduced with
+    tcr_reduce_sum_f64, partials combined in fp64 as the NCCL allreduce
+    would, one final rounding."""
+    import torch
+
+    n = 1 << 33
+    free, _ = torch.cuda.mem_get_info()
+    if free < 2 * n + (4 << 30):
+        pytest.skip("needs > 20 GiB of free device memory")
+    x = gen.generate_tensor(gen.SEED_C4, 0, n, gen.UNIFORM_PM1)
+    es = oracle.ExactSum(0, 0)
+    chunk = 1 << 30
+    for lo in range(0, n, chunk):  # oracle over 1 GiB-element host chunks
+        bits = x[lo:lo + chunk].view(torch.int16).cpu().numpy().view(np.uint16)
+        es = es + oracle.exact_sum_fp16(bits, threads=os.cpu_count() or 8)
+    for algo in ("default", "tcgen05", "shuffle"):
+        g = _reduce(tcr, x, algo)
+        assert oracle.within_tolerance(g, es), (algo, g, es.f64())
+    P = 8
+    parts = torch.empty(P, dtype=torch.float64, device="cuda")
+    for r in range(P):
+        lo, hi = r * n // P, (r + 1) * n // P
+        tcr.tcr_reduce_sum_f64(x[lo:hi], parts[r:r + 1])
+    tot = torch.empty(1, dtype=torch.float32, device="cuda")
+    tcr.tcr_round_f64_to_f32(parts.sum().reshape(1), tot)
+    torch.cuda.synchronize()
+    assert oracle.within_tolerance(float(tot.item()), es)
+    del x

@@ -68,6 +68,59 @@ def _worker(rank, world, port, n, q):
     dist.destroy_process_group()
 
 
+def _worker_exact(rank, world, port, n, q):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    import tcr_inputs as gen
+    from paper_1903_03640_b200.sharded import shard_range, sharded_reduce_sum_exact
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard_range(n, world, rank)
+    bits = gen.generate(gen.SEED_C4, lo, hi - lo, gen.WIDE)
+
+    def reducer(x, acc, s):  # stand-in for tcr_reduce_sum_exact: limbs of the exact shard sum
+        es = oracle.exact_sum_fp16(x)
+        t = es.T
+        acc.copy_(torch.tensor([t & ((1 << 40) - 1), (t >> 40) & ((1 << 40) - 1), t >> 80,
+                                es.n_nan, es.n_pinf, es.n_ninf], dtype=torch.int64))
+
+    def finalize(acc, o, s):  # stand-in for tcr_exact_finalize (host decode + RNE)
+        a = acc.tolist()
+        t = a[0] + (a[1] << 40) + (a[2] << 80)
+        o.fill_(oracle.round_to_f32(t * oracle.UNIT))
+        q.put((rank, t, float(o.item())))
+
+    out = torch.empty(1, dtype=torch.float32)
+    acc = torch.empty(6, dtype=torch.int64)
+    sharded_reduce_sum_exact(bits, out, acc, reducer=reducer, finalize=finalize)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_exact_limb_allreduce(world):
+    import oracle
+    import tcr_inputs as gen
+
+    n = 2_000_003
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_exact, args=(r, world, port, n, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in ps:
+        p.join(60)
+        assert p.exitcode == 0
+    es = oracle.exact_sum_fp16(gen.generate(gen.SEED_C4, 0, n, gen.WIDE))
+    assert {t for _, t, _ in res} == {es.T}          # integer allreduce is exact
+    assert {g for _, _, g in res} == {es.f32()}      # bitwise, every rank, every world size
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_gloo_fp64_partial_allreduce(world):
     import oracle
