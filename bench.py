@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--prefetch", type=int, help="TCR_CFG_TC05_PREFETCH")
     ap.add_argument("--split", type=int, help="TCR_CFG_TC05_SPLIT")
     ap.add_argument("--interleave", type=int, help="TCR_CFG_TC05_INTERLEAVE")
+    ap.add_argument("--exact-unroll", type=int, help="TCR_CFG_EXACT_UNROLL")
+    ap.add_argument("--exact-bps", type=int, help="TCR_CFG_EXACT_BLOCKS_PER_SM")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -196,7 +198,9 @@ def main():
                      (tcr.TCR_CFG_TC05_STAGE_KB, args.stage_kb), (tcr.TCR_CFG_TC05_SLOTS, args.slots),
                      (tcr.TCR_CFG_TC05_CHAIN, args.tc_chain), (tcr.TCR_CFG_TC05_CTAS_PER_SM, args.ctas),
                      (tcr.TCR_CFG_TC05_PREFETCH, args.prefetch), (tcr.TCR_CFG_TC05_SPLIT, args.split),
-                     (tcr.TCR_CFG_TC05_INTERLEAVE, args.interleave)):
+                     (tcr.TCR_CFG_TC05_INTERLEAVE, args.interleave),
+                     (tcr.TCR_CFG_EXACT_UNROLL, args.exact_unroll),
+                     (tcr.TCR_CFG_EXACT_BLOCKS_PER_SM, args.exact_bps)):
         if val is not None:
             tcr.tcr_set_config(key, val)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -214,8 +214,10 @@ typedef enum {
     TCR_CFG_TC05_CTAS_PER_SM = 8, /* tcgen05: CTAs per SM (1..4)              */
     TCR_CFG_TC05_PREFETCH = 9,    /* tcgen05: L2 prefetch distance in chunks (0 = off) */
     TCR_CFG_TC05_SPLIT = 10,      /* tcgen05: bulk copies per stage (1, 2, 4, 8) */
-    TCR_CFG_TC05_INTERLEAVE = 11  /* tcgen05: 0 = each CTA streams a contiguous run
+    TCR_CFG_TC05_INTERLEAVE = 11, /* tcgen05: 0 = each CTA streams a contiguous run
                                      of chunks, 1 = chunks dealt round-robin    */
+    TCR_CFG_EXACT_UNROLL = 12,    /* exact kernel: 16-byte loads per lane in flight (4, 8) */
+    TCR_CFG_EXACT_BLOCKS_PER_SM = 13 /* exact kernel: CTAs per SM (1..8)        */
 } tcr_config_key;
 tcr_status tcr_set_config(tcr_config_key key, int value);
 int tcr_get_config(tcr_config_key key); /* -1 for an unknown key */

@@ -54,6 +54,8 @@ TCR_CFG_TC05_CTAS_PER_SM = 8
 TCR_CFG_TC05_PREFETCH = 9
 TCR_CFG_TC05_SPLIT = 10
 TCR_CFG_TC05_INTERLEAVE = 11
+TCR_CFG_EXACT_UNROLL = 12
+TCR_CFG_EXACT_BLOCKS_PER_SM = 13
 
 
 class TcrError(RuntimeError):

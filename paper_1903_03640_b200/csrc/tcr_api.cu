@@ -44,6 +44,8 @@ struct Config {
     int tc05_prefetch = 0;
     int tc05_split = 1;
     int tc05_interleave = 0;
+    int exact_unroll = 8;
+    int exact_bps = 3;
 };
 Config g_cfg;
 std::mutex g_cfg_mu;
@@ -93,6 +95,8 @@ LaunchCfg make_cfg(const DeviceInfo& di) {
     c.tc05_prefetch = g_cfg.tc05_prefetch;
     c.tc05_split = g_cfg.tc05_split;
     c.tc05_interleave = g_cfg.tc05_interleave;
+    c.exact_unroll = g_cfg.exact_unroll;
+    c.exact_bps = g_cfg.exact_bps;
     return c;
 }
 
@@ -417,6 +421,14 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             if (value != 0 && value != 1) break;
             g_cfg.tc05_interleave = value;
             return TCR_OK;
+        case TCR_CFG_EXACT_UNROLL:
+            if (value != 4 && value != 8) break;
+            g_cfg.exact_unroll = value;
+            return TCR_OK;
+        case TCR_CFG_EXACT_BLOCKS_PER_SM:
+            if (value < 1 || value > 8) break;
+            g_cfg.exact_bps = value;
+            return TCR_OK;
     }
     g_last_error = "invalid config key or value";
     return TCR_ERR_INVALID_VALUE;
@@ -437,6 +449,8 @@ int tcr_get_config(tcr_config_key key) {
         case TCR_CFG_TC05_PREFETCH: return g_cfg.tc05_prefetch;
         case TCR_CFG_TC05_SPLIT: return g_cfg.tc05_split;
         case TCR_CFG_TC05_INTERLEAVE: return g_cfg.tc05_interleave;
+        case TCR_CFG_EXACT_UNROLL: return g_cfg.exact_unroll;
+        case TCR_CFG_EXACT_BLOCKS_PER_SM: return g_cfg.exact_bps;
     }
     return -1;
 }

@@ -34,42 +34,54 @@ constexpr int kFlushIter = 64;  // 64 iterations x 4 vectors x 4 halves = 1024 p
 typedef __int128 i128;
 typedef unsigned __int128 u128;
 
-// Scaled binary64 of the low / high binary16 of a 32-bit word (x 2^-1008).
+// Scaled binary64 of the low / high binary16 of a 32-bit word (x 2^-1008):
+// the high 32 bits of the binary64 are sign | 0000 | e(5) | f(10) | 0...,
+// i.e. the binary16 arithmetic-shifted right by 6 (from bit 31) with the
+// sign copies in bits 25..30 masked off.  Low 32 bits are zero.
 __device__ __forceinline__ double scaled_lo(uint32_t w) {
-    const uint32_t hi = ((w << 10) & 0x01FFFC00u) | ((w << 16) & 0x80000000u);
+    const uint32_t hi = (uint32_t)((int)(w << 16) >> 6) & 0x81FFFC00u;
     return __hiloint2double((int)hi, 0);
 }
 __device__ __forceinline__ double scaled_hi(uint32_t w) {
-    const uint32_t hi = ((w >> 6) & 0x01FFFC00u) | (w & 0x80000000u);
+    const uint32_t hi = (uint32_t)((int)w >> 6) & 0x81FFFC00u;
     return __hiloint2double((int)hi, 0);
 }
 
-// Count and zero the non-finite halves of v (exponent field all ones).
-__device__ __forceinline__ void strip_specials(uint32_t (&w)[4], uint32_t (&cnt)[3]) {
-#pragma unroll
+// Non-finite detection: x * 0 is NaN exactly when x is inf or NaN, so one
+// HFMA2 per 32-bit word folds the test into a half2 "probe" that stays +-0
+// unless a special value went by; it is checked once per iteration.
+__device__ __forceinline__ uint32_t probe_word(uint32_t w, uint32_t probe) {
+    const __half2 r = __hfma2(*reinterpret_cast<const __half2*>(&w), __float2half2_rn(0.0f),
+                              *reinterpret_cast<const __half2*>(&probe));
+    return *reinterpret_cast<const uint32_t*>(&r);
+}
+
+// Rare path: count the non-finite halves of v and subtract the scaled
+// binary64 values they contributed (exactly: every partial sum stays a
+// multiple of 2^-1032 below 2^-979).
+__device__ __forceinline__ void fix_specials(const uint4& v, double& a0, double& a1,
+                                             uint32_t (&cnt)[3]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     for (int k = 0; k < 4; ++k) {
-#pragma unroll
         for (int h = 0; h < 2; ++h) {
             const uint32_t half = (w[k] >> (16 * h)) & 0xFFFFu;
             if ((half & 0x7C00u) == 0x7C00u) {
                 if (half & 0x3FFu) ++cnt[0];            // NaN
                 else if (half & 0x8000u) ++cnt[2];      // -inf
                 else ++cnt[1];                          // +inf
-                w[k] &= ~(0xFFFFu << (16 * h));
+                if (h == 0) a0 -= scaled_lo(w[k]);
+                else a1 -= scaled_hi(w[k]);
             }
         }
     }
 }
 
 __device__ __forceinline__ void exact_vec(const uint4& v, double& a0, double& a1,
-                                          uint32_t (&cnt)[3]) {
-    uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    uint32_t sp = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) sp |= ((w[k] & 0x7C007C00u) + 0x04000400u) & 0x80008000u;
-    if (sp) strip_specials(w, cnt);  // rare
+                                          uint32_t& probe) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+        probe = probe_word(w[k], probe);
         a0 += scaled_lo(w[k]);
         a1 += scaled_hi(w[k]);
     }
@@ -167,7 +179,8 @@ __device__ void finalize(const long long* acc, float* out_f32, double* out_f64) 
     if (out_f64) *out_f64 = d;
 }
 
-__global__ void __launch_bounds__(kExactWarps * 32, 4)
+template <int U>
+__global__ void __launch_bounds__(kExactWarps * 32, (U <= 4 ? 4 : 3))
 reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc, float* out_f32,
                     double* out_f64, DevWorkspace ws) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -180,11 +193,12 @@ reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc
     const size_t W = (size_t)gridDim.x * kExactWarps;
     const size_t w = (size_t)blockIdx.x * kExactWarps + warp;
     const uint4* base = reinterpret_cast<const uint4*>(xa) + lane;
-    constexpr int U = kExactUnroll;
+    constexpr int kFlush = kFlushIter * kExactUnroll / U;  // <= 1024 halves per accumulator
 
     double a0 = 0.0, a1 = 0.0;
     i128 acc = 0;
     uint32_t cnt[3] = {0u, 0u, 0u};
+    uint32_t probe = 0u;
     int it = 0;
     size_t t = w;
     for (; t + (size_t)(U - 1) * W < T; t += (size_t)U * W) {
@@ -193,17 +207,28 @@ reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc
         for (int u = 0; u < U; ++u) v[u] = ldg_stream(base + (t + (size_t)u * W) * 32);
         __syncwarp();  // scheduling fence: all U loads issue before the first consumer
 #pragma unroll
-        for (int u = 0; u < U; ++u) exact_vec(v[u], a0, a1, cnt);
-        if (++it == kFlushIter) {
+        for (int u = 0; u < U; ++u) exact_vec(v[u], a0, a1, probe);
+        if (probe & 0x7FFF7FFFu) {  // some half was inf or NaN (rare): reload and fix
+#pragma unroll 1
+            for (int u = 0; u < U; ++u)
+                fix_specials(ldg_stream(base + (t + (size_t)u * W) * 32), a0, a1, cnt);
+            probe = 0u;
+        }
+        if (++it == kFlush) {
             it = 0;
             acc += (i128)to_units(a0) + (i128)to_units(a1);
             a0 = a1 = 0.0;
         }
     }
-    for (; t < T; t += W) exact_vec(ldg_stream(base + t * 32), a0, a1, cnt);
+    auto one = [&](const uint4& v) {
+        uint32_t p = 0u;
+        exact_vec(v, a0, a1, p);
+        if (p & 0x7FFF7FFFu) fix_specials(v, a0, a1, cnt);
+    };
+    for (; t < T; t += W) one(ldg_stream(base + t * 32));
     if (w == W - 1) {  // ragged head and tail
-        if (head) exact_vec(load_ragged(x, (int)head, lane), a0, a1, cnt);
-        if (tail) exact_vec(load_ragged(xa + T * kTileElems, tail, lane), a0, a1, cnt);
+        if (head) one(load_ragged(x, (int)head, lane));
+        if (tail) one(load_ragged(xa + T * kTileElems, tail, lane));
     }
     acc += (i128)to_units(a0) + (i128)to_units(a1);
 
@@ -286,7 +311,7 @@ int exact_grid(size_t n, const LaunchCfg& cfg, int capacity_words) {
     const size_t tiles = n / kTileElems;
     const size_t per_cta = (size_t)kExactWarps * kExactUnroll;
     size_t g = (tiles + per_cta - 1) / per_cta;
-    size_t gmax = (size_t)cfg.sms * 4;  // 4 resident CTAs per SM (launch bounds)
+    size_t gmax = (size_t)cfg.sms * (cfg.exact_bps < 1 ? 4 : cfg.exact_bps);
     const size_t cap = (size_t)capacity_words / 5;  // 5 int64 words per CTA partial
     if (gmax > cap) gmax = cap;
     if (g > gmax) g = gmax;
@@ -297,7 +322,12 @@ cudaError_t launch_reduce_exact(const uint16_t* x, size_t n, long long* out_acc,
                                 double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                 cudaStream_t stream) {
     const int g = exact_grid(n, cfg, ws.capacity);
-    reduce_exact_kernel<<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32, out_f64, ws);
+    if (cfg.exact_unroll == 8)
+        reduce_exact_kernel<8><<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32,
+                                                                   out_f64, ws);
+    else
+        reduce_exact_kernel<4><<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32,
+                                                                   out_f64, ws);
     return cudaGetLastError();
 }
 

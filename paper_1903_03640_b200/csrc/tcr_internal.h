@@ -31,6 +31,8 @@ struct LaunchCfg {
     int tc05_prefetch;  // tcgen05 kernel: L2 prefetch distance in chunks
     int tc05_split;     // tcgen05 kernel: bulk copies per stage
     int tc05_interleave;  // tcgen05 kernel: chunk-to-CTA mapping (0 contiguous, 1 interleaved)
+    int exact_unroll;     // exact kernel: 16-byte loads in flight per lane (4 or 8)
+    int exact_bps;        // exact kernel: CTAs per SM
 };
 
 // Each launcher enqueues exactly one kernel on `stream` and returns the
