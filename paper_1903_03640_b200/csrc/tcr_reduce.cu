@@ -134,7 +134,14 @@ int stream_grid(size_t n, const LaunchCfg& cfg) {
     const size_t tiles = n / kTileElems;
     const size_t per_cta = (size_t)kStreamWarps * cfg.unroll;  // tiles one CTA covers per iteration
     size_t g = (tiles + per_cta - 1) / per_cta;
-    const size_t gmax = (size_t)cfg.sms * cfg.blocks_per_sm;
+    // Large inputs (HBM-bound): oversubscribe with blocks_per_sm CTAs per SM
+    // (measured best at 2^30).  Below 2^28 elements the launch is latency
+    // bound and a second wave costs more than it hides: cap the grid at one
+    // resident wave (the __launch_bounds__ minimum CTAs per SM).
+    const int resident = cfg.unroll <= 8 ? 4 : 2;
+    const int per_sm = (n < ((size_t)1 << 28) && cfg.blocks_per_sm > resident) ? resident
+                                                                               : cfg.blocks_per_sm;
+    const size_t gmax = (size_t)cfg.sms * per_sm;
     if (g > gmax) g = gmax;
     if (g < 1) g = 1;
     return (int)g;
