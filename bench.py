@@ -206,10 +206,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hook (never used for a reported number): TCR_BENCH_SHARED_GPU=1 maps
+    # every rank to cuda:0 and uses gloo, to exercise the N > 1 code path on a
+    # one-GPU box.  The ranks' kernels are independent (nothing on the device
+    # waits for a peer); the allreduce runs on the host.
+    shared_gpu = os.environ.get("TCR_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(dev)
     exact = args.algo == "exact"
     algo = tcr.ALGOS["default" if exact else args.algo]
@@ -369,6 +379,8 @@ def main():
             "clocks": clk.summary(),
             "result": result,
         }
+        if shared_gpu:
+            line["test_mode"] = "shared-gpu gloo (not a measurement)"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

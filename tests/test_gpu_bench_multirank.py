@@ -1,0 +1,30 @@
+"""The bench's N > 1 code path (sharding, allreduce of the fp64 partial /
+exact limbs, max-over-ranks timing, rank-0 JSON) under torchrun with two
+ranks on the single GPU of the test box (gloo, TCR_BENCH_SHARED_GPU=1 --
+a code-path test, not a measurement)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["default", "exact"])
+def test_bench_two_ranks_shared_gpu(algo):
+    env = dict(os.environ, TCR_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29400 + (algo == "exact")),
+           "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--e2e-steps", "1",
+           "--n-per-rank", str(1 << 24), "--algo", algo]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 prints exactly one JSON line
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["n_total"] == 2 << 24
+    assert d["gpu_launches"] >= 3 and d["e2e"]["h2d_bytes_per_step"] == 2 << 24
+    assert d["test_mode"].startswith("shared-gpu")
