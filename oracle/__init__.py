@@ -82,24 +82,37 @@ def _load():
         lib.oracle_exact_segment_sums_fp16.argtypes = [
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(_Result)]
         lib.oracle_exact_segment_sums_fp16.restype = ctypes.c_int
+        lib.oracle_exact_bins_bf16.argtypes = [
+            ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_exact_bins_bf16.restype = ctypes.c_int
         _lib = lib
     return _lib
 
 
 @dataclass(frozen=True)
 class ExactSum:
-    """Exact result of R(X): T = sum x_i * 2^24 and A = sum |x_i| * 2^24 (ints)."""
+    """Exact result of R(X): T = sum x_i / unit and A = sum |x_i| / unit (ints).
+
+    unit = 2^unit_exp: 2^-24 for binary16 inputs, 2^-133 for bfloat16.
+    """
 
     T: int
     A: int
     n_nan: int = 0
     n_pinf: int = 0
     n_ninf: int = 0
+    unit_exp: int = -24
 
     def __add__(self, other: "ExactSum") -> "ExactSum":
         # Exact homomorphism R(X ++ Y) = R(X) + R(Y) (SPEC.md S:84).
+        if self.unit_exp != other.unit_exp:
+            raise ValueError("cannot add sums in different units")
         return ExactSum(self.T + other.T, self.A + other.A, self.n_nan + other.n_nan,
-                        self.n_pinf + other.n_pinf, self.n_ninf + other.n_ninf)
+                        self.n_pinf + other.n_pinf, self.n_ninf + other.n_ninf, self.unit_exp)
+
+    @property
+    def unit(self) -> Fraction:
+        return Fraction(2) ** self.unit_exp
 
     @property
     def finite(self) -> bool:
@@ -119,11 +132,11 @@ class ExactSum:
     @property
     def value(self) -> Fraction:
         """R(X) as an exact rational."""
-        return self.T * UNIT
+        return self.T * self.unit
 
     @property
     def abs_value(self) -> Fraction:
-        return self.A * UNIT
+        return self.A * self.unit
 
     def f32(self) -> float:
         """Correctly rounded (RNE) binary32 value of R(X), as a Python float."""
@@ -195,6 +208,33 @@ def exact_segment_sums_fp16(x, offsets) -> list[ExactSum]:
     return [_from_struct(res[j]) for j in range(s)]
 
 
+def exact_sum_bf16(x) -> ExactSum:
+    """Exact R(X) of bfloat16 bit patterns (uint16) -- NEXT-4.
+
+    The C loop bins the integer significands by exponent (``exact_sum.c``);
+    the bins are combined here in Python integers: T = sum_e bin[e] *
+    2^max(e-1, 0) in units of 2^-133 (exact, no overflow).
+    """
+    bits = np.ascontiguousarray(np.asarray(x, dtype=np.uint16).reshape(-1))
+    bins = np.zeros(256, dtype=np.int64)
+    abins = np.zeros(256, dtype=np.uint64)
+    counts = np.zeros(3, dtype=np.uint64)
+    _load().oracle_exact_bins_bf16(bits.ctypes.data, bits.size, bins.ctypes.data,
+                                   abins.ctypes.data, counts.ctypes.data)
+    T = sum(int(bins[e]) << max(e - 1, 0) for e in range(256))
+    A = sum(int(abins[e]) << max(e - 1, 0) for e in range(256))
+    return ExactSum(T, A, int(counts[0]), int(counts[1]), int(counts[2]), unit_exp=-133)
+
+
+def bf16_value(h: int) -> Fraction:
+    """Exact value of one finite bfloat16 bit pattern, from the definition."""
+    s, e, f = (h >> 15) & 1, (h >> 7) & 0xFF, h & 0x7F
+    if e == 0xFF:
+        raise ValueError("non-finite")
+    v = Fraction(f, 128) * Fraction(2) ** -126 if e == 0 else (1 + Fraction(f, 128)) * Fraction(2) ** (e - 127)
+    return -v if s else v
+
+
 def exact_sum_fraction(values) -> Fraction:
     """Pure-Python exact sum of binary16 inputs (brute force for tiny n).
 
@@ -264,6 +304,7 @@ def error_units(g: float, es: ExactSum) -> Fraction:
 
 
 __all__ = [
-    "ExactSum", "UNIT", "build", "exact_sum_fp16", "exact_segment_sums_fp16",
+    "ExactSum", "UNIT", "build", "exact_sum_fp16", "exact_segment_sums_fp16", "exact_sum_bf16",
+    "bf16_value",
     "exact_sum_fraction", "round_to_f32", "within_tolerance", "error_units",
 ]

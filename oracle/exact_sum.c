@@ -110,3 +110,39 @@ int oracle_exact_segment_sums_fp16(const uint16_t *x, const int64_t *offsets,
     }
     return 0;
 }
+
+/*
+ * bfloat16 (NEXT-4): value = (-1)^s * 2^(e-127) * (1 + f/128) for
+ * 1 <= e <= 254, (-1)^s * f * 2^-133 for e == 0; every finite bfloat16 is
+ * an integer multiple of 2^-133 below 2^128, so the exact sum needs ~262
+ * bits.  The oracle keeps, per biased exponent e, the signed sum of the
+ * integer significands sig = (e == 0 ? f : 128 + f) < 2^8 in an int64 bin
+ * (safe for n < 2^55) and the sum of |sig|; the caller forms
+ * T = sum_e bin[e] * 2^max(e-1, 0) in arbitrary precision (units 2^-133).
+ * bins / abs_bins: caller-owned int64[256] / uint64[256], overwritten.
+ * counts[3] = NaN, +inf, -inf inputs.
+ */
+int oracle_exact_bins_bf16(const uint16_t *x, size_t n, int64_t *bins, uint64_t *abs_bins,
+                           uint64_t *counts) {
+    for (int e = 0; e < 256; ++e) {
+        bins[e] = 0;
+        abs_bins[e] = 0;
+    }
+    counts[0] = counts[1] = counts[2] = 0;
+    for (size_t i = 0; i < n; ++i) {
+        const uint16_t h = x[i];
+        const unsigned s = (h >> 15) & 1u;
+        const unsigned e = (h >> 7) & 0xffu;
+        const unsigned f = h & 0x7fu;
+        if (e == 0xffu) {
+            if (f) ++counts[0];
+            else if (s) ++counts[2];
+            else ++counts[1];
+            continue;
+        }
+        const int64_t sig = (int64_t)(e == 0 ? f : 128u + f);
+        bins[e] += s ? -sig : sig;
+        abs_bins[e] += (uint64_t)sig;
+    }
+    return 0;
+}

@@ -104,6 +104,54 @@ def generate(seed: int, start: int, count: int, dist: int = UNIFORM_PM1) -> np.n
     raise ValueError(f"unknown dist {dist}")
 
 
+# ---------------------------------------------------------------------------
+# bfloat16 streams (NEXT-4).  Same (seed, index) hash; values:
+#   UNIFORM_PM1 / UNIFORM_01: the same binary32 v as above, RNE to bfloat16;
+#   ONES: 0x3F80;  ALTERNATING: +-pairs as above;  SMALLINT: {-2..2};
+#   WIDE: sign = bit 63, biased exponent = 64 + (z >> 32) mod 127 (64..190,
+#         so sums of < 2^60 elements stay far inside the binary32 range),
+#         mantissa = z & 0x7f.
+# ---------------------------------------------------------------------------
+
+
+def f32_to_bf16_rne(v: np.ndarray) -> np.ndarray:
+    """IEEE round-to-nearest-even binary32 -> bfloat16 bits (finite inputs)."""
+    b = np.asarray(v, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = (b + np.uint64(0x7FFF) + ((b >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)
+    return b.astype(np.uint16)
+
+
+def generate_bf16(seed: int, start: int, count: int, dist: int = UNIFORM_PM1) -> np.ndarray:
+    """bfloat16 bit patterns x[start .. start+count) of the (seed, dist) stream."""
+    idx = np.arange(start, start + count, dtype=np.uint64)
+    if dist in (UNIFORM_PM1, UNIFORM_01, ALTERNATING):
+        base = idx & ~np.uint64(1) if dist == ALTERNATING else idx
+        z = splitmix64(seed, base)
+        r = (z >> np.uint64(40)).astype(np.float32)
+        if dist == UNIFORM_01:
+            v = r * np.float32(2.0 ** -24)
+        else:
+            v = r * np.float32(2.0 ** -23) - np.float32(1.0)
+        b = f32_to_bf16_rne(v)
+        if dist == ALTERNATING:
+            b = b.copy()
+            b[(idx & np.uint64(1)).astype(bool)] ^= np.uint16(0x8000)
+        return b
+    if dist == ONES:
+        return np.full(count, 0x3F80, dtype=np.uint16)
+    if dist == WIDE:
+        z = splitmix64(seed, idx)
+        sign = (z >> np.uint64(63)).astype(np.uint16)
+        e = (np.uint64(64) + (z >> np.uint64(32)) % np.uint64(127)).astype(np.uint16)
+        f = (z & np.uint64(0x7F)).astype(np.uint16)
+        return (sign << np.uint16(15)) | (e << np.uint16(7)) | f
+    if dist == SMALLINT:
+        z = splitmix64(seed, idx)
+        v = ((z >> np.uint64(32)) % np.uint64(5)).astype(np.float32) - np.float32(2)
+        return f32_to_bf16_rne(v)
+    raise ValueError(f"unknown dist {dist}")
+
+
 def loguniform_lengths(seed: int, num_segments: int, lo: int = 256, hi: int = 65536) -> np.ndarray:
     """Segment lengths, log-uniform integers in [lo, hi] (reading G18).
 
@@ -146,6 +194,8 @@ def _device_lib():
             ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
             ctypes.c_int, ctypes.c_void_p]
         lib.tcr_inputs_generate.restype = ctypes.c_int
+        lib.tcr_inputs_generate_bf16.argtypes = lib.tcr_inputs_generate.argtypes
+        lib.tcr_inputs_generate_bf16.restype = ctypes.c_int
         _dev = lib
     return _dev
 
@@ -160,12 +210,20 @@ def generate_device(out_ptr: int, seed: int, start: int, count: int, dist: int =
         raise RuntimeError(f"tcr_inputs_generate failed with code {rc}")
 
 
-def generate_tensor(seed: int, start: int, count: int, dist: int = UNIFORM_PM1, device="cuda"):
-    """torch.float16 tensor of the stream generated on ``device`` (CUDA)."""
+def generate_tensor(seed: int, start: int, count: int, dist: int = UNIFORM_PM1, device="cuda",
+                    bf16: bool = False):
+    """torch.float16 (or bfloat16) tensor of the stream generated on ``device`` (CUDA)."""
     import torch
 
-    t = torch.empty(count, dtype=torch.float16, device=device)
+    t = torch.empty(count, dtype=torch.bfloat16 if bf16 else torch.float16, device=device)
     if count:
-        generate_device(t.data_ptr(), seed, start, count, dist,
-                        torch.cuda.current_stream(t.device).cuda_stream)
+        stream = torch.cuda.current_stream(t.device).cuda_stream
+        if bf16:
+            rc = _device_lib().tcr_inputs_generate_bf16(
+                ctypes.c_void_p(t.data_ptr()), ctypes.c_uint64(seed), ctypes.c_uint64(start),
+                ctypes.c_uint64(count), int(dist), ctypes.c_void_p(stream))
+            if rc != 0:
+                raise RuntimeError(f"tcr_inputs_generate_bf16 failed with code {rc}")
+        else:
+            generate_device(t.data_ptr(), seed, start, count, dist, stream)
     return t

@@ -2,6 +2,7 @@
 // (tcr_inputs/__init__.py holds the host implementation and the definition).
 // Holds none of the reduction's arithmetic.  Built into libtcr_inputs.so.
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -47,6 +48,40 @@ __device__ __forceinline__ uint16_t gen_one(uint64_t seed, uint64_t i, int dist)
     }
 }
 
+__device__ __forceinline__ uint16_t gen_one_bf16(uint64_t seed, uint64_t i, int dist) {
+    switch (dist) {
+        case 0:
+        case 1:
+        case 3: {
+            const uint64_t z = splitmix64(seed, dist == 3 ? (i & ~1ull) : i);
+            const float r = (float)(uint32_t)(z >> 40);
+            const float v = dist == 1 ? r * 0x1p-24f : r * 0x1p-23f - 1.0f;
+            const uint16_t b = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+            return (dist == 3 && (i & 1ull)) ? (uint16_t)(b ^ 0x8000u) : b;
+        }
+        case 2: return 0x3F80;
+        case 4: {
+            const uint64_t z = splitmix64(seed, i);
+            const uint16_t sign = (uint16_t)(z >> 63);
+            const uint16_t e = (uint16_t)(64ull + (z >> 32) % 127ull);
+            const uint16_t f = (uint16_t)(z & 0x7Full);
+            return (uint16_t)((sign << 15) | (e << 7) | f);
+        }
+        default: {
+            const uint64_t z = splitmix64(seed, i);
+            const float v = (float)(int)((z >> 32) % 5ull) - 2.0f;
+            return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+        }
+    }
+}
+
+__global__ void gen_kernel_bf16(uint16_t* __restrict__ out, uint64_t seed, uint64_t start,
+                                uint64_t count, int dist) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += stride)
+        out[k] = gen_one_bf16(seed, start + k, dist);
+}
+
 __global__ void gen_kernel(uint16_t* __restrict__ out, uint64_t seed, uint64_t start,
                            uint64_t count, int dist) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -56,8 +91,8 @@ __global__ void gen_kernel(uint16_t* __restrict__ out, uint64_t seed, uint64_t s
 
 }  // namespace
 
-extern "C" int tcr_inputs_generate(void* out, uint64_t seed, uint64_t start, uint64_t count,
-                                   int dist, void* stream) {
+static int launch_gen(bool bf16, void* out, uint64_t seed, uint64_t start, uint64_t count,
+                      int dist, void* stream) {
     if (count == 0) return 0;
     if (!out || dist < 0 || dist > 5) return 1;
     int dev = 0, sms = 148;
@@ -66,7 +101,21 @@ extern "C" int tcr_inputs_generate(void* out, uint64_t seed, uint64_t start, uin
     uint64_t blocks = (count + 255) / 256;
     const uint64_t cap = (uint64_t)sms * 8;
     if (blocks > cap) blocks = cap;
-    gen_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((uint16_t*)out, seed, start,
-                                                                     count, dist);
+    if (bf16)
+        gen_kernel_bf16<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((uint16_t*)out, seed,
+                                                                             start, count, dist);
+    else
+        gen_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((uint16_t*)out, seed,
+                                                                        start, count, dist);
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+extern "C" int tcr_inputs_generate(void* out, uint64_t seed, uint64_t start, uint64_t count,
+                                   int dist, void* stream) {
+    return launch_gen(false, out, seed, start, count, dist, stream);
+}
+
+extern "C" int tcr_inputs_generate_bf16(void* out, uint64_t seed, uint64_t start, uint64_t count,
+                                        int dist, void* stream) {
+    return launch_gen(true, out, seed, start, count, dist, stream);
 }
