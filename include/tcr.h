@@ -87,6 +87,13 @@ typedef enum {
                              FADD chains + shfl_xor tree, no tensor cores    */
 } tcr_algo;
 
+/* Input element type for the _ex entry points (NEXT-4). */
+typedef enum {
+    TCR_DTYPE_F16 = 0,  /* IEEE-754 binary16 (the north star)                */
+    TCR_DTYPE_BF16 = 1  /* bfloat16: the same MMA encoding with .bf16 / kind::f16-BF16
+                           operands and B = bfloat16 ones                    */
+} tcr_dtype;
+
 /*
  * tcr_reduce_sum -- R(X) of n binary16 values x[0..n) into *out (binary32).
  * The north-star entry point: MMA-encoded, one kernel launch, writes *out
@@ -119,6 +126,16 @@ tcr_status tcr_reduce_sum_algo(const tcr_half *x, size_t n, float *out_f32, doub
                                tcr_algo algo, tcr_stream stream);
 
 /*
+ * tcr_reduce_sum_ex -- tcr_reduce_sum_algo for either 16-bit input type:
+ * x holds n elements of `dtype` (binary16 or bfloat16 bit patterns).
+ * Same accuracy contract (|g - R| <= 2^-20 * sum|x_i| while the sum is
+ * inside the binary32 range) and error behaviour; TCR_ERR_INVALID_VALUE for
+ * an unknown dtype.  (The exact and host entry points are binary16 only.)
+ */
+tcr_status tcr_reduce_sum_ex(const void *x, size_t n, tcr_dtype dtype, float *out_f32,
+                             double *out_f64, tcr_algo algo, tcr_stream stream);
+
+/*
  * tcr_reduce_sum_segmented -- per-segment R over CSR offsets:
  * out[j] = R(x[offsets[j] .. offsets[j+1])) for j in [0, num_segments).
  * offsets: device int64[num_segments + 1], non-decreasing, offsets[0] >= 0,
@@ -134,6 +151,10 @@ tcr_status tcr_reduce_sum_segmented(const tcr_half *x, const int64_t *offsets,
                                     size_t num_segments, float *out, tcr_stream stream);
 tcr_status tcr_reduce_sum_segmented_shuffle(const tcr_half *x, const int64_t *offsets,
                                             size_t num_segments, float *out, tcr_stream stream);
+/* Segmented for either input type; algo = DEFAULT / MMA_SYNC (MMA) or SHUFFLE. */
+tcr_status tcr_reduce_sum_segmented_ex(const void *x, tcr_dtype dtype, const int64_t *offsets,
+                                       size_t num_segments, float *out, tcr_algo algo,
+                                       tcr_stream stream);
 
 /*
  * tcr_reduce_sum_batched -- num_segments contiguous segments of segment_len

@@ -41,6 +41,8 @@ TCR_ALGO_MMA_SYNC = 1
 TCR_ALGO_TCGEN05 = 2
 TCR_ALGO_SHUFFLE = 3
 ALGOS = {"default": 0, "mma_sync": 1, "tcgen05": 2, "shuffle": 3}
+TCR_DTYPE_F16 = 0
+TCR_DTYPE_BF16 = 1
 
 TCR_CFG_DEFAULT_ALGO = 0
 TCR_CFG_BLOCKS_PER_SM = 1
@@ -81,6 +83,8 @@ _SIGS = {
     "tcr_reduce_sum_f64": [_P, _SZ, _P, _P],
     "tcr_reduce_sum_algo": [_P, _SZ, _P, _P, _I, _P],
     "tcr_reduce_sum_segmented": [_P, _P, _SZ, _P, _P],
+    "tcr_reduce_sum_ex": [_P, _SZ, _I, _P, _P, _I, _P],
+    "tcr_reduce_sum_segmented_ex": [_P, _I, _P, _SZ, _P, _I, _P],
     "tcr_reduce_sum_segmented_shuffle": [_P, _P, _SZ, _P, _P],
     "tcr_reduce_sum_batched": [_P, _SZ, _SZ, _P, _P],
     "tcr_reduce_sum_batched_shuffle": [_P, _SZ, _SZ, _P, _P],
@@ -167,6 +171,39 @@ def tcr_reduce_sum_algo(x, out_f32=None, out_f64=None, algo=TCR_ALGO_DEFAULT, n=
         algo = ALGOS[algo]
     _check(_lib.tcr_reduce_sum_algo(_ptr(x), _numel(x, n), _ptr(out_f32), _ptr(out_f64),
                                     int(algo), _stream(stream, x)), "tcr_reduce_sum_algo")
+
+
+def _dtype_of(x, dtype):
+    if dtype is not None:
+        return int(dtype)
+    try:
+        import torch
+
+        if getattr(x, "dtype", None) == torch.bfloat16:
+            return TCR_DTYPE_BF16
+    except ImportError:  # pragma: no cover
+        pass
+    return TCR_DTYPE_F16
+
+
+def tcr_reduce_sum_ex(x, out_f32=None, out_f64=None, algo=TCR_ALGO_DEFAULT, dtype=None, n=None,
+                      stream=None) -> None:
+    """Sum of binary16 or bfloat16 x (dtype from the tensor unless given)."""
+    if isinstance(algo, str):
+        algo = ALGOS[algo]
+    _check(_lib.tcr_reduce_sum_ex(_ptr(x), _numel(x, n), _dtype_of(x, dtype), _ptr(out_f32),
+                                  _ptr(out_f64), int(algo), _stream(stream, x)),
+           "tcr_reduce_sum_ex")
+
+
+def tcr_reduce_sum_segmented_ex(x, offsets, out, algo=TCR_ALGO_DEFAULT, dtype=None,
+                                num_segments=None, stream=None) -> None:
+    if isinstance(algo, str):
+        algo = ALGOS[algo]
+    s = int(num_segments) if num_segments is not None else int(out.numel())
+    _check(_lib.tcr_reduce_sum_segmented_ex(_ptr(x), _dtype_of(x, dtype), _ptr(offsets), s,
+                                            _ptr(out), int(algo), _stream(stream, x)),
+           "tcr_reduce_sum_segmented_ex")
 
 
 def tcr_reduce_sum_segmented(x, offsets, out, num_segments=None, stream=None) -> None:

@@ -11,6 +11,7 @@ constexpr int kWarp = 32;
 constexpr int kTileElems = 256;  // one 16x16 fp16 MMA A operand = m^2 with m = 16
 constexpr int kVecElems = 8;     // one 16-byte vector = 8 binary16 = one lane's A fragment
 constexpr uint32_t kOnesH2 = 0x3C003C00u;  // two binary16 1.0: the all-ones B
+constexpr uint32_t kOnesBf2 = 0x3F803F80u;  // two bfloat16 1.0 (NEXT-4 bfloat16 inputs)
 
 // ---------------------------------------------------------------------------
 // Loads
@@ -51,6 +52,20 @@ __device__ __forceinline__ void mma_rowsum(float (&c)[4], const uint4& a) {
         "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(kOnesH2), "r"(kOnesH2));
+}
+
+// bfloat16 inputs (NEXT-4): the same encoding with .bf16 operands.
+__device__ __forceinline__ void mma_rowsum_bf16(float (&c)[4], const uint4& a) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(kOnesBf2), "r"(kOnesBf2));
+}
+
+template <bool kBf16>
+__device__ __forceinline__ void mma_rowsum_t(float (&c)[4], const uint4& a) {
+    if constexpr (kBf16) mma_rowsum_bf16(c, a);
+    else mma_rowsum(c, a);
 }
 
 // Flush the carried fp32 accumulator into the lane's fp64 accumulator and
@@ -113,6 +128,21 @@ __device__ __forceinline__ float vec_sum_f32(const uint4& a) {
     const float2 p2 = __half22float2(*reinterpret_cast<const __half2*>(&a.z));
     const float2 p3 = __half22float2(*reinterpret_cast<const __half2*>(&a.w));
     return ((p0.x + p0.y) + (p1.x + p1.y)) + ((p2.x + p2.y) + (p3.x + p3.y));
+}
+
+// bfloat16 -> binary32 is exact: the bfloat16 is the top half of the binary32.
+__device__ __forceinline__ float vec_sum_f32_bf16(const uint4& a) {
+    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+    float p[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] = __uint_as_float(w[k] << 16) + __uint_as_float(w[k] & 0xFFFF0000u);
+    return (p[0] + p[1]) + (p[2] + p[3]);
+}
+
+template <bool kBf16>
+__device__ __forceinline__ float vec_sum_t(const uint4& a) {
+    if constexpr (kBf16) return vec_sum_f32_bf16(a);
+    else return vec_sum_f32(a);
 }
 
 // Zero the halves of a 16-byte vector whose element index (vector base

@@ -37,13 +37,13 @@ struct LaunchCfg {
 
 // Each launcher enqueues exactly one kernel on `stream` and returns the
 // cudaGetLastError() of the launch.
-cudaError_t launch_reduce_stream(bool mma, const uint16_t* x, size_t n, float* out_f32,
+cudaError_t launch_reduce_stream(bool mma, bool bf16, const uint16_t* x, size_t n, float* out_f32,
                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                  cudaStream_t stream);
-cudaError_t launch_reduce_tcgen05(const uint16_t* x, size_t n, float* out_f32, double* out_f64,
-                                  const DevWorkspace& ws, const LaunchCfg& cfg,
+cudaError_t launch_reduce_tcgen05(bool bf16, const uint16_t* x, size_t n, float* out_f32,
+                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                   cudaStream_t stream);
-cudaError_t launch_reduce_segmented(bool mma, bool batched, const uint16_t* x,
+cudaError_t launch_reduce_segmented(bool mma, bool bf16, bool batched, const uint16_t* x,
                                     const int64_t* offsets, size_t num_segments,
                                     size_t segment_len, float* out, const DevWorkspace& ws,
                                     const LaunchCfg& cfg, cudaStream_t stream);

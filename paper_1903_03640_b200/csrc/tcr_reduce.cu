@@ -55,10 +55,10 @@ __device__ __forceinline__ void complete_block_and_grid(double lane_val, float* 
     }
 }
 
-template <bool kMma>
+template <bool kMma, bool kBf16>
 __device__ __forceinline__ void consume(const uint4& v, float (&c)[4], float& f) {
-    if constexpr (kMma) mma_rowsum(c, v);
-    else f += vec_sum_f32(v);
+    if constexpr (kMma) mma_rowsum_t<kBf16>(c, v);
+    else f += vec_sum_t<kBf16>(v);
 }
 
 template <bool kMma>
@@ -72,7 +72,7 @@ __device__ __forceinline__ void flush(float (&c)[4], float& f, double& acc, int 
 // __launch_bounds__ minimum CTAs/SM: without it ptxas budgets registers for
 // full occupancy (32 regs at 256 threads) and sinks the U loads below their
 // consumers, which leaves ~2 loads in flight per warp.
-template <bool kMma, int U, int WARPS>
+template <bool kMma, bool kBf16, int U, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, (U <= 8 ? 4 : 2))
 reduce_stream_kernel(const uint16_t* __restrict__ x, size_t n, int flush_every, float* out_f32,
                      double* out_f64, DevWorkspace ws) {
@@ -100,8 +100,8 @@ reduce_stream_kernel(const uint16_t* __restrict__ x, size_t n, int flush_every, 
         __syncwarp();  // scheduling fence: all U loads issue before the first consumer
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (u & 1) consume<kMma>(v[u], cB, fB);
-            else consume<kMma>(v[u], cA, fA);
+            if (u & 1) consume<kMma, kBf16>(v[u], cB, fB);
+            else consume<kMma, kBf16>(v[u], cA, fA);
         }
         if (++it == flush_every) {
             it = 0;
@@ -112,16 +112,16 @@ reduce_stream_kernel(const uint16_t* __restrict__ x, size_t n, int flush_every, 
     flush<kMma>(cA, fA, acc, lane);
     flush<kMma>(cB, fB, acc, lane);
     for (; t < T; t += W) {  // fewer than U tiles left for this warp
-        consume<kMma>(ldg_stream(base + t * 32), cA, fA);
+        consume<kMma, kBf16>(ldg_stream(base + t * 32), cA, fA);
         flush<kMma>(cA, fA, acc, lane);
     }
     if (w == W - 1) {  // ragged head and tail: zero-padded tiles (reading G5)
         if (head) {
-            consume<kMma>(load_ragged(x, (int)head, lane), cA, fA);
+            consume<kMma, kBf16>(load_ragged(x, (int)head, lane), cA, fA);
             flush<kMma>(cA, fA, acc, lane);
         }
         if (tail) {
-            consume<kMma>(load_ragged(xa + T * kTileElems, tail, lane), cA, fA);
+            consume<kMma, kBf16>(load_ragged(xa + T * kTileElems, tail, lane), cA, fA);
             flush<kMma>(cA, fA, acc, lane);
         }
     }
@@ -147,7 +147,7 @@ int stream_grid(size_t n, const LaunchCfg& cfg) {
     return (int)g;
 }
 
-template <bool kMma>
+template <bool kMma, bool kBf16>
 static cudaError_t launch_stream_t(const uint16_t* x, size_t n, float* out_f32, double* out_f64,
                                    const DevWorkspace& ws, const LaunchCfg& cfg,
                                    cudaStream_t stream) {
@@ -156,26 +156,29 @@ static cudaError_t launch_stream_t(const uint16_t* x, size_t n, float* out_f32, 
     const int fe = 2 * cfg.chain / cfg.unroll < 1 ? 1 : 2 * cfg.chain / cfg.unroll;
     switch (cfg.unroll) {
         case 4:
-            reduce_stream_kernel<kMma, 4, kStreamWarps>
+            reduce_stream_kernel<kMma, kBf16, 4, kStreamWarps>
                 <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
             break;
         case 16:
-            reduce_stream_kernel<kMma, 16, kStreamWarps>
+            reduce_stream_kernel<kMma, kBf16, 16, kStreamWarps>
                 <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
             break;
         default:
-            reduce_stream_kernel<kMma, 8, kStreamWarps>
+            reduce_stream_kernel<kMma, kBf16, 8, kStreamWarps>
                 <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
             break;
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_reduce_stream(bool mma, const uint16_t* x, size_t n, float* out_f32,
+cudaError_t launch_reduce_stream(bool mma, bool bf16, const uint16_t* x, size_t n, float* out_f32,
                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                  cudaStream_t stream) {
-    return mma ? launch_stream_t<true>(x, n, out_f32, out_f64, ws, cfg, stream)
-               : launch_stream_t<false>(x, n, out_f32, out_f64, ws, cfg, stream);
+    if (bf16)
+        return mma ? launch_stream_t<true, true>(x, n, out_f32, out_f64, ws, cfg, stream)
+                   : launch_stream_t<false, true>(x, n, out_f32, out_f64, ws, cfg, stream);
+    return mma ? launch_stream_t<true, false>(x, n, out_f32, out_f64, ws, cfg, stream)
+               : launch_stream_t<false, false>(x, n, out_f32, out_f64, ws, cfg, stream);
 }
 
 // ---------------------------------------------------------------------------

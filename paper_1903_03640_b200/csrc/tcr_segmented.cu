@@ -16,7 +16,7 @@ constexpr unsigned long long kBatchSeg = 8;  // segments per scheduler atomic (g
 // Reduce elements [s, e) of the 16-byte-aligned array xb (element indices
 // relative to xb).  Returns the lane's fp64 share; the sum over lanes is the
 // segment total.
-template <bool kMma, int U>
+template <bool kMma, bool kBf16, int U>
 __device__ __forceinline__ double seg_reduce(const uint4* __restrict__ xb, int64_t s, int64_t e,
                                              int lane) {
     double acc = 0.0;
@@ -45,11 +45,11 @@ __device__ __forceinline__ double seg_reduce(const uint4* __restrict__ xb, int64
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if constexpr (kMma) {
-                if (u & 1) mma_rowsum(cB, v[u]);
-                else mma_rowsum(cA, v[u]);
+                if (u & 1) mma_rowsum_t<kBf16>(cB, v[u]);
+                else mma_rowsum_t<kBf16>(cA, v[u]);
             } else {
-                if (u & 1) fB += vec_sum_f32(v[u]);
-                else fA += vec_sum_f32(v[u]);
+                if (u & 1) fB += vec_sum_t<kBf16>(v[u]);
+                else fA += vec_sum_t<kBf16>(v[u]);
             }
         }
         if constexpr (kMma) {
@@ -63,7 +63,7 @@ __device__ __forceinline__ double seg_reduce(const uint4* __restrict__ xb, int64
     return acc;
 }
 
-template <bool kMma, bool kBatched, int U, int WARPS>
+template <bool kMma, bool kBf16, bool kBatched, int U, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 4)
 reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restrict__ offsets,
                         size_t S, size_t L, float* __restrict__ out, DevWorkspace ws) {
@@ -102,7 +102,7 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
         const bool last = (j + 1 == batch_end);
         unsigned long long gn = 0;
         if (last) gn = grab(j);  // next batch start, in flight during this segment
-        const double acc = seg_reduce<kMma, U>(xb, s + shift, e + shift, lane);
+        const double acc = seg_reduce<kMma, kBf16, U>(xb, s + shift, e + shift, lane);
         unsigned long long jn;
         if (last) {
             gn = __shfl_sync(0xffffffffu, gn, 0);
@@ -133,7 +133,19 @@ constexpr int kSegWarps = 8;
 constexpr int kSegUnroll = 8;
 constexpr int kSegCtasPerSm = 4;  // resident CTAs per SM at <= 64 registers (launch bounds)
 
-cudaError_t launch_reduce_segmented(bool mma, bool batched, const uint16_t* x,
+template <bool kMma, bool kBf16>
+static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, const uint16_t* x,
+                         const int64_t* offsets, size_t S, size_t L, float* out,
+                         const DevWorkspace& ws, cudaStream_t stream) {
+    if (batched)
+        reduce_segmented_kernel<kMma, kBf16, true, kSegUnroll, kSegWarps>
+            <<<grid, block, 0, stream>>>(x, offsets, S, L, out, ws);
+    else
+        reduce_segmented_kernel<kMma, kBf16, false, kSegUnroll, kSegWarps>
+            <<<grid, block, 0, stream>>>(x, offsets, S, L, out, ws);
+}
+
+cudaError_t launch_reduce_segmented(bool mma, bool bf16, bool batched, const uint16_t* x,
                                     const int64_t* offsets, size_t num_segments,
                                     size_t segment_len, float* out, const DevWorkspace& ws,
                                     const LaunchCfg& cfg, cudaStream_t stream) {
@@ -143,19 +155,11 @@ cudaError_t launch_reduce_segmented(bool mma, bool batched, const uint16_t* x,
     if (g < 1) g = 1;
     const dim3 grid((unsigned)g), block(kSegWarps * 32);
     if (mma) {
-        if (batched)
-            reduce_segmented_kernel<true, true, kSegUnroll, kSegWarps>
-                <<<grid, block, 0, stream>>>(x, offsets, num_segments, segment_len, out, ws);
-        else
-            reduce_segmented_kernel<true, false, kSegUnroll, kSegWarps>
-                <<<grid, block, 0, stream>>>(x, offsets, num_segments, segment_len, out, ws);
+        if (bf16) launch_seg_t<true, true>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream);
+        else launch_seg_t<true, false>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream);
     } else {
-        if (batched)
-            reduce_segmented_kernel<false, true, kSegUnroll, kSegWarps>
-                <<<grid, block, 0, stream>>>(x, offsets, num_segments, segment_len, out, ws);
-        else
-            reduce_segmented_kernel<false, false, kSegUnroll, kSegWarps>
-                <<<grid, block, 0, stream>>>(x, offsets, num_segments, segment_len, out, ws);
+        if (bf16) launch_seg_t<false, true>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream);
+        else launch_seg_t<false, false>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream);
     }
     return cudaGetLastError();
 }

@@ -106,6 +106,9 @@ struct Tc05Params {
     int prefetch;          // L2 prefetch distance in chunks (0 = off)
     int split;             // bulk copies per stage
     int interleave;        // 0: CTA b owns a contiguous run of chunks; 1: chunks b, b+G, b+2G, ...
+    uint32_t idesc;        // instruction descriptor (kind::f16 with F16 or BF16 operands)
+    uint32_t one_bits;     // 1.0 in the input type (the all-ones B)
+    int bf16;              // inputs are bfloat16 (ragged mma.sync path)
 };
 
 // Accumulator schedule: MMA number j of this CTA (j = 0, 1, ...) goes to
@@ -147,7 +150,7 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
     const int per_round = prm.slots * prm.chain;
     const long long total_mma = (long long)nchunks * kmma;
 
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) ones[i] = 0x3C00;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) ones[i] = (uint16_t)prm.one_bits;
     sm100::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -218,7 +221,7 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
                     }
                     const uint32_t d = tmem + (uint32_t)buf * buf_cols +
                                        ((uint32_t)pos & last_slot) * kSlotCols;
-                    sm100::mma_f16_ss(d, adesc, bdesc, kIdesc, pos >= prm.slots ? 1u : 0u);
+                    sm100::mma_f16_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
                     --left;
                     if (++pos == per_round || left == 0) {
                         sm100::mma_commit(&tfull[buf]);
@@ -276,18 +279,14 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
             const int tail = (int)(rem - Tr * kTileElems);
             float c[4] = {0.f, 0.f, 0.f, 0.f};
             const uint4* base = reinterpret_cast<const uint4*>(xr) + lane;
-            for (size_t t = e; t < Tr; t += 4) {
-                mma_rowsum(c, ldg_stream(base + t * 32));
+            auto tile = [&](const uint4& v) {
+                if (prm.bf16) mma_rowsum_bf16(c, v);
+                else mma_rowsum(c, v);
                 flush_rows(c, acc, lane);
-            }
-            if (e == 0 && head) {
-                mma_rowsum(c, load_ragged(x, (int)head, lane));
-                flush_rows(c, acc, lane);
-            }
-            if (e == 1 && tail) {
-                mma_rowsum(c, load_ragged(xr + Tr * kTileElems, tail, lane));
-                flush_rows(c, acc, lane);
-            }
+            };
+            for (size_t t = e; t < Tr; t += 4) tile(ldg_stream(base + t * 32));
+            if (e == 0 && head) tile(load_ragged(x, (int)head, lane));
+            if (e == 1 && tail) tile(load_ragged(xr + Tr * kTileElems, tail, lane));
         }
     }
     sm100::tc_fence_before();
@@ -318,10 +317,13 @@ int tcgen05_grid(size_t n, const LaunchCfg& cfg) {
     return g < 1 ? 1 : (int)g;
 }
 
-cudaError_t launch_reduce_tcgen05(const uint16_t* x, size_t n, float* out_f32, double* out_f64,
-                                  const DevWorkspace& ws, const LaunchCfg& cfg,
+cudaError_t launch_reduce_tcgen05(bool bf16, const uint16_t* x, size_t n, float* out_f32,
+                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                   cudaStream_t stream) {
     Tc05Params prm;
+    prm.bf16 = bf16 ? 1 : 0;
+    prm.idesc = kIdesc | (bf16 ? ((1u << 7) | (1u << 10)) : 0u);  // a_format = b_format = BF16
+    prm.one_bits = bf16 ? 0x3F80u : 0x3C00u;
     prm.stages = cfg.tc05_stages;
     prm.stage_bytes = (uint32_t)cfg.tc05_stage_kb * 1024u;
     prm.slots = cfg.tc05_slots;
