@@ -165,6 +165,8 @@ def main():
     ap.add_argument("--algo", default="default",
                     choices=["default", "mma_sync", "tcgen05", "shuffle", "exact"])
     ap.add_argument("--workload", default="c3", choices=["c3", "c5"])
+    ap.add_argument("--dtype", default="f16", choices=["f16", "bf16"],
+                    help="input element type (bf16 = NEXT-4; c3 workload, non-exact algos)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n-per-rank", type=int, default=N_PER_RANK)
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -222,6 +224,8 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(dev)
     exact = args.algo == "exact"
+    if args.dtype == "bf16" and (exact or args.workload != "c3"):
+        raise SystemExit("--dtype bf16 supports the c3 workload with the MMA / shuffle paths")
     algo = tcr.ALGOS["default" if exact else args.algo]
     peak, peak_src = _peaks()
 
@@ -229,7 +233,8 @@ def main():
     if args.workload == "c3":
         n = args.n_per_rank
         seed = gen.SEED_C3 if world == 1 else gen.SEED_C4
-        x = gen.generate_tensor(seed, rank * n, n, gen.UNIFORM_PM1, device=dev)
+        x = gen.generate_tensor(seed, rank * n, n, gen.UNIFORM_PM1, device=dev,
+                                bf16=args.dtype == "bf16")
         bytes_per_step = 2 * n
         elems_per_step = n
         workload = (f"c3: sum of n=2^{n.bit_length() - 1} fp16 uniform[-1,1] per GPU"
@@ -261,9 +266,9 @@ def main():
                 tcr.tcr_reduce_sum_exact(x, acc=acc6, out_f32=out32 if world == 1 else None,
                                          stream=stream)
             elif world == 1:
-                tcr.tcr_reduce_sum_algo(x, out_f32=out32, algo=algo, stream=stream)
+                tcr.tcr_reduce_sum_ex(x, out_f32=out32, algo=algo, stream=stream)
             else:
-                tcr.tcr_reduce_sum_algo(x, out_f64=out64, algo=algo, stream=stream)
+                tcr.tcr_reduce_sum_ex(x, out_f64=out64, algo=algo, stream=stream)
             if ev_k1 is not None:
                 ev_k1.record(stream)
             if args.workload == "c3" and world > 1:
@@ -355,7 +360,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (splitmix64-seeded, generated on the device)",
             "config": {"workload": workload, "algo": algo_name, "n_per_rank": n,
                        "knobs": {k: tcr.tcr_get_config(v) for k, v in (

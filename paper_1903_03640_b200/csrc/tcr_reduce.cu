@@ -12,48 +12,11 @@
 //                   in index order -- replaces the paper's relaunch per level
 //                   ("synchronization among blocks is not possible ... unless
 //                   the kernel is terminated").
+#include "tcr_complete.cuh"
 #include "tcr_device.cuh"
 #include "tcr_internal.h"
 
 namespace tcr {
-
-// Levels 2-4.  Every thread of the CTA calls this with its lane value; the
-// total lands in out_f32 / out_f64 (device pointers, either may be null).
-template <bool kMma, int WARPS>
-__device__ __forceinline__ void complete_block_and_grid(double lane_val, float* out_f32,
-                                                        double* out_f64, const DevWorkspace& ws) {
-    __shared__ double s_warp[WARPS];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double wt = warp_collapse<kMma>(lane_val);
-    if (lane == 0) s_warp[warp] = wt;
-    __syncthreads();
-    if (warp != 0) return;
-    const double bt = warp_collapse<kMma>(lane < WARPS ? s_warp[lane] : 0.0);
-    if (gridDim.x == 1) {
-        if (lane == 0) {
-            if (out_f32) *out_f32 = (float)bt;
-            if (out_f64) *out_f64 = bt;
-        }
-        return;
-    }
-    unsigned last = 0;
-    if (lane == 0) {
-        ws.partials[blockIdx.x] = bt;
-        __threadfence();  // release the partial before taking a ticket
-        last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) return;
-    __threadfence();  // acquire: every other CTA's partial is visible
-    double v = 0.0;
-    for (int i = lane; i < (int)gridDim.x; i += 32) v += __ldcg(ws.partials + i);  // fixed order
-    const double tot = warp_collapse<kMma>(v);
-    if (lane == 0) {
-        if (out_f32) *out_f32 = (float)tot;
-        if (out_f64) *out_f64 = tot;
-        *ws.ticket = 0u;  // self-reset for the next launch on this stream
-    }
-}
 
 template <bool kMma, bool kBf16>
 __device__ __forceinline__ void consume(const uint4& v, float (&c)[4], float& f) {

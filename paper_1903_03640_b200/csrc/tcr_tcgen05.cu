@@ -25,6 +25,7 @@
 #include <map>
 #include <mutex>
 
+#include "tcr_complete.cuh"
 #include "tcr_device.cuh"
 #include "tcr_internal.h"
 #include "tcr_sm100.cuh"
@@ -60,43 +61,6 @@ constexpr uint32_t kHeaderBytes = 1024;              // ones tile + barriers + T
 constexpr uint32_t kIdesc = sm100::idesc_f16_f32(128, 16);
 
 }  // namespace
-
-// Levels 2-4 (identical to the streaming kernel's, instantiated for 6 warps).
-template <int WARPS>
-__device__ __forceinline__ void tc_complete(double lane_val, float* out_f32, double* out_f64,
-                                            const DevWorkspace& ws) {
-    __shared__ double s_warp[WARPS];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double wt = warp_collapse_mma(lane_val);
-    if (lane == 0) s_warp[warp] = wt;
-    __syncthreads();
-    if (warp != 0) return;
-    const double bt = warp_collapse_mma(lane < WARPS ? s_warp[lane] : 0.0);
-    if (gridDim.x == 1) {
-        if (lane == 0) {
-            if (out_f32) *out_f32 = (float)bt;
-            if (out_f64) *out_f64 = bt;
-        }
-        return;
-    }
-    unsigned last = 0;
-    if (lane == 0) {
-        ws.partials[blockIdx.x] = bt;
-        __threadfence();
-        last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) return;
-    __threadfence();
-    double v = 0.0;
-    for (int i = lane; i < (int)gridDim.x; i += 32) v += __ldcg(ws.partials + i);
-    const double tot = warp_collapse_mma(v);
-    if (lane == 0) {
-        if (out_f32) *out_f32 = (float)tot;
-        if (out_f64) *out_f64 = tot;
-        *ws.ticket = 0u;
-    }
-}
 
 struct Tc05Params {
     int stages;            // SMEM ring stages
@@ -292,7 +256,7 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
     sm100::tc_fence_before();
     __syncthreads();
     if (warp == 1) sm100::tmem_dealloc(tmem, tmem_cols);
-    tc_complete<kTcWarps>(acc, out_f32, out_f64, ws);
+    complete_block_and_grid<true, kTcWarps>(acc, out_f32, out_f64, ws);
 }
 
 // CTAs of this kernel that can be co-resident on one SM for `cfg`: the
