@@ -16,108 +16,147 @@ constexpr unsigned long long kBatchSeg = 8;  // segments per scheduler atomic (g
 // Reduce elements [s, e) of the 16-byte-aligned array xb (element indices
 // relative to xb).  Returns the lane's fp64 share; the sum over lanes is the
 // segment total.
-template <bool kMma, bool kBf16, int U>
-__device__ __forceinline__ double seg_reduce(const uint4* __restrict__ xb, int64_t s, int64_t e,
-                                             int lane) {
-    double acc = 0.0;
-    if (e <= s) return acc;
-    float cA[4] = {0.f, 0.f, 0.f, 0.f}, cB[4] = {0.f, 0.f, 0.f, 0.f};
-    float fA = 0.f, fB = 0.f;
-    const int64_t v0 = s >> 3, v1 = (e + 7) >> 3;  // vectors touching [s, e)
-    const int64_t f0 = (s + 7) >> 3, f1 = e >> 3;  // vectors entirely inside
-    // Every group of U tiles (32*U vectors) is one memory round trip: interior
-    // groups load unmasked; the first and last groups load only the vectors
-    // that touch the segment (predicated) and zero the halves outside it.
-    for (int64_t vb = v0; vb < v1; vb += 32 * U) {
-        uint4 v[U];
-        if (vb >= f0 && vb + 32 * U <= f1) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = ldg_stream(xb + vb + u * 32 + lane);
-        } else {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t vi = vb + u * 32 + lane;
-                v[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (vi < v1) v[u] = mask_vec(ldg_stream(xb + vi), vi * 8, s, e);
-            }
-        }
-        __syncwarp();  // scheduling fence: all U loads issue before the first consumer
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if constexpr (kMma) {
-                if (u & 1) mma_rowsum_t<kBf16>(cB, v[u]);
-                else mma_rowsum_t<kBf16>(cA, v[u]);
-            } else {
-                if (u & 1) fB += vec_sum_t<kBf16>(v[u]);
-                else fA += vec_sum_t<kBf16>(v[u]);
-            }
-        }
-        if constexpr (kMma) {
-            flush_rows(cA, acc, lane);
-            flush_rows(cB, acc, lane);
-        } else {
-            acc += (double)fA + (double)fB;
-            fA = fB = 0.f;
-        }
+// A warp takes a batch of consecutive segments (one global atomic per batch,
+// guided self-scheduling) and streams the CONTIGUOUS union of the batch in
+// groups of U tiles (one memory round trip each, all loads issued before the
+// first MMA).  Each 256-element tile is attributed to the segments it
+// overlaps, in order: a tile inside the current segment is one MMA
+// (D = A x 1, C = 0 -- the paper's per-group formulation); a tile
+// crossing a boundary gets one zero-masked MMA per overlapped segment (the
+// paper's zero padding, reading G5); when a segment ends its row sums are
+// collapsed (D' = 1 x D, three DMMAs) and written to out[j].  Long segments
+// therefore stream at full width and many short segments share a round trip.
+// The next batch's index and offsets are fetched during the current batch.
+template <bool kMma, bool kBf16>
+__device__ __forceinline__ void seg_piece(const uint4& v, double& acc, int lane) {
+    if constexpr (kMma) {
+        float c[4] = {0.f, 0.f, 0.f, 0.f};
+        mma_rowsum_t<kBf16>(c, v);
+        flush_rows(c, acc, lane);
+    } else {
+        acc += (double)vec_sum_t<kBf16>(v);
     }
-    return acc;
 }
 
 template <bool kMma, bool kBf16, bool kBatched, int U, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 4)
 reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restrict__ offsets,
-                        size_t S, size_t L, float* __restrict__ out, DevWorkspace ws) {
+                        size_t S, size_t L, int batch, float* __restrict__ out, DevWorkspace ws) {
     const int lane = threadIdx.x & 31;
     const uintptr_t addr = (uintptr_t)x;
     const int64_t shift = (int64_t)((addr & 15u) >> 1);
     const uint4* xb = reinterpret_cast<const uint4*>(addr & ~(uintptr_t)15u);
     const unsigned total_warps = gridDim.x * WARPS;
-
-    // Guided self-scheduling: a warp takes a batch of kBatchSeg consecutive
-    // segments per atomic while plenty remain, single segments near the end
-    // (one global atomic per segment saturates the L2 atomic unit at ~4 ns
-    // per segment -- the whole C5 kernel time).
-    const unsigned long long tail_zone = 2ull * total_warps * kBatchSeg;
-    auto grab = [&](unsigned long long hint) -> unsigned long long {
-        unsigned long long got = 0;
-        const unsigned long long b = (S > hint + tail_zone) ? kBatchSeg : 1ull;
-        if (lane == 0) got = atomicAdd(ws.seg_next, b) | (b << 56);
-        return got;  // start index in bits 0..55, batch size in 56..63 (lane 0)
-    };
-    auto bounds = [&](unsigned long long jj, int64_t& ss, int64_t& ee) {
-        if constexpr (kBatched) {
-            ss = (int64_t)(jj * L);
-            ee = ss + (int64_t)L;
-        } else {
-            ss = __ldg(offsets + jj);
-            ee = __ldg(offsets + jj + 1);
-        }
-    };
+    const unsigned long long tail_zone = 2ull * total_warps * (unsigned long long)batch;
     const unsigned long long kIdx = (1ull << 56) - 1;
-    unsigned long long g = __shfl_sync(0xffffffffu, grab(0), 0);
-    unsigned long long j = g & kIdx, batch_end = j + (g >> 56);
-    int64_t s = 0, e = 0;
-    if (j < S) bounds(j, s, e);
-    while (j < S) {
-        const bool last = (j + 1 == batch_end);
-        unsigned long long gn = 0;
-        if (last) gn = grab(j);  // next batch start, in flight during this segment
-        const double acc = seg_reduce<kMma, kBf16, U>(xb, s + shift, e + shift, lane);
-        unsigned long long jn;
-        if (last) {
-            gn = __shfl_sync(0xffffffffu, gn, 0);
-            jn = gn & kIdx;
-            batch_end = jn + (gn >> 56);
+
+    auto grab = [&](unsigned long long hint) -> unsigned long long {  // lane 0 holds the result
+        unsigned long long got = 0;
+        const unsigned long long b = (S > hint + tail_zone) ? (unsigned long long)batch : 1ull;
+        if (lane == 0) got = atomicAdd(ws.seg_next, b) | (b << 56);
+        return got;
+    };
+    // CSR: lane k <= nb holds offsets[jb + k] + shift (one load per lane per batch)
+    auto load_offs = [&](unsigned long long jb, int nb) -> int64_t {
+        if constexpr (kBatched) {
+            return 0;
         } else {
-            jn = j + 1;
+            return (lane <= nb && jb + lane <= S) ? __ldg(offsets + jb + lane) + shift : 0;
         }
-        int64_t sn = 0, en = 0;  // next bounds: their latency overlaps the collapse
-        if (jn < S) bounds(jn, sn, en);
-        const double tot = warp_collapse<kMma>(acc);
-        if (lane == 0) out[j] = (float)tot;
-        j = jn;
-        s = sn;
-        e = en;
+    };
+    unsigned long long g = __shfl_sync(0xffffffffu, grab(0), 0);
+    unsigned long long jb = g & kIdx;
+    int nb = (int)(g >> 56);
+    unsigned long long pend = grab(jb);
+    int64_t offl = load_offs(jb, nb);
+
+    while (jb < S) {
+        if ((unsigned long long)nb > S - jb) nb = (int)(S - jb);
+        auto off = [&](int k) -> int64_t {  // start of segment jb + k (k <= nb), element units
+            if constexpr (kBatched) return (int64_t)((jb + (unsigned long long)k) * L) + shift;
+            else return __shfl_sync(0xffffffffu, offl, k);
+        };
+        // the next batch: index now, offsets in flight during this batch
+        const unsigned long long p = __shfl_sync(0xffffffffu, pend, 0);
+        const unsigned long long jb2 = p & kIdx;
+        const int nb2 = (int)(p >> 56);
+        pend = grab(jb2);
+        const int64_t offl2 = (jb2 < S) ? load_offs(jb2, nb2) : 0;
+
+        const int64_t r0 = off(0), r1 = off(nb);
+        // Tiles sit on absolute 256-element boundaries (relative to xb), so the
+        // arithmetic of a segment never depends on which batch / warp reduced
+        // it (bitwise determinism under dynamic scheduling).
+        const int64_t Vlo = r0 >> 3, V1 = (r1 + 7) >> 3;
+        const int64_t V0 = Vlo & ~(int64_t)31;
+        int cs = 0;
+        int64_t sb = r0, se = off(1);
+        double acc = 0.0;
+        for (int64_t vb = V0; vb < V1; vb += 32 * U) {
+            uint4 v[U];
+            const int64_t f0 = (r0 + 7) >> 3, f1 = r1 >> 3;
+            if (vb >= f0 && vb + 32 * U <= f1) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = ldg_stream(xb + vb + u * 32 + lane);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t vi = vb + u * 32 + lane;
+                    v[u] = make_uint4(0u, 0u, 0u, 0u);
+                    if (vi >= Vlo && vi < V1) v[u] = mask_vec(ldg_stream(xb + vi), vi * 8, r0, r1);
+                }
+            }
+            __syncwarp();  // scheduling fence: all U loads issue before the first consumer
+            const int64_t g0 = vb * 8, g1 = g0 + (int64_t)U * kTileElems;
+            if (cs < nb && sb <= g0 && se > g1) {
+                // the whole group lies inside segment cs (the common case for long
+                // segments): U independent tiles, no per-tile control flow; each
+                // tile is its own MMA with C = 0, flushed in tile order
+                if constexpr (kMma) {
+                    float c[U][4];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        c[u][0] = c[u][1] = c[u][2] = c[u][3] = 0.f;
+                        mma_rowsum_t<kBf16>(c[u], v[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) flush_rows(c[u], acc, lane);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) acc += (double)vec_sum_t<kBf16>(v[u]);
+                }
+                continue;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t t0 = (vb + u * 32) * 8, t1 = t0 + kTileElems;  // tile elements
+                if (t0 >= r1) break;
+                while (cs < nb) {
+                    if (sb >= t1) break;  // current segment starts after this tile
+                    if (sb <= t0 && se >= t1) {  // tile entirely inside segment cs
+                        seg_piece<kMma, kBf16>(v[u], acc, lane);
+                    } else if (se > sb && se > t0) {  // the part of the tile inside [sb, se)
+                        seg_piece<kMma, kBf16>(mask_vec(v[u], (vb + u * 32 + lane) * 8, sb, se), acc,
+                                               lane);
+                    }
+                    if (se > t1) break;  // segment continues in the next tile
+                    const double tot = warp_collapse<kMma>(acc);  // segment cs ends in this tile
+                    if (lane == 0) out[jb + cs] = (float)tot;
+                    acc = 0.0;
+                    ++cs;
+                    sb = se;
+                    if (cs < nb) se = off(cs + 1);
+                }
+            }
+        }
+        for (; cs < nb; ++cs) {  // trailing (empty) segments of the batch
+            const double tot = warp_collapse<kMma>(acc);
+            if (lane == 0) out[jb + cs] = (float)tot;
+            acc = 0.0;
+        }
+        jb = jb2;
+        nb = nb2;
+        offl = offl2;
     }
     if (lane == 0) {
         __threadfence();
@@ -130,19 +169,24 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
 }
 
 constexpr int kSegWarps = 8;
-constexpr int kSegUnroll = 8;
+constexpr int kSegUnroll = 8;  // tiles per group (one round trip)
 constexpr int kSegCtasPerSm = 4;  // resident CTAs per SM at <= 64 registers (launch bounds)
 
 template <bool kMma, bool kBf16>
 static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, const uint16_t* x,
                          const int64_t* offsets, size_t S, size_t L, float* out,
                          const DevWorkspace& ws, cudaStream_t stream) {
-    if (batched)
+    if (batched) {
+        // ~16K elements per batch for short fixed lengths, at least 8 segments
+        size_t b = L ? ((size_t)16384 / L) : 255;
+        if (b < kBatchSeg) b = kBatchSeg;
+        if (b > 255) b = 255;
         reduce_segmented_kernel<kMma, kBf16, true, kSegUnroll, kSegWarps>
-            <<<grid, block, 0, stream>>>(x, offsets, S, L, out, ws);
-    else
+            <<<grid, block, 0, stream>>>(x, offsets, S, L, (int)b, out, ws);
+    } else {
         reduce_segmented_kernel<kMma, kBf16, false, kSegUnroll, kSegWarps>
-            <<<grid, block, 0, stream>>>(x, offsets, S, L, out, ws);
+            <<<grid, block, 0, stream>>>(x, offsets, S, L, (int)kBatchSeg, out, ws);
+    }
 }
 
 cudaError_t launch_reduce_segmented(bool mma, bool bf16, bool batched, const uint16_t* x,
