@@ -168,6 +168,50 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
     }
 }
 
+// Fixed-length rows of T whole tiles (L = 256*T, T in {1, 2, 4, 8}, x 16-byte
+// aligned): every group of 8 tiles holds 8/T complete rows, so a warp issues
+// its 8 loads, 8 independent MMAs (C = 0), folds them per row and collapses
+// the 8/T rows with no data-dependent control flow.  Rows are dealt to warps
+// statically (all rows cost the same: no scheduler, no atomics).
+template <bool kMma, bool kBf16, int T, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 4)
+reduce_rows_kernel(const uint16_t* __restrict__ x, size_t S, float* __restrict__ out) {
+    constexpr int R = 8 / T;  // rows per group
+    const int lane = threadIdx.x & 31;
+    const uint4* xv = reinterpret_cast<const uint4*>(x) + lane;
+    const size_t groups = (S + R - 1) / R;
+    const size_t W = (size_t)gridDim.x * WARPS;
+    for (size_t gi = (size_t)blockIdx.x * WARPS + (threadIdx.x >> 5); gi < groups; gi += W) {
+        const size_t row0 = gi * R;
+        const int rows = (int)((S - row0) < (size_t)R ? (S - row0) : (size_t)R);
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            v[u] = make_uint4(0u, 0u, 0u, 0u);
+            if (u / T < rows) v[u] = ldg_stream(xv + (row0 * T + u) * 32);
+        }
+        __syncwarp();  // scheduling fence: all loads issue before the first consumer
+        double acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if constexpr (kMma) {
+                float c[4] = {0.f, 0.f, 0.f, 0.f};
+                mma_rowsum_t<kBf16>(c, v[u]);
+                flush_rows(c, acc[u / T], lane);
+            } else {
+                acc[u / T] += (double)vec_sum_t<kBf16>(v[u]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double tot = warp_collapse<kMma>(acc[r]);
+            if (lane == 0 && r < rows) out[row0 + r] = (float)tot;
+        }
+    }
+}
+
 constexpr int kSegWarps = 8;
 constexpr int kSegUnroll = 8;  // tiles per group (one round trip)
 constexpr int kSegCtasPerSm = 4;  // resident CTAs per SM at <= 64 registers (launch bounds)
@@ -175,7 +219,23 @@ constexpr int kSegCtasPerSm = 4;  // resident CTAs per SM at <= 64 registers (la
 template <bool kMma, bool kBf16>
 static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, const uint16_t* x,
                          const int64_t* offsets, size_t S, size_t L, float* out,
-                         const DevWorkspace& ws, cudaStream_t stream) {
+                         const DevWorkspace& ws, cudaStream_t stream, int sms) {
+    if (batched && ((uintptr_t)x & 15u) == 0 &&
+        (L == 256 || L == 512 || L == 1024 || L == 2048)) {
+        const size_t groups = (S + 8 * 256 / L - 1) / (8 * 256 / L);
+        size_t g = (groups + kSegWarps - 1) / kSegWarps;
+        const size_t gmax = (size_t)sms * kSegCtasPerSm;
+        if (g > gmax) g = gmax;
+        if (g < 1) g = 1;
+        const dim3 rgrid((unsigned)g);
+        switch (L) {
+            case 256: reduce_rows_kernel<kMma, kBf16, 1, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
+            case 512: reduce_rows_kernel<kMma, kBf16, 2, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
+            case 1024: reduce_rows_kernel<kMma, kBf16, 4, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
+            default: reduce_rows_kernel<kMma, kBf16, 8, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
+        }
+        return;
+    }
     if (batched) {
         // ~16K elements per batch for short fixed lengths, at least 8 segments
         size_t b = L ? ((size_t)16384 / L) : 255;
@@ -199,11 +259,11 @@ cudaError_t launch_reduce_segmented(bool mma, bool bf16, bool batched, const uin
     if (g < 1) g = 1;
     const dim3 grid((unsigned)g), block(kSegWarps * 32);
     if (mma) {
-        if (bf16) launch_seg_t<true, true>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream);
-        else launch_seg_t<true, false>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream);
+        if (bf16) launch_seg_t<true, true>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream, cfg.sms);
+        else launch_seg_t<true, false>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream, cfg.sms);
     } else {
-        if (bf16) launch_seg_t<false, true>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream);
-        else launch_seg_t<false, false>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream);
+        if (bf16) launch_seg_t<false, true>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream, cfg.sms);
+        else launch_seg_t<false, false>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream, cfg.sms);
     }
     return cudaGetLastError();
 }

@@ -98,16 +98,20 @@ def test_loguniform_mix(tcr, mma):
 def test_batched(tcr, mma):
     import torch
 
-    for L, S in ((1, 1000), (7, 333), (256, 4096), (1000, 777), (4096, 1024), (65536, 17)):
+    # aligned x with L in {256, 512, 1024, 2048} takes the whole-tile rows kernel
+    cases = ((1, 1000), (7, 333), (256, 4096), (256, 4093), (512, 999), (1000, 777),
+             (1024, 1025), (2048, 33), (4096, 1024), (65536, 17))
+    for L, S in cases:
         bits = gen.generate(L, 0, L * S, gen.UNIFORM_PM1)
-        x = _dev(bits, 2)
-        out = torch.empty(S, dtype=torch.float32, device="cuda")
-        f = tcr.tcr_reduce_sum_batched if mma else tcr.tcr_reduce_sum_batched_shuffle
-        f(x, L, out)
-        torch.cuda.synchronize()
         ref = oracle.exact_segment_sums_fp16(bits, np.arange(S + 1, dtype=np.int64) * L)
-        g = out.cpu().numpy()
-        assert all(oracle.within_tolerance(float(g[j]), ref[j]) for j in range(S)), (L, S)
+        for xoff in (0, 2):
+            x = _dev(bits, xoff)
+            out = torch.full((S,), float("nan"), dtype=torch.float32, device="cuda")
+            f = tcr.tcr_reduce_sum_batched if mma else tcr.tcr_reduce_sum_batched_shuffle
+            f(x, L, out)
+            torch.cuda.synchronize()
+            g = out.cpu().numpy()
+            assert all(oracle.within_tolerance(float(g[j]), ref[j]) for j in range(S)), (L, S, xoff)
 
 
 def test_empty_and_zero_segments(tcr):
