@@ -85,6 +85,9 @@ def _load():
         lib.oracle_exact_bins_bf16.argtypes = [
             ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         lib.oracle_exact_bins_bf16.restype = ctypes.c_int
+        lib.oracle_exact_sum_fp8.argtypes = [
+            ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(_Result)]
+        lib.oracle_exact_sum_fp8.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -226,6 +229,33 @@ def exact_sum_bf16(x) -> ExactSum:
     return ExactSum(T, A, int(counts[0]), int(counts[1]), int(counts[2]), unit_exp=-133)
 
 
+FP8_E4M3, FP8_E5M2 = 0, 1
+_FP8_UNIT_EXP = {FP8_E4M3: -9, FP8_E5M2: -16}
+
+
+def exact_sum_fp8(x, fmt: int) -> ExactSum:
+    """Exact R(X) of fp8 bit patterns (uint8): fmt 0 = E4M3 (units 2^-9),
+    fmt 1 = E5M2 (units 2^-16) -- NEXT-4.  Plain loop in ``exact_sum.c``."""
+    bits = np.ascontiguousarray(np.asarray(x, dtype=np.uint8).reshape(-1))
+    r = _Result()
+    _load().oracle_exact_sum_fp8(bits.ctypes.data, bits.size, int(fmt), ctypes.byref(r))
+    es = _from_struct(r)
+    return ExactSum(es.T, es.A, es.n_nan, es.n_pinf, es.n_ninf, unit_exp=_FP8_UNIT_EXP[fmt])
+
+
+def fp8_value(h: int, fmt: int) -> Fraction:
+    """Exact value of one finite fp8 bit pattern, from the OCP FP8 definition."""
+    eb, mb, bias = (4, 3, 7) if fmt == FP8_E4M3 else (5, 2, 15)
+    s, e, f = (h >> 7) & 1, (h >> mb) & ((1 << eb) - 1), h & ((1 << mb) - 1)
+    if (fmt == FP8_E4M3 and e == 15 and f == 7) or (fmt == FP8_E5M2 and e == 31):
+        raise ValueError("non-finite")
+    if e == 0:
+        v = Fraction(f, 1 << mb) * Fraction(2) ** (1 - bias)
+    else:
+        v = (1 + Fraction(f, 1 << mb)) * Fraction(2) ** (e - bias)
+    return -v if s else v
+
+
 def bf16_value(h: int) -> Fraction:
     """Exact value of one finite bfloat16 bit pattern, from the definition."""
     s, e, f = (h >> 15) & 1, (h >> 7) & 0xFF, h & 0x7F
@@ -305,6 +335,6 @@ def error_units(g: float, es: ExactSum) -> Fraction:
 
 __all__ = [
     "ExactSum", "UNIT", "build", "exact_sum_fp16", "exact_segment_sums_fp16", "exact_sum_bf16",
-    "bf16_value",
+    "bf16_value", "exact_sum_fp8", "fp8_value", "FP8_E4M3", "FP8_E5M2",
     "exact_sum_fraction", "round_to_f32", "within_tolerance", "error_units",
 ]

@@ -146,3 +146,45 @@ int oracle_exact_bins_bf16(const uint16_t *x, size_t n, int64_t *bins, uint64_t 
     }
     return 0;
 }
+
+/*
+ * fp8 (NEXT-4): OCP FP8 formats, exact sum as a signed 128-bit integer.
+ *   fmt 0 = E4M3 (E4M3FN): s.eeee.mmm, bias 7, no infinities, NaN = s.1111.111;
+ *           value = (8+f) * 2^(e-10) for e >= 1, f * 2^-9 for e == 0
+ *           -> units of 2^-9: u = (e == 0 ? f : (8+f) << (e-1)).
+ *   fmt 1 = E5M2: s.eeeee.mm, bias 15, e == 31: f == 0 -> inf, else NaN;
+ *           value = (4+f) * 2^(e-17) for e >= 1, f * 2^-16 for e == 0
+ *           -> units of 2^-16: u = (e == 0 ? f : (4+f) << (e-1)).
+ * Writes the same record as the binary16 oracle (T, A in those units).
+ */
+int oracle_exact_sum_fp8(const uint8_t *x, size_t n, int fmt, oracle_sum_result *r) {
+    const int ebits = fmt == 0 ? 4 : 5, mbits = fmt == 0 ? 3 : 2;
+    const unsigned emax = (1u << ebits) - 1u, mmask = (1u << mbits) - 1u;
+    i128 t = 0;
+    u128 a = 0;
+    uint64_t n_nan = 0, n_pinf = 0, n_ninf = 0;
+    for (size_t i = 0; i < n; ++i) {
+        const uint8_t h = x[i];
+        const unsigned s = (h >> 7) & 1u;
+        const unsigned e = (h >> mbits) & emax;
+        const unsigned f = h & mmask;
+        if (fmt == 0 && e == emax && f == mmask) { ++n_nan; continue; }
+        if (fmt == 1 && e == emax) {
+            if (f) ++n_nan;
+            else if (s) ++n_ninf;
+            else ++n_pinf;
+            continue;
+        }
+        const i128 u = e == 0 ? (i128)f : (i128)((1u << mbits) + f) << (e - 1);
+        t += s ? -u : u;
+        a += (u128)u;
+    }
+    r->t_lo = (uint64_t)(u128)t;
+    r->t_hi = (int64_t)(t >> 64);
+    r->a_lo = (uint64_t)a;
+    r->a_hi = (uint64_t)(a >> 64);
+    r->n_nan = n_nan;
+    r->n_pinf = n_pinf;
+    r->n_ninf = n_ninf;
+    return 0;
+}

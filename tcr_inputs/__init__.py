@@ -152,6 +152,70 @@ def generate_bf16(seed: int, start: int, count: int, dist: int = UNIFORM_PM1) ->
     raise ValueError(f"unknown dist {dist}")
 
 
+# ---------------------------------------------------------------------------
+# fp8 streams (NEXT-4): fmt 0 = E4M3 (OCP E4M3FN), 1 = E5M2.  Same (seed,
+# index) hash; UNIFORM_PM1 / UNIFORM_01 / ALTERNATING: the same binary32 v as
+# above, rounded to nearest-even into the format (saturating to the largest
+# finite value); ONES: 1.0; WIDE: random finite bit patterns (sign, any
+# exponent below the all-ones one, any mantissa); SMALLINT: {-2..2}.
+# ---------------------------------------------------------------------------
+FP8_E4M3, FP8_E5M2 = 0, 1
+_FP8 = {FP8_E4M3: (3, 7, 448.0), FP8_E5M2: (2, 15, 57344.0)}  # mantissa bits, bias, max
+
+
+def f32_to_fp8_rne(v: np.ndarray, fmt: int) -> np.ndarray:
+    """Round binary32 values to fp8 bit patterns, nearest-even, saturating."""
+    mb, bias, vmax = _FP8[fmt]
+    v = np.asarray(v, dtype=np.float64)
+    a = np.abs(v)
+    # floor(log2 a) via frexp (exact): a = m * 2^k, m in [0.5, 1)
+    _, k = np.frexp(np.where(a > 0, a, 1.0))
+    e = (k - 1).astype(np.float64)
+    q = np.exp2(np.maximum(e, 1 - bias) - mb)           # quantum (power of two)
+    m = np.rint(a / q)                                  # exact division; rint = half-to-even
+    r = np.minimum(m * q, vmax)
+    # encode
+    _, k2 = np.frexp(np.where(r > 0, r, 1.0))
+    e2 = k2 - 1
+    sub = e2 < 1 - bias
+    be = np.where(sub | (r == 0), 0, e2 + bias)
+    frac = np.where(sub | (r == 0), r / np.exp2(1 - bias - mb), (r / np.exp2(e2) - 1.0) * (1 << mb))
+    bits = (np.signbit(v).astype(np.int64) << 7) | (be.astype(np.int64) << mb) | np.rint(frac).astype(np.int64)
+    return bits.astype(np.uint8)
+
+
+def generate_fp8(seed: int, start: int, count: int, dist: int = UNIFORM_PM1,
+                 fmt: int = FP8_E4M3) -> np.ndarray:
+    """fp8 bit patterns x[start .. start+count) of the (seed, dist) stream."""
+    idx = np.arange(start, start + count, dtype=np.uint64)
+    mb, bias, _ = _FP8[fmt]
+    if dist in (UNIFORM_PM1, UNIFORM_01, ALTERNATING):
+        base = idx & ~np.uint64(1) if dist == ALTERNATING else idx
+        z = splitmix64(seed, base)
+        r = (z >> np.uint64(40)).astype(np.float32)
+        v = r * np.float32(2.0 ** -24) if dist == UNIFORM_01 else \
+            r * np.float32(2.0 ** -23) - np.float32(1.0)
+        b = f32_to_fp8_rne(v, fmt)
+        if dist == ALTERNATING:
+            b = b.copy()
+            b[(idx & np.uint64(1)).astype(bool)] ^= np.uint8(0x80)
+        return b
+    if dist == ONES:
+        return np.full(count, 0x38 if fmt == FP8_E4M3 else 0x3C, dtype=np.uint8)
+    if dist == WIDE:
+        z = splitmix64(seed, idx)
+        eb = 8 - 1 - mb
+        sign = (z >> np.uint64(63)).astype(np.uint8)
+        e = ((z >> np.uint64(32)) % np.uint64((1 << eb) - 1)).astype(np.uint8)  # never all-ones
+        f = (z & np.uint64((1 << mb) - 1)).astype(np.uint8)
+        return (sign << np.uint8(7)) | (e << np.uint8(mb)) | f
+    if dist == SMALLINT:
+        z = splitmix64(seed, idx)
+        v = ((z >> np.uint64(32)) % np.uint64(5)).astype(np.float32) - np.float32(2)
+        return f32_to_fp8_rne(v, fmt)
+    raise ValueError(f"unknown dist {dist}")
+
+
 def loguniform_lengths(seed: int, num_segments: int, lo: int = 256, hi: int = 65536) -> np.ndarray:
     """Segment lengths, log-uniform integers in [lo, hi] (reading G18).
 
