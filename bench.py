@@ -165,8 +165,8 @@ def main():
     ap.add_argument("--algo", default="default",
                     choices=["default", "mma_sync", "tcgen05", "shuffle", "exact"])
     ap.add_argument("--workload", default="c3", choices=["c3", "c5"])
-    ap.add_argument("--dtype", default="f16", choices=["f16", "bf16"],
-                    help="input element type (bf16 = NEXT-4; c3 workload, non-exact algos)")
+    ap.add_argument("--dtype", default="f16", choices=["f16", "bf16", "e4m3", "e5m2"],
+                    help="input element type (bf16 / fp8 = NEXT-4; c3 workload, non-exact algos)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n-per-rank", type=int, default=N_PER_RANK)
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -224,8 +224,8 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(dev)
     exact = args.algo == "exact"
-    if args.dtype == "bf16" and (exact or args.workload != "c3"):
-        raise SystemExit("--dtype bf16 supports the c3 workload with the MMA / shuffle paths")
+    if args.dtype != "f16" and (exact or args.workload != "c3"):
+        raise SystemExit("--dtype bf16/e4m3/e5m2 supports the c3 workload with the MMA / shuffle paths")
     algo = tcr.ALGOS["default" if exact else args.algo]
     peak, peak_src = _peaks()
 
@@ -233,9 +233,13 @@ def main():
     if args.workload == "c3":
         n = args.n_per_rank
         seed = gen.SEED_C3 if world == 1 else gen.SEED_C4
-        x = gen.generate_tensor(seed, rank * n, n, gen.UNIFORM_PM1, device=dev,
-                                bf16=args.dtype == "bf16")
-        bytes_per_step = 2 * n
+        if args.dtype in ("e4m3", "e5m2"):
+            fmt8 = gen.FP8_E4M3 if args.dtype == "e4m3" else gen.FP8_E5M2
+            x = gen.generate_tensor_fp8(seed, rank * n, n, gen.UNIFORM_PM1, fmt8, device=dev)
+        else:
+            x = gen.generate_tensor(seed, rank * n, n, gen.UNIFORM_PM1, device=dev,
+                                    bf16=args.dtype == "bf16")
+        bytes_per_step = x.element_size() * n
         elems_per_step = n
         workload = (f"c3: sum of n=2^{n.bit_length() - 1} fp16 uniform[-1,1] per GPU"
                     if world == 1 else
@@ -319,9 +323,10 @@ def main():
 
     # ---------------- end to end through the public API with host buffers ----------------
     e2e = None
-    if args.workload == "c3" and args.e2e_steps > 0:
+    if args.workload == "c3" and args.e2e_steps > 0 and args.dtype == "f16":
         host = torch.empty(n, dtype=torch.int16, pin_memory=True)
-        host.copy_(x.view(torch.int16))
+        host.copy_(x.view(torch.int16) if x.element_size() == 2 else
+                   gen.generate_tensor(gen.SEED_C3, 0, n, gen.UNIFORM_PM1, device=dev).view(torch.int16))
         res_t = torch.empty(1, dtype=torch.float32, device=dev)
         hs = torch.cuda.Stream(dev)
         tcr.tcr_reduce_sum_host(host, n=n, stream=hs.cuda_stream)  # warm-up

@@ -90,8 +90,11 @@ typedef enum {
 /* Input element type for the _ex entry points (NEXT-4). */
 typedef enum {
     TCR_DTYPE_F16 = 0,  /* IEEE-754 binary16 (the north star)                */
-    TCR_DTYPE_BF16 = 1  /* bfloat16: the same MMA encoding with .bf16 / kind::f16-BF16
+    TCR_DTYPE_BF16 = 1, /* bfloat16: the same MMA encoding with .bf16 / kind::f16-BF16
                            operands and B = bfloat16 ones                    */
+    TCR_DTYPE_E4M3 = 2, /* OCP fp8 E4M3FN (1 byte): mma.sync m16n8k32 .e4m3 /
+                           tcgen05 kind::f8f6f4, B = fp8 ones (tcr_reduce_sum_ex only) */
+    TCR_DTYPE_E5M2 = 3  /* OCP fp8 E5M2 (1 byte), as E4M3                     */
 } tcr_dtype;
 
 /*
@@ -126,8 +129,9 @@ tcr_status tcr_reduce_sum_algo(const tcr_half *x, size_t n, float *out_f32, doub
                                tcr_algo algo, tcr_stream stream);
 
 /*
- * tcr_reduce_sum_ex -- tcr_reduce_sum_algo for either 16-bit input type:
- * x holds n elements of `dtype` (binary16 or bfloat16 bit patterns).
+ * tcr_reduce_sum_ex -- tcr_reduce_sum_algo for any supported input type:
+ * x holds n elements of `dtype` (binary16 / bfloat16 / fp8 bit patterns;
+ * element-aligned; fp8 elements are 1 byte).
  * Same accuracy contract (|g - R| <= 2^-20 * sum|x_i| while the sum is
  * inside the binary32 range) and error behaviour; TCR_ERR_INVALID_VALUE for
  * an unknown dtype.  (The exact and host entry points are binary16 only.)

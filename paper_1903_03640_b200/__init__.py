@@ -43,6 +43,8 @@ TCR_ALGO_SHUFFLE = 3
 ALGOS = {"default": 0, "mma_sync": 1, "tcgen05": 2, "shuffle": 3}
 TCR_DTYPE_F16 = 0
 TCR_DTYPE_BF16 = 1
+TCR_DTYPE_E4M3 = 2
+TCR_DTYPE_E5M2 = 3
 
 TCR_CFG_DEFAULT_ALGO = 0
 TCR_CFG_BLOCKS_PER_SM = 1
@@ -179,8 +181,13 @@ def _dtype_of(x, dtype):
     try:
         import torch
 
-        if getattr(x, "dtype", None) == torch.bfloat16:
+        dt = getattr(x, "dtype", None)
+        if dt == torch.bfloat16:
             return TCR_DTYPE_BF16
+        if dt == torch.float8_e4m3fn:
+            return TCR_DTYPE_E4M3
+        if dt == torch.float8_e5m2:
+            return TCR_DTYPE_E5M2
     except ImportError:  # pragma: no cover
         pass
     return TCR_DTYPE_F16

@@ -176,9 +176,10 @@ tcr_status after_launch(cudaError_t e, const char* where, int launches = 1) {
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
 tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_f64, int algo,
-                       cudaStream_t stream, bool bf16 = false) {
+                       cudaStream_t stream, int fmt = 0) {
     if ((!x && n) || (!out_f32 && !out_f64)) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
-    if (!aligned(x, 2) || (out_f32 && !aligned(out_f32, 4)) || (out_f64 && !aligned(out_f64, 8)))
+    if (!aligned(x, fmt >= 2 ? 1 : 2) || (out_f32 && !aligned(out_f32, 4)) ||
+        (out_f64 && !aligned(out_f64, 8)))
         return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
     if (algo == TCR_ALGO_DEFAULT) {
         std::lock_guard<std::mutex> lk(g_cfg_mu);
@@ -193,9 +194,9 @@ tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_
     const LaunchCfg cfg = make_cfg(di);
     cudaError_t e;
     if (algo == TCR_ALGO_TCGEN05)
-        e = tcr::launch_reduce_tcgen05(bf16, x, n, out_f32, out_f64, ws->dev, cfg, stream);
+        e = tcr::launch_reduce_tcgen05(fmt, x, n, out_f32, out_f64, ws->dev, cfg, stream);
     else
-        e = tcr::launch_reduce_stream(algo == TCR_ALGO_MMA_SYNC, bf16, x, n, out_f32, out_f64, ws->dev,
+        e = tcr::launch_reduce_stream(algo == TCR_ALGO_MMA_SYNC, fmt, x, n, out_f32, out_f64, ws->dev,
                                       cfg, stream);
     return after_launch(e, "reduce kernel launch");
 }
@@ -242,17 +243,17 @@ tcr_status tcr_reduce_sum_algo(const tcr_half* x, size_t n, float* out_f32, doub
 
 tcr_status tcr_reduce_sum_ex(const void* x, size_t n, tcr_dtype dtype, float* out_f32,
                              double* out_f64, tcr_algo algo, tcr_stream stream) {
-    if (dtype != TCR_DTYPE_F16 && dtype != TCR_DTYPE_BF16)
+    if (dtype < TCR_DTYPE_F16 || dtype > TCR_DTYPE_E5M2)
         return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
     return reduce_impl(static_cast<const tcr_half*>(x), n, out_f32, out_f64, (int)algo,
-                       (cudaStream_t)stream, dtype == TCR_DTYPE_BF16);
+                       (cudaStream_t)stream, (int)dtype);
 }
 
 tcr_status tcr_reduce_sum_segmented_ex(const void* x, tcr_dtype dtype, const int64_t* offsets,
                                        size_t num_segments, float* out, tcr_algo algo,
                                        tcr_stream stream) {
     if (dtype != TCR_DTYPE_F16 && dtype != TCR_DTYPE_BF16)
-        return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
+        return fail(TCR_ERR_INVALID_VALUE, "segmented: dtype must be F16 or BF16");
     if (algo != TCR_ALGO_DEFAULT && algo != TCR_ALGO_MMA_SYNC && algo != TCR_ALGO_SHUFFLE)
         return fail(TCR_ERR_INVALID_VALUE, "segmented algo must be DEFAULT, MMA_SYNC or SHUFFLE");
     return segmented_impl(algo != TCR_ALGO_SHUFFLE, false, static_cast<const tcr_half*>(x), offsets,
@@ -323,7 +324,7 @@ tcr_status tcr_reduce_sum_host(const tcr_half* x, size_t n, float* out, tcr_stre
         if ((e = cudaMemcpyAsync(buf, x + lo, cnt * sizeof(uint16_t), cudaMemcpyHostToDevice,
                                  stream)))
             return cuda_fail(e, "cudaMemcpyAsync(H2D)");
-        if ((e = tcr::launch_reduce_stream(true, false, static_cast<const uint16_t*>(buf), cnt, nullptr,
+        if ((e = tcr::launch_reduce_stream(true, 0, static_cast<const uint16_t*>(buf), cnt, nullptr,
                                            ws->chunk_partials + c, ws->dev, cfg, stream)))
             return cuda_fail(e, "reduce kernel launch");
         ++launches;

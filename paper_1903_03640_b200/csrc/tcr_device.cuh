@@ -68,6 +68,33 @@ __device__ __forceinline__ void mma_rowsum_t(float (&c)[4], const uint4& a) {
     else mma_rowsum(c, a);
 }
 
+// Element formats of the flat reduction (NEXT-4): every one keeps the tile at
+// 512 bytes = one 16-byte vector per lane.  fp8 uses m16n8k32 (16 elements
+// per lane, 512 per tile) with B = fp8 ones; the C/D fragment is unchanged.
+enum Fmt : int { kF16 = 0, kBF16 = 1, kE4M3 = 2, kE5M2 = 3 };
+template <int F> struct FmtInfo { static constexpr int kBytes = F >= kE4M3 ? 1 : 2; };
+
+__device__ __forceinline__ void mma_rowsum_e4m3(float (&c)[4], const uint4& a) {
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.f32.e4m3.e4m3.f32 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(0x38383838u), "r"(0x38383838u));
+}
+__device__ __forceinline__ void mma_rowsum_e5m2(float (&c)[4], const uint4& a) {
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.f32.e5m2.e5m2.f32 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(0x3C3C3C3Cu), "r"(0x3C3C3C3Cu));
+}
+
+template <int F>
+__device__ __forceinline__ void mma_rowsum_f(float (&c)[4], const uint4& a) {
+    if constexpr (F == kF16) mma_rowsum(c, a);
+    else if constexpr (F == kBF16) mma_rowsum_bf16(c, a);
+    else if constexpr (F == kE4M3) mma_rowsum_e4m3(c, a);
+    else mma_rowsum_e5m2(c, a);
+}
+
 // Flush the carried fp32 accumulator into the lane's fp64 accumulator and
 // reset it (bounded chain, reading G9).  Rows g and g+8 appear in lanes
 // 4g..4g+3 (c0 and c2); lane t==0 keeps row g, t==1 keeps row g+8, t>=2
@@ -143,6 +170,42 @@ template <bool kBf16>
 __device__ __forceinline__ float vec_sum_t(const uint4& a) {
     if constexpr (kBf16) return vec_sum_f32_bf16(a);
     else return vec_sum_f32(a);
+}
+
+// fp8 -> binary16 pairs are exact (cvt.rn.f16x2.{e4m3,e5m2}x2), then binary32.
+template <int F>
+__device__ __forceinline__ float fp8x2_sum(uint16_t b) {
+    uint32_t h2;
+    if constexpr (F == kE4M3) asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(b));
+    else asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(h2) : "h"(b));
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h2));
+    return f.x + f.y;
+}
+
+template <int F>
+__device__ __forceinline__ float vec_sum_f(const uint4& a) {
+    if constexpr (F == kF16) return vec_sum_f32(a);
+    else if constexpr (F == kBF16) return vec_sum_f32_bf16(a);
+    else {
+        const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+        float p[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            p[k] = fp8x2_sum<F>((uint16_t)(w[k] & 0xFFFFu)) + fp8x2_sum<F>((uint16_t)(w[k] >> 16));
+        return (p[0] + p[1]) + (p[2] + p[3]);
+    }
+}
+
+// A lane's 16 bytes of a ragged tile: bytes p[16*lane + k] for 16*lane + k <
+// cnt_bytes, zero elsewhere (byte loads, never out of bounds).
+__device__ __forceinline__ uint4 load_ragged_bytes(const uint8_t* p, int cnt_bytes, int lane) {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int i = 16 * lane + k;
+        if (i < cnt_bytes) w[k >> 2] |= (uint32_t)__ldg(p + i) << (8 * (k & 3));
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // Zero the halves of a 16-byte vector whose element index (vector base

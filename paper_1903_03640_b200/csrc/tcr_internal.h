@@ -37,10 +37,11 @@ struct LaunchCfg {
 
 // Each launcher enqueues exactly one kernel on `stream` and returns the
 // cudaGetLastError() of the launch.
-cudaError_t launch_reduce_stream(bool mma, bool bf16, const uint16_t* x, size_t n, float* out_f32,
+// fmt: 0 binary16, 1 bfloat16, 2 fp8 E4M3, 3 fp8 E5M2 (n counts elements)
+cudaError_t launch_reduce_stream(bool mma, int fmt, const uint16_t* x, size_t n, float* out_f32,
                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                  cudaStream_t stream);
-cudaError_t launch_reduce_tcgen05(bool bf16, const uint16_t* x, size_t n, float* out_f32,
+cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x, size_t n, float* out_f32,
                                   double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                   cudaStream_t stream);
 cudaError_t launch_reduce_segmented(bool mma, bool bf16, bool batched, const uint16_t* x,
@@ -61,6 +62,6 @@ cudaError_t launch_probe_mma(int algo, const uint16_t* a, const float* c, float*
 // Grid size of the streaming kernels for n elements (shared by the API's
 // workspace sizing and the launchers).
 int stream_grid(size_t n, const LaunchCfg& cfg);
-int tcgen05_grid(size_t n, const LaunchCfg& cfg);
+int tcgen05_grid(size_t nbytes, const LaunchCfg& cfg);
 
 }  // namespace tcr

@@ -18,10 +18,10 @@
 
 namespace tcr {
 
-template <bool kMma, bool kBf16>
+template <bool kMma, int F>
 __device__ __forceinline__ void consume(const uint4& v, float (&c)[4], float& f) {
-    if constexpr (kMma) mma_rowsum_t<kBf16>(c, v);
-    else f += vec_sum_t<kBf16>(v);
+    if constexpr (kMma) mma_rowsum_f<F>(c, v);
+    else f += vec_sum_f<F>(v);
 }
 
 template <bool kMma>
@@ -34,19 +34,23 @@ __device__ __forceinline__ void flush(float (&c)[4], float& f, double& acc, int 
 // U tiles (one 16-byte vector per lane each) in flight per iteration.
 // __launch_bounds__ minimum CTAs/SM: without it ptxas budgets registers for
 // full occupancy (32 regs at 256 threads) and sinks the U loads below their
-// consumers, which leaves ~2 loads in flight per warp.
-template <bool kMma, bool kBf16, int U, int WARPS>
+// consumers, which leaves ~2 loads in flight per warp.  F = element format
+// (binary16, bfloat16, fp8 E4M3 / E5M2); all index math is in bytes.
+template <bool kMma, int F, int U, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, (U <= 8 ? 4 : 2))
-reduce_stream_kernel(const uint16_t* __restrict__ x, size_t n, int flush_every, float* out_f32,
+reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, float* out_f32,
                      double* out_f64, DevWorkspace ws) {
+    constexpr int ES = FmtInfo<F>::kBytes;
+    constexpr int kTileBytes = 512;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // head: elements before the first 16-byte boundary (x is 2-byte aligned)
-    size_t head = ((16u - ((uintptr_t)x & 15u)) & 15u) >> 1;
-    if (head > n) head = n;
-    const uint16_t* xa = x + head;
-    const size_t nb = n - head;
-    const size_t T = nb / kTileElems;
-    const int tail = (int)(nb - T * kTileElems);
+    const size_t nbytes = n * ES;
+    // head: bytes before the first 16-byte boundary (x is element aligned)
+    size_t head = (16u - ((uintptr_t)x & 15u)) & 15u;
+    if (head > nbytes) head = nbytes;
+    const uint8_t* xa = x + head;
+    const size_t nb = nbytes - head;
+    const size_t T = nb / kTileBytes;
+    const int tail = (int)(nb - T * kTileBytes);
     const size_t W = (size_t)gridDim.x * WARPS;
     const size_t w = (size_t)blockIdx.x * WARPS + warp;
     const uint4* base = reinterpret_cast<const uint4*>(xa) + lane;
@@ -63,8 +67,8 @@ reduce_stream_kernel(const uint16_t* __restrict__ x, size_t n, int flush_every, 
         __syncwarp();  // scheduling fence: all U loads issue before the first consumer
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (u & 1) consume<kMma, kBf16>(v[u], cB, fB);
-            else consume<kMma, kBf16>(v[u], cA, fA);
+            if (u & 1) consume<kMma, F>(v[u], cB, fB);
+            else consume<kMma, F>(v[u], cA, fA);
         }
         if (++it == flush_every) {
             it = 0;
@@ -75,16 +79,16 @@ reduce_stream_kernel(const uint16_t* __restrict__ x, size_t n, int flush_every, 
     flush<kMma>(cA, fA, acc, lane);
     flush<kMma>(cB, fB, acc, lane);
     for (; t < T; t += W) {  // fewer than U tiles left for this warp
-        consume<kMma, kBf16>(ldg_stream(base + t * 32), cA, fA);
+        consume<kMma, F>(ldg_stream(base + t * 32), cA, fA);
         flush<kMma>(cA, fA, acc, lane);
     }
     if (w == W - 1) {  // ragged head and tail: zero-padded tiles (reading G5)
         if (head) {
-            consume<kMma, kBf16>(load_ragged(x, (int)head, lane), cA, fA);
+            consume<kMma, F>(load_ragged_bytes(x, (int)head, lane), cA, fA);
             flush<kMma>(cA, fA, acc, lane);
         }
         if (tail) {
-            consume<kMma, kBf16>(load_ragged(xa + T * kTileElems, tail, lane), cA, fA);
+            consume<kMma, F>(load_ragged_bytes(xa + T * kTileBytes, tail, lane), cA, fA);
             flush<kMma>(cA, fA, acc, lane);
         }
     }
@@ -94,7 +98,7 @@ reduce_stream_kernel(const uint16_t* __restrict__ x, size_t n, int flush_every, 
 constexpr int kStreamWarps = 8;  // 256 threads per CTA
 
 int stream_grid(size_t n, const LaunchCfg& cfg) {
-    const size_t tiles = n / kTileElems;
+    const size_t tiles = n / kTileElems;  // (n in 2-byte element equivalents)
     const size_t per_cta = (size_t)kStreamWarps * cfg.unroll;  // tiles one CTA covers per iteration
     size_t g = (tiles + per_cta - 1) / per_cta;
     // Large inputs (HBM-bound): oversubscribe with blocks_per_sm CTAs per SM
@@ -110,38 +114,48 @@ int stream_grid(size_t n, const LaunchCfg& cfg) {
     return (int)g;
 }
 
-template <bool kMma, bool kBf16>
-static cudaError_t launch_stream_t(const uint16_t* x, size_t n, float* out_f32, double* out_f64,
+template <bool kMma, int F>
+static cudaError_t launch_stream_t(const uint16_t* x16, size_t n, float* out_f32, double* out_f64,
                                    const DevWorkspace& ws, const LaunchCfg& cfg,
                                    cudaStream_t stream) {
-    const int g = stream_grid(n, cfg);
+    const uint8_t* x = reinterpret_cast<const uint8_t*>(x16);
+    const int g = stream_grid(n * FmtInfo<F>::kBytes / 2, cfg);
     // two interleaved accumulators take unroll/2 tiles each per iteration
     const int fe = 2 * cfg.chain / cfg.unroll < 1 ? 1 : 2 * cfg.chain / cfg.unroll;
     switch (cfg.unroll) {
         case 4:
-            reduce_stream_kernel<kMma, kBf16, 4, kStreamWarps>
+            reduce_stream_kernel<kMma, F, 4, kStreamWarps>
                 <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
             break;
         case 16:
-            reduce_stream_kernel<kMma, kBf16, 16, kStreamWarps>
+            reduce_stream_kernel<kMma, F, 16, kStreamWarps>
                 <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
             break;
         default:
-            reduce_stream_kernel<kMma, kBf16, 8, kStreamWarps>
+            reduce_stream_kernel<kMma, F, 8, kStreamWarps>
                 <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
             break;
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_reduce_stream(bool mma, bool bf16, const uint16_t* x, size_t n, float* out_f32,
+template <int F>
+static cudaError_t launch_stream_f(bool mma, const uint16_t* x, size_t n, float* out_f32,
+                                   double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                   cudaStream_t stream) {
+    return mma ? launch_stream_t<true, F>(x, n, out_f32, out_f64, ws, cfg, stream)
+               : launch_stream_t<false, F>(x, n, out_f32, out_f64, ws, cfg, stream);
+}
+
+cudaError_t launch_reduce_stream(bool mma, int fmt, const uint16_t* x, size_t n, float* out_f32,
                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                  cudaStream_t stream) {
-    if (bf16)
-        return mma ? launch_stream_t<true, true>(x, n, out_f32, out_f64, ws, cfg, stream)
-                   : launch_stream_t<false, true>(x, n, out_f32, out_f64, ws, cfg, stream);
-    return mma ? launch_stream_t<true, false>(x, n, out_f32, out_f64, ws, cfg, stream)
-               : launch_stream_t<false, false>(x, n, out_f32, out_f64, ws, cfg, stream);
+    switch (fmt) {
+        case kBF16: return launch_stream_f<kBF16>(mma, x, n, out_f32, out_f64, ws, cfg, stream);
+        case kE4M3: return launch_stream_f<kE4M3>(mma, x, n, out_f32, out_f64, ws, cfg, stream);
+        case kE5M2: return launch_stream_f<kE5M2>(mma, x, n, out_f32, out_f64, ws, cfg, stream);
+        default: return launch_stream_f<kF16>(mma, x, n, out_f32, out_f64, ws, cfg, stream);
+    }
 }
 
 // ---------------------------------------------------------------------------

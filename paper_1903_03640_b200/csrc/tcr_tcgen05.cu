@@ -72,7 +72,7 @@ struct Tc05Params {
     int interleave;        // 0: CTA b owns a contiguous run of chunks; 1: chunks b, b+G, b+2G, ...
     uint32_t idesc;        // instruction descriptor (kind::f16 with F16 or BF16 operands)
     uint32_t one_bits;     // 1.0 in the input type (the all-ones B)
-    int bf16;              // inputs are bfloat16 (ragged mma.sync path)
+    int fmt;               // element format (0 f16, 1 bf16, 2 e4m3, 3 e5m2)
 };
 
 // Accumulator schedule: MMA number j of this CTA (j = 0, 1, ...) goes to
@@ -83,13 +83,13 @@ struct Tc05Params {
 // truncation, reading G10), and the epilogue drains one buffer per round
 // while the tensor core fills the other.
 __global__ void __launch_bounds__(kTcWarps * 32)
-reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, float* out_f32,
+reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, float* out_f32,
                       double* out_f64, DevWorkspace ws) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int stages = prm.stages;
     const uint32_t stage_bytes = prm.stage_bytes;
     const uint32_t buf_cols = (uint32_t)prm.slots * kSlotCols;
-    uint16_t* ones = reinterpret_cast<uint16_t*>(smem);             // 512 B: 16x16 fp16 ones
+    uint32_t* ones = reinterpret_cast<uint32_t*>(smem);             // 512 B of ones (B operand)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + 512);       // [stages]
     uint64_t* empty = full + stages;                                // [stages]
     uint64_t* tfull = empty + stages;                               // [2]
@@ -99,12 +99,13 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    size_t head = ((16u - ((uintptr_t)x & 15u)) & 15u) >> 1;
-    if (head > n) head = n;
-    const uint16_t* xa = x + head;
-    const size_t nb = n - head;
-    const size_t chunk_elems = stage_bytes / 2;
-    const size_t C = nb / chunk_elems;
+    // all index math in bytes (n elements of 1 or 2 bytes)
+    const size_t nbytes = n * (prm.fmt >= 2 ? 1u : 2u);
+    size_t head = (16u - ((uintptr_t)x & 15u)) & 15u;
+    if (head > nbytes) head = nbytes;
+    const uint8_t* xa = x + head;
+    const size_t nb = nbytes - head;
+    const size_t C = nb / stage_bytes;
     const size_t G = gridDim.x, b = blockIdx.x;
     const size_t c_begin = prm.interleave ? b : b * C / G;
     const int nchunks = prm.interleave ? (int)(C > b ? (C - b + G - 1) / G : 0)
@@ -114,7 +115,7 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
     const int per_round = prm.slots * prm.chain;
     const long long total_mma = (long long)nchunks * kmma;
 
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) ones[i] = (uint16_t)prm.one_bits;
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) ones[i] = prm.one_bits;
     sm100::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -139,7 +140,7 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
         if (lane == 0 && nchunks > 0) {  // producer
             const uint64_t pol = sm100::policy_evict_first();
             const uint32_t piece = stage_bytes / (uint32_t)prm.split;
-            const uint8_t* src = reinterpret_cast<const uint8_t*>(xa + c_begin * chunk_elems);
+            const uint8_t* src = xa + c_begin * (size_t)stage_bytes;
             for (int i = 0; i < prm.prefetch && i < nchunks; ++i)
                 sm100::prefetch_l2(src + (size_t)i * chunk_step, stage_bytes);
             int s = 0;
@@ -185,7 +186,10 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
                     }
                     const uint32_t d = tmem + (uint32_t)buf * buf_cols +
                                        ((uint32_t)pos & last_slot) * kSlotCols;
-                    sm100::mma_f16_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
+                    if (prm.fmt >= 2)
+                        sm100::mma_f8_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
+                    else
+                        sm100::mma_f16_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
                     --left;
                     if (++pos == per_round || left == 0) {
                         sm100::mma_commit(&tfull[buf]);
@@ -235,22 +239,26 @@ reduce_tcgen05_kernel(const uint16_t* __restrict__ x, size_t n, Tc05Params prm, 
         }
         if (blockIdx.x == gridDim.x - 1) {
             // Ragged work (< one chunk past the last full chunk, and the
-            // unaligned head): 256-element mma.sync tiles, zero padded.
+            // unaligned head): 512-byte mma.sync tiles, zero padded.
             const int e = warp - 2;
-            const uint16_t* xr = xa + C * chunk_elems;
-            const size_t rem = nb - C * chunk_elems;
-            const size_t Tr = rem / kTileElems;
-            const int tail = (int)(rem - Tr * kTileElems);
+            const uint8_t* xr = xa + C * (size_t)stage_bytes;
+            const size_t rem = nb - C * (size_t)stage_bytes;
+            const size_t Tr = rem / 512;
+            const int tail = (int)(rem - Tr * 512);
             float c[4] = {0.f, 0.f, 0.f, 0.f};
             const uint4* base = reinterpret_cast<const uint4*>(xr) + lane;
             auto tile = [&](const uint4& v) {
-                if (prm.bf16) mma_rowsum_bf16(c, v);
-                else mma_rowsum(c, v);
+                switch (prm.fmt) {
+                    case 1: mma_rowsum_bf16(c, v); break;
+                    case 2: mma_rowsum_e4m3(c, v); break;
+                    case 3: mma_rowsum_e5m2(c, v); break;
+                    default: mma_rowsum(c, v); break;
+                }
                 flush_rows(c, acc, lane);
             };
             for (size_t t = e; t < Tr; t += 4) tile(ldg_stream(base + t * 32));
-            if (e == 0 && head) tile(load_ragged(x, (int)head, lane));
-            if (e == 1 && tail) tile(load_ragged(xr + Tr * kTileElems, tail, lane));
+            if (e == 0 && head) tile(load_ragged_bytes(x, (int)head, lane));
+            if (e == 1 && tail) tile(load_ragged_bytes(xr + Tr * 512, tail, lane));
         }
     }
     sm100::tc_fence_before();
@@ -273,21 +281,24 @@ static int tc05_resident(const LaunchCfg& cfg) {
     return r < 1 ? 1 : r;
 }
 
-int tcgen05_grid(size_t n, const LaunchCfg& cfg) {
-    const size_t chunk_elems = (size_t)cfg.tc05_stage_kb * 512;
-    const size_t C = n / chunk_elems;
+int tcgen05_grid(size_t nbytes, const LaunchCfg& cfg) {
+    const size_t C = nbytes / ((size_t)cfg.tc05_stage_kb * 1024);
     const size_t gmax = (size_t)cfg.sms * (size_t)tc05_resident(cfg);
     size_t g = C < gmax ? C : gmax;
     return g < 1 ? 1 : (int)g;
 }
 
-cudaError_t launch_reduce_tcgen05(bool bf16, const uint16_t* x, size_t n, float* out_f32,
+cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x16, size_t n, float* out_f32,
                                   double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                   cudaStream_t stream) {
+    const uint8_t* x = reinterpret_cast<const uint8_t*>(x16);
     Tc05Params prm;
-    prm.bf16 = bf16 ? 1 : 0;
-    prm.idesc = kIdesc | (bf16 ? ((1u << 7) | (1u << 10)) : 0u);  // a_format = b_format = BF16
-    prm.one_bits = bf16 ? 0x3F80u : 0x3C00u;
+    prm.fmt = fmt;
+    // kind::f16: a/b_format F16 = 0, BF16 = 1; kind::f8f6f4: E4M3 = 0, E5M2 = 1 (bits 7-9, 10-12)
+    const uint32_t ab = (fmt == 1 || fmt == 3) ? ((1u << 7) | (1u << 10)) : 0u;
+    prm.idesc = kIdesc | ab;
+    prm.one_bits = fmt == 1 ? 0x3F803F80u : fmt == 2 ? 0x38383838u : fmt == 3 ? 0x3C3C3C3Cu
+                                                                   : 0x3C003C00u;
     prm.stages = cfg.tc05_stages;
     prm.stage_bytes = (uint32_t)cfg.tc05_stage_kb * 1024u;
     prm.slots = cfg.tc05_slots;
@@ -315,7 +326,7 @@ cudaError_t launch_reduce_tcgen05(bool bf16, const uint16_t* x, size_t n, float*
             configured[dev] = smem;
         }
     }
-    const int g = tcgen05_grid(n, cfg);
+    const int g = tcgen05_grid(n * (fmt >= 2 ? 1u : 2u), cfg);
     reduce_tcgen05_kernel<<<g, kTcWarps * 32, smem, stream>>>(x, n, prm, out_f32, out_f64, ws);
     return cudaGetLastError();
 }

@@ -260,6 +260,10 @@ def _device_lib():
         lib.tcr_inputs_generate.restype = ctypes.c_int
         lib.tcr_inputs_generate_bf16.argtypes = lib.tcr_inputs_generate.argtypes
         lib.tcr_inputs_generate_bf16.restype = ctypes.c_int
+        lib.tcr_inputs_generate_fp8.argtypes = [
+            ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+            ctypes.c_int, ctypes.c_void_p]
+        lib.tcr_inputs_generate_fp8.restype = ctypes.c_int
         _dev = lib
     return _dev
 
@@ -272,6 +276,23 @@ def generate_device(out_ptr: int, seed: int, start: int, count: int, dist: int =
         ctypes.c_uint64(count), int(dist), ctypes.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(f"tcr_inputs_generate failed with code {rc}")
+
+
+def generate_tensor_fp8(seed: int, start: int, count: int, dist: int = UNIFORM_PM1,
+                        fmt: int = FP8_E4M3, device="cuda"):
+    """torch float8 (e4m3fn / e5m2) tensor of the fp8 stream generated on the device."""
+    import torch
+
+    t = torch.empty(count, dtype=torch.float8_e4m3fn if fmt == FP8_E4M3 else torch.float8_e5m2,
+                    device=device)
+    if count:
+        rc = _device_lib().tcr_inputs_generate_fp8(
+            ctypes.c_void_p(t.data_ptr()), ctypes.c_uint64(seed), ctypes.c_uint64(start),
+            ctypes.c_uint64(count), int(dist), int(fmt),
+            ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream))
+        if rc != 0:
+            raise RuntimeError(f"tcr_inputs_generate_fp8 failed with code {rc}")
+    return t
 
 
 def generate_tensor(seed: int, start: int, count: int, dist: int = UNIFORM_PM1, device="cuda",

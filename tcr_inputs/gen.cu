@@ -3,6 +3,7 @@
 // Holds none of the reduction's arithmetic.  Built into libtcr_inputs.so.
 #include <cstdint>
 #include <cuda_bf16.h>
+#include <cuda_fp8.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -82,6 +83,43 @@ __global__ void gen_kernel_bf16(uint16_t* __restrict__ out, uint64_t seed, uint6
         out[k] = gen_one_bf16(seed, start + k, dist);
 }
 
+__device__ __forceinline__ uint8_t gen_one_fp8(uint64_t seed, uint64_t i, int dist, int fmt) {
+    const __nv_fp8_interpretation_t it = fmt == 0 ? __NV_E4M3 : __NV_E5M2;
+    const int mb = fmt == 0 ? 3 : 2;
+    switch (dist) {
+        case 0:
+        case 1:
+        case 3: {
+            const uint64_t z = splitmix64(seed, dist == 3 ? (i & ~1ull) : i);
+            const float r = (float)(uint32_t)(z >> 40);
+            const float v = dist == 1 ? r * 0x1p-24f : r * 0x1p-23f - 1.0f;
+            const uint8_t b = (uint8_t)__nv_cvt_float_to_fp8(v, __NV_SATFINITE, it);
+            return (dist == 3 && (i & 1ull)) ? (uint8_t)(b ^ 0x80u) : b;
+        }
+        case 2: return fmt == 0 ? 0x38 : 0x3C;
+        case 4: {
+            const uint64_t z = splitmix64(seed, i);
+            const int eb = 7 - mb;
+            const uint8_t sign = (uint8_t)(z >> 63);
+            const uint8_t e = (uint8_t)((z >> 32) % (uint64_t)((1 << eb) - 1));
+            const uint8_t f = (uint8_t)(z & (uint64_t)((1 << mb) - 1));
+            return (uint8_t)((sign << 7) | (e << mb) | f);
+        }
+        default: {
+            const uint64_t z = splitmix64(seed, i);
+            const float v = (float)(int)((z >> 32) % 5ull) - 2.0f;
+            return (uint8_t)__nv_cvt_float_to_fp8(v, __NV_SATFINITE, it);
+        }
+    }
+}
+
+__global__ void gen_kernel_fp8(uint8_t* __restrict__ out, uint64_t seed, uint64_t start,
+                               uint64_t count, int dist, int fmt) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += stride)
+        out[k] = gen_one_fp8(seed, start + k, dist, fmt);
+}
+
 __global__ void gen_kernel(uint16_t* __restrict__ out, uint64_t seed, uint64_t start,
                            uint64_t count, int dist) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -113,6 +151,21 @@ static int launch_gen(bool bf16, void* out, uint64_t seed, uint64_t start, uint6
 extern "C" int tcr_inputs_generate(void* out, uint64_t seed, uint64_t start, uint64_t count,
                                    int dist, void* stream) {
     return launch_gen(false, out, seed, start, count, dist, stream);
+}
+
+extern "C" int tcr_inputs_generate_fp8(void* out, uint64_t seed, uint64_t start, uint64_t count,
+                                       int dist, int fmt, void* stream) {
+    if (count == 0) return 0;
+    if (!out || dist < 0 || dist > 5 || fmt < 0 || fmt > 1) return 1;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint64_t blocks = (count + 255) / 256;
+    const uint64_t cap = (uint64_t)sms * 8;
+    if (blocks > cap) blocks = cap;
+    gen_kernel_fp8<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((uint8_t*)out, seed, start,
+                                                                        count, dist, fmt);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
 extern "C" int tcr_inputs_generate_bf16(void* out, uint64_t seed, uint64_t start, uint64_t count,
