@@ -183,7 +183,9 @@ tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_
         return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
     if (algo == TCR_ALGO_DEFAULT) {
         std::lock_guard<std::mutex> lk(g_cfg_mu);
-        algo = g_cfg.default_algo;
+        // fp8: mma.sync .e4m3/.e5m2 is converted to fp16 HMMAs on sm_100a; the
+        // native fp8 tensor path is tcgen05 kind::f8f6f4 (measured fastest)
+        algo = fmt >= 2 ? TCR_ALGO_TCGEN05 : g_cfg.default_algo;
     }
     if (algo < TCR_ALGO_MMA_SYNC || algo > TCR_ALGO_SHUFFLE)
         return fail(TCR_ERR_INVALID_VALUE, "unknown algo");

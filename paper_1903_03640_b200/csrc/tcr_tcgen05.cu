@@ -82,6 +82,7 @@ struct Tc05Params {
 // between neighbours), each accumulator carries `chain` tiles (bounded
 // truncation, reading G10), and the epilogue drains one buffer per round
 // while the tensor core fills the other.
+template <bool kF8>
 __global__ void __launch_bounds__(kTcWarps * 32)
 reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, float* out_f32,
                       double* out_f64, DevWorkspace ws) {
@@ -186,7 +187,7 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
                     }
                     const uint32_t d = tmem + (uint32_t)buf * buf_cols +
                                        ((uint32_t)pos & last_slot) * kSlotCols;
-                    if (prm.fmt >= 2)
+                    if constexpr (kF8)
                         sm100::mma_f8_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
                     else
                         sm100::mma_f16_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
@@ -320,14 +321,19 @@ cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x16, size_t n, float*
         static std::map<int, size_t> configured;
         std::lock_guard<std::mutex> lk(mu);
         if (smem > configured[dev]) {
-            if ((e = cudaFuncSetAttribute(reduce_tcgen05_kernel,
+            if ((e = cudaFuncSetAttribute(reduce_tcgen05_kernel<false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) ||
+                (e = cudaFuncSetAttribute(reduce_tcgen05_kernel<true>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
                 return e;
             configured[dev] = smem;
         }
     }
     const int g = tcgen05_grid(n * (fmt >= 2 ? 1u : 2u), cfg);
-    reduce_tcgen05_kernel<<<g, kTcWarps * 32, smem, stream>>>(x, n, prm, out_f32, out_f64, ws);
+    if (fmt >= 2)
+        reduce_tcgen05_kernel<true><<<g, kTcWarps * 32, smem, stream>>>(x, n, prm, out_f32, out_f64, ws);
+    else
+        reduce_tcgen05_kernel<false><<<g, kTcWarps * 32, smem, stream>>>(x, n, prm, out_f32, out_f64, ws);
     return cudaGetLastError();
 }
 
