@@ -163,7 +163,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--algo", default="default",
-                    choices=["default", "mma_sync", "tcgen05", "shuffle", "exact"])
+                    choices=["default", "mma_sync", "tcgen05", "shuffle", "bulk", "exact"])
     ap.add_argument("--workload", default="c3", choices=["c3", "c5"])
     ap.add_argument("--dtype", default="f16", choices=["f16", "bf16", "e4m3", "e5m2"],
                     help="input element type (bf16 / fp8 = NEXT-4; c3 workload, non-exact algos)")
@@ -182,6 +182,9 @@ def main():
     ap.add_argument("--prefetch", type=int, help="TCR_CFG_TC05_PREFETCH")
     ap.add_argument("--split", type=int, help="TCR_CFG_TC05_SPLIT")
     ap.add_argument("--interleave", type=int, help="TCR_CFG_TC05_INTERLEAVE")
+    ap.add_argument("--bulk-stages", type=int, help="TCR_CFG_BULK_STAGES")
+    ap.add_argument("--bulk-kb", type=int, help="TCR_CFG_BULK_STAGE_KB")
+    ap.add_argument("--bulk-ctas", type=int, help="TCR_CFG_BULK_CTAS_PER_SM")
     ap.add_argument("--exact-unroll", type=int, help="TCR_CFG_EXACT_UNROLL")
     ap.add_argument("--exact-bps", type=int, help="TCR_CFG_EXACT_BLOCKS_PER_SM")
     args = ap.parse_args()
@@ -201,6 +204,9 @@ def main():
                      (tcr.TCR_CFG_TC05_CHAIN, args.tc_chain), (tcr.TCR_CFG_TC05_CTAS_PER_SM, args.ctas),
                      (tcr.TCR_CFG_TC05_PREFETCH, args.prefetch), (tcr.TCR_CFG_TC05_SPLIT, args.split),
                      (tcr.TCR_CFG_TC05_INTERLEAVE, args.interleave),
+                     (tcr.TCR_CFG_BULK_STAGES, args.bulk_stages),
+                     (tcr.TCR_CFG_BULK_STAGE_KB, args.bulk_kb),
+                     (tcr.TCR_CFG_BULK_CTAS_PER_SM, args.bulk_ctas),
                      (tcr.TCR_CFG_EXACT_UNROLL, args.exact_unroll),
                      (tcr.TCR_CFG_EXACT_BLOCKS_PER_SM, args.exact_bps)):
         if val is not None:
@@ -319,7 +325,7 @@ def main():
     value = world * elems_per_step * K / (total_ms * 1e-3) / 1e9  # Gelem/s, whole job
     achieved = bytes_per_step / (kern_ms * 1e-3) / 1e9              # GB/s of the dominant kernel
     algo_name = args.algo if args.algo != "default" else \
-        {1: "mma_sync", 2: "tcgen05", 3: "shuffle"}[tcr.tcr_get_config(tcr.TCR_CFG_DEFAULT_ALGO)]
+        {1: "mma_sync", 2: "tcgen05", 3: "shuffle", 4: "bulk"}[tcr.tcr_get_config(tcr.TCR_CFG_DEFAULT_ALGO)]
 
     # ---------------- end to end through the public API with host buffers ----------------
     e2e = None

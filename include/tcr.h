@@ -83,8 +83,10 @@ typedef enum {
     TCR_ALGO_DEFAULT = 0, /* the library's fastest MMA-encoded kernel        */
     TCR_ALGO_MMA_SYNC = 1, /* mma.sync m16n8k16 (A from 128-bit loads)       */
     TCR_ALGO_TCGEN05 = 2, /* cp.async.bulk -> SMEM -> tcgen05.mma, D in TMEM */
-    TCR_ALGO_SHUFFLE = 3  /* classic comparison path (§II): fp32
+    TCR_ALGO_SHUFFLE = 3, /* classic comparison path (§II): fp32
                              FADD chains + shfl_xor tree, no tensor cores    */
+    TCR_ALGO_BULK_MMA = 4 /* cp.async.bulk (TMA) -> SMEM ring -> ld.shared.v4 ->
+                             mma.sync m16n8k16 by 8 consumer warps           */
 } tcr_algo;
 
 /* Input element type for the _ex entry points (NEXT-4). */
@@ -244,7 +246,10 @@ typedef enum {
     TCR_CFG_TC05_INTERLEAVE = 11, /* tcgen05: 0 = each CTA streams a contiguous run
                                      of chunks, 1 = chunks dealt round-robin    */
     TCR_CFG_EXACT_UNROLL = 12,    /* exact kernel: 16-byte loads per lane in flight (4, 8) */
-    TCR_CFG_EXACT_BLOCKS_PER_SM = 13 /* exact kernel: CTAs per SM (1..8)        */
+    TCR_CFG_EXACT_BLOCKS_PER_SM = 13, /* exact kernel: CTAs per SM (1..8)       */
+    TCR_CFG_BULK_STAGES = 14,     /* bulk kernel: SMEM ring stages (2..32)      */
+    TCR_CFG_BULK_STAGE_KB = 15,   /* bulk kernel: KiB per stage (4..64, x4)     */
+    TCR_CFG_BULK_CTAS_PER_SM = 16 /* bulk kernel: CTAs per SM (clamped by SMEM) */
 } tcr_config_key;
 tcr_status tcr_set_config(tcr_config_key key, int value);
 int tcr_get_config(tcr_config_key key); /* -1 for an unknown key */

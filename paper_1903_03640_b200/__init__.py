@@ -40,7 +40,8 @@ TCR_ALGO_DEFAULT = 0
 TCR_ALGO_MMA_SYNC = 1
 TCR_ALGO_TCGEN05 = 2
 TCR_ALGO_SHUFFLE = 3
-ALGOS = {"default": 0, "mma_sync": 1, "tcgen05": 2, "shuffle": 3}
+TCR_ALGO_BULK_MMA = 4
+ALGOS = {"default": 0, "mma_sync": 1, "tcgen05": 2, "shuffle": 3, "bulk": 4}
 TCR_DTYPE_F16 = 0
 TCR_DTYPE_BF16 = 1
 TCR_DTYPE_E4M3 = 2
@@ -60,6 +61,9 @@ TCR_CFG_TC05_SPLIT = 10
 TCR_CFG_TC05_INTERLEAVE = 11
 TCR_CFG_EXACT_UNROLL = 12
 TCR_CFG_EXACT_BLOCKS_PER_SM = 13
+TCR_CFG_BULK_STAGES = 14
+TCR_CFG_BULK_STAGE_KB = 15
+TCR_CFG_BULK_CTAS_PER_SM = 16
 
 
 class TcrError(RuntimeError):

@@ -44,6 +44,9 @@ struct Config {
     int tc05_prefetch = 0;
     int tc05_split = 1;
     int tc05_interleave = 0;
+    int bulk_stages = 6;
+    int bulk_stage_kb = 16;
+    int bulk_ctas = 2;
     int exact_unroll = 8;
     int exact_bps = 3;
 };
@@ -95,6 +98,9 @@ LaunchCfg make_cfg(const DeviceInfo& di) {
     c.tc05_prefetch = g_cfg.tc05_prefetch;
     c.tc05_split = g_cfg.tc05_split;
     c.tc05_interleave = g_cfg.tc05_interleave;
+    c.bulk_stages = g_cfg.bulk_stages;
+    c.bulk_stage_kb = g_cfg.bulk_stage_kb;
+    c.bulk_ctas = g_cfg.bulk_ctas;
     c.exact_unroll = g_cfg.exact_unroll;
     c.exact_bps = g_cfg.exact_bps;
     return c;
@@ -187,7 +193,7 @@ tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_
         // native fp8 tensor path is tcgen05 kind::f8f6f4 (measured fastest)
         algo = fmt >= 2 ? TCR_ALGO_TCGEN05 : g_cfg.default_algo;
     }
-    if (algo < TCR_ALGO_MMA_SYNC || algo > TCR_ALGO_SHUFFLE)
+    if (algo < TCR_ALGO_MMA_SYNC || algo > TCR_ALGO_BULK_MMA)
         return fail(TCR_ERR_INVALID_VALUE, "unknown algo");
     DeviceInfo di;
     Workspace* ws = nullptr;
@@ -197,6 +203,8 @@ tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_
     cudaError_t e;
     if (algo == TCR_ALGO_TCGEN05)
         e = tcr::launch_reduce_tcgen05(fmt, x, n, out_f32, out_f64, ws->dev, cfg, stream);
+    else if (algo == TCR_ALGO_BULK_MMA)
+        e = tcr::launch_reduce_bulk(fmt, x, n, out_f32, out_f64, ws->dev, cfg, stream);
     else
         e = tcr::launch_reduce_stream(algo == TCR_ALGO_MMA_SYNC, fmt, x, n, out_f32, out_f64, ws->dev,
                                       cfg, stream);
@@ -397,7 +405,7 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
     std::lock_guard<std::mutex> lk(g_cfg_mu);
     switch (key) {
         case TCR_CFG_DEFAULT_ALGO:
-            if (value < TCR_ALGO_MMA_SYNC || value > TCR_ALGO_SHUFFLE) break;
+            if (value < TCR_ALGO_MMA_SYNC || value > TCR_ALGO_BULK_MMA) break;
             g_cfg.default_algo = value;
             return TCR_OK;
         case TCR_CFG_BLOCKS_PER_SM:
@@ -444,6 +452,18 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             if (value != 0 && value != 1) break;
             g_cfg.tc05_interleave = value;
             return TCR_OK;
+        case TCR_CFG_BULK_STAGES:
+            if (value < 2 || value > 32) break;
+            g_cfg.bulk_stages = value;
+            return TCR_OK;
+        case TCR_CFG_BULK_STAGE_KB:
+            if (value < 4 || value > 64 || value % 4) break;
+            g_cfg.bulk_stage_kb = value;
+            return TCR_OK;
+        case TCR_CFG_BULK_CTAS_PER_SM:
+            if (value < 1 || value > 8) break;
+            g_cfg.bulk_ctas = value;
+            return TCR_OK;
         case TCR_CFG_EXACT_UNROLL:
             if (value != 4 && value != 8) break;
             g_cfg.exact_unroll = value;
@@ -472,6 +492,9 @@ int tcr_get_config(tcr_config_key key) {
         case TCR_CFG_TC05_PREFETCH: return g_cfg.tc05_prefetch;
         case TCR_CFG_TC05_SPLIT: return g_cfg.tc05_split;
         case TCR_CFG_TC05_INTERLEAVE: return g_cfg.tc05_interleave;
+        case TCR_CFG_BULK_STAGES: return g_cfg.bulk_stages;
+        case TCR_CFG_BULK_STAGE_KB: return g_cfg.bulk_stage_kb;
+        case TCR_CFG_BULK_CTAS_PER_SM: return g_cfg.bulk_ctas;
         case TCR_CFG_EXACT_UNROLL: return g_cfg.exact_unroll;
         case TCR_CFG_EXACT_BLOCKS_PER_SM: return g_cfg.exact_bps;
     }

@@ -31,6 +31,9 @@ struct LaunchCfg {
     int tc05_prefetch;  // tcgen05 kernel: L2 prefetch distance in chunks
     int tc05_split;     // tcgen05 kernel: bulk copies per stage
     int tc05_interleave;  // tcgen05 kernel: chunk-to-CTA mapping (0 contiguous, 1 interleaved)
+    int bulk_stages;      // bulk (TMA -> SMEM -> mma.sync) kernel: ring stages
+    int bulk_stage_kb;    // bulk kernel: KiB per stage (multiple of 4)
+    int bulk_ctas;        // bulk kernel: CTAs per SM
     int exact_unroll;     // exact kernel: 16-byte loads in flight per lane (4 or 8)
     int exact_bps;        // exact kernel: CTAs per SM
 };
@@ -48,6 +51,9 @@ cudaError_t launch_reduce_segmented(bool mma, bool bf16, bool batched, const uin
                                     const int64_t* offsets, size_t num_segments,
                                     size_t segment_len, float* out, const DevWorkspace& ws,
                                     const LaunchCfg& cfg, cudaStream_t stream);
+cudaError_t launch_reduce_bulk(int fmt, const uint16_t* x, size_t n, float* out_f32,
+                               double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                               cudaStream_t stream);
 cudaError_t launch_reduce_exact(const uint16_t* x, size_t n, long long* out_acc, float* out_f32,
                                 double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                 cudaStream_t stream);

@@ -8,7 +8,7 @@ import oracle
 import tcr_inputs as gen
 
 pytestmark = pytest.mark.gpu
-ALGOS = ["mma_sync", "tcgen05", "shuffle"]
+ALGOS = ["mma_sync", "tcgen05", "shuffle", "bulk"]
 
 
 @pytest.fixture(scope="module")

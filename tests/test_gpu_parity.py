@@ -17,7 +17,7 @@ import tcr_inputs as gen
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["mma_sync", "tcgen05", "shuffle"]
+ALGOS = ["mma_sync", "tcgen05", "shuffle", "bulk"]
 DISTS = [gen.UNIFORM_PM1, gen.UNIFORM_01, gen.ONES, gen.ALTERNATING, gen.WIDE]
 
 
@@ -203,11 +203,21 @@ def test_config_knobs(tcr):
                 assert oracle.within_tolerance(g, es), (st, kb, sl, ch, ct, pf, sp, il, g, es.f64())
                 assert g == _reduce(tcr, x, "tcgen05")
             tcr.tcr_set_config(tcr.TCR_CFG_TC05_INTERLEAVE, 0)
+        for st, kb, ct, ch in ((2, 4, 1, 4), (6, 16, 2, 4), (12, 16, 1, 16), (3, 32, 2, 2), (3, 64, 1, 8)):
+            tcr.tcr_set_config(tcr.TCR_CFG_BULK_STAGES, st)
+            tcr.tcr_set_config(tcr.TCR_CFG_BULK_STAGE_KB, kb)
+            tcr.tcr_set_config(tcr.TCR_CFG_BULK_CTAS_PER_SM, ct)
+            tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, ch)
+            g = _reduce(tcr, x, "bulk")
+            assert oracle.within_tolerance(g, es), (st, kb, ct, ch, g, es.f64())
+            assert g == _reduce(tcr, x, "bulk")
     finally:
         tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
         tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 8)
         tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
-        for key, val in ((tcr.TCR_CFG_TC05_STAGES, 4), (tcr.TCR_CFG_TC05_STAGE_KB, 16),
+        for key, val in ((tcr.TCR_CFG_BULK_STAGES, 6), (tcr.TCR_CFG_BULK_STAGE_KB, 16),
+                         (tcr.TCR_CFG_BULK_CTAS_PER_SM, 2), (tcr.TCR_CFG_CHAIN, 4),
+                         (tcr.TCR_CFG_TC05_STAGES, 4), (tcr.TCR_CFG_TC05_STAGE_KB, 16),
                          (tcr.TCR_CFG_TC05_SLOTS, 4), (tcr.TCR_CFG_TC05_CHAIN, 4),
                          (tcr.TCR_CFG_TC05_CTAS_PER_SM, 3), (tcr.TCR_CFG_TC05_PREFETCH, 0),
                          (tcr.TCR_CFG_TC05_SPLIT, 1)):
