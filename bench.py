@@ -65,6 +65,8 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.trace = []  # (perf_counter, sm_mhz, reason mask)
+        self.window = None
         self._stop = threading.Event()
         try:
             import pynvml
@@ -79,14 +81,27 @@ class ClockSampler:
     def _run(self):
         while not self._stop.is_set():
             try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
                 mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and bit != 0x1:
-                        self.reasons.add(name)
+                self.trace.append((time.perf_counter(), mhz, mask))
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(0.001)
+
+    def set_window(self, t0: float, t1: float):
+        """Keep the samples taken inside the timed region [t0, t1] (wall clock);
+        if the region was too short for any, the nearest sample on each side."""
+        inside = [s for s in self.trace if t0 <= s[0] <= t1]
+        if not inside and self.trace:
+            before = [s for s in self.trace if s[0] < t0][-1:]
+            after = [s for s in self.trace if s[0] > t1][:1]
+            inside = before + after
+        self.window = (t1 - t0) * 1e3
+        self.samples = [s[1] for s in inside]
+        for _, _, mask in inside:
+            for bit, name in self.REASONS.items():
+                if mask & bit and bit != 0x1:
+                    self.reasons.add(name)
 
     def __enter__(self):
         if self.nv:
@@ -103,7 +118,8 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "timed_region_ms": self.window, "source": "NVML, sampled every ~1 ms"}
 
 
 def _cpu_count():
@@ -160,8 +176,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--algo", default="default",
                     choices=["default", "mma_sync", "tcgen05", "shuffle", "bulk", "exact"])
     ap.add_argument("--workload", default="c3", choices=["c3", "c5"])
@@ -289,6 +305,7 @@ def main():
                     dist.all_reduce(out64)  # the paper's distributed merge, over NVLink
                     tcr.tcr_round_f64_to_f32(out64, out32, stream=stream)
 
+    clk = ClockSampler(torch.cuda.current_device()).__enter__()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -301,12 +318,16 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = tcr.tcr_launch_count()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        t_start.record(stream)
-        for i in range(K):
-            step(*kev[i])
-        t_end.record(stream)
-        torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    t_start.record(stream)
+    for i in range(K):
+        step(*kev[i])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
+    time.sleep(0.01)
+    clk.__exit__(None, None, None)
+    clk.set_window(w0, w1)
     launches = tcr.tcr_launch_count() - launches0
     if world > 1:
         dist.barrier()
