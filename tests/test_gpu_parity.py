@@ -357,3 +357,39 @@ def test_full_size_c4_on_one_gpu(tcr):
     torch.cuda.synchronize()
     assert oracle.within_tolerance(float(tot.item()), es)
     del x
+
+
+@pytest.mark.parametrize("algo", ALGOS + ["exact"])
+def test_one_hot_every_position_counted_once(tcr, algo):
+    """SURVEY T-D(i): a single nonzero element (distinct power of two, so a
+    double count or a drop changes the bits) at every position of 8 tiles
+    plus the ragged edges, for several misalignments: the sum must be exact."""
+    import torch
+
+    n = 8 * 256 + 37
+    buf = torch.zeros(n + 64, dtype=torch.int16, device="cuda")
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    for off in (0, 5):
+        x = buf[off:off + n].view(torch.float16)
+        for p in range(n):
+            v = float(2.0 ** ((p % 23) - 11))
+            x[p] = v
+            if algo == "exact":
+                tcr.tcr_reduce_sum_exact(x, out_f32=o32)
+            else:
+                tcr.tcr_reduce_sum_algo(x, out_f32=o32, algo=algo)
+            x[p] = 0.0
+            assert float(o32.item()) == v, (algo, off, p)
+
+
+def test_release_workspaces_and_reuse(tcr):
+    import torch
+
+    bits = gen.generate(8, 0, 1 << 20, gen.UNIFORM_PM1)
+    es = oracle.exact_sum_fp16(bits)
+    x = _dev(bits)
+    assert oracle.within_tolerance(_reduce(tcr, x, "default"), es)
+    torch.cuda.synchronize()
+    tcr.tcr_release_workspaces()
+    assert oracle.within_tolerance(_reduce(tcr, x, "default"), es)
+    assert oracle.within_tolerance(_reduce(tcr, x, "tcgen05"), es)
