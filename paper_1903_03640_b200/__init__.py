@@ -325,21 +325,34 @@ def tcr_status_string(s: int) -> str:
 # Convenience (allocating) wrappers --------------------------------------------------
 
 
-def reduce_sum(x, algo: str | int = "default", stream=None):
-    """Allocate a float32 device scalar and reduce x into it; returns the tensor."""
+def reduce_sum(x, algo: str | int = "default", exact: bool = False, out_dtype=None, stream=None):
+    """Sum of a CUDA tensor (float16, bfloat16, float8_e4m3fn or float8_e5m2),
+    returned as a 1-element device tensor (float32, or float64 with
+    ``out_dtype=torch.float64``).  ``exact=True`` (float16 only) returns the
+    correctly rounded exact sum (tcr_reduce_sum_exact)."""
     import torch
 
-    out = torch.empty(1, dtype=torch.float32, device=x.device)
-    tcr_reduce_sum_algo(x, out_f32=out, algo=algo, stream=stream)
+    x = x.reshape(-1) if x.is_contiguous() else x.contiguous().reshape(-1)
+    f64 = out_dtype == torch.float64
+    out = torch.empty(1, dtype=torch.float64 if f64 else torch.float32, device=x.device)
+    if exact:
+        if x.dtype != torch.float16:
+            raise TypeError("exact=True supports float16 input")
+        tcr_reduce_sum_exact(x, out_f32=None if f64 else out, out_f64=out if f64 else None,
+                             stream=stream)
+    else:
+        tcr_reduce_sum_ex(x, out_f32=None if f64 else out, out_f64=out if f64 else None,
+                          algo=algo, stream=stream)
     return out
 
 
 def reduce_sum_segmented(x, offsets, mma: bool = True, stream=None):
+    """Per-segment sums of a float16 / bfloat16 CUDA tensor over CSR int64 offsets."""
     import torch
 
     out = torch.empty(offsets.numel() - 1, dtype=torch.float32, device=x.device)
-    f = tcr_reduce_sum_segmented if mma else tcr_reduce_sum_segmented_shuffle
-    f(x, offsets, out, stream=stream)
+    tcr_reduce_sum_segmented_ex(x, offsets, out, algo="mma_sync" if mma else "shuffle",
+                                stream=stream)
     return out
 
 

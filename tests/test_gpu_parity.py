@@ -393,3 +393,25 @@ def test_release_workspaces_and_reuse(tcr):
     tcr.tcr_release_workspaces()
     assert oracle.within_tolerance(_reduce(tcr, x, "default"), es)
     assert oracle.within_tolerance(_reduce(tcr, x, "tcgen05"), es)
+
+
+def test_convenience_wrappers(tcr):
+    import torch
+
+    bits = gen.generate(12, 0, 100_003, gen.UNIFORM_PM1)
+    es = oracle.exact_sum_fp16(bits)
+    x = _dev(bits)
+    assert oracle.within_tolerance(float(tcr.reduce_sum(x).item()), es)
+    assert float(tcr.reduce_sum(x, exact=True).item()) == es.f32()
+    assert float(tcr.reduce_sum(x, exact=True, out_dtype=torch.float64).item()) == es.f64()
+    assert oracle.within_tolerance(float(tcr.reduce_sum(x.view(2, -1) if x.numel() % 2 == 0 else x).item()), es)
+    b16 = gen.generate_bf16(3, 0, 5000, gen.UNIFORM_PM1)
+    xb = torch.from_numpy(b16.view(np.int16)).cuda().view(torch.bfloat16)
+    assert oracle.within_tolerance(float(tcr.reduce_sum(xb).item()), oracle.exact_sum_bf16(b16))
+    f8 = gen.generate_fp8(3, 0, 5000, gen.UNIFORM_PM1, gen.FP8_E4M3)
+    x8 = torch.from_numpy(f8).cuda().view(torch.float8_e4m3fn)
+    assert oracle.within_tolerance(float(tcr.reduce_sum(x8).item()), oracle.exact_sum_fp8(f8, 0))
+    off = torch.tensor([0, 10, 10, 5000], dtype=torch.int64, device="cuda")
+    seg = tcr.reduce_sum_segmented(xb, off).cpu().tolist()
+    ref = [oracle.exact_sum_bf16(b16[a:b]) for a, b in ((0, 10), (10, 10), (10, 5000))]
+    assert all(oracle.within_tolerance(g, r) for g, r in zip(seg, ref))
