@@ -184,6 +184,9 @@ def main():
     ap.add_argument("--dtype", default="f16", choices=["f16", "bf16", "e4m3", "e5m2"],
                     help="input element type (bf16 / fp8 = NEXT-4; c3 workload, non-exact algos)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--combine", default="nccl", choices=["nccl", "peer"],
+                    help="c3/c4 cross-GPU combine: one NCCL allreduce of the fp64 partials, "
+                         "or the fused in-kernel NVLink mailbox combine (NEXT-2, peer.py)")
     ap.add_argument("--n-per-rank", type=int, default=N_PER_RANK)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -250,6 +253,17 @@ def main():
         raise SystemExit("--dtype bf16/e4m3/e5m2 supports the c3 workload with the MMA / shuffle paths")
     algo = tcr.ALGOS["default" if exact else args.algo]
     peak, peak_src = _peaks()
+    peer = None
+    if args.combine == "peer":
+        if exact or args.workload != "c3" or args.algo not in ("default", "mma_sync", "shuffle"):
+            raise SystemExit("--combine peer supports the c3/c4 workload with mma_sync / shuffle")
+        if shared_gpu and world > 1:
+            raise SystemExit("--combine peer makes the ranks' kernels wait on one another: "
+                             "never on one shared GPU")
+        from paper_1903_03640_b200.peer import PeerGroup
+
+        peer = PeerGroup()
+        algo = tcr.ALGOS["mma_sync" if args.algo == "default" else args.algo]
 
     # ---------------- inputs (untimed), resident in HBM ----------------
     if args.workload == "c3":
@@ -288,6 +302,8 @@ def main():
                 ev_k0.record(stream)
             if args.workload == "c5":
                 tcr.tcr_reduce_sum_segmented(x, toff, seg_out, stream=stream)
+            elif peer is not None:  # reduction + cross-GPU combine in ONE launch
+                peer.reduce_sum(x, out_f32=out32, algo=algo, stream=stream)
             elif exact:
                 tcr.tcr_reduce_sum_exact(x, acc=acc6, out_f32=out32 if world == 1 else None,
                                          stream=stream)
@@ -297,7 +313,7 @@ def main():
                 tcr.tcr_reduce_sum_ex(x, out_f64=out64, algo=algo, stream=stream)
             if ev_k1 is not None:
                 ev_k1.record(stream)
-            if args.workload == "c3" and world > 1:
+            if args.workload == "c3" and world > 1 and peer is None:
                 if exact:  # integer limbs: the allreduce is exact, result independent of N
                     dist.all_reduce(acc6)
                     tcr.tcr_exact_finalize(acc6, out_f32=out32, stream=stream)
@@ -403,6 +419,9 @@ def main():
                            ("tc05_prefetch", tcr.TCR_CFG_TC05_PREFETCH), ("tc05_split", tcr.TCR_CFG_TC05_SPLIT),
                            ("tc05_interleave", tcr.TCR_CFG_TC05_INTERLEAVE))},
                        "n_total": n * world, "l2": "inputs larger than L2 (no flush needed)",
+                       "combine": ("fused in-kernel NVLink mailbox combine (peer.py)" if peer
+                                   else "NCCL allreduce of fp64 partials") if world > 1 or peer
+                                  else "none (single GPU)",
                        "parallelism": f"dp{world}" if world > 1 else "single"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(algo_name, args.workload),
@@ -419,6 +438,8 @@ def main():
         if shared_gpu:
             line["test_mode"] = "shared-gpu gloo (not a measurement)"
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        peer.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -215,6 +215,79 @@ tcr_status tcr_exact_finalize(const int64_t *acc, float *out_f32, double *out_f6
 tcr_status tcr_round_f64_to_f32(const double *in, float *out, tcr_stream stream);
 
 /*
+ * ---------------------------------------------------------------------------
+ * Fused cross-GPU combine (NEXT-2; the paper's distributed reduction, P:89,
+ * §II: "the results of different compute nodes must be merged with message
+ * passing").  Instead of a separate NCCL allreduce, the kernel's last CTA
+ * pushes the rank's fp64 partial over NVLink into every peer's MAILBOX
+ * (a TCR_PEER_MAILBOX_BYTES device allocation per rank, mapped into the
+ * other processes by CUDA IPC), waits for the peers' partials in its own
+ * mailbox, sums them in rank order 0..P-1 and writes the group total: every
+ * rank gets the bitwise identical result (D' replicated, Eq. 12) from ONE
+ * launch, with no host synchronisation.  Each mailbox counts its rank's
+ * combines on the device (the epoch that tags the partials), so the launch
+ * can be captured in a CUDA graph and replayed.
+ *
+ * Group setup (once): each rank tcr_peer_mailbox_alloc()s its mailbox,
+ * exports it with tcr_peer_ipc_handle(), the handles are exchanged out of
+ * band (e.g. torch.distributed.all_gather_object), and each rank
+ * tcr_peer_ipc_open()s the peers' handles.  mailboxes[r] is then rank r's
+ * mailbox as seen by this process (its own pointer for r == rank).
+ * Teardown: all ranks quiesce (stream sync + a barrier), close the peers'
+ * mappings (tcr_peer_ipc_close), then free their own mailbox.
+ * ---------------------------------------------------------------------------
+ */
+#define TCR_MAX_PEERS 8           /* ranks per peer group (one NVLink node) */
+#define TCR_PEER_MAILBOX_BYTES 512
+#define TCR_IPC_HANDLE_BYTES 64
+
+/* Allocates (cudaMalloc, IPC-exportable) and zeroes a mailbox on the current
+ * device; synchronous.  Free with tcr_peer_mailbox_free. */
+tcr_status tcr_peer_mailbox_alloc(void **mailbox);
+tcr_status tcr_peer_mailbox_free(void *mailbox);
+/* Stream-ordered zeroing: clears the error word and restarts the combine
+ * count; every rank of the group must reset before the next combine. */
+tcr_status tcr_peer_mailbox_reset(void *mailbox, tcr_stream stream);
+/* Synchronous read of the mailbox's error word: *timed_out = 1 if a combine
+ * on this rank gave up waiting (its result was NaN); reset to clear. */
+tcr_status tcr_peer_mailbox_error(const void *mailbox, int *timed_out);
+/* handle: host buffer of TCR_IPC_HANDLE_BYTES (cudaIpcMemHandle_t). */
+tcr_status tcr_peer_ipc_handle(const void *mailbox, void *handle);
+tcr_status tcr_peer_ipc_open(const void *handle, void **peer_mailbox);
+tcr_status tcr_peer_ipc_close(void *peer_mailbox);
+
+/*
+ * tcr_reduce_sum_peer -- sum of this rank's shard x[0..n) (dtype as in
+ * tcr_reduce_sum_ex) fused with the group combine: out_f32[0] / out_f64[0]
+ * = the total over all nranks shards (binary64 sum of the ranks' fp64
+ * partials in rank order; out_f32 its RNE rounding).  One kernel launch on
+ * `stream`.
+ *   algo:      TCR_ALGO_DEFAULT / MMA_SYNC (the north-star kernel) or SHUFFLE.
+ *   mailboxes: HOST array of nranks device pointers, indexed by rank.
+ *   nranks:    1..TCR_MAX_PEERS; rank: this process's index.
+ * Every rank of the group must make the same sequence of calls, each rank's
+ * calls stream-ordered (one stream, or ordered by events); a rank whose peers do
+ * not arrive within TCR_CFG_PEER_TIMEOUT_MS writes NaN and sets its
+ * mailbox's error word (the group must then be reset on every rank).
+ */
+tcr_status tcr_reduce_sum_peer(const void *x, size_t n, tcr_dtype dtype, tcr_algo algo,
+                               void *const *mailboxes, int nranks, int rank, float *out_f32,
+                               double *out_f64, tcr_stream stream);
+
+/*
+ * tcr_reduce_sum_peer_emulated -- the same kernel and protocol with all
+ * nranks ranks emulated in ONE cooperative launch on this device (grid slice
+ * r = rank r, reducing the shard [r*n/P, (r+1)*n/P) of x, as
+ * shard_range() in sharded.py): testing and measurement of the fused
+ * combine on a single GPU.  out_f32 / out_f64: device arrays of nranks
+ * entries (rank r's result in [r]); mailboxes as above (nranks distinct
+ * mailboxes, any of which may be IPC mappings).
+ */
+tcr_status tcr_reduce_sum_peer_emulated(const void *x, size_t n, tcr_dtype dtype, tcr_algo algo,
+                                        void *const *mailboxes, int nranks, float *out_f32,
+                                        double *out_f64, tcr_stream stream);
+
+/*
  * tcr_probe_mma -- hardware characterisation (not part of the reduction):
  * executes ONE MMA of the given algo (TCR_ALGO_MMA_SYNC: m16n8k16;
  * TCR_ALGO_TCGEN05: M=128,N=16,K=16) with A = a (row-major 16x16 for
@@ -249,7 +322,9 @@ typedef enum {
     TCR_CFG_EXACT_BLOCKS_PER_SM = 13, /* exact kernel: CTAs per SM (1..8)       */
     TCR_CFG_BULK_STAGES = 14,     /* bulk kernel: SMEM ring stages (2..32)      */
     TCR_CFG_BULK_STAGE_KB = 15,   /* bulk kernel: KiB per stage (4..64, x4)     */
-    TCR_CFG_BULK_CTAS_PER_SM = 16 /* bulk kernel: CTAs per SM (clamped by SMEM) */
+    TCR_CFG_BULK_CTAS_PER_SM = 16, /* bulk kernel: CTAs per SM (clamped by SMEM) */
+    TCR_CFG_PEER_TIMEOUT_MS = 17  /* fused peer combine: bound on the wait for the
+                                     peers' partials (default 10000 ms)          */
 } tcr_config_key;
 tcr_status tcr_set_config(tcr_config_key key, int value);
 int tcr_get_config(tcr_config_key key); /* -1 for an unknown key */

@@ -64,6 +64,11 @@ TCR_CFG_EXACT_BLOCKS_PER_SM = 13
 TCR_CFG_BULK_STAGES = 14
 TCR_CFG_BULK_STAGE_KB = 15
 TCR_CFG_BULK_CTAS_PER_SM = 16
+TCR_CFG_PEER_TIMEOUT_MS = 17
+
+TCR_MAX_PEERS = 8
+TCR_PEER_MAILBOX_BYTES = 512
+TCR_IPC_HANDLE_BYTES = 64
 
 
 class TcrError(RuntimeError):
@@ -101,6 +106,15 @@ _SIGS = {
     "tcr_probe_mma": [_P, _P, _P, _I, _P],
     "tcr_set_config": [_I, _I],
     "tcr_release_workspaces": [],
+    "tcr_reduce_sum_peer": [_P, _SZ, _I, _I, _P, _I, _I, _P, _P, _P],
+    "tcr_reduce_sum_peer_emulated": [_P, _SZ, _I, _I, _P, _I, _P, _P, _P],
+    "tcr_peer_mailbox_alloc": [_P],
+    "tcr_peer_mailbox_free": [_P],
+    "tcr_peer_mailbox_reset": [_P, _P],
+    "tcr_peer_mailbox_error": [_P, _P],
+    "tcr_peer_ipc_handle": [_P, _P],
+    "tcr_peer_ipc_open": [_P, _P],
+    "tcr_peer_ipc_close": [_P],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -292,6 +306,78 @@ def tcr_probe_mma(a, c, d, algo=TCR_ALGO_MMA_SYNC, stream=None) -> None:
         algo = ALGOS[algo]
     _check(_lib.tcr_probe_mma(_ptr(a), _ptr(c), _ptr(d), int(algo), _stream(stream, a)),
            "tcr_probe_mma")
+
+
+# Fused cross-GPU combine (NEXT-2) ------------------------------------------------
+
+
+def _mailbox_array(mailboxes):
+    arr = (ctypes.c_void_p * len(mailboxes))(*[int(m) for m in mailboxes])
+    return arr
+
+
+def tcr_peer_mailbox_alloc() -> int:
+    """A zeroed TCR_PEER_MAILBOX_BYTES mailbox on the current device (address)."""
+    p = ctypes.c_void_p()
+    _check(_lib.tcr_peer_mailbox_alloc(ctypes.byref(p)), "tcr_peer_mailbox_alloc")
+    return int(p.value)
+
+
+def tcr_peer_mailbox_free(mailbox: int) -> None:
+    _check(_lib.tcr_peer_mailbox_free(mailbox), "tcr_peer_mailbox_free")
+
+
+def tcr_peer_mailbox_reset(mailbox: int, stream=None) -> None:
+    _check(_lib.tcr_peer_mailbox_reset(mailbox, _stream(stream)), "tcr_peer_mailbox_reset")
+
+
+def tcr_peer_mailbox_error(mailbox: int) -> bool:
+    """True if a combine on this mailbox's rank timed out (synchronous)."""
+    v = ctypes.c_int()
+    _check(_lib.tcr_peer_mailbox_error(mailbox, ctypes.byref(v)), "tcr_peer_mailbox_error")
+    return bool(v.value)
+
+
+def tcr_peer_ipc_handle(mailbox: int) -> bytes:
+    buf = ctypes.create_string_buffer(TCR_IPC_HANDLE_BYTES)
+    _check(_lib.tcr_peer_ipc_handle(mailbox, buf), "tcr_peer_ipc_handle")
+    return buf.raw
+
+
+def tcr_peer_ipc_open(handle: bytes) -> int:
+    if len(handle) != TCR_IPC_HANDLE_BYTES:
+        raise ValueError("IPC handle must be TCR_IPC_HANDLE_BYTES long")
+    p = ctypes.c_void_p()
+    _check(_lib.tcr_peer_ipc_open(ctypes.create_string_buffer(handle, len(handle)),
+                                  ctypes.byref(p)), "tcr_peer_ipc_open")
+    return int(p.value)
+
+
+def tcr_peer_ipc_close(peer_mailbox: int) -> None:
+    _check(_lib.tcr_peer_ipc_close(peer_mailbox), "tcr_peer_ipc_close")
+
+
+def tcr_reduce_sum_peer(x, mailboxes, rank, out_f32=None, out_f64=None, algo=TCR_ALGO_DEFAULT,
+                        dtype=None, n=None, stream=None) -> None:
+    """This rank's shard reduced and combined with its peers' in one launch."""
+    if isinstance(algo, str):
+        algo = ALGOS[algo]
+    _check(_lib.tcr_reduce_sum_peer(_ptr(x), _numel(x, n), _dtype_of(x, dtype), int(algo),
+                                    _mailbox_array(mailboxes), len(mailboxes), int(rank),
+                                    _ptr(out_f32), _ptr(out_f64), _stream(stream, x)),
+           "tcr_reduce_sum_peer")
+
+
+def tcr_reduce_sum_peer_emulated(x, mailboxes, out_f32=None, out_f64=None,
+                                 algo=TCR_ALGO_DEFAULT, dtype=None, n=None, stream=None) -> None:
+    """All len(mailboxes) ranks emulated in one cooperative launch (out_*[r] per rank)."""
+    if isinstance(algo, str):
+        algo = ALGOS[algo]
+    _check(_lib.tcr_reduce_sum_peer_emulated(_ptr(x), _numel(x, n), _dtype_of(x, dtype),
+                                             int(algo), _mailbox_array(mailboxes),
+                                             len(mailboxes), _ptr(out_f32),
+                                             _ptr(out_f64), _stream(stream, x)),
+           "tcr_reduce_sum_peer_emulated")
 
 
 def tcr_set_config(key: int, value: int) -> None:

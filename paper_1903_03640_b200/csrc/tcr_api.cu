@@ -49,6 +49,7 @@ struct Config {
     int bulk_ctas = 2;
     int exact_unroll = 8;
     int exact_bps = 3;
+    int peer_timeout_ms = 10000;
 };
 Config g_cfg;
 std::mutex g_cfg_mu;
@@ -142,7 +143,8 @@ tcr_status get_workspace(int dev, const DeviceInfo& di, cudaStream_t stream, Wor
     }
     auto* ws = new Workspace();
     const int capacity = di.sms * 32;  // 32 = max resident CTAs per SM
-    const size_t bytes = sizeof(double) * (size_t)capacity + 64;
+    constexpr size_t kCounterBytes = 128;
+    const size_t bytes = sizeof(double) * (size_t)capacity + kCounterBytes;
     cudaError_t e = cudaMalloc(&ws->block, bytes);
     if (e != cudaSuccess) {
         delete ws;
@@ -152,10 +154,10 @@ tcr_status get_workspace(int dev, const DeviceInfo& di, cudaStream_t stream, Wor
     ws->dev.partials = reinterpret_cast<double*>(p);
     char* ctr = p + sizeof(double) * (size_t)capacity;
     ws->dev.seg_next = reinterpret_cast<unsigned long long*>(ctr);
-    ws->dev.ticket = reinterpret_cast<unsigned*>(ctr + 8);
-    ws->dev.seg_exit = reinterpret_cast<unsigned*>(ctr + 12);
+    ws->dev.seg_exit = reinterpret_cast<unsigned*>(ctr + 8);
+    ws->dev.ticket = reinterpret_cast<unsigned*>(ctr + 16);  // kMaxPeers tickets
     ws->dev.capacity = capacity;
-    e = cudaMemsetAsync(ctr, 0, 64, stream);
+    e = cudaMemsetAsync(ctr, 0, kCounterBytes, stream);
     if (e != cudaSuccess) {
         cudaFree(ws->block);
         delete ws;
@@ -209,6 +211,44 @@ tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_
         e = tcr::launch_reduce_stream(algo == TCR_ALGO_MMA_SYNC, fmt, x, n, out_f32, out_f64, ws->dev,
                                       cfg, stream);
     return after_launch(e, "reduce kernel launch");
+}
+
+tcr_status peer_impl(const void* x, size_t n, int dtype, int algo, void* const* mailboxes,
+                     int nranks, int rank, float* out_f32, double* out_f64, bool emulate,
+                     cudaStream_t stream) {
+    if (dtype < TCR_DTYPE_F16 || dtype > TCR_DTYPE_E5M2)
+        return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
+    if (algo == TCR_ALGO_DEFAULT) algo = TCR_ALGO_MMA_SYNC;
+    if (algo != TCR_ALGO_MMA_SYNC && algo != TCR_ALGO_SHUFFLE)
+        return fail(TCR_ERR_INVALID_VALUE, "peer combine algo must be DEFAULT, MMA_SYNC or SHUFFLE");
+    if (nranks < 1 || nranks > tcr::kMaxPeers || rank < 0 || rank >= nranks)
+        return fail(TCR_ERR_INVALID_VALUE, "nranks must be 1..TCR_MAX_PEERS and 0 <= rank < nranks");
+    if (!mailboxes || (!x && n) || (!out_f32 && !out_f64))
+        return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    if (!aligned(x, dtype >= TCR_DTYPE_E4M3 ? 1 : 2) || (out_f32 && !aligned(out_f32, 4)) ||
+        (out_f64 && !aligned(out_f64, 8)))
+        return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
+    tcr::PeerCombine pc{};
+    for (int r = 0; r < nranks; ++r) {
+        if (!mailboxes[r] || !aligned(mailboxes[r], 16))
+            return fail(TCR_ERR_INVALID_VALUE, "null or misaligned mailbox");
+        pc.mbox[r] = mailboxes[r];
+    }
+    pc.nranks = nranks;
+    pc.rank = rank;
+    {
+        std::lock_guard<std::mutex> lk(g_cfg_mu);
+        pc.timeout_ns = (unsigned long long)g_cfg.peer_timeout_ms * 1000000ull;
+    }
+    DeviceInfo di;
+    Workspace* ws = nullptr;
+    tcr_status s = prologue(stream, &di, &ws);
+    if (s != TCR_OK) return s;
+    const LaunchCfg cfg = make_cfg(di);
+    return after_launch(tcr::launch_reduce_stream_peer(algo == TCR_ALGO_MMA_SYNC, dtype,
+                                                       static_cast<const uint16_t*>(x), n, out_f32,
+                                                       out_f64, ws->dev, cfg, pc, emulate, stream),
+                        emulate ? "peer-emulated reduce launch" : "peer reduce launch");
 }
 
 tcr_status segmented_impl(bool mma, bool batched, const tcr_half* x, const int64_t* offsets,
@@ -401,6 +441,86 @@ tcr_status tcr_probe_mma(const tcr_half* a, const float* c, float* d, tcr_algo a
     return fail(TCR_ERR_INVALID_VALUE, "probe algo must be MMA_SYNC or TCGEN05");
 }
 
+tcr_status tcr_reduce_sum_peer(const void* x, size_t n, tcr_dtype dtype, tcr_algo algo,
+                               void* const* mailboxes, int nranks, int rank, float* out_f32,
+                               double* out_f64, tcr_stream stream) {
+    return peer_impl(x, n, (int)dtype, (int)algo, mailboxes, nranks, rank, out_f32, out_f64, false,
+                     (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_peer_emulated(const void* x, size_t n, tcr_dtype dtype, tcr_algo algo,
+                                        void* const* mailboxes, int nranks, float* out_f32,
+                                        double* out_f64, tcr_stream stream) {
+    return peer_impl(x, n, (int)dtype, (int)algo, mailboxes, nranks, 0, out_f32, out_f64, true,
+                     (cudaStream_t)stream);
+}
+
+tcr_status tcr_peer_mailbox_alloc(void** mailbox) {
+    if (!mailbox) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    DeviceInfo di;
+    int dev;
+    tcr_status s = current_device(&dev, &di);
+    if (s != TCR_OK) return s;
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, tcr::kMailboxBytes);  // plain cudaMalloc: IPC-exportable
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(mailbox)");
+    if ((e = cudaMemset(p, 0, tcr::kMailboxBytes))) {
+        cudaFree(p);
+        return cuda_fail(e, "cudaMemset(mailbox)");
+    }
+    *mailbox = p;
+    return TCR_OK;
+}
+
+tcr_status tcr_peer_mailbox_free(void* mailbox) {
+    if (!mailbox) return TCR_OK;
+    cudaError_t e = cudaFree(mailbox);
+    return e == cudaSuccess ? TCR_OK : cuda_fail(e, "cudaFree(mailbox)");
+}
+
+tcr_status tcr_peer_mailbox_reset(void* mailbox, tcr_stream stream) {
+    if (!mailbox) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    cudaError_t e = cudaMemsetAsync(mailbox, 0, tcr::kMailboxBytes, (cudaStream_t)stream);
+    return e == cudaSuccess ? TCR_OK : cuda_fail(e, "cudaMemsetAsync(mailbox)");
+}
+
+tcr_status tcr_peer_mailbox_error(const void* mailbox, int* timed_out) {
+    if (!mailbox || !timed_out) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    unsigned w = 0;
+    cudaError_t e = cudaMemcpy(&w, static_cast<const char*>(mailbox) + tcr::kMailboxErrOffset,
+                               sizeof w, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(mailbox error)");
+    *timed_out = w ? 1 : 0;
+    return TCR_OK;
+}
+
+tcr_status tcr_peer_ipc_handle(const void* mailbox, void* handle) {
+    if (!mailbox || !handle) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    static_assert(sizeof(cudaIpcMemHandle_t) == TCR_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(mailbox));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    memcpy(handle, &h, sizeof h);
+    return TCR_OK;
+}
+
+tcr_status tcr_peer_ipc_open(const void* handle, void** peer_mailbox) {
+    if (!handle || !peer_mailbox) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    *peer_mailbox = p;
+    return TCR_OK;
+}
+
+tcr_status tcr_peer_ipc_close(void* peer_mailbox) {
+    if (!peer_mailbox) return TCR_OK;
+    cudaError_t e = cudaIpcCloseMemHandle(peer_mailbox);
+    return e == cudaSuccess ? TCR_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
 tcr_status tcr_set_config(tcr_config_key key, int value) {
     std::lock_guard<std::mutex> lk(g_cfg_mu);
     switch (key) {
@@ -472,6 +592,10 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             if (value < 1 || value > 8) break;
             g_cfg.exact_bps = value;
             return TCR_OK;
+        case TCR_CFG_PEER_TIMEOUT_MS:
+            if (value < 1 || value > 600000) break;
+            g_cfg.peer_timeout_ms = value;
+            return TCR_OK;
     }
     g_last_error = "invalid config key or value";
     return TCR_ERR_INVALID_VALUE;
@@ -497,6 +621,7 @@ int tcr_get_config(tcr_config_key key) {
         case TCR_CFG_BULK_CTAS_PER_SM: return g_cfg.bulk_ctas;
         case TCR_CFG_EXACT_UNROLL: return g_cfg.exact_unroll;
         case TCR_CFG_EXACT_BLOCKS_PER_SM: return g_cfg.exact_bps;
+        case TCR_CFG_PEER_TIMEOUT_MS: return g_cfg.peer_timeout_ms;
     }
     return -1;
 }

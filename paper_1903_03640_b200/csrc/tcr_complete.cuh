@@ -6,25 +6,33 @@
 
 #include "tcr_device.cuh"
 #include "tcr_internal.h"
+#include "tcr_peer.cuh"
 
 namespace tcr {
 
 // Levels 2-4.  Every thread of the CTA calls this with its lane value; the
 // total lands in out_f32 / out_f64 (device pointers, either may be null).
+// With a peer group (pc && pc->nranks > 0) the last CTA then runs the fused
+// cross-GPU combine (tcr_peer.cuh) as rank `me` and writes the group total.
 template <bool kMma, int WARPS>
 __device__ __forceinline__ void complete_block_and_grid(double lane_val, float* out_f32,
-                                                        double* out_f64, const DevWorkspace& ws) {
+                                                        double* out_f64, const DevWorkspace& ws,
+                                                        const PeerCombine* pc = nullptr,
+                                                        int me = 0) {
     __shared__ double s_warp[WARPS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double wt = warp_collapse<kMma>(lane_val);
     if (lane == 0) s_warp[warp] = wt;
     __syncthreads();
     if (warp != 0) return;
+    const bool peer = pc && pc->nranks > 0;
+    const unsigned long long prev = peer ? peer_counter(*pc, me) : 0ull;
     const double bt = warp_collapse<kMma>(lane < WARPS ? s_warp[lane] : 0.0);
     if (gridDim.x == 1) {
+        const double t = peer ? peer_combine(bt, *pc, me, lane, prev) : bt;
         if (lane == 0) {
-            if (out_f32) *out_f32 = (float)bt;
-            if (out_f64) *out_f64 = bt;
+            if (out_f32) *out_f32 = (float)t;
+            if (out_f64) *out_f64 = t;
         }
         return;
     }
@@ -39,7 +47,8 @@ __device__ __forceinline__ void complete_block_and_grid(double lane_val, float* 
     __threadfence();  // acquire: every other CTA's partial is visible
     double v = 0.0;
     for (int i = lane; i < (int)gridDim.x; i += 32) v += __ldcg(ws.partials + i);  // fixed order
-    const double tot = warp_collapse<kMma>(v);
+    double tot = warp_collapse<kMma>(v);
+    if (peer) tot = peer_combine(tot, *pc, me, lane, prev);
     if (lane == 0) {
         if (out_f32) *out_f32 = (float)tot;
         if (out_f64) *out_f64 = tot;

@@ -11,10 +11,26 @@ namespace tcr {
 // Library-owned per-(device, stream) workspace, passed by value to kernels.
 struct DevWorkspace {
     double* partials;               // [capacity] fp64 partial of every CTA (level >= 3)
-    unsigned* ticket;               // last-CTA completion ticket (self-resetting)
+    unsigned* ticket;               // last-CTA completion ticket (self-resetting); kMaxPeers
+                                    // consecutive tickets (one per emulated rank)
     unsigned long long* seg_next;   // segmented: next segment index (self-resetting)
     unsigned* seg_exit;             // segmented: warps that finished (self-resetting)
     int capacity;                   // entries in partials
+};
+
+// NEXT-2 fused cross-GPU combine (tcr_peer.cuh).  A mailbox is a small
+// device allocation on every rank; slot [parity][src] of rank d's mailbox
+// receives src's fp64 partial for the epoch of that parity.
+constexpr int kMaxPeers = 8;           // ranks per peer group (one NVLink node)
+constexpr int kMailboxBytes = 512;     // 2 x kMaxPeers x 16 B slots + error word + epoch
+constexpr int kMailboxErrOffset = 256; // uint32: set to 1 when a wait timed out
+constexpr int kMailboxEpochOffset = 264;  // uint64: combines completed by the owning rank
+
+struct PeerCombine {
+    void* mbox[kMaxPeers];        // mailbox of every rank (own + mapped peers), by rank
+    int nranks;                   // 0 = no combine (single-GPU result)
+    int rank;                     // this process's rank (emulation: base rank 0)
+    unsigned long long timeout_ns;  // bound on the wait for the peers' partials
 };
 
 struct LaunchCfg {
@@ -44,6 +60,14 @@ struct LaunchCfg {
 cudaError_t launch_reduce_stream(bool mma, int fmt, const uint16_t* x, size_t n, float* out_f32,
                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                  cudaStream_t stream);
+// Flat reduction fused with the cross-GPU combine (NEXT-2).  emulate = false:
+// one rank of a real peer group (pc.rank); emulate = true: ONE cooperative
+// launch whose grid.y slices are pc.nranks emulated ranks, slice r reducing
+// the shard [r n / P, (r+1) n / P) of x and writing out_*[r].
+cudaError_t launch_reduce_stream_peer(bool mma, int fmt, const uint16_t* x, size_t n,
+                                      float* out_f32, double* out_f64, const DevWorkspace& ws,
+                                      const LaunchCfg& cfg, const PeerCombine& pc, bool emulate,
+                                      cudaStream_t stream);
 cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x, size_t n, float* out_f32,
                                   double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                   cudaStream_t stream);

@@ -39,10 +39,22 @@ __device__ __forceinline__ void flush(float (&c)[4], float& f, double& acc, int 
 template <bool kMma, int F, int U, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, (U <= 8 ? 4 : 2))
 reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, float* out_f32,
-                     double* out_f64, DevWorkspace ws) {
+                     double* out_f64, DevWorkspace ws, PeerCombine pc) {
     constexpr int ES = FmtInfo<F>::kBytes;
     constexpr int kTileBytes = 512;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int me = pc.rank;
+    if (gridDim.y > 1) {  // emulated peer group: slice y is rank y, reducing its shard
+        const size_t P = gridDim.y, r = blockIdx.y;
+        const size_t lo = r * n / P, hi = (r + 1) * n / P;
+        x += lo * ES;
+        n = hi - lo;
+        ws.partials += r * gridDim.x;
+        ws.ticket += r;
+        if (out_f32) out_f32 += r;
+        if (out_f64) out_f64 += r;
+        me = (int)r;
+    }
     const size_t nbytes = n * ES;
     // head: bytes before the first 16-byte boundary (x is element aligned)
     size_t head = (16u - ((uintptr_t)x & 15u)) & 15u;
@@ -92,7 +104,7 @@ reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, f
             flush<kMma>(cA, fA, acc, lane);
         }
     }
-    complete_block_and_grid<kMma, WARPS>(acc, out_f32, out_f64, ws);
+    complete_block_and_grid<kMma, WARPS>(acc, out_f32, out_f64, ws, &pc, me);
 }
 
 constexpr int kStreamWarps = 8;  // 256 threads per CTA
@@ -114,48 +126,89 @@ int stream_grid(size_t n, const LaunchCfg& cfg) {
     return (int)g;
 }
 
+template <bool kMma, int F, int U>
+static cudaError_t launch_stream_u(const uint8_t* x, size_t n, int fe, float* out_f32,
+                                   double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                   const PeerCombine& pc, bool emulate, cudaStream_t stream) {
+    auto kernel = reduce_stream_kernel<kMma, F, U, kStreamWarps>;
+    if (!emulate) {
+        const int g = stream_grid(n * FmtInfo<F>::kBytes / 2, cfg);
+        kernel<<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws, pc);
+        return cudaGetLastError();
+    }
+    // Emulated peer group: the ranks' last CTAs wait on one another, so all
+    // P grid slices must be co-resident -- a cooperative launch guarantees it
+    // (B200_PROFILING.md: emulate ranks as one kernel, never as separate launches).
+    const int P = pc.nranks;
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kStreamWarps * 32, 0);
+    if (e != cudaSuccess) return e;
+    int g = stream_grid(n / (size_t)P * FmtInfo<F>::kBytes / 2, cfg);
+    const int cap = occ * cfg.sms / P;
+    if (g > cap) g = cap;
+    if (g < 1) return cudaErrorCooperativeLaunchTooLarge;
+    const uint8_t* xa = x;
+    size_t na = n;
+    int fea = fe;
+    float* o32 = out_f32;
+    double* o64 = out_f64;
+    DevWorkspace wsa = ws;
+    PeerCombine pca = pc;
+    void* args[] = {(void*)&xa, (void*)&na, (void*)&fea, (void*)&o32, (void*)&o64, (void*)&wsa,
+                    (void*)&pca};
+    return cudaLaunchCooperativeKernel((const void*)kernel, dim3(g, P), dim3(kStreamWarps * 32),
+                                       args, 0, stream);
+}
+
 template <bool kMma, int F>
 static cudaError_t launch_stream_t(const uint16_t* x16, size_t n, float* out_f32, double* out_f64,
                                    const DevWorkspace& ws, const LaunchCfg& cfg,
-                                   cudaStream_t stream) {
+                                   const PeerCombine& pc, bool emulate, cudaStream_t stream) {
     const uint8_t* x = reinterpret_cast<const uint8_t*>(x16);
-    const int g = stream_grid(n * FmtInfo<F>::kBytes / 2, cfg);
     // two interleaved accumulators take unroll/2 tiles each per iteration
     const int fe = 2 * cfg.chain / cfg.unroll < 1 ? 1 : 2 * cfg.chain / cfg.unroll;
     switch (cfg.unroll) {
         case 4:
-            reduce_stream_kernel<kMma, F, 4, kStreamWarps>
-                <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
-            break;
+            return launch_stream_u<kMma, F, 4>(x, n, fe, out_f32, out_f64, ws, cfg, pc, emulate,
+                                               stream);
         case 16:
-            reduce_stream_kernel<kMma, F, 16, kStreamWarps>
-                <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
-            break;
+            return launch_stream_u<kMma, F, 16>(x, n, fe, out_f32, out_f64, ws, cfg, pc, emulate,
+                                                stream);
         default:
-            reduce_stream_kernel<kMma, F, 8, kStreamWarps>
-                <<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws);
-            break;
+            return launch_stream_u<kMma, F, 8>(x, n, fe, out_f32, out_f64, ws, cfg, pc, emulate,
+                                               stream);
     }
-    return cudaGetLastError();
 }
 
 template <int F>
 static cudaError_t launch_stream_f(bool mma, const uint16_t* x, size_t n, float* out_f32,
                                    double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
-                                   cudaStream_t stream) {
-    return mma ? launch_stream_t<true, F>(x, n, out_f32, out_f64, ws, cfg, stream)
-               : launch_stream_t<false, F>(x, n, out_f32, out_f64, ws, cfg, stream);
+                                   const PeerCombine& pc, bool emulate, cudaStream_t stream) {
+    return mma ? launch_stream_t<true, F>(x, n, out_f32, out_f64, ws, cfg, pc, emulate, stream)
+               : launch_stream_t<false, F>(x, n, out_f32, out_f64, ws, cfg, pc, emulate, stream);
+}
+
+cudaError_t launch_reduce_stream_peer(bool mma, int fmt, const uint16_t* x, size_t n,
+                                      float* out_f32, double* out_f64, const DevWorkspace& ws,
+                                      const LaunchCfg& cfg, const PeerCombine& pc, bool emulate,
+                                      cudaStream_t stream) {
+    switch (fmt) {
+        case kBF16:
+            return launch_stream_f<kBF16>(mma, x, n, out_f32, out_f64, ws, cfg, pc, emulate, stream);
+        case kE4M3:
+            return launch_stream_f<kE4M3>(mma, x, n, out_f32, out_f64, ws, cfg, pc, emulate, stream);
+        case kE5M2:
+            return launch_stream_f<kE5M2>(mma, x, n, out_f32, out_f64, ws, cfg, pc, emulate, stream);
+        default:
+            return launch_stream_f<kF16>(mma, x, n, out_f32, out_f64, ws, cfg, pc, emulate, stream);
+    }
 }
 
 cudaError_t launch_reduce_stream(bool mma, int fmt, const uint16_t* x, size_t n, float* out_f32,
                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                  cudaStream_t stream) {
-    switch (fmt) {
-        case kBF16: return launch_stream_f<kBF16>(mma, x, n, out_f32, out_f64, ws, cfg, stream);
-        case kE4M3: return launch_stream_f<kE4M3>(mma, x, n, out_f32, out_f64, ws, cfg, stream);
-        case kE5M2: return launch_stream_f<kE5M2>(mma, x, n, out_f32, out_f64, ws, cfg, stream);
-        default: return launch_stream_f<kF16>(mma, x, n, out_f32, out_f64, ws, cfg, stream);
-    }
+    PeerCombine none{};
+    return launch_reduce_stream_peer(mma, fmt, x, n, out_f32, out_f64, ws, cfg, none, false, stream);
 }
 
 // ---------------------------------------------------------------------------

@@ -135,8 +135,9 @@ def test_round_to_f32_matches_numpy_for_doubles():
                   2.0 ** -149, 2.0 ** -150, 3 * 2.0 ** -150, 2.0 ** -126 * (1 - 2.0 ** -24),
                   3.4028235677973366e38, 3.4028235677973362e38 * (1 + 2.0 ** -25)]),
     ])
-    for v in vals.tolist():
-        assert oracle.round_to_f32(Fraction(v)) == float(np.float32(v)), v
+    with np.errstate(over="ignore"):  # values past FLT_MAX round to inf, on purpose
+        for v in vals.tolist():
+            assert oracle.round_to_f32(Fraction(v)) == float(np.float32(v)), v
 
 
 def test_within_tolerance_boundary_is_exact():
