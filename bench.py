@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import sys
@@ -184,9 +185,11 @@ def main():
     ap.add_argument("--dtype", default="f16", choices=["f16", "bf16", "e4m3", "e5m2"],
                     help="input element type (bf16 / fp8 = NEXT-4; c3 workload, non-exact algos)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--combine", default="nccl", choices=["nccl", "peer"],
+    ap.add_argument("--combine", default="auto", choices=["auto", "nccl", "peer"],
                     help="c3/c4 cross-GPU combine: one NCCL allreduce of the fp64 partials, "
-                         "or the fused in-kernel NVLink mailbox combine (NEXT-2, peer.py)")
+                         "or the fused in-kernel NVLink mailbox combine (NEXT-2, peer.py); "
+                         "auto = peer for N > 1 when its setup and a check against the NCCL "
+                         "combine pass on every rank, else nccl")
     ap.add_argument("--n-per-rank", type=int, default=N_PER_RANK)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -253,17 +256,31 @@ def main():
         raise SystemExit("--dtype bf16/e4m3/e5m2 supports the c3 workload with the MMA / shuffle paths")
     algo = tcr.ALGOS["default" if exact else args.algo]
     peak, peak_src = _peaks()
-    peer = None
+    peer, combine_note = None, None
+    peer_cfg = args.workload == "c3" and not exact and args.algo in ("default", "mma_sync", "shuffle")
     if args.combine == "peer":
-        if exact or args.workload != "c3" or args.algo not in ("default", "mma_sync", "shuffle"):
+        if not peer_cfg:
             raise SystemExit("--combine peer supports the c3/c4 workload with mma_sync / shuffle")
         if shared_gpu and world > 1:
             raise SystemExit("--combine peer makes the ranks' kernels wait on one another: "
                              "never on one shared GPU")
+    if args.combine == "peer" or (args.combine == "auto" and world > 1 and not shared_gpu
+                                  and peer_cfg):
         from paper_1903_03640_b200.peer import PeerGroup
 
-        peer = PeerGroup()
-        algo = tcr.ALGOS["mma_sync" if args.algo == "default" else args.algo]
+        try:
+            peer = PeerGroup()
+        except Exception as e:  # e.g. no CUDA IPC between these devices
+            if args.combine == "peer":
+                raise
+            peer, combine_note = None, f"peer setup failed ({e}); NCCL combine used"
+        if world > 1:  # every rank must take the same combine
+            ok = torch.tensor([1 if peer is not None else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() == 0 and peer is not None:
+                peer, combine_note = None, "peer setup failed on another rank; NCCL combine used"
+        if peer is not None:
+            algo = tcr.ALGOS["mma_sync" if args.algo == "default" else args.algo]
 
     # ---------------- inputs (untimed), resident in HBM ----------------
     if args.workload == "c3":
@@ -295,6 +312,26 @@ def main():
     out64 = torch.empty(1, dtype=torch.float64, device=dev)
     acc6 = torch.empty(6, dtype=torch.int64, device=dev)
     torch.cuda.synchronize()
+
+    if peer is not None and world > 1:
+        # check the fused combine against the NCCL combine once, on every rank
+        ref64 = torch.empty(1, dtype=torch.float64, device=dev)
+        p64 = torch.empty(1, dtype=torch.float64, device=dev)
+        with torch.cuda.stream(stream):
+            tcr.tcr_reduce_sum_ex(x, out_f64=ref64, algo=algo, stream=stream)
+            dist.all_reduce(ref64)
+            peer.reduce_sum(x, out_f64=p64, algo=algo, stream=stream)
+        torch.cuda.synchronize()
+        r, g = ref64.item(), p64.item()
+        good = math.isfinite(g) and abs(g - r) <= 1e-9 * max(1.0, abs(r)) and not peer.timed_out()
+        ok = torch.tensor([1 if good else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 0:
+            if args.combine == "peer":
+                raise SystemExit(f"fused peer combine disagrees with NCCL: {g!r} vs {r!r}")
+            peer.close()
+            peer, combine_note = None, "peer combine check failed; NCCL combine used"
+            algo = tcr.ALGOS["default" if exact else args.algo]
 
     def step(ev_k0=None, ev_k1=None):
         with torch.cuda.stream(stream):
@@ -422,6 +459,7 @@ def main():
                        "combine": ("fused in-kernel NVLink mailbox combine (peer.py)" if peer
                                    else "NCCL allreduce of fp64 partials") if world > 1 or peer
                                   else "none (single GPU)",
+                       "combine_note": combine_note,
                        "parallelism": f"dp{world}" if world > 1 else "single"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(algo_name, args.workload),
@@ -439,6 +477,8 @@ def main():
             line["test_mode"] = "shared-gpu gloo (not a measurement)"
         print(json.dumps(line), flush=True)
     if peer is not None:
+        if peer.timed_out():
+            print(f"warning: rank {rank}: a fused combine timed out", file=sys.stderr, flush=True)
         peer.close()
     if world > 1:
         dist.destroy_process_group()
