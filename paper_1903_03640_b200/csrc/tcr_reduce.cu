@@ -36,7 +36,11 @@ __device__ __forceinline__ void flush(float (&c)[4], float& f, double& acc, int 
 // full occupancy (32 regs at 256 threads) and sinks the U loads below their
 // consumers, which leaves ~2 loads in flight per warp.  F = element format
 // (binary16, bfloat16, fp8 E4M3 / E5M2); all index math is in bytes.
-template <bool kMma, int F, int U, int WARPS>
+// kPeer: the NEXT-2 variant (fused cross-GPU combine, tcr_peer.cuh; grid.y
+// slices = emulated ranks).  A separate instantiation, so that the plain
+// kernel's code is untouched by it (measured: folding the peer path into
+// the plain kernel as a runtime branch cost 3 % at 2^30).
+template <bool kMma, int F, int U, int WARPS, bool kPeer>
 __global__ void __launch_bounds__(WARPS * 32, (U <= 8 ? 4 : 2))
 reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, float* out_f32,
                      double* out_f64, DevWorkspace ws, PeerCombine pc) {
@@ -44,7 +48,7 @@ reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, f
     constexpr int kTileBytes = 512;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int me = pc.rank;
-    if (gridDim.y > 1) {  // emulated peer group: slice y is rank y, reducing its shard
+    if (kPeer && gridDim.y > 1) {  // emulated peer group: slice y is rank y, reducing its shard
         const size_t P = gridDim.y, r = blockIdx.y;
         const size_t lo = r * n / P, hi = (r + 1) * n / P;
         x += lo * ES;
@@ -104,7 +108,7 @@ reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, f
             flush<kMma>(cA, fA, acc, lane);
         }
     }
-    complete_block_and_grid<kMma, WARPS>(acc, out_f32, out_f64, ws, &pc, me);
+    complete_block_and_grid<kMma, WARPS>(acc, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
 }
 
 constexpr int kStreamWarps = 8;  // 256 threads per CTA
@@ -126,11 +130,11 @@ int stream_grid(size_t n, const LaunchCfg& cfg) {
     return (int)g;
 }
 
-template <bool kMma, int F, int U>
+template <bool kMma, int F, int U, bool kPeer>
 static cudaError_t launch_stream_u(const uint8_t* x, size_t n, int fe, float* out_f32,
                                    double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                    const PeerCombine& pc, bool emulate, cudaStream_t stream) {
-    auto kernel = reduce_stream_kernel<kMma, F, U, kStreamWarps>;
+    auto kernel = reduce_stream_kernel<kMma, F, U, kStreamWarps, kPeer>;
     if (!emulate) {
         const int g = stream_grid(n * FmtInfo<F>::kBytes / 2, cfg);
         kernel<<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws, pc);
@@ -165,18 +169,24 @@ static cudaError_t launch_stream_t(const uint16_t* x16, size_t n, float* out_f32
                                    const DevWorkspace& ws, const LaunchCfg& cfg,
                                    const PeerCombine& pc, bool emulate, cudaStream_t stream) {
     const uint8_t* x = reinterpret_cast<const uint8_t*>(x16);
+    if (pc.nranks > 0) {
+        // the peer variant is instantiated at the default unroll only (build size)
+        const int fe = 2 * cfg.chain / 4 < 1 ? 1 : 2 * cfg.chain / 4;
+        return launch_stream_u<kMma, F, 4, true>(x, n, fe, out_f32, out_f64, ws, cfg, pc, emulate,
+                                                 stream);
+    }
     // two interleaved accumulators take unroll/2 tiles each per iteration
     const int fe = 2 * cfg.chain / cfg.unroll < 1 ? 1 : 2 * cfg.chain / cfg.unroll;
     switch (cfg.unroll) {
         case 4:
-            return launch_stream_u<kMma, F, 4>(x, n, fe, out_f32, out_f64, ws, cfg, pc, emulate,
-                                               stream);
+            return launch_stream_u<kMma, F, 4, false>(x, n, fe, out_f32, out_f64, ws, cfg, pc,
+                                                      false, stream);
         case 16:
-            return launch_stream_u<kMma, F, 16>(x, n, fe, out_f32, out_f64, ws, cfg, pc, emulate,
-                                                stream);
+            return launch_stream_u<kMma, F, 16, false>(x, n, fe, out_f32, out_f64, ws, cfg, pc,
+                                                       false, stream);
         default:
-            return launch_stream_u<kMma, F, 8>(x, n, fe, out_f32, out_f64, ws, cfg, pc, emulate,
-                                               stream);
+            return launch_stream_u<kMma, F, 8, false>(x, n, fe, out_f32, out_f64, ws, cfg, pc,
+                                                      false, stream);
     }
 }
 
