@@ -364,8 +364,14 @@ def main():
     torch.cuda.synchronize()
 
     K = args.steps
+    # A step that is ONE launch of the dominant kernel (N = 1, or the fused
+    # peer combine) runs back to back with no events inside the timed region:
+    # the kernel's average launch duration is then the region / K (launch
+    # gaps included -- a per-step event pair would add its own gap, ~3 %).
+    # A step with an NCCL call keeps one event pair around the kernel.
+    single_launch_step = world == 1 or peer is not None
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(K)]
+           for _ in range(0 if single_launch_step else K)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -374,7 +380,7 @@ def main():
     w0 = time.perf_counter()
     t_start.record(stream)
     for i in range(K):
-        step(*kev[i])
+        step(*kev[i]) if kev else step()
     t_end.record(stream)
     torch.cuda.synchronize()
     w1 = time.perf_counter()
@@ -386,7 +392,12 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     total_ms = t_start.elapsed_time(t_end)
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    if single_launch_step:
+        if launches != K:
+            raise SystemExit(f"expected one launch per step, counted {launches} for {K} steps")
+        kern_ms = total_ms / K
+    else:
+        kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
     if world > 1:
         t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -398,8 +409,13 @@ def main():
 
     value = world * elems_per_step * K / (total_ms * 1e-3) / 1e9  # Gelem/s, whole job
     achieved = bytes_per_step / (kern_ms * 1e-3) / 1e9              # GB/s of the dominant kernel
-    algo_name = args.algo if args.algo != "default" else \
-        {1: "mma_sync", 2: "tcgen05", 3: "shuffle", 4: "bulk"}[tcr.tcr_get_config(tcr.TCR_CFG_DEFAULT_ALGO)]
+    if args.algo != "default":
+        algo_name = args.algo
+    elif args.dtype in ("e4m3", "e5m2") and peer is None:
+        algo_name = "tcgen05"  # the library's DEFAULT for fp8 (kind::f8f6f4)
+    else:
+        algo_name = {1: "mma_sync", 2: "tcgen05", 3: "shuffle", 4: "bulk"}[
+            tcr.tcr_get_config(tcr.TCR_CFG_DEFAULT_ALGO)]
 
     # ---------------- end to end through the public API with host buffers ----------------
     e2e = None
@@ -462,8 +478,13 @@ def main():
                        "combine_note": combine_note,
                        "parallelism": f"dp{world}" if world > 1 else "single"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": _traffic(algo_name, args.workload),
+                         "frac": achieved / peak, "traffic": _traffic(
+                             algo_name,
+                             args.workload if args.dtype == "f16" else f"{args.workload}-{args.dtype}"),
                          "peak_source": peak_src, "kernel_ms": kern_ms,
+                         "kernel_ms_method": ("timed region / K (one launch per step, back to back)"
+                                              if single_launch_step else
+                                              "mean of per-step CUDA event pairs around the kernel"),
                          "algorithmic_bytes_per_launch": bytes_per_step},
             "hbm_gbs": world * bytes_per_step * K / (total_ms * 1e-3) / 1e9,
             "frac_of_8tbs": world * bytes_per_step * K / (total_ms * 1e-3) / (world * 8e12),
