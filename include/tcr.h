@@ -304,12 +304,15 @@ tcr_status tcr_probe_mma(const tcr_half *a, const float *c, float *d, tcr_algo a
 typedef enum {
     TCR_CFG_DEFAULT_ALGO = 0,     /* tcr_algo used by tcr_reduce_sum        */
     TCR_CFG_BLOCKS_PER_SM = 1,    /* CTAs per SM of the streaming kernels   */
-    TCR_CFG_UNROLL = 2,           /* 16-byte loads in flight per lane (mma.sync/shuffle) */
+    TCR_CFG_UNROLL = 2,           /* 16-byte loads in flight per lane (mma.sync/shuffle):
+                                     4, 8, 16, or 0 = auto (default: 16 below
+                                     2^26 elements, 4 from there on)            */
     TCR_CFG_TC05_STAGES = 3,      /* SMEM ring stages of the tcgen05 kernel */
     TCR_CFG_TC05_STAGE_KB = 4,    /* KiB per stage of the tcgen05 kernel    */
     TCR_CFG_CHAIN = 5,            /* mma_sync/shuffle: carried chain K, tiles per
                                      fp32 accumulator before its fp64 flush
-                                     (rounded to a multiple of unroll/2)       */
+                                     (rounded to a multiple of unroll/2; at
+                                     unroll 16 at least 4)                     */
     TCR_CFG_TC05_SLOTS = 6,       /* tcgen05: independent TMEM accumulators per
                                      buffer (1, 2, 4, 8, 16)                    */
     TCR_CFG_TC05_CHAIN = 7,       /* tcgen05: MMAs carried per accumulator (K) */

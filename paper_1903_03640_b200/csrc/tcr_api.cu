@@ -34,7 +34,7 @@ struct Config {
     // Defaults = the measured best on B200 at n = 2^30 (profiles/r01/tuning.md).
     int default_algo = TCR_ALGO_MMA_SYNC;
     int blocks_per_sm = 8;
-    int unroll = 4;
+    int unroll = 0;       // 0 = auto: 16 below 2^26 elements, 4 above
     int chain = 4;        // carried chain K (tiles per fp32 accumulator before a flush)
     int tc05_stages = 4;
     int tc05_stage_kb = 16;
@@ -533,7 +533,7 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             g_cfg.blocks_per_sm = value;
             return TCR_OK;
         case TCR_CFG_UNROLL:
-            if (value != 4 && value != 8 && value != 16) break;
+            if (value != 0 && value != 4 && value != 8 && value != 16) break;
             g_cfg.unroll = value;
             return TCR_OK;
         case TCR_CFG_TC05_STAGES:

@@ -30,6 +30,24 @@ __device__ __forceinline__ void flush(float (&c)[4], float& f, double& acc, int 
     else { acc += (double)f; f = 0.0f; }
 }
 
+// The U vectors of one batch, alternately into the two accumulators.  With
+// mid_flush (U = 16 at the default chain K = 4) both are flushed after the
+// first half of the batch, so no accumulator carries more than K tiles.
+template <bool kMma, int F, int U>
+__device__ __forceinline__ void consume_batch(const uint4 (&v)[U], float (&cA)[4], float (&cB)[4],
+                                              float& fA, float& fB, double& acc, int lane,
+                                              bool mid_flush) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (u & 1) consume<kMma, F>(v[u], cB, fB);
+        else consume<kMma, F>(v[u], cA, fA);
+        if (U == 16 && u == U / 2 - 1 && mid_flush) {
+            flush<kMma>(cA, fA, acc, lane);
+            flush<kMma>(cB, fB, acc, lane);
+        }
+    }
+}
+
 // Grid-stride over 512-byte tiles: warp w handles tiles w, w+W, w+2W, ...,
 // U tiles (one 16-byte vector per lane each) in flight per iteration.
 // __launch_bounds__ minimum CTAs/SM: without it ptxas budgets registers for
@@ -42,8 +60,8 @@ __device__ __forceinline__ void flush(float (&c)[4], float& f, double& acc, int 
 // the plain kernel as a runtime branch cost 3 % at 2^30).
 template <bool kMma, int F, int U, int WARPS, bool kPeer>
 __global__ void __launch_bounds__(WARPS * 32, (U <= 8 ? 4 : 2))
-reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, float* out_f32,
-                     double* out_f64, DevWorkspace ws, PeerCombine pc) {
+reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, int mid_flush,
+                     float* out_f32, double* out_f64, DevWorkspace ws, PeerCombine pc) {
     constexpr int ES = FmtInfo<F>::kBytes;
     constexpr int kTileBytes = 512;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -81,23 +99,26 @@ reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, f
 #pragma unroll
         for (int u = 0; u < U; ++u) v[u] = ldg_stream(base + (t + (size_t)u * W) * 32);
         __syncwarp();  // scheduling fence: all U loads issue before the first consumer
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (u & 1) consume<kMma, F>(v[u], cB, fB);
-            else consume<kMma, F>(v[u], cA, fA);
-        }
+        consume_batch<kMma, F, U>(v, cA, cB, fA, fB, acc, lane, mid_flush != 0);
         if (++it == flush_every) {
             it = 0;
             flush<kMma>(cA, fA, acc, lane);
             flush<kMma>(cB, fB, acc, lane);
         }
     }
+    if (t < T) {  // fewer than U tiles left for this warp: one predicated batch
+        // (all loads in flight together -- one latency, not one per tile;
+        // a zero vector adds exactly nothing)
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            v[u] = (t + (size_t)u * W < T) ? ldg_stream(base + (t + (size_t)u * W) * 32)
+                                           : make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+        consume_batch<kMma, F, U>(v, cA, cB, fA, fB, acc, lane, mid_flush != 0);
+    }
     flush<kMma>(cA, fA, acc, lane);
     flush<kMma>(cB, fB, acc, lane);
-    for (; t < T; t += W) {  // fewer than U tiles left for this warp
-        consume<kMma, F>(ldg_stream(base + t * 32), cA, fA);
-        flush<kMma>(cA, fA, acc, lane);
-    }
     if (w == W - 1) {  // ragged head and tail: zero-padded tiles (reading G5)
         if (head) {
             consume<kMma, F>(load_ragged_bytes(x, (int)head, lane), cA, fA);
@@ -135,9 +156,10 @@ static cudaError_t launch_stream_u(const uint8_t* x, size_t n, int fe, float* ou
                                    double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                    const PeerCombine& pc, bool emulate, cudaStream_t stream) {
     auto kernel = reduce_stream_kernel<kMma, F, U, kStreamWarps, kPeer>;
+    const int mid = (U == 16 && 2 * cfg.chain < U) ? 1 : 0;
     if (!emulate) {
         const int g = stream_grid(n * FmtInfo<F>::kBytes / 2, cfg);
-        kernel<<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, out_f32, out_f64, ws, pc);
+        kernel<<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, mid, out_f32, out_f64, ws, pc);
         return cudaGetLastError();
     }
     // Emulated peer group: the ranks' last CTAs wait on one another, so all
@@ -153,28 +175,38 @@ static cudaError_t launch_stream_u(const uint8_t* x, size_t n, int fe, float* ou
     if (g < 1) return cudaErrorCooperativeLaunchTooLarge;
     const uint8_t* xa = x;
     size_t na = n;
-    int fea = fe;
+    int fea = fe, mida = mid;
     float* o32 = out_f32;
     double* o64 = out_f64;
     DevWorkspace wsa = ws;
     PeerCombine pca = pc;
-    void* args[] = {(void*)&xa, (void*)&na, (void*)&fea, (void*)&o32, (void*)&o64, (void*)&wsa,
-                    (void*)&pca};
+    void* args[] = {(void*)&xa, (void*)&na, (void*)&fea, (void*)&mida, (void*)&o32, (void*)&o64,
+                    (void*)&wsa, (void*)&pca};
     return cudaLaunchCooperativeKernel((const void*)kernel, dim3(g, P), dim3(kStreamWarps * 32),
                                        args, 0, stream);
 }
 
+// Inputs below this many 2-byte element equivalents are latency bound: the
+// auto unroll (TCR_CFG_UNROLL = 0) puts 16 loads per lane in flight there
+// (one or two load rounds per warp instead of four; -0.4 to -0.7 us at
+// 2^22..2^25, profiles/r01/c2_sweep2.txt) and 4 above (the measured best
+// at 2^30).
+constexpr size_t kSmallN = (size_t)1 << 26;
+
 template <bool kMma, int F>
 static cudaError_t launch_stream_t(const uint16_t* x16, size_t n, float* out_f32, double* out_f64,
-                                   const DevWorkspace& ws, const LaunchCfg& cfg,
+                                   const DevWorkspace& ws, const LaunchCfg& cfg_in,
                                    const PeerCombine& pc, bool emulate, cudaStream_t stream) {
     const uint8_t* x = reinterpret_cast<const uint8_t*>(x16);
+    LaunchCfg cfg = cfg_in;
     if (pc.nranks > 0) {
-        // the peer variant is instantiated at the default unroll only (build size)
+        // the peer variant is instantiated at unroll 4 only (build size)
+        cfg.unroll = 4;
         const int fe = 2 * cfg.chain / 4 < 1 ? 1 : 2 * cfg.chain / 4;
         return launch_stream_u<kMma, F, 4, true>(x, n, fe, out_f32, out_f64, ws, cfg, pc, emulate,
                                                  stream);
     }
+    if (cfg.unroll == 0) cfg.unroll = (n * FmtInfo<F>::kBytes / 2 < kSmallN) ? 16 : 4;
     // two interleaved accumulators take unroll/2 tiles each per iteration
     const int fe = 2 * cfg.chain / cfg.unroll < 1 ? 1 : 2 * cfg.chain / cfg.unroll;
     switch (cfg.unroll) {

@@ -3,6 +3,8 @@ paths vs the warp-shuffle path.
   cold: a 512 MiB buffer is written between timed launches (outside the
         events; its dirty lines are written back during the timed kernel);
         per-launch CUDA-event time, median of 200.
+  cold_clean: the same with the 512 MiB buffer READ instead (L2 left full of
+        clean lines: no write-back inside the timed kernel).
   warm: 100 back-to-back launches captured in a CUDA graph, replay time / 100
         (no host launch gaps; the input stays in L2).
 Library calls only."""
@@ -42,33 +44,37 @@ def graph_time(fn, reps=100):
     return a.elapsed_time(b) * 1e3 / (5 * reps)
 
 
-for algo in ("mma_sync", "tcgen05", "shuffle"):
+flush16 = flush.view(torch.float16)
+fout = torch.empty(1, dtype=torch.float32, device="cuda")
+
+
+def cold_time(fn, clean):
     ts = []
     for i in range(230):
-        flush.fill_(i & 0xFF)
+        if clean:
+            tcr.tcr_reduce_sum_algo(flush16, out_f32=fout, algo="mma_sync")  # read-only sweep
+        else:
+            flush.fill_(i & 0xFF)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        tcr.tcr_reduce_sum_algo(x, out_f32=out, algo=algo)
+        fn()
         b.record()
         torch.cuda.synchronize()
         if i >= 30:
             ts.append(a.elapsed_time(b) * 1e3)
-    for mode, us in (("cold", statistics.median(ts)),
+    return statistics.median(ts)
+
+
+for algo in ("mma_sync", "tcgen05", "shuffle"):
+    fn = lambda: tcr.tcr_reduce_sum_algo(x, out_f32=out, algo=algo)  # noqa: E731
+    for mode, us in (("cold", cold_time(fn, False)), ("cold_clean", cold_time(fn, True)),
                      ("warm", graph_time(lambda: tcr.tcr_reduce_sum_algo(x, out_f32=out, algo=algo)))):
         res[f"{algo}:{mode}"] = {"us": us, "GB/s": 2 * n / (us * 1e-6) / 1e9, "Gelem/s": n / (us * 1e-6) / 1e9}
-        print(f"{algo:9s} {mode}: {us:7.2f} us  {2*n/(us*1e-6)/1e9:8.1f} GB/s  {n/(us*1e-6)/1e9:8.1f} Gelem/s")
+        print(f"{algo:9s} {mode:10s}: {us:7.2f} us  {2*n/(us*1e-6)/1e9:8.1f} GB/s  {n/(us*1e-6)/1e9:8.1f} Gelem/s")
 # torch.sum as a library reference point
-ts = []
-for i in range(230):
-    flush.fill_(i & 0xFF)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    torch.sum(x, dtype=torch.float32)
-    b.record()
-    torch.cuda.synchronize()
-    if i >= 30:
-        ts.append(a.elapsed_time(b) * 1e3)
-for mode, us in (("cold", statistics.median(ts)), ("warm", graph_time(lambda: torch.sum(x, dtype=torch.float32)))):
+tfn = lambda: torch.sum(x, dtype=torch.float32)  # noqa: E731
+for mode, us in (("cold", cold_time(tfn, False)), ("cold_clean", cold_time(tfn, True)),
+                 ("warm", graph_time(tfn))):
     res[f"torch.sum:{mode}"] = {"us": us, "GB/s": 2 * n / (us * 1e-6) / 1e9}
-    print(f"torch.sum {mode}: {us:7.2f} us  {2*n/(us*1e-6)/1e9:8.1f} GB/s")
+    print(f"torch.sum {mode:10s}: {us:7.2f} us  {2*n/(us*1e-6)/1e9:8.1f} GB/s")
 json.dump(res, open("gpurun_out/c2_compare.json", "w"), indent=1)

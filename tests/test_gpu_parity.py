@@ -171,7 +171,7 @@ def test_config_knobs(tcr):
     es = oracle.exact_sum_fp16(bits, threads=4)
     x = _dev(bits, 1)
     try:
-        for unroll in (4, 8, 16):
+        for unroll in (0, 4, 8, 16):
             for bps in (1, 2, 4, 8):
                 for chain in (2, 4, 16):
                     tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, unroll)
@@ -180,7 +180,7 @@ def test_config_knobs(tcr):
                     for algo in ("mma_sync", "shuffle"):
                         g = _reduce(tcr, x, algo)
                         assert oracle.within_tolerance(g, es), (unroll, bps, chain, algo)
-        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
+        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 0)
         tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 8)
         tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
         for stages, kb in ((2, 4), (4, 8), (8, 16), (6, 32), (3, 64)):
@@ -212,7 +212,7 @@ def test_config_knobs(tcr):
             assert oracle.within_tolerance(g, es), (st, kb, ct, ch, g, es.f64())
             assert g == _reduce(tcr, x, "bulk")
     finally:
-        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
+        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 0)
         tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 8)
         tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
         for key, val in ((tcr.TCR_CFG_BULK_STAGES, 6), (tcr.TCR_CFG_BULK_STAGE_KB, 16),

@@ -69,7 +69,7 @@ def test_precision_vs_chain_length():
         tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 8)
         tcr.tcr_set_config(tcr.TCR_CFG_TC05_CTAS_PER_SM, 3)
         tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
-        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
+        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 0)
         tcr.tcr_set_config(tcr.TCR_CFG_TC05_CHAIN, 4)
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/precision.json", "w") as f:
