@@ -28,3 +28,38 @@ def test_bench_two_ranks_shared_gpu(algo):
     assert d["n_gpus"] == 2 and d["config"]["n_total"] == 2 << 24
     assert d["gpu_launches"] >= 3 and d["e2e"]["h2d_bytes_per_step"] == 2 << 24
     assert d["test_mode"].startswith("shared-gpu")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extra", [[], ["--impl", "reference"], ["--workload", "c5"]])
+def test_bench_json_contract_single_gpu(extra):
+    """bench.py at N = 1: one JSON line carrying every key of the contract."""
+    cmd = [sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--e2e-steps", "1",
+           "--n-per-rank", str(1 << 24)] + extra
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
+              "cpu_baseline"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3
+    assert d["higher_is_better"] is True and d["value"] > 0
+    assert "workload" in d["config"]
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    if extra[:2] == ["--impl", "reference"]:
+        assert d["impl"] == "reference"
+        assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+        return
+    rf = d["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and rf["peak"] > 0
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    assert d["gpu_launches"] == 5  # one launch of the reduction kernel per step
+    ck = d["clocks"]
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(ck)
+    if "c5" not in extra:
+        e = d["e2e"]
+        assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 << 24 and e["d2h_bytes_per_step"] == 4

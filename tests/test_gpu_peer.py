@@ -57,12 +57,18 @@ def _shards(n, P):
 @pytest.mark.parametrize("algo", ["mma_sync", "shuffle"])
 @pytest.mark.parametrize("n", [0, 1, 4097, 1_000_003])
 def test_single_rank_equals_f64_entry(tcr, mailboxes, algo, n):
-    """nranks = 1: the fused kernel is the ordinary reduction plus 0.0 + v."""
+    """nranks = 1: the fused kernel is the ordinary reduction plus 0.0 + v
+    (compared at the peer variant's fixed unroll of 4, so both launches use
+    the same grid and chain)."""
     import torch
 
     x = _dev(gen.generate(3, 0, n, gen.UNIFORM_PM1))
     ref = torch.empty(1, dtype=torch.float64, device="cuda")
-    tcr.tcr_reduce_sum_ex(x, out_f64=ref, algo=algo)
+    tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
+    try:
+        tcr.tcr_reduce_sum_ex(x, out_f64=ref, algo=algo)
+    finally:
+        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 0)
     o64 = torch.full((1,), float("nan"), dtype=torch.float64, device="cuda")
     o32 = torch.full((1,), float("nan"), dtype=torch.float32, device="cuda")
     for _ in range(3):  # consecutive epochs on the same mailbox
