@@ -138,7 +138,8 @@ tcr_status tcr_reduce_sum_algo(const tcr_half *x, size_t n, float *out_f32, doub
  * element-aligned; fp8 elements are 1 byte).
  * Same accuracy contract (|g - R| <= 2^-20 * sum|x_i| while the sum is
  * inside the binary32 range) and error behaviour; TCR_ERR_INVALID_VALUE for
- * an unknown dtype.  (The exact and host entry points are binary16 only.)
+ * an unknown dtype.  (The exact, host and peer entry points are binary16
+ * only, except tcr_reduce_sum_peer, which takes a dtype too.)
  */
 tcr_status tcr_reduce_sum_ex(const void *x, size_t n, tcr_dtype dtype, float *out_f32,
                              double *out_f64, tcr_algo algo, tcr_stream stream);
@@ -159,7 +160,8 @@ tcr_status tcr_reduce_sum_segmented(const tcr_half *x, const int64_t *offsets,
                                     size_t num_segments, float *out, tcr_stream stream);
 tcr_status tcr_reduce_sum_segmented_shuffle(const tcr_half *x, const int64_t *offsets,
                                             size_t num_segments, float *out, tcr_stream stream);
-/* Segmented for either input type; algo = DEFAULT / MMA_SYNC (MMA) or SHUFFLE. */
+/* Segmented for any input type (binary16, bfloat16, fp8 E4M3 / E5M2; offsets
+ * in elements of that type); algo = DEFAULT / MMA_SYNC (MMA) or SHUFFLE. */
 tcr_status tcr_reduce_sum_segmented_ex(const void *x, tcr_dtype dtype, const int64_t *offsets,
                                        size_t num_segments, float *out, tcr_algo algo,
                                        tcr_stream stream);
@@ -172,6 +174,10 @@ tcr_status tcr_reduce_sum_batched(const tcr_half *x, size_t num_segments, size_t
                                   float *out, tcr_stream stream);
 tcr_status tcr_reduce_sum_batched_shuffle(const tcr_half *x, size_t num_segments,
                                           size_t segment_len, float *out, tcr_stream stream);
+/* Batched for any input type (segment_len in elements of that type). */
+tcr_status tcr_reduce_sum_batched_ex(const void *x, tcr_dtype dtype, size_t num_segments,
+                                     size_t segment_len, float *out, tcr_algo algo,
+                                     tcr_stream stream);
 
 /*
  * tcr_reduce_sum_host -- end-to-end form: x is a HOST pointer (pinned

@@ -96,6 +96,7 @@ _SIGS = {
     "tcr_reduce_sum_segmented": [_P, _P, _SZ, _P, _P],
     "tcr_reduce_sum_ex": [_P, _SZ, _I, _P, _P, _I, _P],
     "tcr_reduce_sum_segmented_ex": [_P, _I, _P, _SZ, _P, _I, _P],
+    "tcr_reduce_sum_batched_ex": [_P, _I, _SZ, _SZ, _P, _I, _P],
     "tcr_reduce_sum_segmented_shuffle": [_P, _P, _SZ, _P, _P],
     "tcr_reduce_sum_batched": [_P, _SZ, _SZ, _P, _P],
     "tcr_reduce_sum_batched_shuffle": [_P, _SZ, _SZ, _P, _P],
@@ -229,6 +230,17 @@ def tcr_reduce_sum_segmented_ex(x, offsets, out, algo=TCR_ALGO_DEFAULT, dtype=No
     _check(_lib.tcr_reduce_sum_segmented_ex(_ptr(x), _dtype_of(x, dtype), _ptr(offsets), s,
                                             _ptr(out), int(algo), _stream(stream, x)),
            "tcr_reduce_sum_segmented_ex")
+
+
+def tcr_reduce_sum_batched_ex(x, segment_len, out, algo=TCR_ALGO_DEFAULT, dtype=None,
+                              num_segments=None, stream=None) -> None:
+    """Batched sums for any input type (segment_len in elements)."""
+    if isinstance(algo, str):
+        algo = ALGOS[algo]
+    s = int(num_segments) if num_segments is not None else int(out.numel())
+    _check(_lib.tcr_reduce_sum_batched_ex(_ptr(x), _dtype_of(x, dtype), s, int(segment_len),
+                                          _ptr(out), int(algo), _stream(stream, x)),
+           "tcr_reduce_sum_batched_ex")
 
 
 def tcr_reduce_sum_segmented(x, offsets, out, num_segments=None, stream=None) -> None:
@@ -433,7 +445,7 @@ def reduce_sum(x, algo: str | int = "default", exact: bool = False, out_dtype=No
 
 
 def reduce_sum_segmented(x, offsets, mma: bool = True, stream=None):
-    """Per-segment sums of a float16 / bfloat16 CUDA tensor over CSR int64 offsets."""
+    """Per-segment sums of a float16 / bfloat16 / float8 CUDA tensor over CSR int64 offsets."""
     import torch
 
     out = torch.empty(offsets.numel() - 1, dtype=torch.float32, device=x.device)

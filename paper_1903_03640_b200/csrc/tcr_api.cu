@@ -251,12 +251,12 @@ tcr_status peer_impl(const void* x, size_t n, int dtype, int algo, void* const* 
                         emulate ? "peer-emulated reduce launch" : "peer reduce launch");
 }
 
-tcr_status segmented_impl(bool mma, bool batched, const tcr_half* x, const int64_t* offsets,
-                          size_t S, size_t L, float* out, cudaStream_t stream, bool bf16 = false) {
+tcr_status segmented_impl(bool mma, bool batched, const void* x, const int64_t* offsets,
+                          size_t S, size_t L, float* out, cudaStream_t stream, int fmt = 0) {
     if (!out && S) return fail(TCR_ERR_INVALID_VALUE, "null out");
     if (!batched && !offsets && S) return fail(TCR_ERR_INVALID_VALUE, "null offsets");
     if (!x && S && (batched ? L != 0 : true)) return fail(TCR_ERR_INVALID_VALUE, "null x");
-    if (!aligned(x, 2) || !aligned(out, 4) || !aligned(offsets, 8))
+    if (!aligned(x, fmt >= TCR_DTYPE_E4M3 ? 1 : 2) || !aligned(out, 4) || !aligned(offsets, 8))
         return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
     if (S == 0) return TCR_OK;
     DeviceInfo di;
@@ -265,8 +265,7 @@ tcr_status segmented_impl(bool mma, bool batched, const tcr_half* x, const int64
     if (s != TCR_OK) return s;
     const LaunchCfg cfg = make_cfg(di);
     return after_launch(
-        tcr::launch_reduce_segmented(mma, bf16, batched, x, offsets, S, L, out, ws->dev, cfg,
-                                     stream),
+        tcr::launch_reduce_segmented(mma, fmt, batched, x, offsets, S, L, out, ws->dev, cfg, stream),
         "segmented kernel launch");
 }
 
@@ -302,12 +301,23 @@ tcr_status tcr_reduce_sum_ex(const void* x, size_t n, tcr_dtype dtype, float* ou
 tcr_status tcr_reduce_sum_segmented_ex(const void* x, tcr_dtype dtype, const int64_t* offsets,
                                        size_t num_segments, float* out, tcr_algo algo,
                                        tcr_stream stream) {
-    if (dtype != TCR_DTYPE_F16 && dtype != TCR_DTYPE_BF16)
-        return fail(TCR_ERR_INVALID_VALUE, "segmented: dtype must be F16 or BF16");
+    if (dtype < TCR_DTYPE_F16 || dtype > TCR_DTYPE_E5M2)
+        return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
     if (algo != TCR_ALGO_DEFAULT && algo != TCR_ALGO_MMA_SYNC && algo != TCR_ALGO_SHUFFLE)
         return fail(TCR_ERR_INVALID_VALUE, "segmented algo must be DEFAULT, MMA_SYNC or SHUFFLE");
-    return segmented_impl(algo != TCR_ALGO_SHUFFLE, false, static_cast<const tcr_half*>(x), offsets,
-                          num_segments, 0, out, (cudaStream_t)stream, dtype == TCR_DTYPE_BF16);
+    return segmented_impl(algo != TCR_ALGO_SHUFFLE, false, x, offsets, num_segments, 0, out,
+                          (cudaStream_t)stream, (int)dtype);
+}
+
+tcr_status tcr_reduce_sum_batched_ex(const void* x, tcr_dtype dtype, size_t num_segments,
+                                     size_t segment_len, float* out, tcr_algo algo,
+                                     tcr_stream stream) {
+    if (dtype < TCR_DTYPE_F16 || dtype > TCR_DTYPE_E5M2)
+        return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
+    if (algo != TCR_ALGO_DEFAULT && algo != TCR_ALGO_MMA_SYNC && algo != TCR_ALGO_SHUFFLE)
+        return fail(TCR_ERR_INVALID_VALUE, "batched algo must be DEFAULT, MMA_SYNC or SHUFFLE");
+    return segmented_impl(algo != TCR_ALGO_SHUFFLE, true, x, nullptr, num_segments, segment_len, out,
+                          (cudaStream_t)stream, (int)dtype);
 }
 
 tcr_status tcr_reduce_sum_segmented(const tcr_half* x, const int64_t* offsets,

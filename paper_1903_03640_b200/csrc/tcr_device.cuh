@@ -222,6 +222,28 @@ __device__ __forceinline__ uint4 mask_vec(uint4 v, int64_t e0, int64_t lo, int64
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// mask_vec for any element format: bytes of elements outside [lo, hi) zeroed
+// (e0 = element index of the vector's first element).
+template <int F>
+__device__ __forceinline__ uint4 mask_vec_f(uint4 v, int64_t e0, int64_t lo, int64_t hi) {
+    if constexpr (FmtInfo<F>::kBytes == 2) {
+        return mask_vec(v, e0, lo, hi);
+    } else {
+        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint32_t m = 0u;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int64_t i = e0 + 4 * k + b;
+                if (i >= lo && i < hi) m |= 0xFFu << (8 * b);
+            }
+            w[k] &= m;
+        }
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
 // A lane's 8 halves of a ragged (masked) tile: elements p[8*lane + k] for
 // 8*lane + k < cnt, zero elsewhere; scalar loads, never out of bounds.
 __device__ __forceinline__ uint4 load_ragged(const uint16_t* p, int cnt, int lane) {

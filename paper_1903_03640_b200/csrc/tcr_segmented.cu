@@ -27,24 +27,30 @@ constexpr unsigned long long kBatchSeg = 8;  // segments per scheduler atomic (g
 // collapsed (D' = 1 x D, three DMMAs) and written to out[j].  Long segments
 // therefore stream at full width and many short segments share a round trip.
 // The next batch's index and offsets are fetched during the current batch.
-template <bool kMma, bool kBf16>
+// F = element format (binary16, bfloat16, fp8 E4M3 / E5M2): a 16-byte vector
+// holds EPV = 16 / bytes elements and a 512-byte tile 32 * EPV; all element
+// indices below are in elements of that format.
+template <bool kMma, int F>
 __device__ __forceinline__ void seg_piece(const uint4& v, double& acc, int lane) {
     if constexpr (kMma) {
         float c[4] = {0.f, 0.f, 0.f, 0.f};
-        mma_rowsum_t<kBf16>(c, v);
+        mma_rowsum_f<F>(c, v);
         flush_rows(c, acc, lane);
     } else {
-        acc += (double)vec_sum_t<kBf16>(v);
+        acc += (double)vec_sum_f<F>(v);
     }
 }
 
-template <bool kMma, bool kBf16, bool kBatched, int U, int WARPS>
+template <bool kMma, int F, bool kBatched, int U, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 4)
-reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restrict__ offsets,
+reduce_segmented_kernel(const uint8_t* __restrict__ x, const int64_t* __restrict__ offsets,
                         size_t S, size_t L, int batch, float* __restrict__ out, DevWorkspace ws) {
+    constexpr int kLogEpv = FmtInfo<F>::kBytes == 2 ? 3 : 4;  // log2(elements per vector)
+    constexpr int64_t kEpv = (int64_t)1 << kLogEpv;
+    constexpr int64_t kTileEl = 32 * kEpv;                     // elements per 512-byte tile
     const int lane = threadIdx.x & 31;
     const uintptr_t addr = (uintptr_t)x;
-    const int64_t shift = (int64_t)((addr & 15u) >> 1);
+    const int64_t shift = (int64_t)((addr & 15u) / FmtInfo<F>::kBytes);
     const uint4* xb = reinterpret_cast<const uint4*>(addr & ~(uintptr_t)15u);
     const unsigned total_warps = gridDim.x * WARPS;
     const unsigned long long tail_zone = 2ull * total_warps * (unsigned long long)batch;
@@ -87,14 +93,14 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
         // Tiles sit on absolute 256-element boundaries (relative to xb), so the
         // arithmetic of a segment never depends on which batch / warp reduced
         // it (bitwise determinism under dynamic scheduling).
-        const int64_t Vlo = r0 >> 3, V1 = (r1 + 7) >> 3;
+        const int64_t Vlo = r0 >> kLogEpv, V1 = (r1 + kEpv - 1) >> kLogEpv;
         const int64_t V0 = Vlo & ~(int64_t)31;
         int cs = 0;
         int64_t sb = r0, se = off(1);
         double acc = 0.0;
         for (int64_t vb = V0; vb < V1; vb += 32 * U) {
             uint4 v[U];
-            const int64_t f0 = (r0 + 7) >> 3, f1 = r1 >> 3;
+            const int64_t f0 = (r0 + kEpv - 1) >> kLogEpv, f1 = r1 >> kLogEpv;
             if (vb >= f0 && vb + 32 * U <= f1) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) v[u] = ldg_stream(xb + vb + u * 32 + lane);
@@ -103,11 +109,12 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
                 for (int u = 0; u < U; ++u) {
                     const int64_t vi = vb + u * 32 + lane;
                     v[u] = make_uint4(0u, 0u, 0u, 0u);
-                    if (vi >= Vlo && vi < V1) v[u] = mask_vec(ldg_stream(xb + vi), vi * 8, r0, r1);
+                    if (vi >= Vlo && vi < V1)
+                        v[u] = mask_vec_f<F>(ldg_stream(xb + vi), vi * kEpv, r0, r1);
                 }
             }
             __syncwarp();  // scheduling fence: all U loads issue before the first consumer
-            const int64_t g0 = vb * 8, g1 = g0 + (int64_t)U * kTileElems;
+            const int64_t g0 = vb * kEpv, g1 = g0 + (int64_t)U * kTileEl;
             if (cs < nb && sb <= g0 && se > g1) {
                 // the whole group lies inside segment cs (the common case for long
                 // segments): U independent tiles, no per-tile control flow; each
@@ -117,27 +124,27 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         c[u][0] = c[u][1] = c[u][2] = c[u][3] = 0.f;
-                        mma_rowsum_t<kBf16>(c[u], v[u]);
+                        mma_rowsum_f<F>(c[u], v[u]);
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) flush_rows(c[u], acc, lane);
                 } else {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) acc += (double)vec_sum_t<kBf16>(v[u]);
+                    for (int u = 0; u < U; ++u) acc += (double)vec_sum_f<F>(v[u]);
                 }
                 continue;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int64_t t0 = (vb + u * 32) * 8, t1 = t0 + kTileElems;  // tile elements
+                const int64_t t0 = (vb + u * 32) * kEpv, t1 = t0 + kTileEl;  // tile elements
                 if (t0 >= r1) break;
                 while (cs < nb) {
                     if (sb >= t1) break;  // current segment starts after this tile
                     if (sb <= t0 && se >= t1) {  // tile entirely inside segment cs
-                        seg_piece<kMma, kBf16>(v[u], acc, lane);
+                        seg_piece<kMma, F>(v[u], acc, lane);
                     } else if (se > sb && se > t0) {  // the part of the tile inside [sb, se)
-                        seg_piece<kMma, kBf16>(mask_vec(v[u], (vb + u * 32 + lane) * 8, sb, se), acc,
-                                               lane);
+                        seg_piece<kMma, F>(mask_vec_f<F>(v[u], (vb + u * 32 + lane) * kEpv, sb, se),
+                                           acc, lane);
                     }
                     if (se > t1) break;  // segment continues in the next tile
                     const double tot = warp_collapse<kMma>(acc);  // segment cs ends in this tile
@@ -168,14 +175,14 @@ reduce_segmented_kernel(const uint16_t* __restrict__ x, const int64_t* __restric
     }
 }
 
-// Fixed-length rows of T whole tiles (L = 256*T, T in {1, 2, 4, 8}, x 16-byte
-// aligned): every group of 8 tiles holds 8/T complete rows, so a warp issues
+// Fixed-length rows of T whole 512-byte tiles (L = T * tile elements, T in
+// {1, 2, 4, 8}, x 16-byte aligned): every group of 8 tiles holds 8/T complete rows, so a warp issues
 // its 8 loads, 8 independent MMAs (C = 0), folds them per row and collapses
 // the 8/T rows with no data-dependent control flow.  Rows are dealt to warps
 // statically (all rows cost the same: no scheduler, no atomics).
-template <bool kMma, bool kBf16, int T, int WARPS>
+template <bool kMma, int F, int T, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 4)
-reduce_rows_kernel(const uint16_t* __restrict__ x, size_t S, float* __restrict__ out) {
+reduce_rows_kernel(const uint8_t* __restrict__ x, size_t S, float* __restrict__ out) {
     constexpr int R = 8 / T;  // rows per group
     const int lane = threadIdx.x & 31;
     const uint4* xv = reinterpret_cast<const uint4*>(x) + lane;
@@ -198,10 +205,10 @@ reduce_rows_kernel(const uint16_t* __restrict__ x, size_t S, float* __restrict__
         for (int u = 0; u < 8; ++u) {
             if constexpr (kMma) {
                 float c[4] = {0.f, 0.f, 0.f, 0.f};
-                mma_rowsum_t<kBf16>(c, v[u]);
+                mma_rowsum_f<F>(c, v[u]);
                 flush_rows(c, acc[u / T], lane);
             } else {
-                acc[u / T] += (double)vec_sum_t<kBf16>(v[u]);
+                acc[u / T] += (double)vec_sum_f<F>(v[u]);
             }
         }
 #pragma unroll
@@ -216,40 +223,54 @@ constexpr int kSegWarps = 8;
 constexpr int kSegUnroll = 8;  // tiles per group (one round trip)
 constexpr int kSegCtasPerSm = 4;  // resident CTAs per SM at <= 64 registers (launch bounds)
 
-template <bool kMma, bool kBf16>
-static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, const uint16_t* x,
+template <bool kMma, int F>
+static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, const uint8_t* x,
                          const int64_t* offsets, size_t S, size_t L, float* out,
                          const DevWorkspace& ws, cudaStream_t stream, int sms) {
+    constexpr size_t kTileEl = 512 / FmtInfo<F>::kBytes;
     if (batched && ((uintptr_t)x & 15u) == 0 &&
-        (L == 256 || L == 512 || L == 1024 || L == 2048)) {
-        const size_t groups = (S + 8 * 256 / L - 1) / (8 * 256 / L);
+        (L == kTileEl || L == 2 * kTileEl || L == 4 * kTileEl || L == 8 * kTileEl)) {
+        const size_t rows_per_group = 8 * kTileEl / L;
+        const size_t groups = (S + rows_per_group - 1) / rows_per_group;
         size_t g = (groups + kSegWarps - 1) / kSegWarps;
         const size_t gmax = (size_t)sms * kSegCtasPerSm;
         if (g > gmax) g = gmax;
         if (g < 1) g = 1;
         const dim3 rgrid((unsigned)g);
-        switch (L) {
-            case 256: reduce_rows_kernel<kMma, kBf16, 1, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
-            case 512: reduce_rows_kernel<kMma, kBf16, 2, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
-            case 1024: reduce_rows_kernel<kMma, kBf16, 4, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
-            default: reduce_rows_kernel<kMma, kBf16, 8, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
+        switch (L / kTileEl) {
+            case 1: reduce_rows_kernel<kMma, F, 1, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
+            case 2: reduce_rows_kernel<kMma, F, 2, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
+            case 4: reduce_rows_kernel<kMma, F, 4, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
+            default: reduce_rows_kernel<kMma, F, 8, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
         }
         return;
     }
     if (batched) {
-        // ~16K elements per batch for short fixed lengths, at least 8 segments
-        size_t b = L ? ((size_t)16384 / L) : 255;
+        // ~32 KiB per batch for short fixed lengths, at least 8 segments
+        size_t b = L ? ((size_t)32768 / FmtInfo<F>::kBytes / L) : 255;
         if (b < kBatchSeg) b = kBatchSeg;
         if (b > 255) b = 255;
-        reduce_segmented_kernel<kMma, kBf16, true, kSegUnroll, kSegWarps>
+        reduce_segmented_kernel<kMma, F, true, kSegUnroll, kSegWarps>
             <<<grid, block, 0, stream>>>(x, offsets, S, L, (int)b, out, ws);
     } else {
-        reduce_segmented_kernel<kMma, kBf16, false, kSegUnroll, kSegWarps>
+        reduce_segmented_kernel<kMma, F, false, kSegUnroll, kSegWarps>
             <<<grid, block, 0, stream>>>(x, offsets, S, L, (int)kBatchSeg, out, ws);
     }
 }
 
-cudaError_t launch_reduce_segmented(bool mma, bool bf16, bool batched, const uint16_t* x,
+template <bool kMma>
+static void launch_seg_m(int fmt, bool batched, const dim3& grid, const dim3& block,
+                         const uint8_t* x, const int64_t* offsets, size_t S, size_t L, float* out,
+                         const DevWorkspace& ws, cudaStream_t stream, int sms) {
+    switch (fmt) {
+        case kBF16: launch_seg_t<kMma, kBF16>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms); break;
+        case kE4M3: launch_seg_t<kMma, kE4M3>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms); break;
+        case kE5M2: launch_seg_t<kMma, kE5M2>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms); break;
+        default: launch_seg_t<kMma, kF16>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms); break;
+    }
+}
+
+cudaError_t launch_reduce_segmented(bool mma, int fmt, bool batched, const void* x,
                                     const int64_t* offsets, size_t num_segments,
                                     size_t segment_len, float* out, const DevWorkspace& ws,
                                     const LaunchCfg& cfg, cudaStream_t stream) {
@@ -258,13 +279,13 @@ cudaError_t launch_reduce_segmented(bool mma, bool bf16, bool batched, const uin
     if (g > gmax) g = gmax;
     if (g < 1) g = 1;
     const dim3 grid((unsigned)g), block(kSegWarps * 32);
-    if (mma) {
-        if (bf16) launch_seg_t<true, true>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream, cfg.sms);
-        else launch_seg_t<true, false>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream, cfg.sms);
-    } else {
-        if (bf16) launch_seg_t<false, true>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream, cfg.sms);
-        else launch_seg_t<false, false>(batched, grid, block, x, offsets, num_segments, segment_len, out, ws, stream, cfg.sms);
-    }
+    const uint8_t* xb = static_cast<const uint8_t*>(x);
+    if (mma)
+        launch_seg_m<true>(fmt, batched, grid, block, xb, offsets, num_segments, segment_len, out, ws,
+                           stream, cfg.sms);
+    else
+        launch_seg_m<false>(fmt, batched, grid, block, xb, offsets, num_segments, segment_len, out, ws,
+                            stream, cfg.sms);
     return cudaGetLastError();
 }
 

@@ -89,3 +89,62 @@ def test_fp8_full_size(tcr, fmt):
     for algo in ALGOS:
         g = _sum(tcr, x, algo)
         assert oracle.within_tolerance(g, es), (algo, g, es.f64())
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("algo", ["mma_sync", "shuffle"])
+def test_fp8_segmented_edges_and_mix(tcr, fmt, algo):
+    """CSR segments of fp8: every segment vs the exact fp8 oracle, with
+    lengths around the 16-element vector and 512-element tile boundaries,
+    empty segments, odd byte offsets, and a log-uniform mix."""
+    import torch
+
+    lens = [0, 1, 2, 15, 16, 17, 31, 511, 512, 513, 0, 1023, 1024, 1025, 8191, 65536, 3, 0, 70001]
+    lens = np.array(lens + list(gen.loguniform_lengths(5, 500)), dtype=np.int64)
+    for start in (0, 5, 17):
+        off = gen.offsets_from_lengths(lens, start=start)
+        bits = gen.generate_fp8(31 + start, 0, int(off[-1]) + 7, gen.WIDE, fmt)
+        for xoff in (0, 3):
+            out = torch.full((len(lens),), float("nan"), dtype=torch.float32, device="cuda")
+            tcr.tcr_reduce_sum_segmented_ex(_dev(bits, xoff, fmt), torch.from_numpy(off).cuda(), out,
+                                            algo=algo)
+            torch.cuda.synchronize()
+            g = out.cpu().numpy()
+            for j in range(len(lens)):
+                es = oracle.exact_sum_fp8(bits[off[j]:off[j + 1]], fmt)
+                assert oracle.within_tolerance(float(g[j]), es), (start, xoff, j, g[j], es.f64())
+                if lens[j] == 0:
+                    assert g[j] == 0.0
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("algo", ["mma_sync", "shuffle"])
+def test_fp8_batched(tcr, fmt, algo):
+    """Fixed-length fp8 rows: L = 512 * T takes the whole-tile rows kernel
+    (16-byte-aligned x), other L and misaligned x the union-stream kernel."""
+    import torch
+
+    for L, S in ((512, 3000), (1024, 999), (2048, 300), (4096, 129), (511, 777), (100, 5000),
+                 (65536, 9)):
+        bits = gen.generate_fp8(L, 0, L * S, gen.UNIFORM_PM1, fmt)
+        ref = [oracle.exact_sum_fp8(bits[j * L:(j + 1) * L], fmt) for j in range(S)]
+        for xoff in (0, 1):
+            out = torch.full((S,), float("nan"), dtype=torch.float32, device="cuda")
+            tcr.tcr_reduce_sum_batched_ex(_dev(bits, xoff, fmt), L, out, algo=algo)
+            torch.cuda.synchronize()
+            g = out.cpu().numpy()
+            assert all(oracle.within_tolerance(float(g[j]), ref[j]) for j in range(S)), (L, S, xoff)
+
+
+def test_fp8_segment_index_bit_exact(tcr):
+    """All-ones fp8 data and pairwise-distinct lengths: out[j] == len(j) exactly."""
+    import torch
+
+    for fmt, one in ((oracle.FP8_E4M3, 0x38), (oracle.FP8_E5M2, 0x3C)):
+        lens = np.random.default_rng(1).permutation(np.arange(0, 4000, 3))
+        off = gen.offsets_from_lengths(lens, start=7)
+        bits = np.full(int(off[-1]) + 16, one, dtype=np.uint8)
+        out = torch.empty(len(lens), dtype=torch.float32, device="cuda")
+        tcr.tcr_reduce_sum_segmented_ex(_dev(bits, 1, fmt), torch.from_numpy(off).cuda(), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), lens.astype(np.float32))
