@@ -8,7 +8,8 @@ median over batches, after warm-up):
              each reducing n/P elements and exchanging partials through the
              mailboxes (the on-chip cost of the protocol; the NVLink latency of
              a real group is not in this number)
-Sizes: 2^24 (C2, latency-bound: the protocol cost is visible) and 2^30 (C3).
+Sizes: 2^24 (C2, latency-bound: the protocol cost is visible), 2^30 (C3)
+and 2^33 (C4's total, 16 GiB: P = 8 emulated is C4's 8-GPU problem on one GPU).
 """
 import json
 import statistics
@@ -48,17 +49,18 @@ def timed(fn, boxes, reps=50, warm=5):
 def main():
     boxes = [tcr.tcr_peer_mailbox_alloc() for _ in range(tcr.TCR_MAX_PEERS)]
     res = {}
-    for logn in (24, 30):
+    for logn in (24, 30, 33):
         n = 1 << logn
         x = gen.generate_tensor(gen.SEED_C3, 0, n, gen.UNIFORM_PM1)
         o = torch.empty(8, dtype=torch.float64, device="cuda")
+        reps = 20 if logn >= 33 else 50
         r = {"plain_us": timed(lambda: tcr.tcr_reduce_sum_ex(x, out_f64=o[:1], algo="mma_sync"),
-                               boxes),
+                               boxes, reps),
              "peer_P1_us": timed(lambda: tcr.tcr_reduce_sum_peer(x, boxes[:1], 0, out_f64=o[:1]),
-                                 boxes)}
+                                 boxes, reps)}
         for P in (1, 2, 4, 8):
             r[f"emulated_P{P}_us"] = timed(
-                lambda: tcr.tcr_reduce_sum_peer_emulated(x, boxes[:P], out_f64=o[:P]), boxes)
+                lambda: tcr.tcr_reduce_sum_peer_emulated(x, boxes[:P], out_f64=o[:P]), boxes, reps)
         r["gbs_plain"] = 2 * n / (r["plain_us"] * 1e-6) / 1e9
         r["gbs_emulated_P8"] = 2 * n / (r["emulated_P8_us"] * 1e-6) / 1e9
         res[f"n=2^{logn}"] = r
