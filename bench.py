@@ -294,20 +294,31 @@ def main():
                                     bf16=args.dtype == "bf16")
         bytes_per_step = x.element_size() * n
         elems_per_step = n
+        job_elems_per_step = world * n
+        job_bytes_per_step = world * bytes_per_step
         workload = (f"c3: sum of n=2^{n.bit_length() - 1} fp16 uniform[-1,1] per GPU"
                     if world == 1 else
                     f"c4: sharded sum, n=2^{(n * world).bit_length() - 1} fp16 over {world} GPUs")
     else:
-        S = 1 << 20
-        lens = gen.loguniform_lengths(gen.SEED_C5, S)
-        off = gen.offsets_from_lengths(lens)
+        from paper_1903_03640_b200.sharded import segment_shard
+
+        S_all = 1 << 20
+        lens = gen.loguniform_lengths(gen.SEED_C5, S_all)
+        off_all = gen.offsets_from_lengths(lens)
+        # N > 1: whole segments sharded by element count (no collective; strong scaling)
+        j0, j1 = segment_shard(off_all, world, rank)
+        S = j1 - j0
+        off = off_all[j0:j1 + 1] - off_all[j0]
         n = int(off[-1])
-        x = gen.generate_tensor(gen.SEED_C5, 0, n, gen.UNIFORM_PM1, device=dev)
+        x = gen.generate_tensor(gen.SEED_C5, int(off_all[j0]), n, gen.UNIFORM_PM1, device=dev)
         toff = torch.from_numpy(off).to(dev)
-        seg_out = torch.empty(S, dtype=torch.float32, device=dev)
+        seg_out = torch.empty(max(S, 1), dtype=torch.float32, device=dev)
         bytes_per_step = 2 * n + 8 * (S + 1) + 4 * S
         elems_per_step = n
-        workload = "c5: 2^20 segments, log-uniform lengths in [256, 65536], fp16 uniform[-1,1]"
+        job_elems_per_step = int(off_all[-1])
+        job_bytes_per_step = 2 * job_elems_per_step + 8 * (S_all + world) + 4 * S_all
+        workload = "c5: 2^20 segments, log-uniform lengths in [256, 65536], fp16 uniform[-1,1]" + (
+            f", segments sharded over {world} GPUs" if world > 1 else "")
     out32 = torch.empty(1, dtype=torch.float32, device=dev)
     out64 = torch.empty(1, dtype=torch.float64, device=dev)
     acc6 = torch.empty(6, dtype=torch.int64, device=dev)
@@ -338,7 +349,7 @@ def main():
             if ev_k0 is not None:
                 ev_k0.record(stream)
             if args.workload == "c5":
-                tcr.tcr_reduce_sum_segmented(x, toff, seg_out, stream=stream)
+                tcr.tcr_reduce_sum_segmented(x, toff, seg_out, num_segments=S, stream=stream)
             elif peer is not None:  # reduction + cross-GPU combine in ONE launch
                 peer.reduce_sum(x, out_f32=out32, algo=algo, stream=stream)
             elif exact:
@@ -407,7 +418,7 @@ def main():
     # here only record the value for the log
     result = float(out32.item()) if args.workload == "c3" else float(seg_out[0].item())
 
-    value = world * elems_per_step * K / (total_ms * 1e-3) / 1e9  # Gelem/s, whole job
+    value = job_elems_per_step * K / (total_ms * 1e-3) / 1e9  # Gelem/s, whole job
     achieved = bytes_per_step / (kern_ms * 1e-3) / 1e9              # GB/s of the dominant kernel
     if args.algo != "default":
         algo_name = args.algo
@@ -461,7 +472,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "scaling": "strong" if args.workload == "c5" and world > 1 else "weak",
+            "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (splitmix64-seeded, generated on the device)",
             "config": {"workload": workload, "algo": algo_name, "n_per_rank": n,
                        "knobs": {k: tcr.tcr_get_config(v) for k, v in (
@@ -471,7 +483,7 @@ def main():
                            ("tc05_chain", tcr.TCR_CFG_TC05_CHAIN), ("tc05_ctas", tcr.TCR_CFG_TC05_CTAS_PER_SM),
                            ("tc05_prefetch", tcr.TCR_CFG_TC05_PREFETCH), ("tc05_split", tcr.TCR_CFG_TC05_SPLIT),
                            ("tc05_interleave", tcr.TCR_CFG_TC05_INTERLEAVE))},
-                       "n_total": n * world, "l2": "inputs larger than L2 (no flush needed)",
+                       "n_total": job_elems_per_step, "l2": "inputs larger than L2 (no flush needed)",
                        "combine": ("fused in-kernel NVLink mailbox combine (peer.py)" if peer
                                    else "NCCL allreduce of fp64 partials") if world > 1 or peer
                                   else "none (single GPU)",
@@ -486,8 +498,8 @@ def main():
                                               if single_launch_step else
                                               "mean of per-step CUDA event pairs around the kernel"),
                          "algorithmic_bytes_per_launch": bytes_per_step},
-            "hbm_gbs": world * bytes_per_step * K / (total_ms * 1e-3) / 1e9,
-            "frac_of_8tbs": world * bytes_per_step * K / (total_ms * 1e-3) / (world * 8e12),
+            "hbm_gbs": job_bytes_per_step * K / (total_ms * 1e-3) / 1e9,
+            "frac_of_8tbs": job_bytes_per_step * K / (total_ms * 1e-3) / (world * 8e12),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -63,3 +63,23 @@ def test_bench_json_contract_single_gpu(extra):
     if "c5" not in extra:
         e = d["e2e"]
         assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 << 24 and e["d2h_bytes_per_step"] == 4
+
+
+@pytest.mark.gpu
+def test_bench_c5_two_ranks_shared_gpu():
+    """C5 at N = 2: whole segments sharded by element count, no collective,
+    strong scaling; job element count = the whole C5 workload."""
+    env = dict(os.environ, TCR_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29407", "bench.py", "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--workload", "c5"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    import tcr_inputs as gen
+
+    total = int(gen.offsets_from_lengths(gen.loguniform_lengths(gen.SEED_C5, 1 << 20))[-1])
+    assert d["scaling"] == "strong" and d["config"]["n_total"] == total and d["n_gpus"] == 2
+    assert d["gpu_launches"] == 3
