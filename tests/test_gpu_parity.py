@@ -344,9 +344,13 @@ def test_full_size_c4_on_one_gpu(tcr):
     for lo in range(0, n, chunk):  # oracle over 1 GiB-element host chunks
         bits = x[lo:lo + chunk].view(torch.int16).cpu().numpy().view(np.uint16)
         es = es + oracle.exact_sum_fp16(bits, threads=os.cpu_count() or 8)
-    for algo in ("default", "tcgen05", "shuffle"):
+    for algo in ("default", "tcgen05", "shuffle", "bulk"):
         g = _reduce(tcr, x, algo)
         assert oracle.within_tolerance(g, es), (algo, g, es.f64())
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    tcr.tcr_reduce_sum_exact(x, out_f32=o32)  # NEXT-3 at 2^33: bitwise
+    torch.cuda.synchronize()
+    assert float(o32.item()) == es.f32()
     P = 8
     parts = torch.empty(P, dtype=torch.float64, device="cuda")
     for r in range(P):
