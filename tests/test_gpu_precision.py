@@ -83,3 +83,47 @@ def test_precision_vs_chain_length():
     # truncating accumulator: the all-positive error grows with the chain
     u01 = {r["K"]: r["err_f64_units"] for r in rows if r["dist"] == "uniform01" and r["algo"] == "tcgen05"}
     assert u01[64] > u01[4]
+
+
+def test_precision_other_encodings():
+    """NEXT-1 x NEXT-4: error of every path for bfloat16 and fp8 inputs at the
+    default chain, against each format's exact oracle (2^24 elements;
+    written to gpurun_out/precision_encodings.json).  bfloat16 has 8
+    significand bits and fp8 3-4, but the products with ones are exact and
+    the accumulation is the same fp32 chain, so the error in units of
+    2^-24 sum|x| stays in the same range as for binary16."""
+    import torch
+
+    import paper_1903_03640_b200 as tcr
+
+    n = (1 << 24) + 3
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    o64 = torch.empty(1, dtype=torch.float64, device="cuda")
+    rows = []
+    for dname, d in (("uniform_pm1", gen.UNIFORM_PM1), ("uniform01", gen.UNIFORM_01),
+                     ("wide", gen.WIDE)):
+        cases = [("bf16", gen.generate_bf16(gen.SEED_C2, 0, n, d), None)]
+        for fmt, name in ((gen.FP8_E4M3, "e4m3"), (gen.FP8_E5M2, "e5m2")):
+            cases.append((name, gen.generate_fp8(gen.SEED_C2, 0, n, d, fmt), fmt))
+        for name, bits, fmt in cases:
+            if fmt is None:
+                es = oracle.exact_sum_bf16(bits)
+                x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
+            else:
+                es = oracle.exact_sum_fp8(bits, fmt)
+                x = torch.from_numpy(bits).cuda().view(
+                    torch.float8_e4m3fn if fmt == gen.FP8_E4M3 else torch.float8_e5m2)
+            if es.abs_value == 0:
+                continue
+            for algo in ("mma_sync", "tcgen05", "shuffle", "bulk"):
+                tcr.tcr_reduce_sum_ex(x, out_f32=o32, out_f64=o64, algo=algo)
+                torch.cuda.synchronize()
+                rows.append({"dtype": name, "dist": dname, "algo": algo,
+                             "err_f64_units": _err_units(float(o64.item()), es),
+                             "err_f32_units": _err_units(float(o32.item()), es)})
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/precision_encodings.json", "w") as f:
+        json.dump({"n": n, "unit": "2^-24 * sum|x|", "rows": rows}, f, indent=1)
+    for r in rows:
+        print(r)
+        assert r["err_f32_units"] <= 16, r
