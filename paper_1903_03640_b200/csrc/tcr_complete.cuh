@@ -8,6 +8,12 @@
 #include "tcr_internal.h"
 #include "tcr_peer.cuh"
 
+#ifndef TCR_COMPLETE_EDGE
+#define TCR_COMPLETE_EDGE(k) \
+    do {                     \
+    } while (0)
+#endif
+
 namespace tcr {
 
 // Levels 2-4.  Every thread of the CTA calls this with its lane value; the
@@ -23,7 +29,9 @@ __device__ __forceinline__ void complete_block_and_grid(double lane_val, float* 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double wt = warp_collapse<kMma>(lane_val);
     if (lane == 0) s_warp[warp] = wt;
+    TCR_COMPLETE_EDGE(4);
     __syncthreads();
+    TCR_COMPLETE_EDGE(5);
     if (warp != 0) return;
     const bool peer = pc && pc->nranks > 0;
     const unsigned long long prev = peer ? peer_counter(*pc, me) : 0ull;
@@ -37,11 +45,14 @@ __device__ __forceinline__ void complete_block_and_grid(double lane_val, float* 
         return;
     }
     unsigned last = 0;
+    TCR_COMPLETE_EDGE(6);
     if (lane == 0) {
         ws.partials[blockIdx.x] = bt;
         __threadfence();  // release the partial before taking a ticket
+        TCR_COMPLETE_EDGE(7);
         last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
     }
+    TCR_COMPLETE_EDGE(8);
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) return;
     __threadfence();  // acquire: every other CTA's partial is visible

@@ -64,6 +64,7 @@ reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, i
                      float* out_f32, double* out_f64, DevWorkspace ws, PeerCombine pc) {
     constexpr int ES = FmtInfo<F>::kBytes;
     constexpr int kTileBytes = 512;
+    TCR_COMPLETE_EDGE(0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int me = pc.rank;
     if (kPeer && gridDim.y > 1) {  // emulated peer group: slice y is rank y, reducing its shard
@@ -129,7 +130,9 @@ reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, i
             flush<kMma>(cA, fA, acc, lane);
         }
     }
+    TCR_COMPLETE_EDGE(2);
     complete_block_and_grid<kMma, WARPS>(acc, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
+    TCR_COMPLETE_EDGE(3);
 }
 
 constexpr int kStreamWarps = 8;  // 256 threads per CTA

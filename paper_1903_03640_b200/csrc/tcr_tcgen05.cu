@@ -25,6 +25,19 @@
 #include <map>
 #include <mutex>
 
+#ifdef TCR_TC05_TRACE
+namespace tcr {
+__device__ unsigned long long g_tc05_edges[10][2048];
+}
+#define TCR_COMPLETE_EDGE(k)                                                               \
+    do {                                                                                   \
+        if (threadIdx.x == 0 && blockIdx.x < 2048) {                                       \
+            unsigned long long t_;                                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+            tcr::g_tc05_edges[k][blockIdx.x] = t_;                                         \
+        }                                                                                  \
+    } while (0)
+#endif
 #include "tcr_complete.cuh"
 #include "tcr_device.cuh"
 #include "tcr_internal.h"
@@ -46,7 +59,13 @@ __device__ __forceinline__ unsigned long long tc05_now() {
     do {                                                                         \
         if (blockIdx.x == 0 && (idx) < 4096) g_tc05_trace[role][idx] = tc05_now(); \
     } while (0)
+// per-CTA phase edges: [0] entry, [1] setup done, [2] data phase done,
+// [3] exit, [4..8] inside complete_block_and_grid (TCR_COMPLETE_EDGE)
+#define TC05_EDGE(k) TCR_COMPLETE_EDGE(k)
 #else
+#define TC05_EDGE(k) \
+    do {             \
+    } while (0)
 #define TC05_TRACE(role, idx) \
     do {                      \
     } while (0)
@@ -87,6 +106,7 @@ __global__ void __launch_bounds__(kTcWarps * 32)
 reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, float* out_f32,
                       double* out_f64, DevWorkspace ws) {
     extern __shared__ __align__(1024) uint8_t smem[];
+    TC05_EDGE(0);
     const int stages = prm.stages;
     const uint32_t stage_bytes = prm.stage_bytes;
     const uint32_t buf_cols = (uint32_t)prm.slots * kSlotCols;
@@ -135,6 +155,7 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
     __syncthreads();
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    TC05_EDGE(1);
 
     double acc = 0.0;
     if (warp == 0) {
@@ -264,8 +285,10 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
     }
     sm100::tc_fence_before();
     __syncthreads();
+    TC05_EDGE(2);
     if (warp == 1) sm100::tmem_dealloc(tmem, tmem_cols);
     complete_block_and_grid<true, kTcWarps>(acc, out_f32, out_f64, ws);
+    TC05_EDGE(3);
 }
 
 // CTAs of this kernel that can be co-resident on one SM for `cfg`: the

@@ -1,6 +1,6 @@
 // tc05_trace.cu -- diagnostic (not part of libtcr): timeline of CTA 0 of the
 // tcgen05 reduction kernel, compiled from the library's own source with
-// -DTCR_TC05_TRACE.  Usage: tc05_trace [stages] [stage_kb] [slots] [chain] [ctas]
+// -DTCR_TC05_TRACE.  Usage: tc05_trace [stages] [stage_kb] [slots] [chain] [ctas] [log2 n]
 // Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a
 //        -DTCR_TC05_TRACE -o scripts/tc05_trace scripts/tc05_trace.cu
 #include <algorithm>
@@ -20,7 +20,8 @@ int main(int argc, char** argv) {
     cfg.tc05_ctas = argc > 5 ? atoi(argv[5]) : 1;
     cfg.tc05_prefetch = 0;
     cfg.tc05_split = 1;
-    const size_t n = (size_t)1 << 30;
+    cfg.tc05_interleave = 0;
+    const size_t n = argc > 6 ? ((size_t)1 << atoi(argv[6])) : ((size_t)1 << 30);
     uint16_t* x;
     cudaMalloc(&x, n * 2);
     cudaMemset(x, 0x3C, n * 2);
@@ -37,7 +38,7 @@ int main(int argc, char** argv) {
     float ms = 0;
     for (int r = 0; r < 5; ++r) {
         cudaEventRecord(a);
-        cudaError_t e = tcr::launch_reduce_tcgen05(x, n, out, nullptr, ws, cfg, 0);
+        cudaError_t e = tcr::launch_reduce_tcgen05(0, x, n, out, nullptr, ws, cfg, 0);
         cudaEventRecord(b);
         if (e || (e = cudaDeviceSynchronize())) {
             printf("error %s\n", cudaGetErrorString(e));
@@ -76,5 +77,35 @@ int main(int argc, char** argv) {
     printf("epilogue rounds (ns): ");
     for (int r = 0; r < 12; ++r) printf("%llu ", tr[3][r] - t0);
     printf("\nlast chunk committed at %llu ns\n", tr[2][m - 1] - t0);
+    // per-CTA phase edges of the last launch, relative to the earliest entry
+    static unsigned long long ed[10][2048];
+    cudaMemcpyFromSymbol(ed, tcr::g_tc05_edges, sizeof(ed));
+    const int G = std::min(tcr::tcgen05_grid(n * 2, cfg), 2048);
+    unsigned long long e0 = ~0ull, eend = 0;
+    for (int b = 0; b < G; ++b) {
+        e0 = std::min(e0, ed[0][b]);
+        eend = std::max(eend, ed[3][b]);
+    }
+    std::vector<double> ent, setup, data, fin;
+    for (int b = 0; b < G; ++b) {
+        ent.push_back((double)(ed[0][b] - e0));
+        setup.push_back((double)(ed[1][b] - ed[0][b]));
+        data.push_back((double)(ed[2][b] - e0));
+        fin.push_back((double)(ed[3][b] - ed[2][b]));
+    }
+    printf("CTAs %d: entry p0 %.0f p50 %.0f p100 %.0f | setup p50 %.0f p100 %.0f | data done p0 %.0f "
+           "p50 %.0f p100 %.0f | completion p50 %.0f p100 %.0f | last exit %.0f ns\n",
+           G, pct(ent, 0), pct(ent, 0.5), pct(ent, 1), pct(setup, 0.5), pct(setup, 1), pct(data, 0),
+           pct(data, 0.5), pct(data, 1), pct(fin, 0.5), pct(fin, 1), (double)(eend - e0));
+    // completion steps: 2 data done -> 4 warp collapse -> 5 syncthreads -> 6 CTA collapse
+    // -> 7 partial stored + threadfence -> 8 ticket returned -> 3 exit
+    const int ks[7] = {2, 4, 5, 6, 7, 8, 3};
+    printf("completion step p50 / p100 (ns):");
+    for (int i = 0; i + 1 < 7; ++i) {
+        std::vector<double> d;
+        for (int b = 0; b < G; ++b) d.push_back((double)(ed[ks[i + 1]][b] - ed[ks[i]][b]));
+        printf("  %d->%d %.0f/%.0f", ks[i], ks[i + 1], pct(d, 0.5), pct(d, 1));
+    }
+    printf("\n");
     return 0;
 }
