@@ -419,3 +419,26 @@ def test_convenience_wrappers(tcr):
     seg = tcr.reduce_sum_segmented(xb, off).cpu().tolist()
     ref = [oracle.exact_sum_bf16(b16[a:b]) for a, b in ((0, 10), (10, 10), (10, 5000))]
     assert all(oracle.within_tolerance(g, r) for g, r in zip(seg, ref))
+
+
+def test_random_fuzz_all_paths(tcr):
+    """150 random flat problems (n in 0..3e6 log-uniform, random misalignment
+    and distribution) through every path, incl. the exact kernel (bitwise)."""
+    import torch
+
+    rng = np.random.default_rng(99)
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    for case in range(150):
+        n = int(np.exp(rng.uniform(0, np.log(3e6)))) if case % 10 else int(rng.integers(0, 40))
+        dist = int(rng.choice(DISTS + [gen.SMALLINT]))
+        bits = gen.generate(1000 + case, 0, n, dist)
+        es = oracle.exact_sum_fp16(bits)
+        x = _dev(bits, int(rng.integers(0, 8)))
+        for algo in ALGOS:
+            g = _reduce(tcr, x, algo)
+            assert oracle.within_tolerance(g, es), (case, n, algo, g, es.f64())
+            if dist in (gen.SMALLINT, gen.ONES):
+                assert g == es.f32(), (case, n, algo)
+        tcr.tcr_reduce_sum_exact(x, out_f32=o32)
+        torch.cuda.synchronize()
+        assert float(o32.item()) == es.f32(), (case, n)

@@ -151,3 +151,39 @@ def test_full_size_c5_sampled(tcr):
     torch.cuda.synchronize()
     assert torch.equal(out, out2)
     del x
+
+
+@pytest.mark.parametrize("mma", [True, False])
+def test_random_fuzz_against_oracle(tcr, mma):
+    """200 random CSR problems: random segment counts (0..300), length mixes
+    (empty, short, tile-crossing, long), start offsets, x misalignment and
+    distributions; every segment vs the exact oracle, empty ones exactly 0,
+    and a second launch bitwise identical."""
+    import torch
+
+    rng = np.random.default_rng(2024 + mma)
+    for case in range(200):
+        S = int(rng.integers(0, 300))
+        kind = rng.integers(0, 4, S)
+        lens = np.where(kind == 0, 0, np.where(kind == 1, rng.integers(1, 40, S),
+                        np.where(kind == 2, rng.integers(200, 600, S), rng.integers(1000, 20000, S))))
+        start = int(rng.integers(0, 50))
+        off = gen.offsets_from_lengths(lens.astype(np.int64), start=start)
+        dist = int(rng.choice([gen.UNIFORM_PM1, gen.UNIFORM_01, gen.WIDE, gen.SMALLINT]))
+        bits = gen.generate(case, 0, int(off[-1]) + 9, dist)
+        xoff = int(rng.integers(0, 8))
+        x = _dev(bits, xoff)
+        if S == 0:
+            out = torch.empty(0, dtype=torch.float32, device="cuda")
+            f = tcr.tcr_reduce_sum_segmented if mma else tcr.tcr_reduce_sum_segmented_shuffle
+            f(x, torch.from_numpy(off).cuda(), out, num_segments=0)
+            continue
+        g = _seg(tcr, x, off, mma)
+        ref = oracle.exact_segment_sums_fp16(bits, off)
+        for j in range(S):
+            assert oracle.within_tolerance(float(g[j]), ref[j]), (case, j, g[j], ref[j].f64())
+            if lens[j] == 0:
+                assert g[j] == 0.0
+            if dist == gen.SMALLINT:
+                assert float(g[j]) == ref[j].f32()
+        assert np.array_equal(g, _seg(tcr, x, off, mma)), case
