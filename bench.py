@@ -257,10 +257,12 @@ def main():
     algo = tcr.ALGOS["default" if exact else args.algo]
     peak, peak_src = _peaks()
     peer, combine_note = None, None
-    peer_cfg = args.workload == "c3" and not exact and args.algo in ("default", "mma_sync", "shuffle")
+    peer_cfg = (args.workload == "c3" and args.dtype == "f16"
+                and args.algo in ("default", "mma_sync", "shuffle", "exact"))
     if args.combine == "peer":
         if not peer_cfg:
-            raise SystemExit("--combine peer supports the c3/c4 workload with mma_sync / shuffle")
+            raise SystemExit("--combine peer supports the f16 c3/c4 workload with mma_sync / "
+                             "shuffle / exact")
         if shared_gpu and world > 1:
             raise SystemExit("--combine peer makes the ranks' kernels wait on one another: "
                              "never on one shared GPU")
@@ -279,7 +281,7 @@ def main():
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             if ok.item() == 0 and peer is not None:
                 peer, combine_note = None, "peer setup failed on another rank; NCCL combine used"
-        if peer is not None:
+        if peer is not None and not exact:
             algo = tcr.ALGOS["mma_sync" if args.algo == "default" else args.algo]
 
     # ---------------- inputs (untimed), resident in HBM ----------------
@@ -329,12 +331,19 @@ def main():
         ref64 = torch.empty(1, dtype=torch.float64, device=dev)
         p64 = torch.empty(1, dtype=torch.float64, device=dev)
         with torch.cuda.stream(stream):
-            tcr.tcr_reduce_sum_ex(x, out_f64=ref64, algo=algo, stream=stream)
-            dist.all_reduce(ref64)
-            peer.reduce_sum(x, out_f64=p64, algo=algo, stream=stream)
+            if exact:  # exact: the fused limb combine must equal the NCCL limb allreduce bitwise
+                tcr.tcr_reduce_sum_exact(x, acc=acc6, stream=stream)
+                dist.all_reduce(acc6)
+                tcr.tcr_exact_finalize(acc6, out_f64=ref64, stream=stream)
+                peer.reduce_sum_exact(x, out_f64=p64, stream=stream)
+            else:
+                tcr.tcr_reduce_sum_ex(x, out_f64=ref64, algo=algo, stream=stream)
+                dist.all_reduce(ref64)
+                peer.reduce_sum(x, out_f64=p64, algo=algo, stream=stream)
         torch.cuda.synchronize()
         r, g = ref64.item(), p64.item()
-        good = math.isfinite(g) and abs(g - r) <= 1e-9 * max(1.0, abs(r)) and not peer.timed_out()
+        tol = 0.0 if exact else 1e-9 * max(1.0, abs(r))
+        good = math.isfinite(g) and abs(g - r) <= tol and not peer.timed_out()
         ok = torch.tensor([1 if good else 0], dtype=torch.int32, device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if ok.item() == 0:
@@ -350,6 +359,8 @@ def main():
                 ev_k0.record(stream)
             if args.workload == "c5":
                 tcr.tcr_reduce_sum_segmented(x, toff, seg_out, num_segments=S, stream=stream)
+            elif peer is not None and exact:  # exact sum + limb combine in ONE launch
+                peer.reduce_sum_exact(x, out_f32=out32, stream=stream)
             elif peer is not None:  # reduction + cross-GPU combine in ONE launch
                 peer.reduce_sum(x, out_f32=out32, algo=algo, stream=stream)
             elif exact:

@@ -244,7 +244,7 @@ tcr_status tcr_round_f64_to_f32(const double *in, float *out, tcr_stream stream)
  * ---------------------------------------------------------------------------
  */
 #define TCR_MAX_PEERS 8           /* ranks per peer group (one NVLink node) */
-#define TCR_PEER_MAILBOX_BYTES 512
+#define TCR_PEER_MAILBOX_BYTES 2048
 #define TCR_IPC_HANDLE_BYTES 64
 
 /* Allocates (cudaMalloc, IPC-exportable) and zeroes a mailbox on the current
@@ -292,6 +292,24 @@ tcr_status tcr_reduce_sum_peer(const void *x, size_t n, tcr_dtype dtype, tcr_alg
 tcr_status tcr_reduce_sum_peer_emulated(const void *x, size_t n, tcr_dtype dtype, tcr_algo algo,
                                         void *const *mailboxes, int nranks, float *out_f32,
                                         double *out_f64, tcr_stream stream);
+
+/*
+ * tcr_reduce_sum_exact_peer -- tcr_reduce_sum_exact of this rank's binary16
+ * shard fused with the group combine of the int64 limb states (NEXT-2 x
+ * NEXT-3): acc[0..6) (may be NULL) receives the group's summed limbs and
+ * out_f32 / out_f64 their correctly rounded value -- bitwise identical on
+ * every rank and for every number of ranks.  Same mailboxes, epochs, stream
+ * ordering and timeout behaviour as tcr_reduce_sum_peer (both kinds of
+ * combine may be interleaved on one group; each advances its epoch).
+ */
+tcr_status tcr_reduce_sum_exact_peer(const tcr_half *x, size_t n, void *const *mailboxes,
+                                     int nranks, int rank, int64_t *acc, float *out_f32,
+                                     double *out_f64, tcr_stream stream);
+/* All ranks emulated in one cooperative launch (acc: 6 words per rank,
+ * out_f32 / out_f64: one per rank), as tcr_reduce_sum_peer_emulated. */
+tcr_status tcr_reduce_sum_exact_peer_emulated(const tcr_half *x, size_t n,
+                                              void *const *mailboxes, int nranks, int64_t *acc,
+                                              float *out_f32, double *out_f64, tcr_stream stream);
 
 /*
  * tcr_probe_mma -- hardware characterisation (not part of the reduction):

@@ -67,7 +67,7 @@ TCR_CFG_BULK_CTAS_PER_SM = 16
 TCR_CFG_PEER_TIMEOUT_MS = 17
 
 TCR_MAX_PEERS = 8
-TCR_PEER_MAILBOX_BYTES = 512
+TCR_PEER_MAILBOX_BYTES = 2048
 TCR_IPC_HANDLE_BYTES = 64
 
 
@@ -109,6 +109,8 @@ _SIGS = {
     "tcr_release_workspaces": [],
     "tcr_reduce_sum_peer": [_P, _SZ, _I, _I, _P, _I, _I, _P, _P, _P],
     "tcr_reduce_sum_peer_emulated": [_P, _SZ, _I, _I, _P, _I, _P, _P, _P],
+    "tcr_reduce_sum_exact_peer": [_P, _SZ, _P, _I, _I, _P, _P, _P, _P],
+    "tcr_reduce_sum_exact_peer_emulated": [_P, _SZ, _P, _I, _P, _P, _P, _P],
     "tcr_peer_mailbox_alloc": [_P],
     "tcr_peer_mailbox_free": [_P],
     "tcr_peer_mailbox_reset": [_P, _P],
@@ -390,6 +392,25 @@ def tcr_reduce_sum_peer_emulated(x, mailboxes, out_f32=None, out_f64=None,
                                              len(mailboxes), _ptr(out_f32),
                                              _ptr(out_f64), _stream(stream, x)),
            "tcr_reduce_sum_peer_emulated")
+
+
+def tcr_reduce_sum_exact_peer(x, mailboxes, rank, acc=None, out_f32=None, out_f64=None, n=None,
+                              stream=None) -> None:
+    """Exact sum of this rank's shard fused with the group's limb combine."""
+    _check(_lib.tcr_reduce_sum_exact_peer(_ptr(x), _numel(x, n), _mailbox_array(mailboxes),
+                                          len(mailboxes), int(rank), _ptr(acc), _ptr(out_f32),
+                                          _ptr(out_f64), _stream(stream, x)),
+           "tcr_reduce_sum_exact_peer")
+
+
+def tcr_reduce_sum_exact_peer_emulated(x, mailboxes, acc=None, out_f32=None, out_f64=None, n=None,
+                                       stream=None) -> None:
+    """All len(mailboxes) ranks of the exact fused combine in one cooperative launch."""
+    _check(_lib.tcr_reduce_sum_exact_peer_emulated(_ptr(x), _numel(x, n),
+                                                   _mailbox_array(mailboxes), len(mailboxes),
+                                                   _ptr(acc), _ptr(out_f32), _ptr(out_f64),
+                                                   _stream(stream, x)),
+           "tcr_reduce_sum_exact_peer_emulated")
 
 
 def tcr_set_config(key: int, value: int) -> None:

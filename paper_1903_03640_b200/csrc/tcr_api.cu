@@ -215,7 +215,8 @@ tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_
 
 tcr_status peer_impl(const void* x, size_t n, int dtype, int algo, void* const* mailboxes,
                      int nranks, int rank, float* out_f32, double* out_f64, bool emulate,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, bool exact = false, int64_t* out_acc = nullptr) {
+    static_assert(tcr::kMailboxBytes == TCR_PEER_MAILBOX_BYTES, "mailbox size");
     if (dtype < TCR_DTYPE_F16 || dtype > TCR_DTYPE_E5M2)
         return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
     if (algo == TCR_ALGO_DEFAULT) algo = TCR_ALGO_MMA_SYNC;
@@ -223,8 +224,9 @@ tcr_status peer_impl(const void* x, size_t n, int dtype, int algo, void* const* 
         return fail(TCR_ERR_INVALID_VALUE, "peer combine algo must be DEFAULT, MMA_SYNC or SHUFFLE");
     if (nranks < 1 || nranks > tcr::kMaxPeers || rank < 0 || rank >= nranks)
         return fail(TCR_ERR_INVALID_VALUE, "nranks must be 1..TCR_MAX_PEERS and 0 <= rank < nranks");
-    if (!mailboxes || (!x && n) || (!out_f32 && !out_f64))
+    if (!mailboxes || (!x && n) || (!out_f32 && !out_f64 && !out_acc))
         return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    if (out_acc && !aligned(out_acc, 8)) return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
     if (!aligned(x, dtype >= TCR_DTYPE_E4M3 ? 1 : 2) || (out_f32 && !aligned(out_f32, 4)) ||
         (out_f64 && !aligned(out_f64, 8)))
         return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
@@ -245,6 +247,12 @@ tcr_status peer_impl(const void* x, size_t n, int dtype, int algo, void* const* 
     tcr_status s = prologue(stream, &di, &ws);
     if (s != TCR_OK) return s;
     const LaunchCfg cfg = make_cfg(di);
+    if (exact)
+        return after_launch(
+            tcr::launch_reduce_exact_peer(static_cast<const uint16_t*>(x), n,
+                                          reinterpret_cast<long long*>(out_acc), out_f32, out_f64,
+                                          ws->dev, cfg, pc, emulate, stream),
+            emulate ? "exact peer-emulated launch" : "exact peer launch");
     return after_launch(tcr::launch_reduce_stream_peer(algo == TCR_ALGO_MMA_SYNC, dtype,
                                                        static_cast<const uint16_t*>(x), n, out_f32,
                                                        out_f64, ws->dev, cfg, pc, emulate, stream),
@@ -463,6 +471,20 @@ tcr_status tcr_reduce_sum_peer_emulated(const void* x, size_t n, tcr_dtype dtype
                                         double* out_f64, tcr_stream stream) {
     return peer_impl(x, n, (int)dtype, (int)algo, mailboxes, nranks, 0, out_f32, out_f64, true,
                      (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_exact_peer(const tcr_half* x, size_t n, void* const* mailboxes,
+                                     int nranks, int rank, int64_t* acc, float* out_f32,
+                                     double* out_f64, tcr_stream stream) {
+    return peer_impl(x, n, TCR_DTYPE_F16, TCR_ALGO_DEFAULT, mailboxes, nranks, rank, out_f32,
+                     out_f64, false, (cudaStream_t)stream, true, acc);
+}
+
+tcr_status tcr_reduce_sum_exact_peer_emulated(const tcr_half* x, size_t n,
+                                              void* const* mailboxes, int nranks, int64_t* acc,
+                                              float* out_f32, double* out_f64, tcr_stream stream) {
+    return peer_impl(x, n, TCR_DTYPE_F16, TCR_ALGO_DEFAULT, mailboxes, nranks, 0, out_f32, out_f64,
+                     true, (cudaStream_t)stream, true, acc);
 }
 
 tcr_status tcr_peer_mailbox_alloc(void** mailbox) {

@@ -22,6 +22,7 @@
 // tcr_exact_finalize() rounds it.
 #include "tcr_device.cuh"
 #include "tcr_internal.h"
+#include "tcr_peer.cuh"
 
 namespace tcr {
 
@@ -179,11 +180,27 @@ __device__ void finalize(const long long* acc, float* out_f32, double* out_f64) 
     if (out_f64) *out_f64 = d;
 }
 
-template <int U>
+// kPeer: the NEXT-2 x NEXT-3 variant -- the last CTA combines the limbs
+// with the peers' over NVLink mailboxes (tcr_peer.cuh); grid.y slices =
+// emulated ranks, as in reduce_stream_kernel.
+template <int U, bool kPeer>
 __global__ void __launch_bounds__(kExactWarps * 32, (U <= 4 ? 4 : 3))
 reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc, float* out_f32,
-                    double* out_f64, DevWorkspace ws) {
+                    double* out_f64, DevWorkspace ws, PeerCombine pc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int me = pc.rank;
+    if (kPeer && gridDim.y > 1) {  // emulated peer group: slice y is rank y
+        const size_t P = gridDim.y, r = blockIdx.y;
+        const size_t lo = r * n / P, hi = (r + 1) * n / P;
+        x += lo;
+        n = hi - lo;
+        ws.partials += 5 * r * gridDim.x;  // 5 int64 words per CTA (stored in the doubles)
+        ws.ticket += r;
+        if (out_acc) out_acc += 6 * r;
+        if (out_f32) out_f32 += r;
+        if (out_f64) out_f64 += r;
+        me = (int)r;
+    }
     size_t head = ((16u - ((uintptr_t)x & 15u)) & 15u) >> 1;
     if (head > n) head = n;
     const uint16_t* xa = x + head;
@@ -244,6 +261,7 @@ reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc
     }
     __syncthreads();
     if (warp != 0) return;
+    const unsigned long long prev = kPeer ? peer_counter(pc, me) : 0ull;
     i128 b = 0;
     long long c[3] = {0, 0, 0};
     if (lane < kExactWarps) {
@@ -286,6 +304,25 @@ reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc
             for (int o = 16; o > 0; o >>= 1) c[k] += __shfl_xor_sync(0xffffffffu, c[k], o);
         if (lane == 0) *ws.ticket = 0u;
     }
+    if constexpr (kPeer) {
+        // every lane computes the limbs (b, c are warp-uniform after the sums)
+        to_limbs(b, res);
+        res[3] = c[0];
+        res[4] = c[1];
+        res[5] = c[2];
+        const bool ok = peer_combine_exact(res, pc, me, lane, prev);
+        if (lane == 0) {
+            if (out_acc)
+                for (int k = 0; k < 6; ++k) out_acc[k] = res[k];
+            if (ok) {
+                finalize(res, out_f32, out_f64);
+            } else {
+                if (out_f32) *out_f32 = __int_as_float(0x7FC00000);
+                if (out_f64) *out_f64 = __longlong_as_double(0x7FF8000000000000ll);
+            }
+        }
+        return;
+    }
     if (lane == 0) {
         to_limbs(b, res);
         res[3] = c[0];
@@ -322,13 +359,48 @@ cudaError_t launch_reduce_exact(const uint16_t* x, size_t n, long long* out_acc,
                                 double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                 cudaStream_t stream) {
     const int g = exact_grid(n, cfg, ws.capacity);
+    const PeerCombine none{};
     if (cfg.exact_unroll == 8)
-        reduce_exact_kernel<8><<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32,
-                                                                   out_f64, ws);
+        reduce_exact_kernel<8, false><<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32,
+                                                                          out_f64, ws, none);
     else
-        reduce_exact_kernel<4><<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32,
-                                                                   out_f64, ws);
+        reduce_exact_kernel<4, false><<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32,
+                                                                          out_f64, ws, none);
     return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_exact_peer(const uint16_t* x, size_t n, long long* out_acc,
+                                     float* out_f32, double* out_f64, const DevWorkspace& ws,
+                                     const LaunchCfg& cfg, const PeerCombine& pc, bool emulate,
+                                     cudaStream_t stream) {
+    auto kernel = reduce_exact_kernel<8, true>;  // the peer variant at the default unroll only
+    LaunchCfg c8 = cfg;
+    c8.exact_unroll = 8;
+    if (!emulate) {
+        const int g = exact_grid(n, c8, ws.capacity);
+        kernel<<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32, out_f64, ws, pc);
+        return cudaGetLastError();
+    }
+    // emulated ranks wait on one another: one cooperative launch (co-residency)
+    const int P = pc.nranks;
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kExactWarps * 32, 0);
+    if (e != cudaSuccess) return e;
+    int g = exact_grid(n / (size_t)P, c8, ws.capacity / P);
+    const int cap = occ * cfg.sms / P;
+    if (g > cap) g = cap;
+    if (g < 1) return cudaErrorCooperativeLaunchTooLarge;
+    const uint16_t* xa = x;
+    size_t na = n;
+    long long* acc = out_acc;
+    float* o32 = out_f32;
+    double* o64 = out_f64;
+    DevWorkspace wsa = ws;
+    PeerCombine pca = pc;
+    void* args[] = {(void*)&xa, (void*)&na, (void*)&acc, (void*)&o32, (void*)&o64, (void*)&wsa,
+                    (void*)&pca};
+    return cudaLaunchCooperativeKernel((const void*)kernel, dim3(g, P), dim3(kExactWarps * 32),
+                                       args, 0, stream);
 }
 
 cudaError_t launch_exact_finalize(const long long* acc, float* out_f32, double* out_f64,

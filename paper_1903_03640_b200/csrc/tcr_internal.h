@@ -22,9 +22,10 @@ struct DevWorkspace {
 // device allocation on every rank; slot [parity][src] of rank d's mailbox
 // receives src's fp64 partial for the epoch of that parity.
 constexpr int kMaxPeers = 8;           // ranks per peer group (one NVLink node)
-constexpr int kMailboxBytes = 512;     // 2 x kMaxPeers x 16 B slots + error word + epoch
+constexpr int kMailboxBytes = 2048;    // fp64 slots, error word, epoch, exact slots
 constexpr int kMailboxErrOffset = 256; // uint32: set to 1 when a wait timed out
 constexpr int kMailboxEpochOffset = 264;  // uint64: combines completed by the owning rank
+constexpr int kMailboxExactOffset = 512;  // 2 x kMaxPeers x 96 B exact-limb slots
 
 struct PeerCombine {
     void* mbox[kMaxPeers];        // mailbox of every rank (own + mapped peers), by rank
@@ -81,6 +82,13 @@ cudaError_t launch_reduce_bulk(int fmt, const uint16_t* x, size_t n, float* out_
 cudaError_t launch_reduce_exact(const uint16_t* x, size_t n, long long* out_acc, float* out_f32,
                                 double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                 cudaStream_t stream);
+// Exact reduction fused with the cross-GPU combine of the int64 limbs
+// (NEXT-2 x NEXT-3); emulate as for launch_reduce_stream_peer (out_acc: 6
+// words per rank, out_f32 / out_f64: one per rank).
+cudaError_t launch_reduce_exact_peer(const uint16_t* x, size_t n, long long* out_acc,
+                                     float* out_f32, double* out_f64, const DevWorkspace& ws,
+                                     const LaunchCfg& cfg, const PeerCombine& pc, bool emulate,
+                                     cudaStream_t stream);
 cudaError_t launch_exact_finalize(const long long* acc, float* out_f32, double* out_f64,
                                   cudaStream_t stream);
 cudaError_t launch_sum_partials(const double* partials, size_t count, float* out_f32,

@@ -120,4 +120,77 @@ __device__ __forceinline__ double peer_combine(double v, const PeerCombine& pc, 
     return tot;
 }
 
+// ---------------------------------------------------------------------------
+// Exact variant (NEXT-2 x NEXT-3): the payload is the rank's int64 limb state
+// acc[6] = {l0, l1, l2, n_nan, n_pinf, n_ninf} (tcr_exact.cu), sent as twelve
+// 8-byte words {epoch32, one 32-bit half of a limb} in a 96-byte slot of the
+// exact region of the mailbox; the sum of the limbs over ranks is exact in
+// any order, so every rank finalizes the identical integer.
+struct __align__(16) MailboxSlotX {
+    unsigned long long w[12];
+};
+
+__device__ __forceinline__ MailboxSlotX* mailbox_slot_x(void* mbox, unsigned parity, int src) {
+    return reinterpret_cast<MailboxSlotX*>(static_cast<char*>(mbox) + kMailboxExactOffset) +
+           parity * kMaxPeers + src;
+}
+
+// All 32 lanes of warp 0 of the rank's last CTA, with the rank's limbs in
+// every lane; on return every lane holds the group's summed limbs.
+__device__ __forceinline__ bool peer_combine_exact(long long (&lim)[6], const PeerCombine& pc,
+                                                   int me, int lane, unsigned long long prev) {
+    const int P = pc.nranks;
+    char* own = static_cast<char*>(mailbox_of(pc, me));
+    const unsigned long long epoch = prev + 1ull;
+    const unsigned par = (unsigned)(epoch & 1ull);
+    const unsigned long long tag = (unsigned long long)(unsigned)epoch << 32;
+    if (lane < P && lane != me) {  // push the 12 halves, 16 bytes per store
+        MailboxSlotX* d = mailbox_slot_x(mailbox_of(pc, lane), par, me);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const unsigned long long u = (unsigned long long)lim[k];
+            st_slot(&d->w[2 * k], tag | (u & 0xFFFFFFFFull), tag | (u >> 32));
+        }
+    }
+    long long got[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) got[k] = lim[k];
+    unsigned ok = 1u;
+    if (lane < P && lane != me) {
+        const MailboxSlotX* src = mailbox_slot_x(own, par, lane);
+        unsigned long long w[12];
+        const unsigned long long t0 = globaltimer_ns();
+        for (;;) {
+            bool all = true;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                ld_slot(&src->w[2 * k], w[2 * k], w[2 * k + 1]);
+                all = all && (w[2 * k] >> 32) == (unsigned)epoch &&
+                      (w[2 * k + 1] >> 32) == (unsigned)epoch;
+            }
+            if (all) break;
+            if (globaltimer_ns() - t0 > pc.timeout_ns) {
+                ok = 0u;
+                break;
+            }
+            __nanosleep(20);
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            got[k] = ok ? (long long)((w[2 * k + 1] << 32) | (w[2 * k] & 0xFFFFFFFFull)) : 0ll;
+    }
+    const unsigned all_ok = __all_sync(0xffffffffu, ok);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        long long t = 0;
+        for (int r = 0; r < P; ++r) t += __shfl_sync(0xffffffffu, got[k], r);
+        lim[k] = t;
+    }
+    if (lane == 0) {
+        *reinterpret_cast<unsigned long long*>(own + kMailboxEpochOffset) = epoch;
+        if (!all_ok) atomicExch(reinterpret_cast<unsigned*>(own + kMailboxErrOffset), 1u);
+    }
+    return all_ok != 0;
+}
+
 }  // namespace tcr

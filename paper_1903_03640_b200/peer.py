@@ -59,6 +59,14 @@ class PeerGroup:
                                       out_f64=out_f64, algo=algo, stream=stream)
         return out_f32 if out_f32 is not None else out_f64
 
+    def reduce_sum_exact(self, x_local, out_f32=None, out_f64=None, acc=None, stream=None):
+        """Bitwise-exact group total (NEXT-3 limbs combined in the kernel):
+        identical on every rank and for every number of ranks."""
+        self.calls += 1
+        self._lib.tcr_reduce_sum_exact_peer(x_local, self.mailboxes, self.rank, acc=acc,
+                                            out_f32=out_f32, out_f64=out_f64, stream=stream)
+        return out_f32 if out_f32 is not None else out_f64
+
     def timed_out(self) -> bool:
         """True if a combine on this rank gave up waiting for a peer (synchronous)."""
         return self._lib.tcr_peer_mailbox_error(self.mailbox)

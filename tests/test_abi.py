@@ -72,6 +72,13 @@ def test_invalid_arguments_rejected_before_device():
     with pytest.raises(tcr.TcrError) as e:
         tcr.tcr_reduce_sum_peer_emulated(0x1000, mb[:2], algo=1, dtype=F16, n=16, stream=0)
     assert e.value.status == tcr.TCR_ERR_INVALID_VALUE  # no output
+    for args in ((mb[:9], 0), (mb[:2], 5), ([0x10000, 0], 0)):
+        with pytest.raises(tcr.TcrError) as e:
+            tcr.tcr_reduce_sum_exact_peer(0x1000, args[0], args[1], out_f32=0x2000, n=16, stream=0)
+        assert e.value.status == tcr.TCR_ERR_INVALID_VALUE, args
+    with pytest.raises(tcr.TcrError) as e:  # no output at all
+        tcr.tcr_reduce_sum_exact_peer_emulated(0x1000, mb[:2], n=16, stream=0)
+    assert e.value.status == tcr.TCR_ERR_INVALID_VALUE
     with pytest.raises(ValueError):
         tcr.tcr_peer_ipc_open(b"short")
 

@@ -267,3 +267,75 @@ def test_ipc_mapped_mailbox_in_fused_kernel(tcr):
     vals, want = msgs["result"]
     assert vals == [want, want]
     assert msgs["peer_error"] == (False,)
+
+
+# ---------------- NEXT-2 x NEXT-3: the exact limb combine ----------------
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_exact_emulated_bitwise(tcr, mailboxes, P):
+    """The fused exact combine: every rank's result is the correctly rounded
+    exact sum, bit for bit, and the summed limbs are the oracle's integer."""
+    import torch
+
+    acc = torch.empty(6 * P, dtype=torch.int64, device="cuda")
+    o32 = torch.empty(P, dtype=torch.float32, device="cuda")
+    o64 = torch.empty(P, dtype=torch.float64, device="cuda")
+    for seed, n, dist in ((1, 3_000_017, gen.WIDE), (2, 777, gen.UNIFORM_PM1),
+                          (3, 1 << 22, gen.UNIFORM_01), (4, 5, gen.SMALLINT)):
+        bits = gen.generate(seed, 0, n, dist)
+        es = oracle.exact_sum_fp16(bits)
+        tcr.tcr_reduce_sum_exact_peer_emulated(_dev(bits), mailboxes[:P], acc=acc, out_f32=o32,
+                                               out_f64=o64)
+        torch.cuda.synchronize()
+        assert o32.cpu().tolist() == [es.f32()] * P, (seed, P)
+        assert o64.cpu().tolist() == [es.f64()] * P, (seed, P)
+        for r in range(P):
+            assert tcr.exact_limbs_to_int(acc[6 * r:6 * r + 6]) == es.T
+
+
+def test_exact_single_rank_equals_exact_entry(tcr, mailboxes):
+    import torch
+
+    bits = gen.generate(8, 0, 1_234_567, gen.WIDE)
+    x = _dev(bits)
+    a = torch.empty(6, dtype=torch.int64, device="cuda")
+    b = torch.empty(6, dtype=torch.int64, device="cuda")
+    tcr.tcr_reduce_sum_exact(x, acc=a)
+    tcr.tcr_reduce_sum_exact_peer(x, mailboxes[:1], 0, acc=b)
+    torch.cuda.synchronize()
+    assert tcr.exact_limbs_to_int(a) == tcr.exact_limbs_to_int(b)
+
+
+def test_exact_and_fp64_combines_interleave(tcr, mailboxes):
+    """Both kinds of combine advance the same device epoch: alternating them
+    on one group stays consistent."""
+    import torch
+
+    P = 4
+    o32 = torch.empty(P, dtype=torch.float32, device="cuda")
+    for i in range(6):
+        bits = gen.generate(50 + i, 0, 100_003, gen.SMALLINT)
+        es = oracle.exact_sum_fp16(bits)
+        if i % 2:
+            tcr.tcr_reduce_sum_exact_peer_emulated(_dev(bits), mailboxes[:P], out_f32=o32)
+        else:
+            tcr.tcr_reduce_sum_peer_emulated(_dev(bits), mailboxes[:P], out_f32=o32)
+        torch.cuda.synchronize()
+        assert o32.cpu().tolist() == [es.f32()] * P, i
+    assert not any(tcr.tcr_peer_mailbox_error(b) for b in mailboxes[:P])
+
+
+def test_exact_specials_in_one_shard(tcr, mailboxes):
+    import math
+
+    import torch
+
+    P, n = 4, 10_000
+    o32 = torch.empty(P, dtype=torch.float32, device="cuda")
+    for special, expect in ((0x7C00, math.inf), (0xFC00, -math.inf), (0x7E00, math.nan)):
+        bits = gen.generate(9, 0, n, gen.UNIFORM_PM1)
+        bits[n - 3] = special  # lands in the last rank's shard
+        tcr.tcr_reduce_sum_exact_peer_emulated(_dev(bits), mailboxes[:P], out_f32=o32)
+        torch.cuda.synchronize()
+        for g in o32.cpu().tolist():
+            assert (math.isnan(g) if math.isnan(expect) else g == expect), (special, g)
