@@ -123,6 +123,26 @@ class ClockSampler:
                 "timed_region_ms": self.window, "source": "NVML, sampled every ~1 ms"}
 
 
+def wait_for_cuda_driver(max_wait_s: float = 90.0) -> None:
+    """Probe cuInit in a child process until it succeeds (bounded).  A shared
+    GPU box was seen once to refuse driver initialisation for a moment right
+    after another process released the GPU; a failed cuInit inside this
+    process would not be retried, so it is probed outside first."""
+    import subprocess
+
+    probe = "import ctypes, sys; sys.exit(ctypes.CDLL('libcuda.so.1').cuInit(0))"
+    t0 = time.time()
+    while True:
+        r = subprocess.run([sys.executable, "-c", probe], capture_output=True)
+        if r.returncode == 0:
+            return
+        if time.time() - t0 > max_wait_s:
+            print(f"warning: cuInit still failing (rc {r.returncode}) after {max_wait_s:.0f} s",
+                  file=sys.stderr)
+            return
+        time.sleep(3.0)
+
+
 def _cpu_count():
     try:
         return len(os.sched_getaffinity(0))
@@ -243,6 +263,7 @@ def main():
     shared_gpu = os.environ.get("TCR_BENCH_SHARED_GPU") == "1"
     if shared_gpu:
         local = 0
+    wait_for_cuda_driver()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
