@@ -222,6 +222,9 @@ def _ipc_worker(rank, port, q):
     import torch
     import torch.distributed as dist
 
+    import bench
+
+    bench.wait_for_cuda_driver()
     torch.cuda.set_device(0)
     import paper_1903_03640_b200 as tcr
 
