@@ -7,9 +7,7 @@
 
 namespace tcr {
 
-constexpr int kWarp = 32;
 constexpr int kTileElems = 256;  // one 16x16 fp16 MMA A operand = m^2 with m = 16
-constexpr int kVecElems = 8;     // one 16-byte vector = 8 binary16 = one lane's A fragment
 constexpr uint32_t kOnesH2 = 0x3C003C00u;  // two binary16 1.0: the all-ones B
 constexpr uint32_t kOnesBf2 = 0x3F803F80u;  // two bfloat16 1.0 (NEXT-4 bfloat16 inputs)
 
@@ -60,12 +58,6 @@ __device__ __forceinline__ void mma_rowsum_bf16(float (&c)[4], const uint4& a) {
         "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(kOnesBf2), "r"(kOnesBf2));
-}
-
-template <bool kBf16>
-__device__ __forceinline__ void mma_rowsum_t(float (&c)[4], const uint4& a) {
-    if constexpr (kBf16) mma_rowsum_bf16(c, a);
-    else mma_rowsum(c, a);
 }
 
 // Element formats of the flat reduction (NEXT-4): every one keeps the tile at
@@ -164,12 +156,6 @@ __device__ __forceinline__ float vec_sum_f32_bf16(const uint4& a) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) p[k] = __uint_as_float(w[k] << 16) + __uint_as_float(w[k] & 0xFFFF0000u);
     return (p[0] + p[1]) + (p[2] + p[3]);
-}
-
-template <bool kBf16>
-__device__ __forceinline__ float vec_sum_t(const uint4& a) {
-    if constexpr (kBf16) return vec_sum_f32_bf16(a);
-    else return vec_sum_f32(a);
 }
 
 // fp8 -> binary16 pairs are exact (cvt.rn.f16x2.{e4m3,e5m2}x2), then binary32.
