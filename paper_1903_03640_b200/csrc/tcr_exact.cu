@@ -242,7 +242,16 @@ reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc
         exact_vec(v, a0, a1, p);
         if (p & 0x7FFF7FFFu) fix_specials(v, a0, a1, cnt);
     };
-    for (; t < T; t += W) one(ldg_stream(base + t * 32));
+    if (t < T) {  // fewer than U tiles left for this warp: one predicated batch (one latency)
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            v[u] = (t + (size_t)u * W < T) ? ldg_stream(base + (t + (size_t)u * W) * 32)
+                                           : make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < U; ++u) one(v[u]);
+    }
     if (w == W - 1) {  // ragged head and tail
         if (head) one(load_ragged(x, (int)head, lane));
         if (tail) one(load_ragged(xa + T * kTileElems, tail, lane));

@@ -58,8 +58,41 @@ def main_c5(a, b, rounds):
         print(f"c5 {k} {a if k == 'A' else b}: median {med:.1f} us  {2 * n / med / 1e3:.1f} GB/s")
 
 
+def main_exact(a, b, rounds):
+    n = 1 << 30
+    x = gen.generate_tensor(gen.SEED_C3, 0, n, gen.UNIFORM_PM1)
+    out = torch.empty(1, dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream()
+    fns = {}
+    for k, path in (("A", a), ("B", b)):
+        f = ctypes.CDLL(path).tcr_reduce_sum_exact
+        f.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_void_p]
+        f.restype = ctypes.c_int
+        fns[k] = f
+    res = {"A": [], "B": []}
+    for f in fns.values():
+        for _ in range(5):
+            assert f(x.data_ptr(), n, None, out.data_ptr(), None, s.cuda_stream) == 0
+    torch.cuda.synchronize()
+    for _ in range(rounds):
+        for k, f in fns.items():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(100):
+                f(x.data_ptr(), n, None, out.data_ptr(), None, s.cuda_stream)
+            e1.record(s)
+            torch.cuda.synchronize()
+            res[k].append(e0.elapsed_time(e1) * 10)
+    for k in res:
+        med = statistics.median(res[k])
+        print(f"exact {k} {a if k == 'A' else b}: median {med:.2f} us  {2 * n / med / 1e3:.1f} GB/s")
+
+
 def main():
     a, b = sys.argv[1], sys.argv[2]
+    if len(sys.argv) > 3 and sys.argv[3] == "exact":
+        return main_exact(a, b, int(sys.argv[4]) if len(sys.argv) > 4 else 10)
     if len(sys.argv) > 3 and sys.argv[3] == "c5":
         return main_c5(a, b, int(sys.argv[4]) if len(sys.argv) > 4 else 10)
     algo = int(sys.argv[3]) if len(sys.argv) > 3 else 1
