@@ -1,4 +1,4 @@
-"""Balanced-batch variant: parity vs the oracle + determinism, then A/B timing."""
+"""Balanced-batch experiment (reverted; needs the TCR_CFG_BALANCE build of the streaming kernel): parity + determinism, then A/B timing."""
 import statistics, sys
 import numpy as np
 import torch
