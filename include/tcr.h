@@ -324,6 +324,16 @@ tcr_status tcr_reduce_sum_exact_peer_emulated(const tcr_half *x, size_t n,
 tcr_status tcr_probe_mma(const tcr_half *a, const float *c, float *d, tcr_algo algo,
                          tcr_stream stream);
 
+/*
+ * tcr_probe_collapse -- the level-2 collapse D' = 1 x D (Eq. 11-12) in
+ * isolation: lane l of one warp holds in[l] (device double[32]); out[l]
+ * (device double[32]) receives lane l's result of the collapse used by the
+ * kernels (TCR_ALGO_MMA_SYNC: three m8n8k4 f64 DMMAs with ones in A;
+ * TCR_ALGO_SHUFFLE: the shfl_xor tree).  Every lane gets the sum (the
+ * replication of Eq. 12).  For the tests (SURVEY T-D(iii)).
+ */
+tcr_status tcr_probe_collapse(const double *in, double *out, tcr_algo algo, tcr_stream stream);
+
 /* Tuning knobs (process-wide; defaults are the measured best on B200). */
 typedef enum {
     TCR_CFG_DEFAULT_ALGO = 0,     /* tcr_algo used by tcr_reduce_sum        */

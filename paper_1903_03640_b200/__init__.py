@@ -105,6 +105,7 @@ _SIGS = {
     "tcr_reduce_sum_exact": [_P, _SZ, _P, _P, _P, _P],
     "tcr_exact_finalize": [_P, _P, _P, _P],
     "tcr_probe_mma": [_P, _P, _P, _I, _P],
+    "tcr_probe_collapse": [_P, _P, _I, _P],
     "tcr_set_config": [_I, _I],
     "tcr_release_workspaces": [],
     "tcr_reduce_sum_peer": [_P, _SZ, _I, _I, _P, _I, _I, _P, _P, _P],
@@ -411,6 +412,14 @@ def tcr_reduce_sum_exact_peer_emulated(x, mailboxes, acc=None, out_f32=None, out
                                                    _ptr(acc), _ptr(out_f32), _ptr(out_f64),
                                                    _stream(stream, x)),
            "tcr_reduce_sum_exact_peer_emulated")
+
+
+def tcr_probe_collapse(inp, out, algo=TCR_ALGO_MMA_SYNC, stream=None) -> None:
+    """out[l] = lane l's result of the level-2 collapse of inp[0..32) (device float64)."""
+    if isinstance(algo, str):
+        algo = ALGOS[algo]
+    _check(_lib.tcr_probe_collapse(_ptr(inp), _ptr(out), int(algo), _stream(stream, inp)),
+           "tcr_probe_collapse")
 
 
 def tcr_set_config(key: int, value: int) -> None:

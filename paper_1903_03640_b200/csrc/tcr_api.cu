@@ -20,6 +20,7 @@ cudaError_t launch_probe_mma_sync(const uint16_t* a, const float* c, float* d,
                                   cudaStream_t stream);
 cudaError_t launch_probe_mma_tcgen05(const uint16_t* a, const float* c, float* d,
                                      cudaStream_t stream);
+cudaError_t launch_probe_collapse(const double* in, double* out, bool mma, cudaStream_t stream);
 }  // namespace tcr
 
 namespace {
@@ -551,6 +552,19 @@ tcr_status tcr_peer_ipc_close(void* peer_mailbox) {
     if (!peer_mailbox) return TCR_OK;
     cudaError_t e = cudaIpcCloseMemHandle(peer_mailbox);
     return e == cudaSuccess ? TCR_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
+tcr_status tcr_probe_collapse(const double* in, double* out, tcr_algo algo, tcr_stream stream) {
+    if (!in || !out) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    if (algo != TCR_ALGO_MMA_SYNC && algo != TCR_ALGO_SHUFFLE)
+        return fail(TCR_ERR_INVALID_VALUE, "collapse probe algo must be MMA_SYNC or SHUFFLE");
+    DeviceInfo di;
+    int dev;
+    tcr_status s = current_device(&dev, &di);
+    if (s != TCR_OK) return s;
+    return after_launch(tcr::launch_probe_collapse(in, out, algo == TCR_ALGO_MMA_SYNC,
+                                                   (cudaStream_t)stream),
+                        "collapse probe");
 }
 
 tcr_status tcr_set_config(tcr_config_key key, int value) {

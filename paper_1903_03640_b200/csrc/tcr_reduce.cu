@@ -314,4 +314,16 @@ cudaError_t launch_probe_mma_sync(const uint16_t* a, const float* c, float* d,
     return cudaGetLastError();
 }
 
+// Level-2 collapse probe: lane l holds in[l]; out[l] = the lane's result of
+// warp_collapse (three DMMAs with ones in A, or the shfl_xor tree).
+__global__ void probe_collapse_kernel(const double* in, double* out, int mma) {
+    const int lane = threadIdx.x & 31;
+    out[lane] = mma ? warp_collapse_mma(in[lane]) : warp_collapse_shfl(in[lane]);
+}
+
+cudaError_t launch_probe_collapse(const double* in, double* out, bool mma, cudaStream_t stream) {
+    probe_collapse_kernel<<<1, 32, 0, stream>>>(in, out, mma ? 1 : 0);
+    return cudaGetLastError();
+}
+
 }  // namespace tcr

@@ -442,3 +442,32 @@ def test_random_fuzz_all_paths(tcr):
         tcr.tcr_reduce_sum_exact(x, out_f32=o32)
         torch.cuda.synchronize()
         assert float(o32.item()) == es.f32(), (case, n)
+
+
+@pytest.mark.parametrize("algo", ["mma_sync", "shuffle"])
+def test_collapse_probe_exactness(tcr, algo):
+    """SURVEY T-D(iii): the level-2 collapse (Eq. 11-12) in isolation.  Every
+    lane receives the sum (replication, Eq. 12); the fp64 DMMA collapse equals
+    the exact sum of the 32 lane values within fp64 rounding (|err| <= 2^-50
+    of sum|v|), and exactly when the partial sums are representable."""
+    from fractions import Fraction
+
+    import torch
+
+    rng = np.random.default_rng(5)
+    inp = torch.empty(32, dtype=torch.float64, device="cuda")
+    out = torch.empty(32, dtype=torch.float64, device="cuda")
+    cases = [np.arange(32, dtype=np.float64), np.ones(32), np.zeros(32),
+             (rng.integers(-2**20, 2**20, 32)).astype(np.float64)]
+    cases += [rng.standard_normal(32) * 2.0 ** rng.integers(-30, 30, 32) for _ in range(200)]
+    for i, v in enumerate(cases):
+        inp.copy_(torch.from_numpy(v))
+        tcr.tcr_probe_collapse(inp, out, algo)
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        assert len(set(o.tolist())) == 1, (i, o)  # replicated in every lane
+        exact = sum((Fraction(float(t)) for t in v), Fraction(0))
+        bound = sum((abs(Fraction(float(t))) for t in v), Fraction(0)) * Fraction(1, 2 ** 50)
+        assert abs(Fraction(float(o[0])) - exact) <= bound, (i, float(o[0]), float(exact))
+        if i < 4:  # integer lane values: every partial sum is exact in fp64
+            assert Fraction(float(o[0])) == exact
