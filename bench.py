@@ -402,9 +402,12 @@ def main():
                     tcr.tcr_round_f64_to_f32(out64, out32, stream=stream)
 
     clk = ClockSampler(torch.cuda.current_device()).__enter__()
+    nvtx = torch.cuda.nvtx  # ranges for profiler filtering (ncu --nvtx); host-side only
+    nvtx.range_push("tcr.warmup")
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    nvtx.range_pop()
 
     K = args.steps
     # A step that is ONE launch of the dominant kernel (N = 1, or the fused
@@ -421,12 +424,14 @@ def main():
     torch.cuda.synchronize()
     launches0 = tcr.tcr_launch_count()
     w0 = time.perf_counter()
+    nvtx.range_push("tcr.timed")
     t_start.record(stream)
     for i in range(K):
         step(*kev[i]) if kev else step()
     t_end.record(stream)
     torch.cuda.synchronize()
     w1 = time.perf_counter()
+    nvtx.range_pop()
     time.sleep(0.01)
     clk.__exit__(None, None, None)
     clk.set_window(w0, w1)
