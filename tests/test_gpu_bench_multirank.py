@@ -12,12 +12,22 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def _free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("algo", ["default", "exact"])
 def test_bench_two_ranks_shared_gpu(algo):
     env = dict(os.environ, TCR_BENCH_SHARED_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(29400 + (algo == "exact")),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--e2e-steps", "1",
            "--n-per-rank", str(1 << 24), "--algo", algo]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
@@ -71,7 +81,7 @@ def test_bench_c5_two_ranks_shared_gpu():
     strong scaling; job element count = the whole C5 workload."""
     env = dict(os.environ, TCR_BENCH_SHARED_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29407", "bench.py", "--gpus", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
            "--steps", "3", "--warmup", "3", "--workload", "c5"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
