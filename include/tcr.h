@@ -95,9 +95,9 @@ typedef enum {
     TCR_DTYPE_BF16 = 1, /* bfloat16: the same MMA encoding with .bf16 / kind::f16-BF16
                            operands and B = bfloat16 ones                    */
     TCR_DTYPE_E4M3 = 2, /* OCP fp8 E4M3FN (1 byte): tcgen05 kind::f8f6f4 (the
-                           default for fp8) or mma.sync m16n8k32 .e4m3 (which
-                           sm_100a runs as fp16 HMMAs), B = fp8 ones;
-                           tcr_reduce_sum_ex only */
+                           default for fp8 from 2^26 elements) or mma.sync
+                           m16n8k32 .e4m3 (sm_100a runs it as fp16 HMMAs; the
+                           default below 2^26), B = fp8 ones */
     TCR_DTYPE_E5M2 = 3  /* OCP fp8 E5M2 (1 byte), as E4M3                     */
 } tcr_dtype;
 

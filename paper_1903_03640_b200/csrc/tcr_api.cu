@@ -193,8 +193,12 @@ tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_
     if (algo == TCR_ALGO_DEFAULT) {
         std::lock_guard<std::mutex> lk(g_cfg_mu);
         // fp8: mma.sync .e4m3/.e5m2 is converted to fp16 HMMAs on sm_100a; the
-        // native fp8 tensor path is tcgen05 kind::f8f6f4 (measured fastest)
-        algo = fmt >= 2 ? TCR_ALGO_TCGEN05 : g_cfg.default_algo;
+        // native fp8 tensor path is tcgen05 kind::f8f6f4, measured fastest at
+        // large n but latency-heavy below 64 MiB (per-CTA TMEM / barrier
+        // set-up), where mma.sync with the auto unroll wins
+        // (scripts/runs/fp8_small.py: 2^24 elements 5.1 vs 11.1 us)
+        algo = fmt >= 2 ? (n < ((size_t)1 << 26) ? TCR_ALGO_MMA_SYNC : TCR_ALGO_TCGEN05)
+                        : g_cfg.default_algo;
     }
     if (algo < TCR_ALGO_MMA_SYNC || algo > TCR_ALGO_BULK_MMA)
         return fail(TCR_ERR_INVALID_VALUE, "unknown algo");
