@@ -471,3 +471,39 @@ def test_collapse_probe_exactness(tcr, algo):
         assert abs(Fraction(float(o[0])) - exact) <= bound, (i, float(o[0]), float(exact))
         if i < 4:  # integer lane values: every partial sum is exact in fp64
             assert Fraction(float(o[0])) == exact
+
+
+def test_host_threads_concurrent_streams(tcr):
+    """Library host code under concurrency: 6 host threads (ctypes releases
+    the GIL), each with its own stream (own workspace), issue reductions of
+    different sizes and algorithms in a loop; every result must equal the
+    single-threaded one bitwise."""
+    import threading
+
+    import torch
+
+    xs = [_dev(gen.generate(200 + i, 0, 100_003 * (i + 1), gen.UNIFORM_PM1), i % 3)
+          for i in range(6)]
+    algos = ["mma_sync", "shuffle", "tcgen05", "bulk", "mma_sync", "shuffle"]
+    ref = [_reduce(tcr, x, a) for x, a in zip(xs, algos)]
+    errors = []
+
+    def worker(i):
+        try:
+            s = torch.cuda.Stream()
+            o = torch.empty(1, dtype=torch.float32, device="cuda")
+            for _ in range(40):
+                tcr.tcr_reduce_sum_algo(xs[i], out_f32=o, algo=algos[i], stream=s)
+                s.synchronize()
+                if float(o.item()) != ref[i]:
+                    errors.append((i, float(o.item()), ref[i]))
+                    return
+        except Exception as e:  # pragma: no cover
+            errors.append((i, repr(e)))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(120)
+    assert not errors, errors[:3]
