@@ -45,7 +45,7 @@ def test_bench_two_ranks_shared_gpu(algo):
 def test_bench_json_contract_single_gpu(extra):
     """bench.py at N = 1: one JSON line carrying every key of the contract."""
     cmd = [sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--e2e-steps", "1",
-           "--n-per-rank", str(1 << 24)] + extra
+           "--n-per-rank", str(1 << 24), "--cpu-seconds", "1"] + extra
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
