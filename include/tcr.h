@@ -325,6 +325,20 @@ tcr_status tcr_probe_mma(const tcr_half *a, const float *c, float *d, tcr_algo a
                          tcr_stream stream);
 
 /*
+ * tcr_reduce_sum_paper_f16 -- STUDY MODE (NEXT-1, not the product path): the
+ * paper's algorithm taken literally (§IV.A, Eq. 9-14): per group
+ * of 256 inputs D = A x 1 and D' = 1 x D with fp16 accumulation
+ * (mma.sync .f16.f16.f16.f16), D'_{1,1} written to memory as binary16, and
+ * one kernel launch per level until one value is left (ceil(log_256 n)
+ * launches).  out: device float, the final binary16 value widened.  Exposes
+ * the fp16 precision loss the paper leaves open -- overflow to inf
+ * once a partial exceeds 65504 -- and the cost of the per-level relaunch that
+ * the product path replaces with one launch.  Library-owned scratch of
+ * ~n/255 binary16 per stream (grown on demand).
+ */
+tcr_status tcr_reduce_sum_paper_f16(const tcr_half *x, size_t n, float *out, tcr_stream stream);
+
+/*
  * tcr_probe_collapse -- the level-2 collapse D' = 1 x D (Eq. 11-12) in
  * isolation: lane l of one warp holds in[l] (device double[32]); out[l]
  * (device double[32]) receives lane l's result of the collapse used by the

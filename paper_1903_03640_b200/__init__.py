@@ -106,6 +106,7 @@ _SIGS = {
     "tcr_exact_finalize": [_P, _P, _P, _P],
     "tcr_probe_mma": [_P, _P, _P, _I, _P],
     "tcr_probe_collapse": [_P, _P, _I, _P],
+    "tcr_reduce_sum_paper_f16": [_P, _SZ, _P, _P],
     "tcr_set_config": [_I, _I],
     "tcr_release_workspaces": [],
     "tcr_reduce_sum_peer": [_P, _SZ, _I, _I, _P, _I, _I, _P, _P, _P],
@@ -412,6 +413,12 @@ def tcr_reduce_sum_exact_peer_emulated(x, mailboxes, acc=None, out_f32=None, out
                                                    _ptr(acc), _ptr(out_f32), _ptr(out_f64),
                                                    _stream(stream, x)),
            "tcr_reduce_sum_exact_peer_emulated")
+
+
+def tcr_reduce_sum_paper_f16(x, out, n=None, stream=None) -> None:
+    """STUDY MODE: the paper's algorithm literally (fp16 everywhere, one launch per level)."""
+    _check(_lib.tcr_reduce_sum_paper_f16(_ptr(x), _numel(x, n), _ptr(out), _stream(stream, x)),
+           "tcr_reduce_sum_paper_f16")
 
 
 def tcr_probe_collapse(inp, out, algo=TCR_ALGO_MMA_SYNC, stream=None) -> None:

@@ -69,6 +69,8 @@ struct Workspace {
     void* staging[2] = {nullptr, nullptr};
     size_t staging_bytes = 0;
     float* dev_out = nullptr;
+    void* paper_scratch = nullptr;  // study mode: binary16 partials of every level
+    size_t paper_scratch_bytes = 0;
 };
 
 std::mutex g_mu;
@@ -558,6 +560,34 @@ tcr_status tcr_peer_ipc_close(void* peer_mailbox) {
     return e == cudaSuccess ? TCR_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
 }
 
+tcr_status tcr_reduce_sum_paper_f16(const tcr_half* x, size_t n, float* out, tcr_stream stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if ((!x && n) || !out) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    if (!aligned(x, 2) || !aligned(out, 4)) return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
+    DeviceInfo di;
+    Workspace* ws = nullptr;
+    tcr_status s = prologue(stream, &di, &ws);
+    if (s != TCR_OK) return s;
+    const size_t need = tcr::paper_scratch_elems(n) * sizeof(uint16_t) + 16;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (ws->paper_scratch_bytes < need) {  // grows once per stream, never shrinks
+            if (ws->paper_scratch) cudaFree(ws->paper_scratch);
+            ws->paper_scratch = nullptr;
+            ws->paper_scratch_bytes = 0;
+            cudaError_t e = cudaMalloc(&ws->paper_scratch, need);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(paper scratch)");
+            ws->paper_scratch_bytes = need;
+        }
+    }
+    int launches = 0;
+    cudaError_t e = tcr::launch_reduce_paper_f16(x, n, static_cast<uint16_t*>(ws->paper_scratch), out,
+                                                 di.sms, stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "paper-mode launch");
+    g_launches.fetch_add(launches, std::memory_order_relaxed);
+    return TCR_OK;
+}
+
 tcr_status tcr_probe_collapse(const double* in, double* out, tcr_algo algo, tcr_stream stream) {
     if (!in || !out) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
     if (algo != TCR_ALGO_MMA_SYNC && algo != TCR_ALGO_SHUFFLE)
@@ -701,6 +731,7 @@ tcr_status tcr_release_workspaces(void) {
         for (void* b : ws->staging)
             if (b) cudaFree(b);
         if (ws->dev_out) cudaFree(ws->dev_out);
+        if (ws->paper_scratch) cudaFree(ws->paper_scratch);
         cudaSetDevice(prev);
         delete ws;
     }

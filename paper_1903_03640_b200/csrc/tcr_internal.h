@@ -91,6 +91,11 @@ cudaError_t launch_reduce_exact_peer(const uint16_t* x, size_t n, long long* out
                                      cudaStream_t stream);
 cudaError_t launch_exact_finalize(const long long* acc, float* out_f32, double* out_f64,
                                   cudaStream_t stream);
+// The paper's algorithm literally (study mode, tcr_paper.cu): fp16 MMAs, fp16
+// partials in `scratch` (paper_scratch_elems(n) binary16), one launch per level.
+size_t paper_scratch_elems(size_t n);
+cudaError_t launch_reduce_paper_f16(const uint16_t* x, size_t n, uint16_t* scratch, float* out_f32,
+                                    int sms, cudaStream_t stream, int* launches);
 cudaError_t launch_sum_partials(const double* partials, size_t count, float* out_f32,
                                 double* out_f64, cudaStream_t stream);
 cudaError_t launch_round_f64(const double* in, float* out, cudaStream_t stream);

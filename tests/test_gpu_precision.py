@@ -127,3 +127,45 @@ def test_precision_other_encodings():
     for r in rows:
         print(r)
         assert r["err_f32_units"] <= 16, r
+
+
+def test_precision_paper_literal_fp16():
+    """NEXT-1: the paper's algorithm taken literally (fp16 accumulate, fp16
+    partials, one launch per level) vs the product path, against the exact
+    oracle; written to gpurun_out/precision_paper.json.  The literal form
+    loses ~11-bit relative precision per level and overflows to inf once a
+    partial passes 65504 -- the answer, on B200, to the paper's open
+    question (P:273)."""
+    import math
+
+    import torch
+
+    import paper_1903_03640_b200 as tcr
+
+    rows = []
+    out = torch.empty(1, dtype=torch.float32, device="cuda")
+    for dname, d in (("uniform_pm1", gen.UNIFORM_PM1), ("uniform01", gen.UNIFORM_01),
+                     ("wide", gen.WIDE)):
+        for lg in (12, 16, 20, 24):
+            bits = gen.generate(gen.SEED_C1, 0, 1 << lg, d)
+            es = oracle.exact_sum_fp16(bits)
+            x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.float16)
+            tcr.tcr_reduce_sum_paper_f16(x, out)
+            torch.cuda.synchronize()
+            g_paper = float(out.item())
+            tcr.tcr_reduce_sum(x, out)
+            torch.cuda.synchronize()
+            g_ours = float(out.item())
+            rows.append({"dist": dname, "log2n": lg, "exact": es.f64(),
+                         "paper_f16": g_paper,
+                         "paper_err_units": (_err_units(g_paper, es) if math.isfinite(g_paper)
+                                             else float("inf")),
+                         "ours_err_units": _err_units(g_ours, es)})
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/precision_paper.json", "w") as f:
+        json.dump({"unit": "2^-24 * sum|x|", "rows": rows}, f, indent=1)
+    for r in rows:
+        print(r)
+        assert r["ours_err_units"] <= 16, r
+    # all-positive data overflows binary16 in the literal algorithm at 2^20
+    assert any(r["dist"] == "uniform01" and math.isinf(r["paper_f16"]) for r in rows)
