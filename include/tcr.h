@@ -339,6 +339,15 @@ tcr_status tcr_probe_mma(const tcr_half *a, const float *c, float *d, tcr_algo a
 tcr_status tcr_reduce_sum_paper_f16(const tcr_half *x, size_t n, float *out, tcr_stream stream);
 
 /*
+ * tcr_reduce_sum_study_fp32 -- STUDY MODE (NEXT-1 comparison point, not the
+ * product path): the classic reduction entirely in binary32 -- the shuffle
+ * path's loads and tree with no fp64 anywhere -- naive (kahan = 0) or with
+ * Kahan compensation of the per-lane and grid-level sums (kahan = 1).
+ */
+tcr_status tcr_reduce_sum_study_fp32(const tcr_half *x, size_t n, int kahan, float *out,
+                                     tcr_stream stream);
+
+/*
  * tcr_probe_collapse -- the level-2 collapse D' = 1 x D (Eq. 11-12) in
  * isolation: lane l of one warp holds in[l] (device double[32]); out[l]
  * (device double[32]) receives lane l's result of the collapse used by the

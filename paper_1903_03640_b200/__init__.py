@@ -107,6 +107,7 @@ _SIGS = {
     "tcr_probe_mma": [_P, _P, _P, _I, _P],
     "tcr_probe_collapse": [_P, _P, _I, _P],
     "tcr_reduce_sum_paper_f16": [_P, _SZ, _P, _P],
+    "tcr_reduce_sum_study_fp32": [_P, _SZ, _I, _P, _P],
     "tcr_set_config": [_I, _I],
     "tcr_release_workspaces": [],
     "tcr_reduce_sum_peer": [_P, _SZ, _I, _I, _P, _I, _I, _P, _P, _P],
@@ -419,6 +420,13 @@ def tcr_reduce_sum_paper_f16(x, out, n=None, stream=None) -> None:
     """STUDY MODE: the paper's algorithm literally (fp16 everywhere, one launch per level)."""
     _check(_lib.tcr_reduce_sum_paper_f16(_ptr(x), _numel(x, n), _ptr(out), _stream(stream, x)),
            "tcr_reduce_sum_paper_f16")
+
+
+def tcr_reduce_sum_study_fp32(x, out, kahan=False, n=None, stream=None) -> None:
+    """STUDY MODE: the classic reduction entirely in binary32 (naive or Kahan)."""
+    _check(_lib.tcr_reduce_sum_study_fp32(_ptr(x), _numel(x, n), 1 if kahan else 0, _ptr(out),
+                                          _stream(stream, x)),
+           "tcr_reduce_sum_study_fp32")
 
 
 def tcr_probe_collapse(inp, out, algo=TCR_ALGO_MMA_SYNC, stream=None) -> None:

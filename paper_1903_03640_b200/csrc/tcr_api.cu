@@ -588,6 +588,19 @@ tcr_status tcr_reduce_sum_paper_f16(const tcr_half* x, size_t n, float* out, tcr
     return TCR_OK;
 }
 
+tcr_status tcr_reduce_sum_study_fp32(const tcr_half* x, size_t n, int kahan, float* out,
+                                     tcr_stream stream) {
+    if ((!x && n) || !out) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    if (!aligned(x, 2) || !aligned(out, 4)) return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
+    DeviceInfo di;
+    Workspace* ws = nullptr;
+    tcr_status s = prologue((cudaStream_t)stream, &di, &ws);
+    if (s != TCR_OK) return s;
+    return after_launch(tcr::launch_study_fp32(x, n, kahan != 0, out, ws->dev, di.sms,
+                                               (cudaStream_t)stream),
+                        "study fp32 launch");
+}
+
 tcr_status tcr_probe_collapse(const double* in, double* out, tcr_algo algo, tcr_stream stream) {
     if (!in || !out) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
     if (algo != TCR_ALGO_MMA_SYNC && algo != TCR_ALGO_SHUFFLE)

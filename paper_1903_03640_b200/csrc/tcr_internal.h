@@ -96,6 +96,10 @@ cudaError_t launch_exact_finalize(const long long* acc, float* out_f32, double* 
 size_t paper_scratch_elems(size_t n);
 cudaError_t launch_reduce_paper_f16(const uint16_t* x, size_t n, uint16_t* scratch, float* out_f32,
                                     int sms, cudaStream_t stream, int* launches);
+// Study mode (NEXT-1): the classic reduction entirely in binary32, naive or
+// Kahan-compensated (lane and grid levels).
+cudaError_t launch_study_fp32(const uint16_t* x, size_t n, bool kahan, float* out,
+                              const DevWorkspace& ws, int sms, cudaStream_t stream);
 cudaError_t launch_sum_partials(const double* partials, size_t count, float* out_f32,
                                 double* out_f64, cudaStream_t stream);
 cudaError_t launch_round_f64(const double* in, float* out, cudaStream_t stream);

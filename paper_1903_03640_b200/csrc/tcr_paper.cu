@@ -65,7 +65,94 @@ paper_level_kernel(const uint16_t* __restrict__ in, size_t len, uint16_t* __rest
     }
 }
 
+// ---------------------------------------------------------------------------
+// NEXT-1 comparison points (study mode): the classic reduction entirely in
+// binary32 -- naive, or with Kahan compensation at the lane and grid levels
+// (A13) -- with the same loads, tree shape and last-CTA completion as the
+// product's shuffle path but no fp64 anywhere.
+// ---------------------------------------------------------------------------
+template <bool kKahan>
+__device__ __forceinline__ void add_f32(float& s, float& c, float v) {
+    if constexpr (kKahan) {
+        const float y = v - c;
+        const float t = s + y;
+        c = (t - s) - y;
+        s = t;
+    } else {
+        s += v;
+    }
+}
+
+template <bool kKahan>
+__global__ void __launch_bounds__(kLevelWarps * 32)
+study_fp32_kernel(const uint16_t* __restrict__ x, size_t n, float* out, DevWorkspace ws) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    size_t head = ((16u - ((uintptr_t)x & 15u)) & 15u) >> 1;
+    if (head > n) head = n;
+    const uint16_t* xa = x + head;
+    const size_t nb = n - head;
+    const size_t T = nb / kTileElems;
+    const int tail = (int)(nb - T * kTileElems);
+    const size_t W = (size_t)gridDim.x * kLevelWarps;
+    const size_t w = (size_t)blockIdx.x * kLevelWarps + warp;
+    const uint4* base = reinterpret_cast<const uint4*>(xa) + lane;
+    float s = 0.f, c = 0.f;
+    size_t t = w;
+    for (; t + 3 * W < T; t += 4 * W) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ldg_stream(base + (t + (size_t)u * W) * 32);
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) add_f32<kKahan>(s, c, vec_sum_f32(v[u]));
+    }
+    for (; t < T; t += W) add_f32<kKahan>(s, c, vec_sum_f32(ldg_stream(base + t * 32)));
+    if (w == W - 1) {
+        if (head) add_f32<kKahan>(s, c, vec_sum_f32(load_ragged(x, (int)head, lane)));
+        if (tail) add_f32<kKahan>(s, c, vec_sum_f32(load_ragged(xa + T * kTileElems, tail, lane)));
+    }
+    float v = s;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);  // binary32 tree
+    __shared__ float s_warp[kLevelWarps];
+    __shared__ unsigned s_last;
+    if (lane == 0) s_warp[warp] = v;
+    __syncthreads();
+    if (warp != 0) return;
+    float b = lane < kLevelWarps ? s_warp[lane] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    float* parts = reinterpret_cast<float*>(ws.partials);
+    if (lane == 0) {
+        parts[blockIdx.x] = b;
+        __threadfence();
+        s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    }
+    __syncwarp();
+    if (!s_last) return;
+    if (lane == 0) {
+        __threadfence();
+        float gs = 0.f, gc = 0.f;
+        for (unsigned i = 0; i < gridDim.x; ++i) add_f32<kKahan>(gs, gc, __ldcg(parts + i));
+        *out = gs;
+        *ws.ticket = 0u;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_study_fp32(const uint16_t* x, size_t n, bool kahan, float* out,
+                              const DevWorkspace& ws, int sms, cudaStream_t stream) {
+    const size_t tiles = n / kTileElems;
+    size_t g = (tiles + 4 * kLevelWarps - 1) / (4 * kLevelWarps);
+    const size_t gmax = (size_t)sms * 4;
+    if (g > gmax) g = gmax;
+    if (g > (size_t)ws.capacity) g = ws.capacity;
+    if (g < 1) g = 1;
+    if (kahan)
+        study_fp32_kernel<true><<<(unsigned)g, kLevelWarps * 32, 0, stream>>>(x, n, out, ws);
+    else
+        study_fp32_kernel<false><<<(unsigned)g, kLevelWarps * 32, 0, stream>>>(x, n, out, ws);
+    return cudaGetLastError();
+}
 
 size_t paper_scratch_elems(size_t n) {
     size_t total = 0;

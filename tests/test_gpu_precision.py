@@ -169,3 +169,43 @@ def test_precision_paper_literal_fp16():
         assert r["ours_err_units"] <= 16, r
     # all-positive data overflows binary16 in the literal algorithm at 2^20
     assert any(r["dist"] == "uniform01" and math.isinf(r["paper_f16"]) for r in rows)
+
+
+def test_precision_fp32_naive_and_kahan():
+    """NEXT-1 comparison points: the classic reduction entirely in binary32,
+    naive and Kahan-compensated (A13), vs the product path (fp32 chains of
+    K = 4, fp64 above) and the MMA path; written to
+    gpurun_out/precision_fp32.json."""
+    import torch
+
+    import paper_1903_03640_b200 as tcr
+
+    rows = []
+    out = torch.empty(1, dtype=torch.float32, device="cuda")
+    o64 = torch.empty(1, dtype=torch.float64, device="cuda")
+    for dname, d in (("uniform_pm1", gen.UNIFORM_PM1), ("uniform01", gen.UNIFORM_01),
+                     ("wide", gen.WIDE)):
+        for lg in (16, 20, 24, 26):
+            bits = gen.generate(gen.SEED_C2, 0, (1 << lg) + 11, d)
+            es = oracle.exact_sum_fp16(bits, threads=8)
+            x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.float16)
+            r = {"dist": dname, "log2n": lg}
+            for name, call in (("fp32_naive", lambda: tcr.tcr_reduce_sum_study_fp32(x, out)),
+                               ("fp32_kahan", lambda: tcr.tcr_reduce_sum_study_fp32(x, out, True)),
+                               ("shuffle_fp64", lambda: tcr.tcr_reduce_sum_algo(
+                                   x, out_f32=out, out_f64=o64, algo="shuffle")),
+                               ("mma_sync", lambda: tcr.tcr_reduce_sum_algo(
+                                   x, out_f32=out, out_f64=o64, algo="mma_sync"))):
+                call()
+                torch.cuda.synchronize()
+                r[name + "_units"] = _err_units(float(out.item()), es)
+            rows.append(r)
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/precision_fp32.json", "w") as f:
+        json.dump({"unit": "2^-24 * sum|x|", "rows": rows}, f, indent=1)
+    for r in rows:
+        print(r)
+        assert r["fp32_kahan_units"] <= 16 and r["mma_sync_units"] <= 16, r
+    # on all-positive data at the largest n, compensation beats the naive sum
+    big = [r for r in rows if r["dist"] == "uniform01" and r["log2n"] == 26][0]
+    assert big["fp32_kahan_units"] <= big["fp32_naive_units"], big
