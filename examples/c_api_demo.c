@@ -1,7 +1,8 @@
 /*
  * c_api_demo.c -- using libtcr from plain C (no Python, no torch): allocate
  * device memory with the CUDA runtime, fill it, and call the C ABI of
- * include/tcr.h.  Prints the MMA-encoded, shuffle and exact sums of
+ * include/tcr.h.  Prints the MMA-encoded, shuffle, exact and (one-rank)
+ * peer-combined sums of
  * x_i = ((i % 7) - 3) * 0.25 for i < n (exactly representable; the exact sum
  * is known in closed form, so the program checks itself).
  *
@@ -44,7 +45,7 @@ int main(int argc, char** argv) {
     tcr_half* x = 0;
     float* out = 0;
     int64_t* acc = 0;
-    if (cudaMalloc((void**)&x, n * sizeof(uint16_t)) || cudaMalloc((void**)&out, 3 * sizeof(float)) ||
+    if (cudaMalloc((void**)&x, n * sizeof(uint16_t)) || cudaMalloc((void**)&out, 4 * sizeof(float)) ||
         cudaMalloc((void**)&acc, 6 * sizeof(int64_t))) {
         fprintf(stderr, "cudaMalloc failed\n");
         return 1;
@@ -53,15 +54,21 @@ int main(int argc, char** argv) {
     CHECK(tcr_reduce_sum(x, n, out, 0));
     CHECK(tcr_reduce_sum_shuffle(x, n, out + 1, 0));
     CHECK(tcr_reduce_sum_exact(x, n, acc, out + 2, 0, 0));
-    float r[3];
+    /* a one-rank peer group: the fused cross-GPU combine with itself */
+    void* mailbox = 0;
+    CHECK(tcr_peer_mailbox_alloc(&mailbox));
+    CHECK(tcr_reduce_sum_peer(x, n, TCR_DTYPE_F16, TCR_ALGO_DEFAULT, &mailbox, 1, 0, out + 3, 0, 0));
+    float r[4];
     cudaMemcpy(r, out, sizeof r, cudaMemcpyDeviceToHost);
     float host_r = 0;
     CHECK(tcr_reduce_sum_host(h, n, &host_r, 0));
     const double want = 0.25 * (double)exact_q;
-    printf("n=%zu exact=%.2f mma=%.2f shuffle=%.2f exact_gpu=%.2f host_entry=%.2f launches=%llu\n", n,
-           want, r[0], r[1], r[2], host_r, (unsigned long long)tcr_launch_count());
+    printf("n=%zu exact=%.2f mma=%.2f shuffle=%.2f exact_gpu=%.2f peer=%.2f host_entry=%.2f "
+           "launches=%llu\n",
+           n, want, r[0], r[1], r[2], r[3], host_r, (unsigned long long)tcr_launch_count());
     const int ok = r[0] == (float)want && r[1] == (float)want && r[2] == (float)want &&
-                   host_r == (float)want;
+                   r[3] == (float)want && host_r == (float)want;
+    tcr_peer_mailbox_free(mailbox);
     tcr_release_workspaces();
     cudaFree(x);
     cudaFree(out);
