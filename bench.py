@@ -74,10 +74,28 @@ class ClockSampler:
 
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.h = self._handle_for_cuda_device(pynvml, index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
             self.nv = None
+
+    @staticmethod
+    def _handle_for_cuda_device(pynvml, index: int):
+        """NVML handle of the CUDA device `index`, matched by UUID or PCI address
+        (CUDA's device order need not be NVML's, e.g. without
+        CUDA_DEVICE_ORDER=PCI_BUS_ID); the index only as a last resort."""
+        import torch
+
+        p = torch.cuda.get_device_properties(index)
+        try:  # UUID first (survives virtualised PCI addresses), then PCI address
+            return pynvml.nvmlDeviceGetHandleByUUID(f"GPU-{p.uuid}".encode())
+        except Exception:
+            pass
+        try:
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(index)
 
     def _run(self):
         while not self._stop.is_set():
