@@ -36,9 +36,21 @@ class PeerGroup:
                 out = [None] * self.world
                 dist.all_gather_object(out, obj, group=group)
                 return out
-        self.mailbox = lib.tcr_peer_mailbox_alloc()
-        handle = lib.tcr_peer_ipc_handle(self.mailbox) if self.world > 1 else b""
+        # Every rank takes part in the handle exchange even if its own set-up
+        # failed (it sends None), so a failure cannot leave the others blocked
+        # in the collective; then all ranks raise together.
+        self.mailbox, handle, err = None, None, None
+        try:
+            self.mailbox = lib.tcr_peer_mailbox_alloc()
+            handle = lib.tcr_peer_ipc_handle(self.mailbox) if self.world > 1 else b""
+        except Exception as e:
+            err = e
         handles = all_gather(handle) if self.world > 1 else [handle]
+        if err is not None or any(h is None for h in handles):
+            if self.mailbox is not None:
+                lib.tcr_peer_mailbox_free(self.mailbox)
+            bad = [r for r, h in enumerate(handles) if h is None]
+            raise RuntimeError(f"peer group set-up failed on rank(s) {bad}: {err!r}")
         self._opened = []
         self.mailboxes = []
         for r in range(self.world):

@@ -303,3 +303,45 @@ def test_gloo_peer_group_protocol(world):
         for v in parts:
             want += v
         assert {res[r][e] for r in range(world)} == {want}, e  # replicated, rank-ordered
+
+
+class _FailingPeerLib(_ShmPeerLib):
+    def tcr_peer_mailbox_alloc(self):
+        if self.rank == 1:
+            raise RuntimeError("simulated allocation failure")
+        return super().tcr_peer_mailbox_alloc()
+
+
+def _worker_peer_fail(rank, world, port, tag, q):
+    import torch.distributed as dist
+
+    from paper_1903_03640_b200.peer import PeerGroup
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lib = _FailingPeerLib(tag, rank)
+    try:
+        PeerGroup(lib=lib)
+        q.put((rank, "constructed"))
+    except RuntimeError as e:
+        q.put((rank, "raised" if "rank(s) [1]" in str(e) else f"other: {e}"))
+    dist.destroy_process_group()
+
+
+def test_gloo_peer_group_setup_failure_raises_on_every_rank():
+    """A rank whose mailbox set-up fails still joins the handle exchange, so no
+    rank blocks, and every rank raises (bench.py then falls back to NCCL)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    tag = f"{os.getpid()}f{port}"
+    ps = [ctx.Process(target=_worker_peer_fail, args=(r, world, port, tag, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(60)
+        assert p.exitcode == 0
+    assert set(res.values()) == {"raised"}, res
