@@ -122,3 +122,30 @@ def test_sass_is_sm100a_with_tensor_core_instructions():
     assert "sm_100a" in sass
     for mnemonic in ("HMMA.16816.F32", "DMMA.8x8x4", "UTCHMMA", "LDTM", "UBLKCP"):
         assert mnemonic in sass, mnemonic
+
+
+def test_sass_fused_peer_kernel_has_mma_and_system_scope_peer_traffic():
+    """NEXT-2 evidence in SASS: the fused kernel (reduce_stream_kernel<..., kPeer
+    = true>) carries the tensor-core tiles (HMMA), the level-2 DMMA collapse,
+    the 16-byte system-scope stores of the push (STG.E.128.STRONG.SYS, to the
+    peers' mapped mailboxes), the system-scope polls and the %globaltimer
+    bound -- one kernel, no separate collective."""
+    import re
+    import shutil
+    import subprocess
+
+    import paper_1903_03640_b200 as tcr
+
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run(["cuobjdump", "-sass", tcr.LIB_PATH], capture_output=True,
+                          text=True, check=True).stdout
+    funcs = re.split(r"\n\s+Function : ", sass)[1:]
+    peer = [f for f in funcs if f.startswith("_ZN3tcr20reduce_stream_kernelILb1ELi0ELi4ELi8ELb1E")]
+    assert peer, "fused peer kernel not found"
+    body = peer[0]
+    for mnemonic in ("HMMA.16816.F32", "DMMA.8x8x4", "STG.E.128.STRONG.SYS", "LDG.E.128.STRONG.SYS",
+                     "SR_GLOBALTIMER", "NANOSLEEP"):
+        assert mnemonic in body, mnemonic
+    plain = [f for f in funcs if f.startswith("_ZN3tcr20reduce_stream_kernelILb1ELi0ELi4ELi8ELb0E")]
+    assert plain and "STRONG.SYS" not in plain[0]  # the plain kernel has no peer traffic
