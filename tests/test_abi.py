@@ -149,3 +149,19 @@ def test_sass_fused_peer_kernel_has_mma_and_system_scope_peer_traffic():
         assert mnemonic in body, mnemonic
     plain = [f for f in funcs if f.startswith("_ZN3tcr20reduce_stream_kernelILb1ELi0ELi4ELi8ELb0E")]
     assert plain and "STRONG.SYS" not in plain[0]  # the plain kernel has no peer traffic
+
+
+def test_product_path_fails_loudly_without_the_library(tmp_path):
+    """No fallback: a copy of the package without libtcr.so refuses to import."""
+    import shutil
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_1903_03640_b200")
+    dst = tmp_path / "paper_1903_03640_b200"
+    shutil.copytree(pkg, dst, ignore=shutil.ignore_patterns("*.so", "csrc", "__pycache__"))
+    r = subprocess.run([sys.executable, "-c", "import paper_1903_03640_b200"], cwd=tmp_path,
+                       capture_output=True, text=True, env={**os.environ, "PYTHONPATH": str(tmp_path)})
+    assert r.returncode != 0
+    assert "ImportError" in r.stderr and "no fallback" in r.stderr
