@@ -209,6 +209,16 @@ tcr_status tcr_reduce_sum_host(const tcr_half *x, size_t n, float *out, tcr_stre
 tcr_status tcr_reduce_sum_exact(const tcr_half *x, size_t n, int64_t *acc, float *out_f32,
                                 double *out_f64, tcr_stream stream);
 
+/*
+ * tcr_reduce_sum_exact_ex -- tcr_reduce_sum_exact for binary16 and the fp8
+ * formats (E4M3, E5M2: every fp8 value is a binary16 value, converted exactly
+ * on the fly; same acc[6] state in units of 2^-24, same finalize).
+ * TCR_ERR_INVALID_VALUE for bfloat16 (its range needs ~270-bit accumulators;
+ * not built).
+ */
+tcr_status tcr_reduce_sum_exact_ex(const void *x, size_t n, tcr_dtype dtype, int64_t *acc,
+                                   float *out_f32, double *out_f64, tcr_stream stream);
+
 /* tcr_exact_finalize -- RNE binary32 / binary64 of an (allreduced) acc[6]. */
 tcr_status tcr_exact_finalize(const int64_t *acc, float *out_f32, double *out_f64,
                               tcr_stream stream);

@@ -104,6 +104,7 @@ _SIGS = {
     "tcr_round_f64_to_f32": [_P, _P, _P],
     "tcr_reduce_sum_exact": [_P, _SZ, _P, _P, _P, _P],
     "tcr_exact_finalize": [_P, _P, _P, _P],
+    "tcr_reduce_sum_exact_ex": [_P, _SZ, _I, _P, _P, _P, _P],
     "tcr_probe_mma": [_P, _P, _P, _I, _P],
     "tcr_probe_collapse": [_P, _P, _I, _P],
     "tcr_reduce_sum_paper_f16": [_P, _SZ, _P, _P],
@@ -299,6 +300,14 @@ def tcr_reduce_sum_exact(x, acc=None, out_f32=None, out_f64=None, n=None, stream
     NaN/+inf/-inf counts) and/or the correctly rounded float32 / float64."""
     _check(_lib.tcr_reduce_sum_exact(_ptr(x), _numel(x, n), _ptr(acc), _ptr(out_f32),
                                      _ptr(out_f64), _stream(stream, x)), "tcr_reduce_sum_exact")
+
+
+def tcr_reduce_sum_exact_ex(x, acc=None, out_f32=None, out_f64=None, dtype=None, n=None,
+                            stream=None) -> None:
+    """Bitwise-exact sum of binary16 or fp8 (E4M3 / E5M2) x."""
+    _check(_lib.tcr_reduce_sum_exact_ex(_ptr(x), _numel(x, n), _dtype_of(x, dtype), _ptr(acc),
+                                        _ptr(out_f32), _ptr(out_f64), _stream(stream, x)),
+           "tcr_reduce_sum_exact_ex")
 
 
 def tcr_exact_finalize(acc, out_f32=None, out_f64=None, stream=None) -> None:

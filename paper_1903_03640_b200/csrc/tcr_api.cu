@@ -425,8 +425,27 @@ tcr_status tcr_reduce_sum_exact(const tcr_half* x, size_t n, int64_t* acc, float
     tcr_status s = prologue((cudaStream_t)stream, &di, &ws);
     if (s != TCR_OK) return s;
     const LaunchCfg cfg = make_cfg(di);
-    return after_launch(tcr::launch_reduce_exact(x, n, reinterpret_cast<long long*>(acc), out_f32,
+    return after_launch(tcr::launch_reduce_exact(0, x, n, reinterpret_cast<long long*>(acc), out_f32,
                                                  out_f64, ws->dev, cfg, (cudaStream_t)stream),
+                        "exact kernel launch");
+}
+
+tcr_status tcr_reduce_sum_exact_ex(const void* x, size_t n, tcr_dtype dtype, int64_t* acc,
+                                   float* out_f32, double* out_f64, tcr_stream stream) {
+    if (dtype != TCR_DTYPE_F16 && dtype != TCR_DTYPE_E4M3 && dtype != TCR_DTYPE_E5M2)
+        return fail(TCR_ERR_INVALID_VALUE, "exact: dtype must be F16, E4M3 or E5M2");
+    if ((!x && n) || (!acc && !out_f32 && !out_f64))
+        return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    if (!aligned(x, dtype == TCR_DTYPE_F16 ? 2 : 1) || !aligned(acc, 8) || !aligned(out_f32, 4) ||
+        !aligned(out_f64, 8))
+        return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
+    DeviceInfo di;
+    Workspace* ws = nullptr;
+    tcr_status s = prologue((cudaStream_t)stream, &di, &ws);
+    if (s != TCR_OK) return s;
+    const LaunchCfg cfg = make_cfg(di);
+    return after_launch(tcr::launch_reduce_exact((int)dtype, x, n, reinterpret_cast<long long*>(acc),
+                                                 out_f32, out_f64, ws->dev, cfg, (cudaStream_t)stream),
                         "exact kernel launch");
 }
 

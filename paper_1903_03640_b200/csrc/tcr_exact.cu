@@ -88,6 +88,55 @@ __device__ __forceinline__ void exact_vec(const uint4& v, double& a0, double& a1
     }
 }
 
+// fp8 (E4M3 / E5M2) -> binary16 is exact (every fp8 value is a binary16
+// value; cvt.rn.f16x2.{e4m3,e5m2}x2): 16 fp8 bytes become two vectors of 8
+// binary16 that go through the same exact accumulation (NEXT-3 x NEXT-4).
+template <int F>
+__device__ __forceinline__ void fp8_to_f16(const uint4& v, uint4& lo, uint4& hi) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint16_t b0 = (uint16_t)(w[k] & 0xFFFFu), b1 = (uint16_t)(w[k] >> 16);
+        if constexpr (F == kE4M3) {
+            asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(o[2 * k]) : "h"(b0));
+            asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(o[2 * k + 1]) : "h"(b1));
+        } else {
+            asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(o[2 * k]) : "h"(b0));
+            asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(o[2 * k + 1]) : "h"(b1));
+        }
+    }
+    lo = make_uint4(o[0], o[1], o[2], o[3]);
+    hi = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+// One loaded 16-byte vector of format F into the accumulators.
+template <int F>
+__device__ __forceinline__ void exact_vec_f(const uint4& v, double& a0, double& a1,
+                                            uint32_t& probe) {
+    if constexpr (F == kF16) {
+        exact_vec(v, a0, a1, probe);
+    } else {
+        uint4 lo, hi;
+        fp8_to_f16<F>(v, lo, hi);
+        exact_vec(lo, a0, a1, probe);
+        exact_vec(hi, a0, a1, probe);
+    }
+}
+
+template <int F>
+__device__ __forceinline__ void fix_specials_f(const uint4& v, double& a0, double& a1,
+                                               uint32_t (&cnt)[3]) {
+    if constexpr (F == kF16) {
+        fix_specials(v, a0, a1, cnt);
+    } else {
+        uint4 lo, hi;
+        fp8_to_f16<F>(v, lo, hi);
+        fix_specials(lo, a0, a1, cnt);
+        fix_specials(hi, a0, a1, cnt);
+    }
+}
+
 // Exact conversion of a flushed accumulator to integer units of 2^-24.
 __device__ __forceinline__ long long to_units(double a) {
     return __double2ll_rn((a * 0x1p1008) * 0x1p24);  // both scalings exact; result < 2^53
@@ -183,16 +232,18 @@ __device__ void finalize(const long long* acc, float* out_f32, double* out_f64) 
 // kPeer: the NEXT-2 x NEXT-3 variant -- the last CTA combines the limbs
 // with the peers' over NVLink mailboxes (tcr_peer.cuh); grid.y slices =
 // emulated ranks, as in reduce_stream_kernel.
-template <int U, bool kPeer>
+template <int U, bool kPeer, int F = kF16>
 __global__ void __launch_bounds__(kExactWarps * 32, (U <= 4 ? 4 : 3))
-reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc, float* out_f32,
+reduce_exact_kernel(const uint8_t* __restrict__ x, size_t n, long long* out_acc, float* out_f32,
                     double* out_f64, DevWorkspace ws, PeerCombine pc) {
+    constexpr int ES = FmtInfo<F>::kBytes;
+    constexpr int kTileBytes = 512;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int me = pc.rank;
     if (kPeer && gridDim.y > 1) {  // emulated peer group: slice y is rank y
         const size_t P = gridDim.y, r = blockIdx.y;
         const size_t lo = r * n / P, hi = (r + 1) * n / P;
-        x += lo;
+        x += lo * ES;
         n = hi - lo;
         ws.partials += 5 * r * gridDim.x;  // 5 int64 words per CTA (stored in the doubles)
         ws.ticket += r;
@@ -201,16 +252,18 @@ reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc
         if (out_f64) out_f64 += r;
         me = (int)r;
     }
-    size_t head = ((16u - ((uintptr_t)x & 15u)) & 15u) >> 1;
-    if (head > n) head = n;
-    const uint16_t* xa = x + head;
-    const size_t nb = n - head;
-    const size_t T = nb / kTileElems;
-    const int tail = (int)(nb - T * kTileElems);
+    const size_t nbytes = n * ES;
+    size_t head = (16u - ((uintptr_t)x & 15u)) & 15u;  // bytes before the first 16-B boundary
+    if (head > nbytes) head = nbytes;
+    const uint8_t* xa = x + head;
+    const size_t nb = nbytes - head;
+    const size_t T = nb / kTileBytes;
+    const int tail = (int)(nb - T * kTileBytes);
     const size_t W = (size_t)gridDim.x * kExactWarps;
     const size_t w = (size_t)blockIdx.x * kExactWarps + warp;
     const uint4* base = reinterpret_cast<const uint4*>(xa) + lane;
-    constexpr int kFlush = kFlushIter * kExactUnroll / U;  // <= 1024 halves per accumulator
+    // <= 1024 binary16 per accumulator between flushes (an fp8 vector is 16 of them)
+    constexpr int kFlush = kFlushIter * kExactUnroll / U / (ES == 1 ? 2 : 1);
 
     double a0 = 0.0, a1 = 0.0;
     i128 acc = 0;
@@ -224,11 +277,11 @@ reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc
         for (int u = 0; u < U; ++u) v[u] = ldg_stream(base + (t + (size_t)u * W) * 32);
         __syncwarp();  // scheduling fence: all U loads issue before the first consumer
 #pragma unroll
-        for (int u = 0; u < U; ++u) exact_vec(v[u], a0, a1, probe);
+        for (int u = 0; u < U; ++u) exact_vec_f<F>(v[u], a0, a1, probe);
         if (probe & 0x7FFF7FFFu) {  // some half was inf or NaN (rare): reload and fix
 #pragma unroll 1
             for (int u = 0; u < U; ++u)
-                fix_specials(ldg_stream(base + (t + (size_t)u * W) * 32), a0, a1, cnt);
+                fix_specials_f<F>(ldg_stream(base + (t + (size_t)u * W) * 32), a0, a1, cnt);
             probe = 0u;
         }
         if (++it == kFlush) {
@@ -239,8 +292,8 @@ reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc
     }
     auto one = [&](const uint4& v) {
         uint32_t p = 0u;
-        exact_vec(v, a0, a1, p);
-        if (p & 0x7FFF7FFFu) fix_specials(v, a0, a1, cnt);
+        exact_vec_f<F>(v, a0, a1, p);
+        if (p & 0x7FFF7FFFu) fix_specials_f<F>(v, a0, a1, cnt);
     };
     if (t < T) {  // fewer than U tiles left for this warp: one predicated batch (one latency)
         uint4 v[U];
@@ -253,8 +306,8 @@ reduce_exact_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc
         for (int u = 0; u < U; ++u) one(v[u]);
     }
     if (w == W - 1) {  // ragged head and tail
-        if (head) one(load_ragged(x, (int)head, lane));
-        if (tail) one(load_ragged(xa + T * kTileElems, tail, lane));
+        if (head) one(load_ragged_bytes(x, (int)head, lane));
+        if (tail) one(load_ragged_bytes(xa + T * kTileBytes, tail, lane));
     }
     acc += (i128)to_units(a0) + (i128)to_units(a1);
 
@@ -364,30 +417,45 @@ int exact_grid(size_t n, const LaunchCfg& cfg, int capacity_words) {
     return g < 1 ? 1 : (int)g;
 }
 
-cudaError_t launch_reduce_exact(const uint16_t* x, size_t n, long long* out_acc, float* out_f32,
-                                double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
-                                cudaStream_t stream) {
-    const int g = exact_grid(n, cfg, ws.capacity);
+template <int F>
+static cudaError_t launch_exact_f(const uint8_t* x, size_t n, long long* out_acc, float* out_f32,
+                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                  cudaStream_t stream) {
+    // grid from the input bytes (in 2-byte element equivalents)
+    const int g = exact_grid(n * FmtInfo<F>::kBytes / 2, cfg, ws.capacity);
     const PeerCombine none{};
     if (cfg.exact_unroll == 8)
-        reduce_exact_kernel<8, false><<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32,
-                                                                          out_f64, ws, none);
+        reduce_exact_kernel<8, false, F><<<g, kExactWarps * 32, 0, stream>>>(
+            x, n, out_acc, out_f32, out_f64, ws, none);
     else
-        reduce_exact_kernel<4, false><<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32,
-                                                                          out_f64, ws, none);
+        reduce_exact_kernel<4, false, F><<<g, kExactWarps * 32, 0, stream>>>(
+            x, n, out_acc, out_f32, out_f64, ws, none);
     return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_exact(int fmt, const void* x, size_t n, long long* out_acc,
+                                float* out_f32, double* out_f64, const DevWorkspace& ws,
+                                const LaunchCfg& cfg, cudaStream_t stream) {
+    const uint8_t* xb = static_cast<const uint8_t*>(x);
+    switch (fmt) {
+        case kE4M3: return launch_exact_f<kE4M3>(xb, n, out_acc, out_f32, out_f64, ws, cfg, stream);
+        case kE5M2: return launch_exact_f<kE5M2>(xb, n, out_acc, out_f32, out_f64, ws, cfg, stream);
+        case kF16: return launch_exact_f<kF16>(xb, n, out_acc, out_f32, out_f64, ws, cfg, stream);
+        default: return cudaErrorInvalidValue;  // bfloat16: not exact-capable
+    }
 }
 
 cudaError_t launch_reduce_exact_peer(const uint16_t* x, size_t n, long long* out_acc,
                                      float* out_f32, double* out_f64, const DevWorkspace& ws,
                                      const LaunchCfg& cfg, const PeerCombine& pc, bool emulate,
                                      cudaStream_t stream) {
-    auto kernel = reduce_exact_kernel<8, true>;  // the peer variant at the default unroll only
+    auto kernel = reduce_exact_kernel<8, true, kF16>;  // the peer variant: binary16, unroll 8
     LaunchCfg c8 = cfg;
     c8.exact_unroll = 8;
     if (!emulate) {
         const int g = exact_grid(n, c8, ws.capacity);
-        kernel<<<g, kExactWarps * 32, 0, stream>>>(x, n, out_acc, out_f32, out_f64, ws, pc);
+        kernel<<<g, kExactWarps * 32, 0, stream>>>(reinterpret_cast<const uint8_t*>(x), n, out_acc,
+                                                   out_f32, out_f64, ws, pc);
         return cudaGetLastError();
     }
     // emulated ranks wait on one another: one cooperative launch (co-residency)
@@ -399,7 +467,7 @@ cudaError_t launch_reduce_exact_peer(const uint16_t* x, size_t n, long long* out
     const int cap = occ * cfg.sms / P;
     if (g > cap) g = cap;
     if (g < 1) return cudaErrorCooperativeLaunchTooLarge;
-    const uint16_t* xa = x;
+    const uint8_t* xa = reinterpret_cast<const uint8_t*>(x);
     size_t na = n;
     long long* acc = out_acc;
     float* o32 = out_f32;

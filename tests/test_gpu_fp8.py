@@ -148,3 +148,56 @@ def test_fp8_segment_index_bit_exact(tcr):
         tcr.tcr_reduce_sum_segmented_ex(_dev(bits, 1, fmt), torch.from_numpy(off).cuda(), out)
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy(), lens.astype(np.float32))
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+def test_fp8_exact_bitwise(tcr, fmt):
+    """NEXT-3 x NEXT-4: tcr_reduce_sum_exact_ex on fp8 is bitwise equal to the
+    exact fp8 oracle (every fp8 value is a binary16 value; same exact
+    accumulation), for ragged sizes, every byte misalignment and all
+    distributions; the limbs are the oracle's integer in units of 2^-24."""
+    import torch
+
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    o64 = torch.empty(1, dtype=torch.float64, device="cuda")
+    acc = torch.empty(6, dtype=torch.int64, device="cuda")
+    for n in (0, 1, 15, 16, 17, 511, 512, 513, 100_003, 3_000_017):
+        for dist in (gen.UNIFORM_PM1, gen.WIDE, gen.UNIFORM_01, gen.SMALLINT):
+            bits = gen.generate_fp8(n + dist, 0, n, dist, fmt)
+            es = oracle.exact_sum_fp8(bits, fmt)
+            for off in ((0, 1, 7) if n < 10_000 else (3,)):
+                tcr.tcr_reduce_sum_exact_ex(_dev(bits, off, fmt), acc=acc, out_f32=o32, out_f64=o64)
+                torch.cuda.synchronize()
+                assert float(o32.item()) == es.f32(), (n, dist, off, o32.item(), es.f64())
+                assert float(o64.item()) == es.f64(), (n, dist, off)
+                T = tcr.exact_limbs_to_int(acc)
+                assert T * oracle.UNIT == es.value, (n, dist, off)
+
+
+def test_fp8_exact_specials(tcr):
+    import math
+
+    import torch
+
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    cases = [(oracle.FP8_E4M3, 0x7F, "nan"), (oracle.FP8_E5M2, 0x7C, "+inf"),
+             (oracle.FP8_E5M2, 0xFC, "-inf"), (oracle.FP8_E5M2, 0x7E, "nan")]
+    for fmt, special, kind in cases:
+        bits = gen.generate_fp8(1, 0, 5000, gen.UNIFORM_PM1, fmt)
+        bits[1234] = special
+        tcr.tcr_reduce_sum_exact_ex(_dev(bits, 0, fmt), out_f32=o32)
+        torch.cuda.synchronize()
+        g = float(o32.item())
+        if kind == "nan":
+            assert math.isnan(g), (fmt, special, g)
+        else:
+            assert g == (math.inf if kind == "+inf" else -math.inf), (fmt, special, g)
+
+
+def test_exact_rejects_bf16(tcr):
+    import torch
+
+    x = torch.zeros(16, dtype=torch.bfloat16, device="cuda")
+    o = torch.empty(1, dtype=torch.float32, device="cuda")
+    with pytest.raises(tcr.TcrError):
+        tcr.tcr_reduce_sum_exact_ex(x, out_f32=o)
