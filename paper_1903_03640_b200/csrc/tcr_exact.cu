@@ -116,11 +116,21 @@ __device__ __forceinline__ void exact_vec_f(const uint4& v, double& a0, double& 
                                             uint32_t& probe) {
     if constexpr (F == kF16) {
         exact_vec(v, a0, a1, probe);
-    } else {
-        uint4 lo, hi;
-        fp8_to_f16<F>(v, lo, hi);
-        exact_vec(lo, a0, a1, probe);
-        exact_vec(hi, a0, a1, probe);
+    } else {  // word by word: two binary16 pairs per 32-bit word, few live registers
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint16_t b = (uint16_t)(w[k] >> (16 * h));
+                uint32_t o;
+                if constexpr (F == kE4M3) asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(o) : "h"(b));
+                else asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(o) : "h"(b));
+                probe = probe_word(o, probe);
+                a0 += scaled_lo(o);
+                a1 += scaled_hi(o);
+            }
+        }
     }
 }
 
