@@ -168,13 +168,16 @@ def _cpu_count():
         return os.cpu_count() or 1
 
 
-def cpu_oracle_leg(bits_sample, threads: int):
-    """Time the exact oracle (as it stands) on a host sample; returns (Gelem/s, seconds)."""
+def cpu_oracle_leg(bits_sample, threads: int, want_sum: bool = False):
+    """Time the exact oracle (as it stands) on a host sample; returns (Gelem/s,
+    seconds) and, with want_sum, the oracle's ExactSum too."""
     import oracle
 
     t0 = time.perf_counter()
-    oracle.exact_sum_fp16(bits_sample, threads=threads)
+    es = oracle.exact_sum_fp16(bits_sample, threads=threads)
     dt = time.perf_counter() - t0
+    if want_sum:
+        return bits_sample.size / dt / 1e9, dt, es
     return bits_sample.size / dt / 1e9, dt
 
 
@@ -516,7 +519,7 @@ def main():
                "api": "tcr_reduce_sum_host (pinned host input, chunked H2D inside the call)"}
         del host
 
-    cpu = None
+    cpu, check = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # the oracle over the workload's own elements (the whole array when it
         # is small enough to copy back), repeated until ~10 s of CPU work
@@ -528,8 +531,9 @@ def main():
                                        device=dev).view(torch.int16).cpu().numpy().view(np.uint16)
         threads = _cpu_count()
         done, spent, passes = 0, 0.0, 0
+        es = None
         while spent < args.cpu_seconds or passes == 0:
-            _, dt = cpu_oracle_leg(bits, threads)
+            _, dt, es = cpu_oracle_leg(bits, threads, want_sum=True)
             done += bits.size
             spent += dt
             passes += 1
@@ -538,6 +542,18 @@ def main():
                          f"({'all' if sample == n else 'part'} of it), exact int128 oracle, "
                          f"{threads} threads, {spent:.1f} s"}
         del bits
+        # the timed steps' own result against the oracle's exact sum of the
+        # same array (c3 at N = 1 with the whole workload in the sample)
+        if (args.workload == "c3" and sample == n and x.element_size() == 2
+                and args.dtype == "f16" and peer is None):
+            import oracle
+
+            g = float(out32.item())
+            check = {"gpu_f32": g, "exact_f64": es.f64(),
+                     "err_units_2^-24_sum_abs": (float(oracle.error_units(g, es) / es.abs_value)
+                                                 if es.abs_value else 0.0),
+                     "within_2^-20_sum_abs": bool(oracle.within_tolerance(g, es)),
+                     "bitwise_equal_rne_exact": g == es.f32()}
 
     if rank == 0:
         line = {
@@ -572,6 +588,7 @@ def main():
             "hbm_gbs": job_bytes_per_step * K / (total_ms * 1e-3) / 1e9,
             "frac_of_8tbs": job_bytes_per_step * K / (total_ms * 1e-3) / (world * 8e12),
             "cpu_baseline": cpu,
+            "check": check,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),

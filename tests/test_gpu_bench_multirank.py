@@ -71,6 +71,7 @@ def test_bench_json_contract_single_gpu(extra):
     ck = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(ck)
     if "c5" not in extra:
+        assert d["check"]["within_2^-20_sum_abs"] is True  # the timed result vs the oracle
         e = d["e2e"]
         assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 << 24 and e["d2h_bytes_per_step"] == 4
 
