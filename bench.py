@@ -491,19 +491,23 @@ def main():
 
     # ---------------- end to end through the public API with host buffers ----------------
     e2e = None
-    if args.workload == "c3" and args.e2e_steps > 0 and args.dtype == "f16":
-        host = torch.empty(n, dtype=torch.int16, pin_memory=True)
-        host.copy_(x.view(torch.int16) if x.element_size() == 2 else
-                   gen.generate_tensor(gen.SEED_C3, 0, n, gen.UNIFORM_PM1, device=dev).view(torch.int16))
+    if args.workload == "c3" and args.e2e_steps > 0:
+        # the step's input bits in pinned host memory (any element type)
+        esz = x.element_size()
+        host = torch.empty(n * esz, dtype=torch.uint8, pin_memory=True)
+        host.copy_(x.view(torch.uint8).reshape(-1))
+        dtype_code = {"f16": tcr.TCR_DTYPE_F16, "bf16": tcr.TCR_DTYPE_BF16,
+                      "e4m3": tcr.TCR_DTYPE_E4M3, "e5m2": tcr.TCR_DTYPE_E5M2}[args.dtype]
         res_t = torch.empty(1, dtype=torch.float32, device=dev)
         hs = torch.cuda.Stream(dev)
-        tcr.tcr_reduce_sum_host(host, n=n, stream=hs.cuda_stream)  # warm-up
+        tcr.tcr_reduce_sum_host_ex(host, dtype_code, n=n, stream=hs.cuda_stream)  # warm-up
         if world > 1:
             dist.barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(hs)
         for _ in range(args.e2e_steps):
-            g = tcr.tcr_reduce_sum_host(host, n=n, stream=hs.cuda_stream)  # H2D + reduce + D2H
+            # H2D + reduce + D2H through the public host entry point
+            g = tcr.tcr_reduce_sum_host_ex(host, dtype_code, n=n, stream=hs.cuda_stream)
             if world > 1:
                 res_t.fill_(g)
                 dist.all_reduce(res_t)
@@ -515,8 +519,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = t.item()
         e2e = {"value": world * n * args.e2e_steps / (e_ms * 1e-3) / 1e9, "unit": "Gelem/s",
-               "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 4, "steps": args.e2e_steps,
-               "api": "tcr_reduce_sum_host (pinned host input, chunked H2D inside the call)"}
+               "h2d_bytes_per_step": esz * n, "d2h_bytes_per_step": 4, "steps": args.e2e_steps,
+               "api": "tcr_reduce_sum_host_ex (pinned host input, chunked H2D inside the call)"}
         del host
 
     cpu, check = None, None

@@ -189,6 +189,9 @@ tcr_status tcr_reduce_sum_batched_ex(const void *x, tcr_dtype dtype, size_t num_
  * returning.  Same accuracy contract as tcr_reduce_sum.
  */
 tcr_status tcr_reduce_sum_host(const tcr_half *x, size_t n, float *out, tcr_stream stream);
+/* The same for any input type (chunks of 128 MiB of input bytes). */
+tcr_status tcr_reduce_sum_host_ex(const void *x, size_t n, tcr_dtype dtype, float *out,
+                                  tcr_stream stream);
 
 /*
  * tcr_reduce_sum_exact -- NEXT-3: the EXACT sum (no rounding before the

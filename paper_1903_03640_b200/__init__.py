@@ -101,6 +101,7 @@ _SIGS = {
     "tcr_reduce_sum_batched": [_P, _SZ, _SZ, _P, _P],
     "tcr_reduce_sum_batched_shuffle": [_P, _SZ, _SZ, _P, _P],
     "tcr_reduce_sum_host": [_P, _SZ, _P, _P],
+    "tcr_reduce_sum_host_ex": [_P, _SZ, _I, _P, _P],
     "tcr_round_f64_to_f32": [_P, _P, _P],
     "tcr_reduce_sum_exact": [_P, _SZ, _P, _P, _P, _P],
     "tcr_exact_finalize": [_P, _P, _P, _P],
@@ -293,6 +294,25 @@ def tcr_reduce_sum_host(x, n=None, stream=None) -> float:
     _check(_lib.tcr_reduce_sum_host(addr, cnt, ctypes.addressof(res), _stream(stream)),
            "tcr_reduce_sum_host")
     return float(res.value)
+
+
+def tcr_reduce_sum_host_ex(x, dtype, n=None, stream=None) -> float:
+    """tcr_reduce_sum_host for any input type (dtype: TCR_DTYPE_*), x a HOST
+    buffer of raw element bits (pinned CPU tensor, numpy array or address)."""
+    res = ctypes.c_float(0.0)
+    if hasattr(x, "ctypes"):  # numpy
+        addr, cnt = x.ctypes.data, x.size
+    else:
+        addr, cnt = _ptr(x), (x.numel() if hasattr(x, "numel") else None)
+    cnt = int(n) if n is not None else int(cnt)
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream().cuda_stream
+    _check(_lib.tcr_reduce_sum_host_ex(addr, cnt, int(dtype), ctypes.addressof(res),
+                                       _stream(stream)),
+           "tcr_reduce_sum_host_ex")
+    return res.value
 
 
 def tcr_reduce_sum_exact(x, acc=None, out_f32=None, out_f64=None, n=None, stream=None) -> None:

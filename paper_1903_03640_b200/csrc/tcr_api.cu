@@ -357,16 +357,19 @@ tcr_status tcr_reduce_sum_batched_shuffle(const tcr_half* x, size_t num_segments
                           (cudaStream_t)stream);
 }
 
-tcr_status tcr_reduce_sum_host(const tcr_half* x, size_t n, float* out, tcr_stream stream_) {
-    cudaStream_t stream = (cudaStream_t)stream_;
+// End-to-end host entry for any input type: chunks of 128 MiB of input bytes
+// through two staging buffers (H2D of chunk c+1 overlaps the kernel of c).
+static tcr_status reduce_host_impl(const void* x, size_t n, int fmt, float* out,
+                                   cudaStream_t stream) {
+    const size_t es = fmt >= TCR_DTYPE_E4M3 ? 1 : 2;
     if ((!x && n) || !out) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
-    if (!aligned(x, 2)) return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
+    if (!aligned(x, es)) return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
     DeviceInfo di;
     Workspace* ws = nullptr;
     tcr_status s = prologue(stream, &di, &ws);
     if (s != TCR_OK) return s;
     const LaunchCfg cfg = make_cfg(di);
-    constexpr size_t kChunk = (size_t)1 << 26;  // elements per staged chunk (128 MiB)
+    const size_t kChunk = ((size_t)1 << 27) / es;  // elements per staged chunk (128 MiB)
     const size_t chunks = n ? (n + kChunk - 1) / kChunk : 0;
     cudaError_t e;
     {
@@ -381,7 +384,7 @@ tcr_status tcr_reduce_sum_host(const tcr_half* x, size_t n, float* out, tcr_stre
                 return cuda_fail(e, "cudaMalloc(chunk partials)");
             ws->chunk_cap = cap;
         }
-        const size_t need = (n < kChunk ? (n ? n : 1) : kChunk) * sizeof(uint16_t);
+        const size_t need = (n < kChunk ? (n ? n : 1) : kChunk) * es;
         if (ws->staging_bytes < need) {
             for (void*& b : ws->staging) {
                 if (b) cudaFree(b);
@@ -392,16 +395,22 @@ tcr_status tcr_reduce_sum_host(const tcr_half* x, size_t n, float* out, tcr_stre
             ws->staging_bytes = need;
         }
     }
+    // the default algorithm of the type (tcgen05 for large fp8 chunks)
+    const bool tc05 = fmt >= TCR_DTYPE_E4M3 && kChunk >= ((size_t)1 << 26);
     int launches = 0;
+    const char* xb = static_cast<const char*>(x);
     for (size_t c = 0; c < chunks; ++c) {
         const size_t lo = c * kChunk, cnt = (n - lo < kChunk) ? n - lo : kChunk;
         void* buf = ws->staging[c & 1];
-        if ((e = cudaMemcpyAsync(buf, x + lo, cnt * sizeof(uint16_t), cudaMemcpyHostToDevice,
-                                 stream)))
+        if ((e = cudaMemcpyAsync(buf, xb + lo * es, cnt * es, cudaMemcpyHostToDevice, stream)))
             return cuda_fail(e, "cudaMemcpyAsync(H2D)");
-        if ((e = tcr::launch_reduce_stream(true, 0, static_cast<const uint16_t*>(buf), cnt, nullptr,
-                                           ws->chunk_partials + c, ws->dev, cfg, stream)))
-            return cuda_fail(e, "reduce kernel launch");
+        const uint16_t* db = static_cast<const uint16_t*>(buf);
+        e = (tc05 && cnt >= ((size_t)1 << 26))
+                ? tcr::launch_reduce_tcgen05(fmt, db, cnt, nullptr, ws->chunk_partials + c, ws->dev,
+                                             cfg, stream)
+                : tcr::launch_reduce_stream(true, fmt, db, cnt, nullptr, ws->chunk_partials + c,
+                                            ws->dev, cfg, stream);
+        if (e) return cuda_fail(e, "reduce kernel launch");
         ++launches;
     }
     if ((e = tcr::launch_sum_partials(ws->chunk_partials, chunks, ws->dev_out, nullptr, stream)))
@@ -412,6 +421,17 @@ tcr_status tcr_reduce_sum_host(const tcr_half* x, size_t n, float* out, tcr_stre
         return cuda_fail(e, "cudaMemcpyAsync(D2H)");
     if ((e = cudaStreamSynchronize(stream))) return cuda_fail(e, "cudaStreamSynchronize");
     return TCR_OK;
+}
+
+tcr_status tcr_reduce_sum_host(const tcr_half* x, size_t n, float* out, tcr_stream stream) {
+    return reduce_host_impl(x, n, TCR_DTYPE_F16, out, (cudaStream_t)stream);
+}
+
+tcr_status tcr_reduce_sum_host_ex(const void* x, size_t n, tcr_dtype dtype, float* out,
+                                  tcr_stream stream) {
+    if (dtype < TCR_DTYPE_F16 || dtype > TCR_DTYPE_E5M2)
+        return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
+    return reduce_host_impl(x, n, (int)dtype, out, (cudaStream_t)stream);
 }
 
 tcr_status tcr_reduce_sum_exact(const tcr_half* x, size_t n, int64_t* acc, float* out_f32,

@@ -507,3 +507,23 @@ def test_host_threads_concurrent_streams(tcr):
     for t in ts:
         t.join(120)
     assert not errors, errors[:3]
+
+
+def test_host_entry_all_dtypes(tcr):
+    """tcr_reduce_sum_host_ex: pinned host bits of every type, vs the oracles."""
+    import torch
+
+    n = (1 << 27) + 12345  # two staging chunks for fp16 / bf16
+    b16 = gen.generate(5, 0, n, gen.UNIFORM_PM1)
+    hb = torch.from_numpy(b16.view(np.int16)).pin_memory()
+    g = tcr.tcr_reduce_sum_host_ex(hb, tcr.TCR_DTYPE_F16, n=n)
+    assert oracle.within_tolerance(g, oracle.exact_sum_fp16(b16, threads=8))
+    bb = gen.generate_bf16(5, 0, n, gen.UNIFORM_PM1)
+    g = tcr.tcr_reduce_sum_host_ex(torch.from_numpy(bb.view(np.int16)).pin_memory(),
+                                   tcr.TCR_DTYPE_BF16, n=n)
+    assert oracle.within_tolerance(g, oracle.exact_sum_bf16(bb))
+    for fmt, code in ((gen.FP8_E4M3, tcr.TCR_DTYPE_E4M3), (gen.FP8_E5M2, tcr.TCR_DTYPE_E5M2)):
+        for m in (100_003, (1 << 28) + 7):  # below and above the tcgen05 chunk switch
+            f8 = gen.generate_fp8(6, 0, m, gen.UNIFORM_PM1, fmt)
+            g = tcr.tcr_reduce_sum_host_ex(torch.from_numpy(f8).pin_memory(), code, n=m)
+            assert oracle.within_tolerance(g, oracle.exact_sum_fp8(f8, fmt)), (fmt, m)
