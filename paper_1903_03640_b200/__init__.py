@@ -500,18 +500,18 @@ def tcr_status_string(s: int) -> str:
 def reduce_sum(x, algo: str | int = "default", exact: bool = False, out_dtype=None, stream=None):
     """Sum of a CUDA tensor (float16, bfloat16, float8_e4m3fn or float8_e5m2),
     returned as a 1-element device tensor (float32, or float64 with
-    ``out_dtype=torch.float64``).  ``exact=True`` (float16 only) returns the
-    correctly rounded exact sum (tcr_reduce_sum_exact)."""
+    ``out_dtype=torch.float64``).  ``exact=True`` (float16 and float8) returns
+    the correctly rounded exact sum (tcr_reduce_sum_exact_ex)."""
     import torch
 
     x = x.reshape(-1) if x.is_contiguous() else x.contiguous().reshape(-1)
     f64 = out_dtype == torch.float64
     out = torch.empty(1, dtype=torch.float64 if f64 else torch.float32, device=x.device)
     if exact:
-        if x.dtype != torch.float16:
-            raise TypeError("exact=True supports float16 input")
-        tcr_reduce_sum_exact(x, out_f32=None if f64 else out, out_f64=out if f64 else None,
-                             stream=stream)
+        if x.dtype == torch.bfloat16:
+            raise TypeError("exact=True supports float16 and float8 input")
+        tcr_reduce_sum_exact_ex(x, out_f32=None if f64 else out, out_f64=out if f64 else None,
+                                stream=stream)
     else:
         tcr_reduce_sum_ex(x, out_f32=None if f64 else out, out_f64=out if f64 else None,
                           algo=algo, stream=stream)

@@ -415,6 +415,7 @@ def test_convenience_wrappers(tcr):
     f8 = gen.generate_fp8(3, 0, 5000, gen.UNIFORM_PM1, gen.FP8_E4M3)
     x8 = torch.from_numpy(f8).cuda().view(torch.float8_e4m3fn)
     assert oracle.within_tolerance(float(tcr.reduce_sum(x8).item()), oracle.exact_sum_fp8(f8, 0))
+    assert float(tcr.reduce_sum(x8, exact=True).item()) == oracle.exact_sum_fp8(f8, 0).f32()
     off = torch.tensor([0, 10, 10, 5000], dtype=torch.int64, device="cuda")
     seg = tcr.reduce_sum_segmented(xb, off).cpu().tolist()
     ref = [oracle.exact_sum_bf16(b16[a:b]) for a, b in ((0, 10), (10, 10), (10, 5000))]
