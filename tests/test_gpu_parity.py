@@ -164,6 +164,8 @@ def test_host_entry_end_to_end(tcr):
     assert oracle.within_tolerance(g, es), (g, es.f64())
     g2 = tcr.tcr_reduce_sum_host(bits[:1000])  # pageable numpy
     assert oracle.within_tolerance(g2, oracle.exact_sum_fp16(bits[:1000]))
+    assert tcr.tcr_reduce_sum_host(bits[:0]) == 0.0  # empty: R = +0 (G5)
+    assert tcr.tcr_reduce_sum_host(bits[:1]) == float(bits[:1].view(np.float16)[0])
 
 
 def test_config_knobs(tcr):
