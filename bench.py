@@ -296,8 +296,10 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(dev)
     exact = args.algo == "exact"
-    if args.dtype != "f16" and (args.workload != "c3" or (exact and args.dtype == "bf16")):
-        raise SystemExit("--dtype bf16/e4m3/e5m2 supports the c3 workload (exact: f16 and fp8)")
+    if args.dtype != "f16" and args.workload != "c3":
+        raise SystemExit("--dtype bf16/e4m3/e5m2 supports the c3 workload")
+    if exact and args.dtype == "bf16" and world > 1:
+        raise SystemExit("exact bfloat16 has no mergeable limb state: single GPU only")
     algo = tcr.ALGOS["default" if exact else args.algo]
     peak, peak_src = _peaks()
     peer, combine_note = None, None
@@ -408,8 +410,9 @@ def main():
             elif peer is not None:  # reduction + cross-GPU combine in ONE launch
                 peer.reduce_sum(x, out_f32=out32, algo=algo, stream=stream)
             elif exact:
-                tcr.tcr_reduce_sum_exact_ex(x, acc=acc6, out_f32=out32 if world == 1 else None,
-                                            stream=stream)
+                tcr.tcr_reduce_sum_exact_ex(x, acc=acc6 if args.dtype != "bf16" else None,
+                                            out_f32=out32 if world == 1 or args.dtype == "bf16"
+                                            else None, stream=stream)
             elif world == 1:
                 tcr.tcr_reduce_sum_ex(x, out_f32=out32, algo=algo, stream=stream)
             else:

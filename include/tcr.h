@@ -213,11 +213,15 @@ tcr_status tcr_reduce_sum_exact(const tcr_half *x, size_t n, int64_t *acc, float
                                 double *out_f64, tcr_stream stream);
 
 /*
- * tcr_reduce_sum_exact_ex -- tcr_reduce_sum_exact for binary16 and the fp8
- * formats (E4M3, E5M2: every fp8 value is a binary16 value, converted exactly
- * on the fly; same acc[6] state in units of 2^-24, same finalize).
- * TCR_ERR_INVALID_VALUE for bfloat16 (its range needs ~270-bit accumulators;
- * not built).
+ * tcr_reduce_sum_exact_ex -- tcr_reduce_sum_exact for every input type:
+ *   binary16, fp8 E4M3 / E5M2 (every fp8 value is a binary16 value, converted
+ *   exactly on the fly): the same acc[6] state in units of 2^-24, the same
+ *   tcr_exact_finalize;
+ *   bfloat16 (range 2^-133..2^128): eight 32-exponent windows, each summed
+ *   exactly (binary64 fast path for iterations inside one window, integer
+ *   slow path otherwise), assembled in a 384-bit integer and rounded once;
+ *   acc must be NULL (no limb state for bfloat16; TCR_ERR_INVALID_VALUE).
+ * Bitwise equal to the exact oracle of the type.
  */
 tcr_status tcr_reduce_sum_exact_ex(const void *x, size_t n, tcr_dtype dtype, int64_t *acc,
                                    float *out_f32, double *out_f64, tcr_stream stream);

@@ -324,7 +324,7 @@ def tcr_reduce_sum_exact(x, acc=None, out_f32=None, out_f64=None, n=None, stream
 
 def tcr_reduce_sum_exact_ex(x, acc=None, out_f32=None, out_f64=None, dtype=None, n=None,
                             stream=None) -> None:
-    """Bitwise-exact sum of binary16 or fp8 (E4M3 / E5M2) x."""
+    """Bitwise-exact sum of binary16, bfloat16 (no acc) or fp8 (E4M3 / E5M2) x."""
     _check(_lib.tcr_reduce_sum_exact_ex(_ptr(x), _numel(x, n), _dtype_of(x, dtype), _ptr(acc),
                                         _ptr(out_f32), _ptr(out_f64), _stream(stream, x)),
            "tcr_reduce_sum_exact_ex")
@@ -500,16 +500,14 @@ def tcr_status_string(s: int) -> str:
 def reduce_sum(x, algo: str | int = "default", exact: bool = False, out_dtype=None, stream=None):
     """Sum of a CUDA tensor (float16, bfloat16, float8_e4m3fn or float8_e5m2),
     returned as a 1-element device tensor (float32, or float64 with
-    ``out_dtype=torch.float64``).  ``exact=True`` (float16 and float8) returns
-    the correctly rounded exact sum (tcr_reduce_sum_exact_ex)."""
+    ``out_dtype=torch.float64``).  ``exact=True`` returns the correctly rounded
+    exact sum (tcr_reduce_sum_exact_ex), for every supported type."""
     import torch
 
     x = x.reshape(-1) if x.is_contiguous() else x.contiguous().reshape(-1)
     f64 = out_dtype == torch.float64
     out = torch.empty(1, dtype=torch.float64 if f64 else torch.float32, device=x.device)
     if exact:
-        if x.dtype == torch.bfloat16:
-            raise TypeError("exact=True supports float16 and float8 input")
         tcr_reduce_sum_exact_ex(x, out_f32=None if f64 else out, out_f64=out if f64 else None,
                                 stream=stream)
     else:

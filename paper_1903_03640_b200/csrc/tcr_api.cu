@@ -145,7 +145,9 @@ tcr_status get_workspace(int dev, const DeviceInfo& di, cudaStream_t stream, Wor
         return TCR_OK;
     }
     auto* ws = new Workspace();
-    const int capacity = di.sms * 32;  // 32 = max resident CTAs per SM
+    // 64 doubles per SM: one fp64 partial per CTA for up to 32 CTAs/SM, or
+    // the 19-word partials of the exact bfloat16 kernel at 3 CTAs/SM
+    const int capacity = di.sms * 64;
     constexpr size_t kCounterBytes = 128;
     const size_t bytes = sizeof(double) * (size_t)capacity + kCounterBytes;
     cudaError_t e = cudaMalloc(&ws->block, bytes);
@@ -452,11 +454,13 @@ tcr_status tcr_reduce_sum_exact(const tcr_half* x, size_t n, int64_t* acc, float
 
 tcr_status tcr_reduce_sum_exact_ex(const void* x, size_t n, tcr_dtype dtype, int64_t* acc,
                                    float* out_f32, double* out_f64, tcr_stream stream) {
-    if (dtype != TCR_DTYPE_F16 && dtype != TCR_DTYPE_E4M3 && dtype != TCR_DTYPE_E5M2)
-        return fail(TCR_ERR_INVALID_VALUE, "exact: dtype must be F16, E4M3 or E5M2");
+    if (dtype < TCR_DTYPE_F16 || dtype > TCR_DTYPE_E5M2)
+        return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
+    if (dtype == TCR_DTYPE_BF16 && acc)
+        return fail(TCR_ERR_INVALID_VALUE, "exact bfloat16: no acc[] state (pass acc = NULL)");
     if ((!x && n) || (!acc && !out_f32 && !out_f64))
         return fail(TCR_ERR_INVALID_VALUE, "null pointer");
-    if (!aligned(x, dtype == TCR_DTYPE_F16 ? 2 : 1) || !aligned(acc, 8) || !aligned(out_f32, 4) ||
+    if (!aligned(x, dtype <= TCR_DTYPE_BF16 ? 2 : 1) || !aligned(acc, 8) || !aligned(out_f32, 4) ||
         !aligned(out_f64, 8))
         return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
     DeviceInfo di;
@@ -464,6 +468,10 @@ tcr_status tcr_reduce_sum_exact_ex(const void* x, size_t n, tcr_dtype dtype, int
     tcr_status s = prologue((cudaStream_t)stream, &di, &ws);
     if (s != TCR_OK) return s;
     const LaunchCfg cfg = make_cfg(di);
+    if (dtype == TCR_DTYPE_BF16)
+        return after_launch(tcr::launch_reduce_exact_bf16(static_cast<const uint16_t*>(x), n, out_f32,
+                                                          out_f64, ws->dev, cfg, (cudaStream_t)stream),
+                            "exact bf16 kernel launch");
     return after_launch(tcr::launch_reduce_exact((int)dtype, x, n, reinterpret_cast<long long*>(acc),
                                                  out_f32, out_f64, ws->dev, cfg, (cudaStream_t)stream),
                         "exact kernel launch");

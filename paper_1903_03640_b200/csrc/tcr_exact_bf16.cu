@@ -1,0 +1,366 @@
+// tcr_exact_bf16.cu -- NEXT-3 x NEXT-4: bitwise-exact sum of bfloat16 (R(X)
+// of Eq. 2, rounded once at the end).
+//
+// bfloat16 spans 2^-133 .. 2^128, so no single fixed-point word holds every
+// input.  Exponents are cut into 8 windows of 32 (k = e >> 5 of the 8-bit
+// biased exponent e).  Inside one window every value, placed into a binary64
+// as bf16 * 2^-896 (hi word = magnitude bits << 13 | sign, lo word 0: exact
+// for normal AND subnormal bf16, the bf16 exponent landing on the binary64
+// exponent field), is a multiple of the window's unit and below 2^40 units,
+// so up to 2^13 of them add exactly in binary64.
+//   fast path  all halves of a warp's iteration lie in one window (or are
+//              zero): one binary64 accumulator for that window, flushed every
+//              64 iterations or when the window changes;
+//   slow path  mixed windows or inf/NaN in the iteration: each half is turned
+//              into an integer of its window's unit and added to a per-lane
+//              int64 slot of that window in shared memory.
+// Window units (unscaled): u_0 = 2^-133, u_k = 2^(32k - 134) for k >= 1.
+// Levels 2-4 add the per-window totals as int128 (order-free); the last CTA
+// assembles T = 2 I_0 + sum_k I_k 2^(32k) in units of 2^-134 in a 384-bit
+// integer and rounds it once (RNE) to binary32 / binary64.
+#include "tcr_device.cuh"
+#include "tcr_internal.h"
+
+namespace tcr {
+
+namespace {
+
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+constexpr int kXbWarps = 8;
+constexpr int kXbU = 4;
+constexpr int kXbFlushIter = 64;        // 64 iterations x 32 halves <= 2^13 per accumulator
+constexpr int kXbWords = 8 * 2 + 3;     // per CTA partial: 8 x int128 + 3 special counts
+
+__device__ __forceinline__ double placed(uint32_t h) {  // bf16 (low 16 bits) * 2^-896
+    const uint32_t hi = ((h & 0x7FFFu) << 13) | ((h & 0x8000u) << 16);
+    return __hiloint2double((int)hi, 0);
+}
+
+// Flushed window accumulator -> integer in the window's unit (exact; < 2^53).
+__device__ __forceinline__ long long win_units(double a, int k) {
+    // k >= 1: a * 2^(1030 - 32k); k = 0: a * 2^1029 (two exact power-of-two steps)
+    const double s2 = k == 0 ? 0x1p514 : ldexp(1.0, 515 - 32 * k);
+    return __double2ll_rn((a * 0x1p515) * s2);
+}
+
+// One finite nonzero bf16 -> (window, integer in the window's unit).
+__device__ __forceinline__ long long half_units(uint32_t h, int& k) {
+    const int e = (int)((h >> 7) & 0xFFu);
+    const long long m = (long long)(h & 0x7Fu);
+    long long v;
+    if (e == 0) {
+        k = 0;
+        v = m;  // subnormal: m * 2^-133
+    } else {
+        k = e >> 5;
+        v = (128 + m) << (k == 0 ? e - 1 : e - 32 * k);
+    }
+    return (h & 0x8000u) ? -v : v;
+}
+
+__device__ __forceinline__ i128 shfl_xor_i128(i128 v, int o) {
+    const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+    const unsigned long long lo2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const unsigned long long hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    return (i128)(((u128)hi2 << 64) | (u128)lo2);
+}
+
+__device__ __forceinline__ i128 warp_sum_i128(i128 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += shfl_xor_i128(v, o);
+    return v;
+}
+
+// 384-bit two's complement accumulator: limbs l[0] (least significant) .. l[5].
+struct Big384 {
+    unsigned long long l[6];
+};
+
+__device__ void big_add_shifted(Big384& B, i128 v, int shift) {  // B += v * 2^shift (mod 2^384)
+    const unsigned long long ext = v < 0 ? ~0ull : 0ull;
+    unsigned long long e[7];  // v sign-extended to 448 bits
+    e[0] = (unsigned long long)v;
+    e[1] = (unsigned long long)(v >> 64);
+    for (int i = 2; i < 7; ++i) e[i] = ext;
+    const int q = shift >> 6, r = shift & 63;
+    unsigned long long carry = 0;
+    for (int i = 0; i < 6; ++i) {
+        const int j = i - q;
+        unsigned long long w = 0;
+        if (j >= 0) w = r ? (e[j] << r) : e[j];
+        if (r && j - 1 >= 0) w |= e[j - 1] >> (64 - r);
+        const unsigned long long a0 = B.l[i];
+        const unsigned long long s1 = a0 + w;
+        const unsigned long long c1 = s1 < a0 ? 1ull : 0ull;
+        const unsigned long long s2 = s1 + carry;
+        const unsigned long long c2 = s2 < s1 ? 1ull : 0ull;
+        B.l[i] = s2;
+        carry = c1 | c2;
+    }
+}
+
+// RNE of the non-negative 384-bit M (units 2^-134) to `bits` significant bits:
+// value = mant * 2^(exp - 134).
+__device__ void big_round(const Big384& M, int bits, unsigned long long& mant, int& exp) {
+    int top = -1;
+    for (int i = 5; i >= 0 && top < 0; --i)
+        if (M.l[i]) top = i * 64 + 63 - __clzll((long long)M.l[i]);
+    if (top < 0) {
+        mant = 0;
+        exp = 0;
+        return;
+    }
+    auto bit = [&](int p) -> unsigned long long { return (M.l[p >> 6] >> (p & 63)) & 1ull; };
+    if (top < bits) {  // fits: exact
+        unsigned long long m = 0;
+        for (int p = top; p >= 0; --p) m = (m << 1) | bit(p);
+        mant = m;
+        exp = 0;
+        return;
+    }
+    const int shift = top - (bits - 1);
+    unsigned long long q = 0;
+    for (int p = top; p >= shift; --p) q = (q << 1) | bit(p);
+    const unsigned long long half = bit(shift - 1);
+    bool sticky = false;
+    for (int p = shift - 2; p >= 0 && !sticky; --p) sticky = bit(p) != 0;
+    if (half && (sticky || (q & 1ull))) ++q;  // may reach 2^bits: still exact below
+    mant = q;
+    exp = shift;
+}
+
+__global__ void __launch_bounds__(kXbWarps * 32, 3)
+reduce_exact_bf16_kernel(const uint16_t* __restrict__ x, size_t n, float* out_f32,
+                         double* out_f64, DevWorkspace ws) {
+    __shared__ long long s_I[8][kXbWarps * 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s_I[k][tid] = 0;
+    uint32_t cnt[3] = {0u, 0u, 0u};  // NaN, +inf, -inf
+
+    size_t head = ((16u - ((uintptr_t)x & 15u)) & 15u) >> 1;
+    if (head > n) head = n;
+    const uint16_t* xa = x + head;
+    const size_t nb = n - head;
+    const size_t T = nb / kTileElems;
+    const int tail = (int)(nb - T * kTileElems);
+    const size_t W = (size_t)gridDim.x * kXbWarps;
+    const size_t w = (size_t)blockIdx.x * kXbWarps + warp;
+    const uint4* base = reinterpret_cast<const uint4*>(xa) + lane;
+
+    double aw = 0.0;
+    int wcur = -1;  // window of aw (warp-uniform)
+    int it = 0;
+    auto flush = [&]() {
+        if (wcur >= 0) s_I[wcur][tid] += win_units(aw, wcur);
+        aw = 0.0;
+        it = 0;
+    };
+    auto slow = [&](const uint4& v) {
+        const uint32_t ws4[4] = {v.x, v.y, v.z, v.w};
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t h = (ws4[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+            if ((h & 0x7F80u) == 0x7F80u) {  // inf / NaN
+                if (h & 0x7Fu) ++cnt[0];
+                else if (h & 0x8000u) ++cnt[2];
+                else ++cnt[1];
+            } else if (h & 0x7FFFu) {
+                int k;
+                const long long u = half_units(h, k);
+                s_I[k][tid] += u;
+            }
+        }
+    };
+    // an iteration's vectors: fast path if every nonzero finite half is in one window
+    auto process = [&](const uint4 (&v)[kXbU], int nv) {
+        // packed over the two halves of each word: window bits (exponent >> 5),
+        // their max, their min over nonzero halves, and an inf/NaN flag
+        uint32_t kmax = 0u, kmin = 0x00070007u, spec = 0u;
+#pragma unroll
+        for (int u = 0; u < kXbU; ++u) {
+            if (u >= nv) break;
+            const uint32_t ws4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t wd = ws4[q];
+                spec |= ((wd & 0x7F807F80u) + 0x00800080u) & 0x80008000u;
+                const uint32_t kk = (wd >> 12) & 0x00070007u;
+                const uint32_t zero = __vcmpeq2(wd & 0x7FFF7FFFu, 0u);  // 0xFFFF per zero half
+                kmax = __vmaxu2(kmax, kk);
+                kmin = __vminu2(kmin, kk | (zero & 0x00070007u));
+            }
+        }
+        const uint32_t lmax = max(kmax & 0xFFFFu, kmax >> 16);
+        const uint32_t lmin = min(kmin & 0xFFFFu, kmin >> 16);
+        const uint32_t wc = __reduce_max_sync(0xffffffffu, lmax);
+        // every nonzero half of the warp is in window wc (<= wc by the max, >= by the min)
+        const bool own_ok = spec == 0u && lmin >= wc;
+        if (__all_sync(0xffffffffu, own_ok)) {
+            const int k = (int)wc;
+            if (k != wcur) {
+                flush();
+                wcur = k;
+            }
+#pragma unroll
+            for (int u = 0; u < kXbU; ++u) {
+                if (u >= nv) break;
+                const uint32_t ws4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    aw += placed(ws4[q] & 0xFFFFu);
+                    aw += placed(ws4[q] >> 16);
+                }
+            }
+            if (++it == kXbFlushIter) flush();
+        } else {
+            flush();
+            for (int u = 0; u < nv; ++u) slow(v[u]);
+        }
+    };
+
+    size_t t = w;
+    for (; t + (size_t)(kXbU - 1) * W < T; t += (size_t)kXbU * W) {
+        uint4 v[kXbU];
+#pragma unroll
+        for (int u = 0; u < kXbU; ++u) v[u] = ldg_stream(base + (t + (size_t)u * W) * 32);
+        __syncwarp();
+        process(v, kXbU);
+    }
+    if (t < T) {  // leftover tiles of this warp: one predicated batch
+        uint4 v[kXbU];
+#pragma unroll
+        for (int u = 0; u < kXbU; ++u)
+            v[u] = (t + (size_t)u * W < T) ? ldg_stream(base + (t + (size_t)u * W) * 32)
+                                           : make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+        process(v, kXbU);
+    }
+    flush();
+    if (w == W - 1) {  // ragged head and tail (zero padded)
+        if (head) slow(load_ragged(x, (int)head, lane));
+        if (tail) slow(load_ragged(xa + T * kTileElems, tail, lane));
+    }
+    __syncwarp();
+
+    // levels 2-4: int128 sums per window (order-free) and the special counts
+    __shared__ long long s_part[kXbWarps][kXbWords];
+    for (int k = 0; k < 8; ++k) {
+        const i128 s = warp_sum_i128((i128)s_I[k][tid]);
+        if (lane == 0) {
+            s_part[warp][2 * k] = (long long)(unsigned long long)s;
+            s_part[warp][2 * k + 1] = (long long)(s >> 64);
+        }
+    }
+    for (int c = 0; c < 3; ++c) {
+        uint32_t s = cnt[c];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) s_part[warp][16 + c] = s;
+    }
+    __syncthreads();
+    if (warp != 0) return;
+    __shared__ unsigned s_last;
+    i128 win[8];
+    long long c3[3] = {0, 0, 0};
+    for (int k = 0; k < 8; ++k) {
+        i128 s = 0;
+        if (lane < kXbWarps)
+            s = (i128)(((u128)(unsigned long long)s_part[lane][2 * k + 1] << 64) |
+                       (u128)(unsigned long long)s_part[lane][2 * k]);
+        win[k] = warp_sum_i128(s);
+    }
+    for (int c = 0; c < 3; ++c) {
+        long long s = lane < kXbWarps ? s_part[lane][16 + c] : 0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        c3[c] = s;
+    }
+    if (gridDim.x > 1) {
+        long long* parts = reinterpret_cast<long long*>(ws.partials);
+        if (lane == 0) {
+            long long* p = parts + (size_t)kXbWords * blockIdx.x;
+            for (int k = 0; k < 8; ++k) {
+                p[2 * k] = (long long)(unsigned long long)win[k];
+                p[2 * k + 1] = (long long)(win[k] >> 64);
+            }
+            for (int c = 0; c < 3; ++c) p[16 + c] = c3[c];
+            __threadfence();
+            s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+        }
+        __syncwarp();
+        if (!__shfl_sync(0xffffffffu, s_last, 0)) return;
+        __threadfence();
+        for (int k = 0; k < 8; ++k) {
+            i128 s = 0;
+            for (int i = lane; i < (int)gridDim.x; i += 32) {
+                const long long* p = parts + (size_t)kXbWords * i;
+                s += (i128)(((u128)(unsigned long long)__ldcg(p + 2 * k + 1) << 64) |
+                            (u128)(unsigned long long)__ldcg(p + 2 * k));
+            }
+            win[k] = warp_sum_i128(s);
+        }
+        for (int c = 0; c < 3; ++c) {
+            long long s = 0;
+            for (int i = lane; i < (int)gridDim.x; i += 32) s += __ldcg(parts + (size_t)kXbWords * i + 16 + c);
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            c3[c] = s;
+        }
+        if (lane == 0) *ws.ticket = 0u;
+    }
+    if (lane != 0) return;
+    float f;
+    double d;
+    if (c3[0] || (c3[1] && c3[2])) {
+        f = __int_as_float(0x7FC00000);
+        d = __longlong_as_double(0x7FF8000000000000ll);
+    } else if (c3[1]) {
+        f = __int_as_float(0x7F800000);
+        d = __longlong_as_double(0x7FF0000000000000ll);
+    } else if (c3[2]) {
+        f = __int_as_float(0xFF800000);
+        d = __longlong_as_double((long long)0xFFF0000000000000ull);
+    } else {
+        Big384 B = {{0, 0, 0, 0, 0, 0}};
+        big_add_shifted(B, win[0], 1);  // u_0 = 2 * 2^-134
+        for (int k = 1; k < 8; ++k) big_add_shifted(B, win[k], 32 * k);
+        const bool neg = (long long)B.l[5] < 0;
+        if (neg) {  // magnitude: two's complement negate
+            unsigned long long carry = 1;
+            for (int i = 0; i < 6; ++i) {
+                const unsigned long long v = ~B.l[i] + carry;
+                carry = (carry && v == 0) ? 1ull : 0ull;
+                B.l[i] = v;
+            }
+        }
+        unsigned long long m;
+        int e;
+        big_round(B, 24, m, e);
+        f = ldexpf((float)m, e - 134);  // m <= 2^24 exact; overflow -> inf (IEEE)
+        big_round(B, 53, m, e);
+        d = ldexp((double)m, e - 134);
+        if (neg) {
+            f = -f;
+            d = -d;
+        }
+    }
+    if (out_f32) *out_f32 = f;
+    if (out_f64) *out_f64 = d;
+}
+
+}  // namespace
+
+cudaError_t launch_reduce_exact_bf16(const uint16_t* x, size_t n, float* out_f32,
+                                     double* out_f64, const DevWorkspace& ws,
+                                     const LaunchCfg& cfg, cudaStream_t stream) {
+    const size_t tiles = n / kTileElems;
+    size_t g = (tiles + (size_t)kXbWarps * kXbU - 1) / ((size_t)kXbWarps * kXbU);
+    size_t gmax = (size_t)cfg.sms * 3;
+    const size_t cap = (size_t)ws.capacity / kXbWords;
+    if (gmax > cap) gmax = cap;
+    if (g > gmax) g = gmax;
+    if (g < 1) g = 1;
+    reduce_exact_bf16_kernel<<<(unsigned)g, kXbWarps * 32, 0, stream>>>(x, n, out_f32, out_f64, ws);
+    return cudaGetLastError();
+}
+
+}  // namespace tcr

@@ -108,3 +108,73 @@ def test_ex_rejects_unknown_dtype(tcr):
     o = torch.empty(1, dtype=torch.float32, device="cuda")
     with pytest.raises(tcr.TcrError):
         tcr.tcr_reduce_sum_ex(x, out_f32=o, dtype=7)
+
+
+def _bdev(bits, off=0):
+    import torch
+
+    buf = torch.zeros(bits.size + off + 16, dtype=torch.int16, device="cuda")
+    x = buf[off:off + bits.size]
+    if bits.size:
+        x.copy_(torch.from_numpy(bits.view(np.int16)))
+    return x.view(torch.bfloat16)
+
+
+def _exact_bf16(tcr, x):
+    import torch
+
+    o32 = torch.full((1,), float("nan"), dtype=torch.float32, device="cuda")
+    o64 = torch.full((1,), float("nan"), dtype=torch.float64, device="cuda")
+    tcr.tcr_reduce_sum_exact_ex(x, out_f32=o32, out_f64=o64)
+    torch.cuda.synchronize()
+    return float(o32.item()), float(o64.item())
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 255, 256, 257, 4097, 100_003, 3_000_017])
+def test_bf16_exact_bitwise(tcr, n):
+    """NEXT-3 x NEXT-4: exact bfloat16 (8 exponent windows) is bitwise equal to
+    the exact bf16 oracle (per-exponent bins), every distribution, misaligned."""
+    for dist in (gen.UNIFORM_PM1, gen.WIDE, gen.UNIFORM_01, gen.SMALLINT, gen.ONES):
+        bits = gen.generate_bf16(n + dist, 0, n, dist)
+        es = oracle.exact_sum_bf16(bits)
+        for off in ((0, 1, 5) if n < 5000 else (3,)):
+            g32, g64 = _exact_bf16(tcr, _bdev(bits, off))
+            assert g32 == es.f32() and g64 == es.f64(), (n, dist, off, g32, g64, es.f64())
+
+
+def test_bf16_exact_extreme_ranges(tcr):
+    """Values from every exponent window at once, subnormals, cancellation of
+    huge values leaving tiny ones, overflow past binary32, and all finite
+    bf16 patterns (their sum is exactly 0)."""
+    rng = np.random.default_rng(11)
+    cases = []
+    for _ in range(20):  # random patterns over the whole finite range
+        h = rng.integers(0, 1 << 16, 50_000).astype(np.uint16)
+        h = h[((h >> 7) & 0xFF) != 0xFF]
+        cases.append(h)
+    big, tiny = 0x7F7F, 0x0001  # max finite, min subnormal
+    cases.append(np.array([big, big ^ 0x8000, tiny] * 1000, dtype=np.uint16))  # -> 1000 * 2^-133
+    cases.append(np.array([big] * 10, dtype=np.uint16))  # overflows binary32 -> inf
+    cases.append(np.array([h for h in range(1 << 16) if ((h >> 7) & 0xFF) != 0xFF], dtype=np.uint16))
+    for i, bits in enumerate(cases):
+        es = oracle.exact_sum_bf16(bits)
+        g32, g64 = _exact_bf16(tcr, _bdev(bits, i % 3))
+        assert g32 == es.f32() and g64 == es.f64(), (i, g32, g64, es.f64())
+
+
+def test_bf16_exact_specials(tcr):
+    import math
+
+    bits = gen.generate_bf16(1, 0, 10_000, gen.UNIFORM_PM1)
+    for special, kind in ((0x7F80, "+inf"), (0xFF80, "-inf"), (0x7FC1, "nan")):
+        b = bits.copy()
+        b[4321] = special
+        g32, g64 = _exact_bf16(tcr, _bdev(b))
+        if kind == "nan":
+            assert math.isnan(g32) and math.isnan(g64)
+        else:
+            assert g32 == g64 == (math.inf if kind == "+inf" else -math.inf)
+    b = bits.copy()
+    b[10], b[20] = 0x7F80, 0xFF80
+    g32, _ = _exact_bf16(tcr, _bdev(b))
+    assert math.isnan(g32)

@@ -194,10 +194,14 @@ def test_fp8_exact_specials(tcr):
             assert g == (math.inf if kind == "+inf" else -math.inf), (fmt, special, g)
 
 
-def test_exact_rejects_bf16(tcr):
+def test_exact_bf16_has_no_acc_state(tcr):
     import torch
 
     x = torch.zeros(16, dtype=torch.bfloat16, device="cuda")
     o = torch.empty(1, dtype=torch.float32, device="cuda")
-    with pytest.raises(tcr.TcrError):
-        tcr.tcr_reduce_sum_exact_ex(x, out_f32=o)
+    acc = torch.empty(6, dtype=torch.int64, device="cuda")
+    with pytest.raises(tcr.TcrError):  # the limb state is binary16 / fp8 only
+        tcr.tcr_reduce_sum_exact_ex(x, acc=acc, out_f32=o)
+    tcr.tcr_reduce_sum_exact_ex(x, out_f32=o)  # bf16 itself is exact-capable
+    torch.cuda.synchronize()
+    assert o.item() == 0.0
