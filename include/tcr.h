@@ -138,8 +138,9 @@ tcr_status tcr_reduce_sum_algo(const tcr_half *x, size_t n, float *out_f32, doub
  * element-aligned; fp8 elements are 1 byte).
  * Same accuracy contract (|g - R| <= 2^-20 * sum|x_i| while the sum is
  * inside the binary32 range) and error behaviour; TCR_ERR_INVALID_VALUE for
- * an unknown dtype.  (The exact, host and peer entry points are binary16
- * only, except tcr_reduce_sum_peer, which takes a dtype too.)
+ * an unknown dtype.  (Other entry points taking a dtype:
+ * tcr_reduce_sum_segmented_ex, tcr_reduce_sum_batched_ex,
+ * tcr_reduce_sum_host_ex, tcr_reduce_sum_exact_ex, tcr_reduce_sum_peer.)
  */
 tcr_status tcr_reduce_sum_ex(const void *x, size_t n, tcr_dtype dtype, float *out_f32,
                              double *out_f64, tcr_algo algo, tcr_stream stream);
