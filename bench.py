@@ -298,8 +298,6 @@ def main():
     exact = args.algo == "exact"
     if args.dtype != "f16" and args.workload != "c3":
         raise SystemExit("--dtype bf16/e4m3/e5m2 supports the c3 workload")
-    if exact and args.dtype == "bf16" and world > 1:
-        raise SystemExit("exact bfloat16 has no mergeable limb state: single GPU only")
     algo = tcr.ALGOS["default" if exact else args.algo]
     peak, peak_src = _peaks()
     peer, combine_note = None, None
@@ -369,7 +367,11 @@ def main():
             f", segments sharded over {world} GPUs" if world > 1 else "")
     out32 = torch.empty(1, dtype=torch.float32, device=dev)
     out64 = torch.empty(1, dtype=torch.float64, device=dev)
-    acc6 = torch.empty(6, dtype=torch.int64, device=dev)
+    dtype_code = {"f16": tcr.TCR_DTYPE_F16, "bf16": tcr.TCR_DTYPE_BF16,
+                  "e4m3": tcr.TCR_DTYPE_E4M3, "e5m2": tcr.TCR_DTYPE_E5M2}[args.dtype]
+    # exact state: 6 int64 limbs (binary16 / fp8) or 27 (bfloat16), integer-summable
+    acc6 = torch.empty(tcr.TCR_EXACT_BF16_ACC_WORDS if args.dtype == "bf16"
+                       else tcr.TCR_EXACT_ACC_WORDS, dtype=torch.int64, device=dev)
     torch.cuda.synchronize()
 
     if peer is not None and world > 1:
@@ -410,9 +412,8 @@ def main():
             elif peer is not None:  # reduction + cross-GPU combine in ONE launch
                 peer.reduce_sum(x, out_f32=out32, algo=algo, stream=stream)
             elif exact:
-                tcr.tcr_reduce_sum_exact_ex(x, acc=acc6 if args.dtype != "bf16" else None,
-                                            out_f32=out32 if world == 1 or args.dtype == "bf16"
-                                            else None, stream=stream)
+                tcr.tcr_reduce_sum_exact_ex(x, acc=acc6, out_f32=out32 if world == 1 else None,
+                                            stream=stream)
             elif world == 1:
                 tcr.tcr_reduce_sum_ex(x, out_f32=out32, algo=algo, stream=stream)
             else:
@@ -422,7 +423,7 @@ def main():
             if args.workload == "c3" and world > 1 and peer is None:
                 if exact:  # integer limbs: the allreduce is exact, result independent of N
                     dist.all_reduce(acc6)
-                    tcr.tcr_exact_finalize(acc6, out_f32=out32, stream=stream)
+                    tcr.tcr_exact_finalize_ex(acc6, dtype_code, out_f32=out32, stream=stream)
                 else:
                     dist.all_reduce(out64)  # the paper's distributed merge, over NVLink
                     tcr.tcr_round_f64_to_f32(out64, out32, stream=stream)
@@ -499,8 +500,6 @@ def main():
         esz = x.element_size()
         host = torch.empty(n * esz, dtype=torch.uint8, pin_memory=True)
         host.copy_(x.view(torch.uint8).reshape(-1))
-        dtype_code = {"f16": tcr.TCR_DTYPE_F16, "bf16": tcr.TCR_DTYPE_BF16,
-                      "e4m3": tcr.TCR_DTYPE_E4M3, "e5m2": tcr.TCR_DTYPE_E5M2}[args.dtype]
         res_t = torch.empty(1, dtype=torch.float32, device=dev)
         hs = torch.cuda.Stream(dev)
         tcr.tcr_reduce_sum_host_ex(host, dtype_code, n=n, stream=hs.cuda_stream)  # warm-up

@@ -221,13 +221,22 @@ tcr_status tcr_reduce_sum_exact(const tcr_half *x, size_t n, int64_t *acc, float
  *   bfloat16 (range 2^-133..2^128): eight 32-exponent windows, each summed
  *   exactly (binary64 fast path for iterations inside one window, integer
  *   slow path otherwise), assembled in a 384-bit integer and rounded once;
- *   acc must be NULL (no limb state for bfloat16; TCR_ERR_INVALID_VALUE).
+ *   acc (if not NULL) holds TCR_EXACT_BF16_ACC_WORDS int64: per window k
+ *   three limbs (I_k = a[3k] + a[3k+1] 2^40 + a[3k+2] 2^80, in units of
+ *   2^-133 for k = 0 and 2^(32k-134) above), then n_nan, n_pinf, n_ninf --
+ *   integer-summable across GPUs like the binary16 limbs.
  * Bitwise equal to the exact oracle of the type.
  */
+#define TCR_EXACT_ACC_WORDS 6
+#define TCR_EXACT_BF16_ACC_WORDS 27
 tcr_status tcr_reduce_sum_exact_ex(const void *x, size_t n, tcr_dtype dtype, int64_t *acc,
                                    float *out_f32, double *out_f64, tcr_stream stream);
 
 /* tcr_exact_finalize -- RNE binary32 / binary64 of an (allreduced) acc[6]. */
+/* tcr_exact_finalize_ex -- the same for an acc of any exact-capable dtype
+ * (6 words for binary16 / fp8, 27 for bfloat16). */
+tcr_status tcr_exact_finalize_ex(const int64_t *acc, tcr_dtype dtype, float *out_f32,
+                                 double *out_f64, tcr_stream stream);
 tcr_status tcr_exact_finalize(const int64_t *acc, float *out_f32, double *out_f64,
                               tcr_stream stream);
 

@@ -66,6 +66,8 @@ TCR_CFG_BULK_STAGE_KB = 15
 TCR_CFG_BULK_CTAS_PER_SM = 16
 TCR_CFG_PEER_TIMEOUT_MS = 17
 
+TCR_EXACT_ACC_WORDS = 6
+TCR_EXACT_BF16_ACC_WORDS = 27
 TCR_MAX_PEERS = 8
 TCR_PEER_MAILBOX_BYTES = 2048
 TCR_IPC_HANDLE_BYTES = 64
@@ -105,6 +107,7 @@ _SIGS = {
     "tcr_round_f64_to_f32": [_P, _P, _P],
     "tcr_reduce_sum_exact": [_P, _SZ, _P, _P, _P, _P],
     "tcr_exact_finalize": [_P, _P, _P, _P],
+    "tcr_exact_finalize_ex": [_P, _I, _P, _P, _P],
     "tcr_reduce_sum_exact_ex": [_P, _SZ, _I, _P, _P, _P, _P],
     "tcr_probe_mma": [_P, _P, _P, _I, _P],
     "tcr_probe_collapse": [_P, _P, _I, _P],
@@ -334,6 +337,26 @@ def tcr_exact_finalize(acc, out_f32=None, out_f64=None, stream=None) -> None:
     """RNE float32 / float64 of an (allreduced) exact accumulator acc[6]."""
     _check(_lib.tcr_exact_finalize(_ptr(acc), _ptr(out_f32), _ptr(out_f64), _stream(stream, acc)),
            "tcr_exact_finalize")
+
+
+def tcr_exact_finalize_ex(acc, dtype, out_f32=None, out_f64=None, stream=None) -> None:
+    """RNE of an (allreduced) exact state of any exact-capable dtype."""
+    _check(_lib.tcr_exact_finalize_ex(_ptr(acc), int(dtype), _ptr(out_f32), _ptr(out_f64),
+                                      _stream(stream, acc)),
+           "tcr_exact_finalize_ex")
+
+
+def exact_bf16_windows_to_value(acc):
+    """Exact rational value of a bfloat16 exact state (27 int64, see tcr.h)."""
+    from fractions import Fraction
+
+    a = [int(v) for v in (acc.tolist() if hasattr(acc, "tolist") else acc)]
+    tot = Fraction(0)
+    for k in range(8):
+        i_k = a[3 * k] + (a[3 * k + 1] << 40) + (a[3 * k + 2] << 80)
+        unit = Fraction(1, 1 << 133) if k == 0 else Fraction(2) ** (32 * k - 134)
+        tot += i_k * unit
+    return tot
 
 
 def exact_limbs_to_int(acc) -> int:

@@ -456,8 +456,6 @@ tcr_status tcr_reduce_sum_exact_ex(const void* x, size_t n, tcr_dtype dtype, int
                                    float* out_f32, double* out_f64, tcr_stream stream) {
     if (dtype < TCR_DTYPE_F16 || dtype > TCR_DTYPE_E5M2)
         return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
-    if (dtype == TCR_DTYPE_BF16 && acc)
-        return fail(TCR_ERR_INVALID_VALUE, "exact bfloat16: no acc[] state (pass acc = NULL)");
     if ((!x && n) || (!acc && !out_f32 && !out_f64))
         return fail(TCR_ERR_INVALID_VALUE, "null pointer");
     if (!aligned(x, dtype <= TCR_DTYPE_BF16 ? 2 : 1) || !aligned(acc, 8) || !aligned(out_f32, 4) ||
@@ -469,7 +467,8 @@ tcr_status tcr_reduce_sum_exact_ex(const void* x, size_t n, tcr_dtype dtype, int
     if (s != TCR_OK) return s;
     const LaunchCfg cfg = make_cfg(di);
     if (dtype == TCR_DTYPE_BF16)
-        return after_launch(tcr::launch_reduce_exact_bf16(static_cast<const uint16_t*>(x), n, out_f32,
+        return after_launch(tcr::launch_reduce_exact_bf16(static_cast<const uint16_t*>(x), n,
+                                                          reinterpret_cast<long long*>(acc), out_f32,
                                                           out_f64, ws->dev, cfg, (cudaStream_t)stream),
                             "exact bf16 kernel launch");
     return after_launch(tcr::launch_reduce_exact((int)dtype, x, n, reinterpret_cast<long long*>(acc),
@@ -486,6 +485,22 @@ tcr_status tcr_exact_finalize(const int64_t* acc, float* out_f32, double* out_f6
     if (s != TCR_OK) return s;
     return after_launch(tcr::launch_exact_finalize(reinterpret_cast<const long long*>(acc),
                                                    out_f32, out_f64, (cudaStream_t)stream),
+                        "exact finalize launch");
+}
+
+tcr_status tcr_exact_finalize_ex(const int64_t* acc, tcr_dtype dtype, float* out_f32,
+                                 double* out_f64, tcr_stream stream) {
+    if (!acc || (!out_f32 && !out_f64)) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
+    if (dtype < TCR_DTYPE_F16 || dtype > TCR_DTYPE_E5M2)
+        return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
+    DeviceInfo di;
+    int dev;
+    tcr_status s = current_device(&dev, &di);
+    if (s != TCR_OK) return s;
+    const long long* a = reinterpret_cast<const long long*>(acc);
+    return after_launch(dtype == TCR_DTYPE_BF16
+                            ? tcr::launch_exact_bf16_finalize(a, out_f32, out_f64, (cudaStream_t)stream)
+                            : tcr::launch_exact_finalize(a, out_f32, out_f64, (cudaStream_t)stream),
                         "exact finalize launch");
 }
 

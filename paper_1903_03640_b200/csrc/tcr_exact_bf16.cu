@@ -131,9 +131,52 @@ __device__ void big_round(const Big384& M, int bits, unsigned long long& mant, i
     exp = shift;
 }
 
+// RNE binary32 / binary64 of T = 2 I_0 + sum_k I_k 2^(32k) (units 2^-134), or
+// the IEEE special value when inf / NaN inputs were counted.
+__device__ void finalize_bf16(const i128 (&win)[8], const long long (&c3)[3], float* out_f32,
+                              double* out_f64) {
+    float f;
+    double d;
+    if (c3[0] || (c3[1] && c3[2])) {
+        f = __int_as_float(0x7FC00000);
+        d = __longlong_as_double(0x7FF8000000000000ll);
+    } else if (c3[1]) {
+        f = __int_as_float(0x7F800000);
+        d = __longlong_as_double(0x7FF0000000000000ll);
+    } else if (c3[2]) {
+        f = __int_as_float(0xFF800000);
+        d = __longlong_as_double((long long)0xFFF0000000000000ull);
+    } else {
+        Big384 B = {{0, 0, 0, 0, 0, 0}};
+        big_add_shifted(B, win[0], 1);  // u_0 = 2 * 2^-134
+        for (int k = 1; k < 8; ++k) big_add_shifted(B, win[k], 32 * k);
+        const bool neg = (long long)B.l[5] < 0;
+        if (neg) {  // magnitude: two's complement negate
+            unsigned long long carry = 1;
+            for (int i = 0; i < 6; ++i) {
+                const unsigned long long v = ~B.l[i] + carry;
+                carry = (carry && v == 0) ? 1ull : 0ull;
+                B.l[i] = v;
+            }
+        }
+        unsigned long long m;
+        int e;
+        big_round(B, 24, m, e);
+        f = ldexpf((float)m, e - 134);  // m <= 2^24 exact; overflow -> inf (IEEE)
+        big_round(B, 53, m, e);
+        d = ldexp((double)m, e - 134);
+        if (neg) {
+            f = -f;
+            d = -d;
+        }
+    }
+    if (out_f32) *out_f32 = f;
+    if (out_f64) *out_f64 = d;
+}
+
 __global__ void __launch_bounds__(kXbWarps * 32, 3)
-reduce_exact_bf16_kernel(const uint16_t* __restrict__ x, size_t n, float* out_f32,
-                         double* out_f64, DevWorkspace ws) {
+reduce_exact_bf16_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc,
+                         float* out_f32, double* out_f64, DevWorkspace ws) {
     __shared__ long long s_I[8][kXbWarps * 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
 #pragma unroll
@@ -308,49 +351,32 @@ reduce_exact_bf16_kernel(const uint16_t* __restrict__ x, size_t n, float* out_f3
         if (lane == 0) *ws.ticket = 0u;
     }
     if (lane != 0) return;
-    float f;
-    double d;
-    if (c3[0] || (c3[1] && c3[2])) {
-        f = __int_as_float(0x7FC00000);
-        d = __longlong_as_double(0x7FF8000000000000ll);
-    } else if (c3[1]) {
-        f = __int_as_float(0x7F800000);
-        d = __longlong_as_double(0x7FF0000000000000ll);
-    } else if (c3[2]) {
-        f = __int_as_float(0xFF800000);
-        d = __longlong_as_double((long long)0xFFF0000000000000ull);
-    } else {
-        Big384 B = {{0, 0, 0, 0, 0, 0}};
-        big_add_shifted(B, win[0], 1);  // u_0 = 2 * 2^-134
-        for (int k = 1; k < 8; ++k) big_add_shifted(B, win[k], 32 * k);
-        const bool neg = (long long)B.l[5] < 0;
-        if (neg) {  // magnitude: two's complement negate
-            unsigned long long carry = 1;
-            for (int i = 0; i < 6; ++i) {
-                const unsigned long long v = ~B.l[i] + carry;
-                carry = (carry && v == 0) ? 1ull : 0ull;
-                B.l[i] = v;
-            }
+    if (out_acc) {  // mergeable state: per window 3 limbs of 40/40/48 bits, then the counts
+        for (int k = 0; k < 8; ++k) {
+            const u128 m = ((u128)1 << 40) - 1;
+            out_acc[3 * k] = (long long)((u128)win[k] & m);
+            out_acc[3 * k + 1] = (long long)(((u128)win[k] >> 40) & m);
+            out_acc[3 * k + 2] = (long long)(win[k] >> 80);
         }
-        unsigned long long m;
-        int e;
-        big_round(B, 24, m, e);
-        f = ldexpf((float)m, e - 134);  // m <= 2^24 exact; overflow -> inf (IEEE)
-        big_round(B, 53, m, e);
-        d = ldexp((double)m, e - 134);
-        if (neg) {
-            f = -f;
-            d = -d;
-        }
+        for (int c = 0; c < 3; ++c) out_acc[24 + c] = c3[c];
     }
-    if (out_f32) *out_f32 = f;
-    if (out_f64) *out_f64 = d;
+    finalize_bf16(win, c3, out_f32, out_f64);
+}
+
+__global__ void exact_bf16_finalize_kernel(const long long* acc, float* out_f32, double* out_f64) {
+    if (threadIdx.x != 0) return;
+    i128 win[8];
+    long long c3[3];
+    for (int k = 0; k < 8; ++k)
+        win[k] = (i128)acc[3 * k] + ((i128)acc[3 * k + 1] << 40) + ((i128)acc[3 * k + 2] << 80);
+    for (int c = 0; c < 3; ++c) c3[c] = acc[24 + c];
+    finalize_bf16(win, c3, out_f32, out_f64);
 }
 
 }  // namespace
 
-cudaError_t launch_reduce_exact_bf16(const uint16_t* x, size_t n, float* out_f32,
-                                     double* out_f64, const DevWorkspace& ws,
+cudaError_t launch_reduce_exact_bf16(const uint16_t* x, size_t n, long long* out_acc,
+                                     float* out_f32, double* out_f64, const DevWorkspace& ws,
                                      const LaunchCfg& cfg, cudaStream_t stream) {
     const size_t tiles = n / kTileElems;
     size_t g = (tiles + (size_t)kXbWarps * kXbU - 1) / ((size_t)kXbWarps * kXbU);
@@ -359,7 +385,14 @@ cudaError_t launch_reduce_exact_bf16(const uint16_t* x, size_t n, float* out_f32
     if (gmax > cap) gmax = cap;
     if (g > gmax) g = gmax;
     if (g < 1) g = 1;
-    reduce_exact_bf16_kernel<<<(unsigned)g, kXbWarps * 32, 0, stream>>>(x, n, out_f32, out_f64, ws);
+    reduce_exact_bf16_kernel<<<(unsigned)g, kXbWarps * 32, 0, stream>>>(x, n, out_acc, out_f32,
+                                                                         out_f64, ws);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_exact_bf16_finalize(const long long* acc, float* out_f32, double* out_f64,
+                                       cudaStream_t stream) {
+    exact_bf16_finalize_kernel<<<1, 32, 0, stream>>>(acc, out_f32, out_f64);
     return cudaGetLastError();
 }
 

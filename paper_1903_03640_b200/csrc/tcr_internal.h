@@ -83,9 +83,12 @@ cudaError_t launch_reduce_exact(int fmt, const void* x, size_t n, long long* out
                                 float* out_f32, double* out_f64, const DevWorkspace& ws,
                                 const LaunchCfg& cfg, cudaStream_t stream);
 // Exact reduction of bfloat16 (tcr_exact_bf16.cu): 8 exponent windows.
-cudaError_t launch_reduce_exact_bf16(const uint16_t* x, size_t n, float* out_f32,
-                                     double* out_f64, const DevWorkspace& ws,
+// out_acc: 27 int64 (8 windows x 3 limbs, 3 special counts), integer-summable.
+cudaError_t launch_reduce_exact_bf16(const uint16_t* x, size_t n, long long* out_acc,
+                                     float* out_f32, double* out_f64, const DevWorkspace& ws,
                                      const LaunchCfg& cfg, cudaStream_t stream);
+cudaError_t launch_exact_bf16_finalize(const long long* acc, float* out_f32, double* out_f64,
+                                       cudaStream_t stream);
 // Exact reduction fused with the cross-GPU combine of the int64 limbs
 // (NEXT-2 x NEXT-3); emulate as for launch_reduce_stream_peer (out_acc: 6
 // words per rank, out_f32 / out_f64: one per rank).

@@ -72,7 +72,7 @@ def sharded_reduce_sum(x_local, out32, partial64, group=None, stream=None, reduc
 
 
 def sharded_reduce_sum_exact(x_local, out32, acc, group=None, stream=None, reducer=None,
-                             finalize=None):
+                             finalize=None, dtype=None):
     """Exact sharded sum (NEXT-3): per-rank tcr_reduce_sum_exact into int64
     acc[6] (integer limbs of the sum in units of 2^-24 plus special-value
     counts), ONE int64 SUM allreduce (exact: limbs stay far below 2^63 for
@@ -85,8 +85,12 @@ def sharded_reduce_sum_exact(x_local, out32, acc, group=None, stream=None, reduc
     if reducer is None or finalize is None:
         import paper_1903_03640_b200 as tcr
 
-        reducer = reducer or (lambda x, a, s: tcr.tcr_reduce_sum_exact(x, acc=a, stream=s))
-        finalize = finalize or (lambda a, o, s: tcr.tcr_exact_finalize(a, out_f32=o, stream=s))
+        # any exact-capable type: acc holds TCR_EXACT_ACC_WORDS (binary16 / fp8)
+        # or TCR_EXACT_BF16_ACC_WORDS (bfloat16) int64
+        code = tcr._dtype_of(x_local, dtype)
+        reducer = reducer or (lambda x, a, s: tcr.tcr_reduce_sum_exact_ex(x, acc=a, stream=s))
+        finalize = finalize or (lambda a, o, s: tcr.tcr_exact_finalize_ex(a, code, out_f32=o,
+                                                                           stream=s))
     ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
     with ctx:
         reducer(x_local, acc, stream)

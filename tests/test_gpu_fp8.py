@@ -194,14 +194,30 @@ def test_fp8_exact_specials(tcr):
             assert g == (math.inf if kind == "+inf" else -math.inf), (fmt, special, g)
 
 
-def test_exact_bf16_has_no_acc_state(tcr):
+def test_exact_bf16_acc_state_is_mergeable(tcr):
+    """The bfloat16 exact state (27 int64: 8 windows x 3 limbs + counts) holds
+    the exact sum, and integer-summing the states of shards then finalizing
+    gives the whole array's correctly rounded sum bitwise (as an int64 SUM
+    allreduce across GPUs would)."""
     import torch
 
-    x = torch.zeros(16, dtype=torch.bfloat16, device="cuda")
-    o = torch.empty(1, dtype=torch.float32, device="cuda")
-    acc = torch.empty(6, dtype=torch.int64, device="cuda")
-    with pytest.raises(tcr.TcrError):  # the limb state is binary16 / fp8 only
-        tcr.tcr_reduce_sum_exact_ex(x, acc=acc, out_f32=o)
-    tcr.tcr_reduce_sum_exact_ex(x, out_f32=o)  # bf16 itself is exact-capable
+    n = 2_000_003
+    bits = gen.generate_bf16(7, 0, n, gen.WIDE)
+    es = oracle.exact_sum_bf16(bits)
+    x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
+    W = tcr.TCR_EXACT_BF16_ACC_WORDS
+    acc = torch.empty(W, dtype=torch.int64, device="cuda")
+    tcr.tcr_reduce_sum_exact_ex(x, acc=acc)
     torch.cuda.synchronize()
-    assert o.item() == 0.0
+    assert tcr.exact_bf16_windows_to_value(acc.cpu()) == es.value
+    P = 3
+    parts = torch.empty(P, W, dtype=torch.int64, device="cuda")
+    for r in range(P):
+        lo, hi = r * n // P, (r + 1) * n // P
+        tcr.tcr_reduce_sum_exact_ex(x[lo:hi], acc=parts[r])
+    tot = parts.sum(dim=0)  # the integer allreduce
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    o64 = torch.empty(1, dtype=torch.float64, device="cuda")
+    tcr.tcr_exact_finalize_ex(tot, tcr.TCR_DTYPE_BF16, out_f32=o32, out_f64=o64)
+    torch.cuda.synchronize()
+    assert float(o32.item()) == es.f32() and float(o64.item()) == es.f64()
