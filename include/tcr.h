@@ -225,6 +225,11 @@ tcr_status tcr_reduce_sum_exact(const tcr_half *x, size_t n, int64_t *acc, float
  *   three limbs (I_k = a[3k] + a[3k+1] 2^40 + a[3k+2] 2^80, in units of
  *   2^-133 for k = 0 and 2^(32k-134) above), then n_nan, n_pinf, n_ninf --
  *   integer-summable across GPUs like the binary16 limbs.
+ * acc length: the ABI takes a bare pointer, so the CALLER must provide at
+ * least TCR_EXACT_ACC_WORDS int64 for binary16 / fp8 and
+ * TCR_EXACT_BF16_ACC_WORDS for bfloat16 (a shorter buffer is overrun; the
+ * Python binding checks the length).  tcr_exact_finalize_ex must be called
+ * with the same dtype as the reduction that wrote acc.
  * Bitwise equal to the exact oracle of the type.
  */
 #define TCR_EXACT_ACC_WORDS 6
@@ -328,6 +333,9 @@ tcr_status tcr_reduce_sum_peer_emulated(const void *x, size_t n, tcr_dtype dtype
  * every rank and for every number of ranks.  Same mailboxes, epochs, stream
  * ordering and timeout behaviour as tcr_reduce_sum_peer (both kinds of
  * combine may be interleaved on one group; each advances its epoch).
+ * binary16 ONLY: x is decoded as binary16 (a bfloat16 or fp8 buffer would be
+ * misread, an fp8 one over-read by 2x); for other types use
+ * tcr_reduce_sum_exact_ex + an int64 allreduce of its state.
  */
 tcr_status tcr_reduce_sum_exact_peer(const tcr_half *x, size_t n, void *const *mailboxes,
                                      int nranks, int rank, int64_t *acc, float *out_f32,

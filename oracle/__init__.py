@@ -14,6 +14,9 @@ Contents
 * :func:`exact_sum_fraction` -- the same definition in pure Python
   ``fractions.Fraction`` arithmetic, for tiny inputs (an independent check of
   the C code).
+* :func:`exact_segment_sums_fp16_array` / ``_fp8_array`` / :func:`exact_segment_sums_bf16`
+  -- the same per segment of a CSR partition, for large segment counts, and
+  :func:`within_tolerance_segments`, the acceptance test over all of them.
 * :func:`within_tolerance` -- the north-star acceptance test
   |g - R| <= 2^-20 * sum|x_i|, evaluated in exact rational arithmetic
   (reading G15).
@@ -80,7 +83,7 @@ def _load():
             ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(_Result)]
         lib.oracle_exact_sum_fp16.restype = ctypes.c_int
         lib.oracle_exact_segment_sums_fp16.argtypes = [
-            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(_Result)]
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
         lib.oracle_exact_segment_sums_fp16.restype = ctypes.c_int
         lib.oracle_exact_bins_bf16.argtypes = [
             ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
@@ -88,6 +91,9 @@ def _load():
         lib.oracle_exact_sum_fp8.argtypes = [
             ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(_Result)]
         lib.oracle_exact_sum_fp8.restype = ctypes.c_int
+        lib.oracle_exact_segment_sums_fp8.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+        lib.oracle_exact_segment_sums_fp8.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -205,10 +211,95 @@ def exact_segment_sums_fp16(x, offsets) -> list[ExactSum]:
     if s and (off[0] < 0 or off[-1] > bits.size):
         raise ValueError("offsets out of range")
     res = (_Result * max(s, 1))()
-    rc = _load().oracle_exact_segment_sums_fp16(bits.ctypes.data, off.ctypes.data, s, res)
+    rc = _load().oracle_exact_segment_sums_fp16(bits.ctypes.data, off.ctypes.data, s,
+                                                ctypes.addressof(res))
     if rc != 0:
         raise ValueError("offsets must be non-decreasing")
     return [_from_struct(res[j]) for j in range(s)]
+
+
+# numpy view of an array of oracle_sum_result records (exact_sum.c)
+_REC_DTYPE = np.dtype([("t_lo", "<u8"), ("t_hi", "<i8"), ("a_lo", "<u8"), ("a_hi", "<u8"),
+                       ("n_nan", "<u8"), ("n_pinf", "<u8"), ("n_ninf", "<u8")])
+
+
+class SegmentSums:
+    """Exact per-segment R(X_j) for many segments, held as the C oracle's
+    records (int128 T and A per segment, in units of 2^unit_exp) rather than
+    one Python object per segment; ``ss[j]`` is the segment's ExactSum."""
+
+    def __init__(self, rec: np.ndarray, unit_exp: int):
+        self.rec = rec
+        self.unit_exp = unit_exp
+
+    def __len__(self) -> int:
+        return self.rec.size
+
+    def __getitem__(self, j: int) -> ExactSum:
+        r = self.rec[j]
+        t = (int(r["t_hi"]) << 64) | int(r["t_lo"])
+        a = (int(r["a_hi"]) << 64) | int(r["a_lo"])
+        return ExactSum(t, a, int(r["n_nan"]), int(r["n_pinf"]), int(r["n_ninf"]), self.unit_exp)
+
+
+def _segment_records(fn, bits, off, threads, *extra) -> np.ndarray:
+    """Call the C per-segment loop ``fn`` over contiguous ranges of segments
+    (one range per thread; the records do not depend on the split)."""
+    s = off.size - 1
+    rec = np.zeros(max(s, 1), dtype=_REC_DTYPE)
+    threads = max(1, min(int(threads), max(1, s)))
+    bounds = [s * k // threads for k in range(threads + 1)]
+
+    def run(k: int) -> int:
+        j0, j1 = bounds[k], bounds[k + 1]
+        return fn(bits.ctypes.data, off.ctypes.data + 8 * j0, j1 - j0, *extra,
+                  rec.ctypes.data + rec.itemsize * j0)
+
+    if threads == 1:
+        rcs = [run(0)]
+    else:
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            rcs = list(ex.map(run, range(threads)))
+    if any(rcs):
+        raise ValueError("offsets must be non-decreasing")
+    return rec[:s]
+
+
+def _check_offsets(off: np.ndarray, size: int) -> None:
+    if off.size < 1:
+        raise ValueError("offsets must hold num_segments + 1 entries")
+    if off.size > 1 and (off[0] < 0 or off[-1] > size):
+        raise ValueError("offsets out of range")
+
+
+def exact_segment_sums_fp16_array(x, offsets, threads: int = 1) -> SegmentSums:
+    """Exact per-segment R for CSR ``offsets`` of binary16 inputs, as records
+    (same C loop as :func:`exact_segment_sums_fp16`), for large S."""
+    bits = _as_bits(x)
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    _check_offsets(off, bits.size)
+    return SegmentSums(_segment_records(_load().oracle_exact_segment_sums_fp16, bits, off, threads),
+                       -24)
+
+
+def exact_segment_sums_fp8_array(x, offsets, fmt: int, threads: int = 1) -> SegmentSums:
+    """Exact per-segment R of fp8 bit patterns (uint8) for CSR ``offsets``."""
+    bits = np.ascontiguousarray(np.asarray(x, dtype=np.uint8).reshape(-1))
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    _check_offsets(off, bits.size)
+    rec = _segment_records(_load().oracle_exact_segment_sums_fp8, bits, off, threads, int(fmt))
+    return SegmentSums(rec, _FP8_UNIT_EXP[fmt])
+
+
+def exact_segment_sums_bf16(x, offsets) -> list[ExactSum]:
+    """Exact per-segment R of bfloat16 bit patterns: :func:`exact_sum_bf16`
+    applied to each segment x[off[j]:off[j+1]]."""
+    bits = np.ascontiguousarray(np.asarray(x, dtype=np.uint16).reshape(-1))
+    off = np.asarray(offsets, dtype=np.int64)
+    _check_offsets(off, bits.size)
+    if np.any(np.diff(off) < 0):
+        raise ValueError("offsets must be non-decreasing")
+    return [exact_sum_bf16(bits[int(off[j]):int(off[j + 1])]) for j in range(off.size - 1)]
 
 
 def exact_sum_bf16(x) -> ExactSum:
@@ -224,8 +315,10 @@ def exact_sum_bf16(x) -> ExactSum:
     counts = np.zeros(3, dtype=np.uint64)
     _load().oracle_exact_bins_bf16(bits.ctypes.data, bits.size, bins.ctypes.data,
                                    abins.ctypes.data, counts.ctypes.data)
-    T = sum(int(bins[e]) << max(e - 1, 0) for e in range(256))
-    A = sum(int(abins[e]) << max(e - 1, 0) for e in range(256))
+    # bins with no inputs contribute nothing: only the occupied exponents are visited
+    used = np.nonzero(abins)[0].tolist()
+    T = sum(int(bins[e]) << max(e - 1, 0) for e in used)
+    A = sum(int(abins[e]) << max(e - 1, 0) for e in used)
     return ExactSum(T, A, int(counts[0]), int(counts[1]), int(counts[2]), unit_exp=-133)
 
 
@@ -328,8 +421,42 @@ def within_tolerance(g: float, es: ExactSum, rel: Fraction = Fraction(1, 1 << 20
     return abs(Fraction(float(g)) - es.value) <= rel * es.abs_value
 
 
+def within_tolerance_segments(g, ss: SegmentSums, rel_log2: int = 20) -> np.ndarray:
+    """:func:`within_tolerance` for every segment: ok[j] iff
+    |g[j] - R_j| <= 2^-rel_log2 * sum|x| over segment j.
+
+    Where T_j, A_j and G_j = g[j] / unit are integers below 2^62 (always, for
+    the configs' fp16 / fp8 segments) the test is the same exact integer
+    comparison |G - T| * 2^rel <= A, written as |G - T| <= floor(A / 2^rel)
+    (equivalent for integer |G - T|) and evaluated on int64 arrays; every
+    other segment (specials, g not a multiple of the unit, larger values)
+    goes through the scalar rational :func:`within_tolerance`.
+    """
+    g = np.asarray(g, dtype=np.float64).reshape(-1)
+    rec = ss.rec
+    if g.size != rec.size:
+        raise ValueError("one result per segment expected")
+    lim = np.uint64(1 << 62)
+    t_lo_s = rec["t_lo"].view(np.int64)
+    fits = ((rec["t_hi"] == (t_lo_s >> 63)) & (np.abs(t_lo_s) < (1 << 62))
+            & (rec["a_hi"] == 0) & (rec["a_lo"] < lim)
+            & (rec["n_nan"] == 0) & (rec["n_pinf"] == 0) & (rec["n_ninf"] == 0))
+    with np.errstate(invalid="ignore", over="ignore"):
+        G = np.ldexp(g, -ss.unit_exp)  # exact: scaling by a power of two
+        fits &= np.isfinite(G) & (np.abs(G) < 2.0 ** 62) & (G == np.floor(G))
+    ok = np.zeros(g.size, dtype=bool)
+    idx = np.nonzero(fits)[0]
+    Gi = G[idx].astype(np.int64)
+    diff = np.abs(Gi - t_lo_s[idx])
+    ok[idx] = diff <= (rec["a_lo"][idx] >> np.uint64(rel_log2)).astype(np.int64)
+    for j in np.nonzero(~fits)[0].tolist():
+        ok[j] = within_tolerance(float(g[j]), ss[j], Fraction(1, 1 << rel_log2))
+    return ok
+
+
 def error_units(g: float, es: ExactSum) -> Fraction:
-    """|g - R(X)| in units of 2^-24 (exact)."""
+    """|g - R(X)| in units of 2^-24 (exact, for every input type: the unit is
+    fixed at 2^-24, not the type's own quantum)."""
     return abs(Fraction(float(g)) - es.value) / UNIT
 
 
@@ -337,4 +464,6 @@ __all__ = [
     "ExactSum", "UNIT", "build", "exact_sum_fp16", "exact_segment_sums_fp16", "exact_sum_bf16",
     "bf16_value", "exact_sum_fp8", "fp8_value", "FP8_E4M3", "FP8_E5M2",
     "exact_sum_fraction", "round_to_f32", "within_tolerance", "error_units",
+    "SegmentSums", "exact_segment_sums_fp16_array", "exact_segment_sums_fp8_array",
+    "exact_segment_sums_bf16", "within_tolerance_segments",
 ]

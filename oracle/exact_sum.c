@@ -28,7 +28,8 @@
  * It also returns A = sum |x_i| * 2^24 exactly (the tolerance scale of the
  * north star: |gpu - R| <= 2^-20 * sum |x_i|).
  *
- * Build: gcc -O2 -shared -fPIC -o liboracle.so exact_sum.c  (see oracle/Makefile)
+ * Build: gcc -O2 -std=c11 -shared -fPIC -o liboracle.so exact_sum.c
+ * (done by oracle.build(), called from __graft_entry__.build()).
  */
 #include <stddef.h>
 #include <stdint.h>
@@ -186,5 +187,19 @@ int oracle_exact_sum_fp8(const uint8_t *x, size_t n, int fmt, oracle_sum_result 
     r->n_nan = n_nan;
     r->n_pinf = n_pinf;
     r->n_ninf = n_ninf;
+    return 0;
+}
+
+/*
+ * Exact per-segment sums of fp8 inputs (CSR, as oracle_exact_segment_sums_fp16):
+ * one oracle_exact_sum_fp8 record per segment.  Returns 0, or -1 if the
+ * offsets are decreasing.
+ */
+int oracle_exact_segment_sums_fp8(const uint8_t *x, const int64_t *offsets, size_t num_segments,
+                                  int fmt, oracle_sum_result *r) {
+    for (size_t j = 0; j < num_segments; ++j) {
+        if (offsets[j + 1] < offsets[j]) return -1;
+        oracle_exact_sum_fp8(x + offsets[j], (size_t)(offsets[j + 1] - offsets[j]), fmt, &r[j]);
+    }
     return 0;
 }

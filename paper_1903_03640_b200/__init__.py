@@ -222,6 +222,28 @@ def _dtype_of(x, dtype):
     return TCR_DTYPE_F16
 
 
+def _check_acc(acc, code: int, fn: str, ranks: int = 1) -> None:
+    """An exact state must be an int64 device tensor of at least the type's
+    word count (the C ABI takes a bare pointer and cannot check its length)."""
+    if acc is None or isinstance(acc, int):
+        return
+    import torch
+
+    words = (TCR_EXACT_BF16_ACC_WORDS if code == TCR_DTYPE_BF16 else TCR_EXACT_ACC_WORDS) * ranks
+    if acc.dtype != torch.int64 or not acc.is_cuda or acc.numel() < words or not acc.is_contiguous():
+        raise ValueError(f"{fn}: acc must be a contiguous int64 CUDA tensor of >= {words} words "
+                         f"for this dtype (got {acc.dtype}, {acc.numel()} words, {acc.device})")
+
+
+def _require_binary16(x, fn: str) -> None:
+    """Entry points that take binary16 only (the fused exact peer combine)."""
+    import torch
+
+    dt = getattr(x, "dtype", None)
+    if dt is not None and dt not in (torch.float16, torch.int16):
+        raise ValueError(f"{fn} takes binary16 input (torch.float16), got {dt}")
+
+
 def tcr_reduce_sum_ex(x, out_f32=None, out_f64=None, algo=TCR_ALGO_DEFAULT, dtype=None, n=None,
                       stream=None) -> None:
     """Sum of binary16 or bfloat16 x (dtype from the tensor unless given)."""
@@ -319,50 +341,41 @@ def tcr_reduce_sum_host_ex(x, dtype, n=None, stream=None) -> float:
 
 
 def tcr_reduce_sum_exact(x, acc=None, out_f32=None, out_f64=None, n=None, stream=None) -> None:
-    """Exact sum: acc (int64[6] device: limbs l0,l1,l2 of T*2^24 in base 2^40,
-    NaN/+inf/-inf counts) and/or the correctly rounded float32 / float64."""
+    """Exact sum of binary16 x: acc (int64[6] device: limbs l0,l1,l2 of the sum
+    in units of 2^-24, base 2^40, then NaN/+inf/-inf counts) and/or the
+    correctly rounded float32 / float64."""
+    _require_binary16(x, "tcr_reduce_sum_exact")
+    _check_acc(acc, TCR_DTYPE_F16, "tcr_reduce_sum_exact")
     _check(_lib.tcr_reduce_sum_exact(_ptr(x), _numel(x, n), _ptr(acc), _ptr(out_f32),
                                      _ptr(out_f64), _stream(stream, x)), "tcr_reduce_sum_exact")
 
 
 def tcr_reduce_sum_exact_ex(x, acc=None, out_f32=None, out_f64=None, dtype=None, n=None,
                             stream=None) -> None:
-    """Bitwise-exact sum of binary16, bfloat16 (no acc) or fp8 (E4M3 / E5M2) x."""
-    _check(_lib.tcr_reduce_sum_exact_ex(_ptr(x), _numel(x, n), _dtype_of(x, dtype), _ptr(acc),
+    """Bitwise-exact sum of binary16, bfloat16 or fp8 (E4M3 / E5M2) x.  acc, if
+    given, receives the mergeable exact state: TCR_EXACT_ACC_WORDS (6) int64
+    for binary16 / fp8, TCR_EXACT_BF16_ACC_WORDS (27) for bfloat16 (tcr.h)."""
+    code = _dtype_of(x, dtype)
+    _check_acc(acc, code, "tcr_reduce_sum_exact_ex")
+    _check(_lib.tcr_reduce_sum_exact_ex(_ptr(x), _numel(x, n), code, _ptr(acc),
                                         _ptr(out_f32), _ptr(out_f64), _stream(stream, x)),
            "tcr_reduce_sum_exact_ex")
 
 
 def tcr_exact_finalize(acc, out_f32=None, out_f64=None, stream=None) -> None:
-    """RNE float32 / float64 of an (allreduced) exact accumulator acc[6]."""
+    """RNE float32 / float64 of an (allreduced) binary16 exact state acc[6]."""
+    _check_acc(acc, TCR_DTYPE_F16, "tcr_exact_finalize")
     _check(_lib.tcr_exact_finalize(_ptr(acc), _ptr(out_f32), _ptr(out_f64), _stream(stream, acc)),
            "tcr_exact_finalize")
 
 
 def tcr_exact_finalize_ex(acc, dtype, out_f32=None, out_f64=None, stream=None) -> None:
-    """RNE of an (allreduced) exact state of any exact-capable dtype."""
+    """RNE of an (allreduced) exact state of any exact-capable dtype (6 int64
+    words for binary16 / fp8, 27 for bfloat16)."""
+    _check_acc(acc, int(dtype), "tcr_exact_finalize_ex")
     _check(_lib.tcr_exact_finalize_ex(_ptr(acc), int(dtype), _ptr(out_f32), _ptr(out_f64),
                                       _stream(stream, acc)),
            "tcr_exact_finalize_ex")
-
-
-def exact_bf16_windows_to_value(acc):
-    """Exact rational value of a bfloat16 exact state (27 int64, see tcr.h)."""
-    from fractions import Fraction
-
-    a = [int(v) for v in (acc.tolist() if hasattr(acc, "tolist") else acc)]
-    tot = Fraction(0)
-    for k in range(8):
-        i_k = a[3 * k] + (a[3 * k + 1] << 40) + (a[3 * k + 2] << 80)
-        unit = Fraction(1, 1 << 133) if k == 0 else Fraction(2) ** (32 * k - 134)
-        tot += i_k * unit
-    return tot
-
-
-def exact_limbs_to_int(acc) -> int:
-    """Python int T (units of 2^-24) from the limbs of acc[6] (host-side decode)."""
-    a = [int(v) for v in acc]
-    return a[0] + (a[1] << 40) + (a[2] << 80)
 
 
 def tcr_round_f64_to_f32(inp, out, stream=None) -> None:
@@ -451,7 +464,10 @@ def tcr_reduce_sum_peer_emulated(x, mailboxes, out_f32=None, out_f64=None,
 
 def tcr_reduce_sum_exact_peer(x, mailboxes, rank, acc=None, out_f32=None, out_f64=None, n=None,
                               stream=None) -> None:
-    """Exact sum of this rank's shard fused with the group's limb combine."""
+    """Exact sum of this rank's binary16 shard fused with the group's limb
+    combine (binary16 only: other types raise)."""
+    _require_binary16(x, "tcr_reduce_sum_exact_peer")
+    _check_acc(acc, TCR_DTYPE_F16, "tcr_reduce_sum_exact_peer")
     _check(_lib.tcr_reduce_sum_exact_peer(_ptr(x), _numel(x, n), _mailbox_array(mailboxes),
                                           len(mailboxes), int(rank), _ptr(acc), _ptr(out_f32),
                                           _ptr(out_f64), _stream(stream, x)),
@@ -460,7 +476,10 @@ def tcr_reduce_sum_exact_peer(x, mailboxes, rank, acc=None, out_f32=None, out_f6
 
 def tcr_reduce_sum_exact_peer_emulated(x, mailboxes, acc=None, out_f32=None, out_f64=None, n=None,
                                        stream=None) -> None:
-    """All len(mailboxes) ranks of the exact fused combine in one cooperative launch."""
+    """All len(mailboxes) ranks of the exact fused combine in one cooperative
+    launch (binary16 only; acc, if given, holds 6 int64 words per rank)."""
+    _require_binary16(x, "tcr_reduce_sum_exact_peer_emulated")
+    _check_acc(acc, TCR_DTYPE_F16, "tcr_reduce_sum_exact_peer_emulated", ranks=len(mailboxes))
     _check(_lib.tcr_reduce_sum_exact_peer_emulated(_ptr(x), _numel(x, n),
                                                    _mailbox_array(mailboxes), len(mailboxes),
                                                    _ptr(acc), _ptr(out_f32), _ptr(out_f64),
@@ -550,4 +569,4 @@ def reduce_sum_segmented(x, offsets, mma: bool = True, stream=None):
 
 
 __all__ = [n for n in dir() if n.startswith("tcr_") or n.startswith("TCR_")] + [
-    "reduce_sum", "reduce_sum_segmented", "exact_limbs_to_int", "TcrError", "LIB_PATH", "ALGOS"]
+    "reduce_sum", "reduce_sum_segmented", "TcrError", "LIB_PATH", "ALGOS"]

@@ -32,7 +32,7 @@ thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
 
 struct Config {
-    // Defaults = the measured best on B200 at n = 2^30 (profiles/r01/tuning.md).
+    // Defaults = the measured best on B200 at n = 2^30 (profiles/r01/retune_final.txt, profiles/r01/sweep_r01a.jsonl).
     int default_algo = TCR_ALGO_MMA_SYNC;
     int blocks_per_sm = 8;
     int unroll = 0;       // 0 = auto: 16 below 2^26 elements, 4 above
@@ -68,6 +68,10 @@ struct Workspace {
     size_t chunk_cap = 0;
     void* staging[2] = {nullptr, nullptr};
     size_t staging_bytes = 0;
+    cudaStream_t copy_stream = nullptr;  // host entry: H2D copies, overlapping the kernels
+    cudaEvent_t copied[2] = {nullptr, nullptr};  // staging[b] filled (copy stream)
+    cudaEvent_t consumed[2] = {nullptr, nullptr};  // staging[b] read by its kernel (stream)
+    cudaEvent_t entry = nullptr;  // the caller's stream position at entry
     float* dev_out = nullptr;
     void* paper_scratch = nullptr;  // study mode: binary16 partials of every level
     size_t paper_scratch_bytes = 0;
@@ -360,7 +364,11 @@ tcr_status tcr_reduce_sum_batched_shuffle(const tcr_half* x, size_t num_segments
 }
 
 // End-to-end host entry for any input type: chunks of 128 MiB of input bytes
-// through two staging buffers (H2D of chunk c+1 overlaps the kernel of c).
+// through two staging buffers.  The H2D copies run on the workspace's copy
+// stream and the kernels on the caller's stream; events order each buffer's
+// reuse (copy c+2 waits for kernel c), so the H2D of chunk c+1 overlaps the
+// kernel of chunk c (with pinned host memory; pageable memory serialises in
+// the driver).  Kernels use the library's default algorithm for the type.
 static tcr_status reduce_host_impl(const void* x, size_t n, int fmt, float* out,
                                    cudaStream_t stream) {
     const size_t es = fmt >= TCR_DTYPE_E4M3 ? 1 : 2;
@@ -396,23 +404,60 @@ static tcr_status reduce_host_impl(const void* x, size_t n, int fmt, float* out,
                 if ((e = cudaMalloc(&b, need))) return cuda_fail(e, "cudaMalloc(staging)");
             ws->staging_bytes = need;
         }
+        if (!ws->copy_stream) {
+            if ((e = cudaStreamCreateWithFlags(&ws->copy_stream, cudaStreamNonBlocking)))
+                return cuda_fail(e, "cudaStreamCreate(copy)");
+            for (int b = 0; b < 2; ++b)
+                if ((e = cudaEventCreateWithFlags(&ws->copied[b], cudaEventDisableTiming)) ||
+                    (e = cudaEventCreateWithFlags(&ws->consumed[b], cudaEventDisableTiming)))
+                    return cuda_fail(e, "cudaEventCreate");
+            if ((e = cudaEventCreateWithFlags(&ws->entry, cudaEventDisableTiming)))
+                return cuda_fail(e, "cudaEventCreate");
+        }
     }
-    // the default algorithm of the type (tcgen05 for large fp8 chunks)
-    const bool tc05 = fmt >= TCR_DTYPE_E4M3 && kChunk >= ((size_t)1 << 26);
+    int algo;
+    {
+        std::lock_guard<std::mutex> lk(g_cfg_mu);
+        algo = g_cfg.default_algo;
+    }
     int launches = 0;
     const char* xb = static_cast<const char*>(x);
+    // the copy stream starts after the caller's earlier work (staging reuse
+    // across calls, and the caller's ordering of x)
+    if ((e = cudaEventRecord(ws->entry, stream)) ||
+        (e = cudaStreamWaitEvent(ws->copy_stream, ws->entry, 0)))
+        return cuda_fail(e, "event ordering");
     for (size_t c = 0; c < chunks; ++c) {
         const size_t lo = c * kChunk, cnt = (n - lo < kChunk) ? n - lo : kChunk;
-        void* buf = ws->staging[c & 1];
-        if ((e = cudaMemcpyAsync(buf, xb + lo * es, cnt * es, cudaMemcpyHostToDevice, stream)))
+        const int b = (int)(c & 1);
+        void* buf = ws->staging[b];
+        if (c >= 2 && (e = cudaStreamWaitEvent(ws->copy_stream, ws->consumed[b], 0)))
+            return cuda_fail(e, "cudaStreamWaitEvent(consumed)");
+        if ((e = cudaMemcpyAsync(buf, xb + lo * es, cnt * es, cudaMemcpyHostToDevice,
+                                 ws->copy_stream)))
             return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+        if ((e = cudaEventRecord(ws->copied[b], ws->copy_stream)) ||
+            (e = cudaStreamWaitEvent(stream, ws->copied[b], 0)))
+            return cuda_fail(e, "event ordering (copied)");
         const uint16_t* db = static_cast<const uint16_t*>(buf);
-        e = (tc05 && cnt >= ((size_t)1 << 26))
-                ? tcr::launch_reduce_tcgen05(fmt, db, cnt, nullptr, ws->chunk_partials + c, ws->dev,
-                                             cfg, stream)
-                : tcr::launch_reduce_stream(true, fmt, db, cnt, nullptr, ws->chunk_partials + c,
-                                            ws->dev, cfg, stream);
+        // the type's default algorithm (reduce_impl's rule): fp8 takes
+        // tcgen05 kind::f8f6f4 from 2^26 elements, mma.sync below; binary16
+        // / bfloat16 take TCR_CFG_DEFAULT_ALGO
+        const int a = fmt >= TCR_DTYPE_E4M3
+                          ? (cnt >= ((size_t)1 << 26) ? TCR_ALGO_TCGEN05 : TCR_ALGO_MMA_SYNC)
+                          : algo;
+        if (a == TCR_ALGO_TCGEN05)
+            e = tcr::launch_reduce_tcgen05(fmt, db, cnt, nullptr, ws->chunk_partials + c, ws->dev,
+                                           cfg, stream);
+        else if (a == TCR_ALGO_BULK_MMA)
+            e = tcr::launch_reduce_bulk(fmt, db, cnt, nullptr, ws->chunk_partials + c, ws->dev, cfg,
+                                        stream);
+        else
+            e = tcr::launch_reduce_stream(a == TCR_ALGO_MMA_SYNC, fmt, db, cnt, nullptr,
+                                          ws->chunk_partials + c, ws->dev, cfg, stream);
         if (e) return cuda_fail(e, "reduce kernel launch");
+        if ((e = cudaEventRecord(ws->consumed[b], stream)))
+            return cuda_fail(e, "cudaEventRecord(consumed)");
         ++launches;
     }
     if ((e = tcr::launch_sum_partials(ws->chunk_partials, chunks, ws->dev_out, nullptr, stream)))
@@ -805,6 +850,14 @@ tcr_status tcr_release_workspaces(void) {
         if (ws->chunk_partials) cudaFree(ws->chunk_partials);
         for (void* b : ws->staging)
             if (b) cudaFree(b);
+        if (ws->copy_stream) {
+            for (int b = 0; b < 2; ++b) {
+                cudaEventDestroy(ws->copied[b]);
+                cudaEventDestroy(ws->consumed[b]);
+            }
+            cudaEventDestroy(ws->entry);
+            cudaStreamDestroy(ws->copy_stream);
+        }
         if (ws->dev_out) cudaFree(ws->dev_out);
         if (ws->paper_scratch) cudaFree(ws->paper_scratch);
         cudaSetDevice(prev);

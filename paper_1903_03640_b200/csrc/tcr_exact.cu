@@ -451,7 +451,7 @@ cudaError_t launch_reduce_exact(int fmt, const void* x, size_t n, long long* out
         case kE4M3: return launch_exact_f<kE4M3>(xb, n, out_acc, out_f32, out_f64, ws, cfg, stream);
         case kE5M2: return launch_exact_f<kE5M2>(xb, n, out_acc, out_f32, out_f64, ws, cfg, stream);
         case kF16: return launch_exact_f<kF16>(xb, n, out_acc, out_f32, out_f64, ws, cfg, stream);
-        default: return cudaErrorInvalidValue;  // bfloat16: not exact-capable
+        default: return cudaErrorInvalidValue;  // bfloat16 has its own kernel (tcr_exact_bf16.cu)
     }
 }
 

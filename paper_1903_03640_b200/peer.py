@@ -73,7 +73,9 @@ class PeerGroup:
 
     def reduce_sum_exact(self, x_local, out_f32=None, out_f64=None, acc=None, stream=None):
         """Bitwise-exact group total (NEXT-3 limbs combined in the kernel):
-        identical on every rank and for every number of ranks."""
+        identical on every rank and for every number of ranks.  binary16 only
+        (the fused exact combine kernel decodes binary16; other types raise)."""
+        self._lib._require_binary16(x_local, "PeerGroup.reduce_sum_exact")
         self.calls += 1
         self._lib.tcr_reduce_sum_exact_peer(x_local, self.mailboxes, self.rank, acc=acc,
                                             out_f32=out_f32, out_f64=out_f64, stream=stream)

@@ -73,11 +73,13 @@ def sharded_reduce_sum(x_local, out32, partial64, group=None, stream=None, reduc
 
 def sharded_reduce_sum_exact(x_local, out32, acc, group=None, stream=None, reducer=None,
                              finalize=None, dtype=None):
-    """Exact sharded sum (NEXT-3): per-rank tcr_reduce_sum_exact into int64
-    acc[6] (integer limbs of the sum in units of 2^-24 plus special-value
-    counts), ONE int64 SUM allreduce (exact: limbs stay far below 2^63 for
-    any realistic rank count), tcr_exact_finalize.  The result is bitwise
-    identical for every number of GPUs.
+    """Exact sharded sum (NEXT-3): per-rank tcr_reduce_sum_exact_ex into the
+    int64 exact state ``acc`` -- TCR_EXACT_ACC_WORDS (6: integer limbs of the
+    sum in the type's unit plus special-value counts) for binary16 / fp8,
+    TCR_EXACT_BF16_ACC_WORDS (27: eight exponent windows of three limbs, plus
+    counts) for bfloat16 -- ONE int64 SUM allreduce (exact: limbs stay far
+    below 2^63 for any realistic rank count), tcr_exact_finalize_ex.  The
+    result is bitwise identical for every number of GPUs.
     """
     import torch
     import torch.distributed as dist
@@ -88,7 +90,9 @@ def sharded_reduce_sum_exact(x_local, out32, acc, group=None, stream=None, reduc
         # any exact-capable type: acc holds TCR_EXACT_ACC_WORDS (binary16 / fp8)
         # or TCR_EXACT_BF16_ACC_WORDS (bfloat16) int64
         code = tcr._dtype_of(x_local, dtype)
-        reducer = reducer or (lambda x, a, s: tcr.tcr_reduce_sum_exact_ex(x, acc=a, stream=s))
+        tcr._check_acc(acc, code, "sharded_reduce_sum_exact")
+        reducer = reducer or (lambda x, a, s: tcr.tcr_reduce_sum_exact_ex(x, acc=a, dtype=code,
+                                                                           stream=s))
         finalize = finalize or (lambda a, o, s: tcr.tcr_exact_finalize_ex(a, code, out_f32=o,
                                                                            stream=s))
     ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()

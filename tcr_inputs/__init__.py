@@ -5,7 +5,8 @@ Each value depends only on (seed, global index i), through the splitmix64
 counter-based hash, so any shard or sample of a workload can be regenerated
 anywhere (DESIGN.md §"Input recipe").  Two implementations of the same
 definition exist: numpy here (host) and ``gen.cu`` (device, built into
-``libtcr_inputs.so``); ``tests/test_inputs.py`` checks them bit for bit.
+``libtcr_inputs.so``); the device-generator tests in ``tests/test_gpu_segmented.py``,
+``tests/test_gpu_fp8.py`` and ``tests/test_gpu_bf16.py`` check them bit for bit.
 
 Distributions (``dist``):
 
@@ -227,6 +228,22 @@ def loguniform_lengths(seed: int, num_segments: int, lo: int = 256, hi: int = 65
     ll = np.log2(float(lo)) + u * (np.log2(float(hi + 1)) - np.log2(float(lo)))
     L = np.floor(np.exp2(ll)).astype(np.int64)
     return np.clip(L, lo, hi)
+
+
+def mixed_lengths(seed: int, num_segments: int, hi: int = 20000) -> np.ndarray:
+    """Segment lengths mixing every case a segmented kernel distinguishes
+    (DESIGN.md §"Input recipe"): class c = z mod 8 of splitmix64(seed ^ 0x3A1, j):
+    c in {0, 1} -> 0 (empty); c in {2, 3} -> 1..7 (inside one 16-byte vector);
+    c == 4 -> 8..600 (tile-crossing); c in {5, 6, 7} -> log-uniform in [600, hi].
+    Host-only, like loguniform_lengths."""
+    z = splitmix64(seed ^ 0x3A1, np.arange(num_segments, dtype=np.uint64))
+    c = (z % np.uint64(8)).astype(np.int64)
+    r = (z >> np.uint64(8)).astype(np.int64)  # 56 further bits
+    u = (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    longl = np.clip(np.floor(np.exp2(np.log2(600.0) + u * (np.log2(hi + 1.0) - np.log2(600.0)))),
+                    600, hi).astype(np.int64)
+    L = np.where(c < 2, 0, np.where(c < 4, 1 + r % 7, np.where(c == 4, 8 + r % 593, longl)))
+    return L.astype(np.int64)
 
 
 def offsets_from_lengths(lengths: np.ndarray, start: int = 0) -> np.ndarray:

@@ -41,11 +41,37 @@ def test_bench_two_ranks_shared_gpu(algo):
 
 
 @pytest.mark.gpu
+def test_bench_c4_strong_two_ranks_shared_gpu():
+    """C4 as BASELINE.json defines it: a fixed global n = 2^33 cut over the
+    ranks (strong scaling), the timed result checked against the exact
+    oracle of the whole array (per-rank shard oracles, exact limb
+    allreduce), a cpu_baseline for the whole job, and T_1 (rank 0 reducing
+    all 2^33 elements alone)."""
+    env = dict(os.environ, TCR_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--e2e-steps", "1"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["config"]["n_total"] == 1 << 33 and d["config"]["n_per_rank"] == 1 << 32
+    assert d["config"]["workload"].startswith("c4")
+    ck = d["check"]
+    assert ck["within_2^-20_sum_abs"] is True and ck["exact_f64"] != 0.0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["value"] > 0 and cb["cores"] >= 2
+    assert d["t1"]["n"] == 1 << 33 and d["t1"]["ms_per_step"] > 0
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("extra", [[], ["--impl", "reference"], ["--workload", "c5"]])
 def test_bench_json_contract_single_gpu(extra):
     """bench.py at N = 1: one JSON line carrying every key of the contract."""
     cmd = [sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--e2e-steps", "1",
-           "--n-per-rank", str(1 << 24), "--cpu-seconds", "1"] + extra
+           "--n-total", str(1 << 24), "--cpu-seconds", "1"] + extra
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
@@ -60,7 +86,9 @@ def test_bench_json_contract_single_gpu(extra):
     assert "workload" in d["config"]
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    assert cb["cpu_model"] and cb["host_ram_gib"] > 0
     if extra[:2] == ["--impl", "reference"]:
+        assert d["config"]["n_total"] == 1 << 24  # the same workload as our arm's line
         assert d["impl"] == "reference"
         assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
         return
@@ -72,6 +100,7 @@ def test_bench_json_contract_single_gpu(extra):
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(ck)
     if "c5" not in extra:
         assert d["check"]["within_2^-20_sum_abs"] is True  # the timed result vs the oracle
+        assert cb["one_thread"]["value"] > 0 and cb["d2h_ms"] > 0
         e = d["e2e"]
         assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 << 24 and e["d2h_bytes_per_step"] == 4
 

@@ -8,6 +8,7 @@ import pytest
 
 import oracle
 import tcr_inputs as gen
+from exact_state_decode import exact_limbs_to_int
 
 pytestmark = pytest.mark.gpu
 
@@ -45,7 +46,7 @@ def _exact(tcr, x):
 
 
 def _check(tcr, a, g32, g64, es):
-    assert tcr.exact_limbs_to_int(a) == es.T
+    assert exact_limbs_to_int(a) == es.T
     assert 0 <= a[0] < (1 << 40) and 0 <= a[1] < (1 << 40)
     assert (a[3], a[4], a[5]) == (es.n_nan, es.n_pinf, es.n_ninf)
     r32, r64 = es.f32(), es.f64()
@@ -124,5 +125,5 @@ def test_exact_sharded_is_independent_of_P(tcr, P):
     tcr.tcr_exact_finalize(tot, out_f32=o32, out_f64=o64)
     torch.cuda.synchronize()
     t = tot.cpu().tolist()
-    assert tcr.exact_limbs_to_int(t) == es.T
+    assert exact_limbs_to_int(t) == es.T
     assert float(o32.item()) == es.f32() and float(o64.item()) == es.f64()

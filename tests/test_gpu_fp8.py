@@ -6,6 +6,7 @@ import pytest
 
 import oracle
 import tcr_inputs as gen
+from exact_state_decode import exact_limbs_to_int, exact_bf16_windows_to_value
 
 pytestmark = pytest.mark.gpu
 ALGOS = ["mma_sync", "tcgen05", "shuffle", "bulk"]
@@ -170,7 +171,7 @@ def test_fp8_exact_bitwise(tcr, fmt):
                 torch.cuda.synchronize()
                 assert float(o32.item()) == es.f32(), (n, dist, off, o32.item(), es.f64())
                 assert float(o64.item()) == es.f64(), (n, dist, off)
-                T = tcr.exact_limbs_to_int(acc)
+                T = exact_limbs_to_int(acc)
                 assert T * oracle.UNIT == es.value, (n, dist, off)
 
 
@@ -209,7 +210,7 @@ def test_exact_bf16_acc_state_is_mergeable(tcr):
     acc = torch.empty(W, dtype=torch.int64, device="cuda")
     tcr.tcr_reduce_sum_exact_ex(x, acc=acc)
     torch.cuda.synchronize()
-    assert tcr.exact_bf16_windows_to_value(acc.cpu()) == es.value
+    assert exact_bf16_windows_to_value(acc.cpu()) == es.value
     P = 3
     parts = torch.empty(P, W, dtype=torch.int64, device="cuda")
     for r in range(P):

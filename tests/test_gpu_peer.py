@@ -19,6 +19,7 @@ import pytest
 
 import oracle
 import tcr_inputs as gen
+from exact_state_decode import exact_limbs_to_int
 
 pytestmark = pytest.mark.gpu
 
@@ -293,7 +294,7 @@ def test_exact_emulated_bitwise(tcr, mailboxes, P):
         assert o32.cpu().tolist() == [es.f32()] * P, (seed, P)
         assert o64.cpu().tolist() == [es.f64()] * P, (seed, P)
         for r in range(P):
-            assert tcr.exact_limbs_to_int(acc[6 * r:6 * r + 6]) == es.T
+            assert exact_limbs_to_int(acc[6 * r:6 * r + 6]) == es.T
 
 
 def test_exact_single_rank_equals_exact_entry(tcr, mailboxes):
@@ -306,7 +307,7 @@ def test_exact_single_rank_equals_exact_entry(tcr, mailboxes):
     tcr.tcr_reduce_sum_exact(x, acc=a)
     tcr.tcr_reduce_sum_exact_peer(x, mailboxes[:1], 0, acc=b)
     torch.cuda.synchronize()
-    assert tcr.exact_limbs_to_int(a) == tcr.exact_limbs_to_int(b)
+    assert exact_limbs_to_int(a) == exact_limbs_to_int(b)
 
 
 def test_exact_and_fp64_combines_interleave(tcr, mailboxes):

@@ -124,35 +124,6 @@ def test_empty_and_zero_segments(tcr):
     torch.cuda.synchronize()
 
 
-def test_full_size_c5_sampled(tcr):
-    """BASELINE config 5: 2^20 log-uniform segments (~1.2e10 elements), in the
-    launch configuration bench.py times; 256 sampled segments vs the oracle
-    (values regenerated on the host from (seed, index))."""
-    import torch
-
-    S = 1 << 20
-    lens = gen.loguniform_lengths(gen.SEED_C5, S)
-    off = gen.offsets_from_lengths(lens)
-    n = int(off[-1])
-    x = gen.generate_tensor(gen.SEED_C5, 0, n, gen.UNIFORM_PM1)
-    toff = torch.from_numpy(off).cuda()
-    out = torch.empty(S, dtype=torch.float32, device="cuda")
-    tcr.tcr_reduce_sum_segmented(x, toff, out)
-    torch.cuda.synchronize()
-    g = out.cpu().numpy()
-    rng = np.random.default_rng(1)
-    sample = np.concatenate([[0, S - 1], rng.integers(0, S, 254)])
-    for j in sample.tolist():
-        bits = gen.generate(gen.SEED_C5, int(off[j]), int(lens[j]), gen.UNIFORM_PM1)
-        es = oracle.exact_sum_fp16(bits)
-        assert oracle.within_tolerance(float(g[j]), es), (j, g[j], es.f64())
-    out2 = torch.empty(S, dtype=torch.float32, device="cuda")
-    tcr.tcr_reduce_sum_segmented(x, toff, out2)
-    torch.cuda.synchronize()
-    assert torch.equal(out, out2)
-    del x
-
-
 @pytest.mark.parametrize("mma", [True, False])
 def test_random_fuzz_against_oracle(tcr, mma):
     """200 random CSR problems: random segment counts (0..300), length mixes
