@@ -95,9 +95,11 @@ typedef enum {
     TCR_DTYPE_BF16 = 1, /* bfloat16: the same MMA encoding with .bf16 / kind::f16-BF16
                            operands and B = bfloat16 ones                    */
     TCR_DTYPE_E4M3 = 2, /* OCP fp8 E4M3FN (1 byte): tcgen05 kind::f8f6f4 (the
-                           default for fp8 from 2^26 elements) or mma.sync
-                           m16n8k32 .e4m3 (sm_100a runs it as fp16 HMMAs; the
-                           default below 2^26), B = fp8 ones */
+                           default for fp8 from 2^26 elements, B = fp8 ones) or
+                           mma.sync: each 512-element tile is converted exactly
+                           to binary16 and reduced as two m16n8k16 against
+                           binary16 ones (what sm_100a runs for m16n8k32 .e4m3;
+                           the default below 2^26) */
     TCR_DTYPE_E5M2 = 3  /* OCP fp8 E5M2 (1 byte), as E4M3                     */
 } tcr_dtype;
 
@@ -418,8 +420,13 @@ typedef enum {
     TCR_CFG_BULK_STAGES = 14,     /* bulk kernel: SMEM ring stages (2..32)      */
     TCR_CFG_BULK_STAGE_KB = 15,   /* bulk kernel: KiB per stage (4..64, x4)     */
     TCR_CFG_BULK_CTAS_PER_SM = 16, /* bulk kernel: CTAs per SM (clamped by SMEM) */
-    TCR_CFG_PEER_TIMEOUT_MS = 17  /* fused peer combine: bound on the wait for the
+    TCR_CFG_PEER_TIMEOUT_MS = 17,  /* fused peer combine: bound on the wait for the
                                      peers' partials (default 10000 ms)          */
+    TCR_CFG_PDL = 18              /* 1 (default): the streaming kernels are launched with
+                                   * programmatic dependent launch -- a call's CTAs are
+                                   * scheduled while the previous kernel on the stream
+                                   * drains and wait (griddepcontrol.wait) for its
+                                   * completion before touching memory; 0: plain launch */
 } tcr_config_key;
 tcr_status tcr_set_config(tcr_config_key key, int value);
 int tcr_get_config(tcr_config_key key); /* -1 for an unknown key */

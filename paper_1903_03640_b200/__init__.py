@@ -65,6 +65,7 @@ TCR_CFG_BULK_STAGES = 14
 TCR_CFG_BULK_STAGE_KB = 15
 TCR_CFG_BULK_CTAS_PER_SM = 16
 TCR_CFG_PEER_TIMEOUT_MS = 17
+TCR_CFG_PDL = 18
 
 TCR_EXACT_ACC_WORDS = 6
 TCR_EXACT_BF16_ACC_WORDS = 27

@@ -51,6 +51,7 @@ struct Config {
     int exact_unroll = 8;
     int exact_bps = 3;
     int peer_timeout_ms = 10000;
+    int pdl = 1;
 };
 Config g_cfg;
 std::mutex g_cfg_mu;
@@ -111,6 +112,7 @@ LaunchCfg make_cfg(const DeviceInfo& di) {
     c.bulk_ctas = g_cfg.bulk_ctas;
     c.exact_unroll = g_cfg.exact_unroll;
     c.exact_bps = g_cfg.exact_bps;
+    c.pdl = g_cfg.pdl;
     return c;
 }
 
@@ -792,6 +794,10 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             if (value < 1 || value > 8) break;
             g_cfg.exact_bps = value;
             return TCR_OK;
+        case TCR_CFG_PDL:
+            if (value < 0 || value > 1) break;
+            g_cfg.pdl = value;
+            return TCR_OK;
         case TCR_CFG_PEER_TIMEOUT_MS:
             if (value < 1 || value > 600000) break;
             g_cfg.peer_timeout_ms = value;
@@ -822,6 +828,7 @@ int tcr_get_config(tcr_config_key key) {
         case TCR_CFG_EXACT_UNROLL: return g_cfg.exact_unroll;
         case TCR_CFG_EXACT_BLOCKS_PER_SM: return g_cfg.exact_bps;
         case TCR_CFG_PEER_TIMEOUT_MS: return g_cfg.peer_timeout_ms;
+        case TCR_CFG_PDL: return g_cfg.pdl;
     }
     return -1;
 }

@@ -61,30 +61,45 @@ __device__ __forceinline__ void mma_rowsum_bf16(float (&c)[4], const uint4& a) {
 }
 
 // Element formats of the flat reduction (NEXT-4): every one keeps the tile at
-// 512 bytes = one 16-byte vector per lane.  fp8 uses m16n8k32 (16 elements
-// per lane, 512 per tile) with B = fp8 ones; the C/D fragment is unchanged.
+// 512 bytes = one 16-byte vector per lane.  An fp8 tile (512 elements, 16 per
+// lane) is the A of an m16n8k32, issued as two m16n8k16 (below); the C/D
+// fragment is unchanged.
 enum Fmt : int { kF16 = 0, kBF16 = 1, kE4M3 = 2, kE5M2 = 3 };
 template <int F> struct FmtInfo { static constexpr int kBytes = F >= kE4M3 ? 1 : 2; };
 
-__device__ __forceinline__ void mma_rowsum_e4m3(float (&c)[4], const uint4& a) {
-    asm volatile("mma.sync.aligned.m16n8k32.row.col.f32.e4m3.e4m3.f32 "
-        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(0x38383838u), "r"(0x38383838u));
-}
-__device__ __forceinline__ void mma_rowsum_e5m2(float (&c)[4], const uint4& a) {
-    asm volatile("mma.sync.aligned.m16n8k32.row.col.f32.e5m2.e5m2.f32 "
-        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(0x3C3C3C3Cu), "r"(0x3C3C3C3Cu));
+// fp8 tile as two binary16 A operands: every fp8 value is a binary16 value
+// (cvt.rn.f16x2.{e4m3,e5m2}x2 is exact), so the 32 products of a row of the
+// m16n8k32 become two m16n8k16 row sums against binary16 ones, chained in
+// fp32 -- the same arithmetic ptxas emits for mma.sync m16n8k32.e4m3 on
+// sm_100a (F2FP unpacks + two HMMA.16816), but converting only A: the
+// instruction form re-converted the constant ones operand at every MMA and
+// spilled at 80 registers (build/obj/tcr_reduce.ptxas.txt, r02).  Lane l's
+// 16 bytes map to halves 0..7 of the first and second operand: a bijection
+// of the tile onto A (reading G1).
+template <int F>
+__device__ __forceinline__ void mma_rowsum_fp8_as_f16(float (&c)[4], const uint4& a) {
+    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+    uint32_t h[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint16_t lo = (uint16_t)(w[k] & 0xFFFFu), hi = (uint16_t)(w[k] >> 16);
+        if constexpr (F == kE4M3) {
+            asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h[2 * k]) : "h"(lo));
+            asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h[2 * k + 1]) : "h"(hi));
+        } else {
+            asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(h[2 * k]) : "h"(lo));
+            asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(h[2 * k + 1]) : "h"(hi));
+        }
+    }
+    mma_rowsum(c, make_uint4(h[0], h[1], h[2], h[3]));
+    mma_rowsum(c, make_uint4(h[4], h[5], h[6], h[7]));
 }
 
 template <int F>
 __device__ __forceinline__ void mma_rowsum_f(float (&c)[4], const uint4& a) {
     if constexpr (F == kF16) mma_rowsum(c, a);
     else if constexpr (F == kBF16) mma_rowsum_bf16(c, a);
-    else if constexpr (F == kE4M3) mma_rowsum_e4m3(c, a);
-    else mma_rowsum_e5m2(c, a);
+    else mma_rowsum_fp8_as_f16<F>(c, a);
 }
 
 // Flush the carried fp32 accumulator into the lane's fp64 accumulator and

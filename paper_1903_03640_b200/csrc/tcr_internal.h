@@ -53,6 +53,7 @@ struct LaunchCfg {
     int bulk_ctas;        // bulk kernel: CTAs per SM
     int exact_unroll;     // exact kernel: 16-byte loads in flight per lane (4 or 8)
     int exact_bps;        // exact kernel: CTAs per SM
+    int pdl;              // streaming kernels: programmatic dependent launch (0 / 1)
 };
 
 // Each launcher enqueues exactly one kernel on `stream` and returns the
@@ -115,7 +116,7 @@ cudaError_t launch_probe_mma(int algo, const uint16_t* a, const float* c, float*
 
 // Grid size of the streaming kernels for n elements (shared by the API's
 // workspace sizing and the launchers).
-int stream_grid(size_t n, const LaunchCfg& cfg);
+int stream_grid(size_t n, const LaunchCfg& cfg, int resident = 0);
 int tcgen05_grid(size_t nbytes, const LaunchCfg& cfg);
 
 }  // namespace tcr

@@ -58,13 +58,26 @@ __device__ __forceinline__ void consume_batch(const uint4 (&v)[U], float (&cA)[4
 // slices = emulated ranks).  A separate instantiation, so that the plain
 // kernel's code is untouched by it (measured: folding the peer path into
 // the plain kernel as a runtime branch cost 3 % at 2^30).
+// Resident CTAs per SM the register budget is sized for (__launch_bounds__):
+// 4 at U <= 8 (64 registers), 2 at U = 16 -- every format at zero spills
+// (build/obj/tcr_reduce.ptxas.txt).
+template <int F, int U>
+constexpr int stream_resident() { return U <= 8 ? 4 : 2; }
+
 template <bool kMma, int F, int U, int WARPS, bool kPeer>
-__global__ void __launch_bounds__(WARPS * 32, (U <= 8 ? 4 : 2))
+__global__ void __launch_bounds__(WARPS * 32, stream_resident<F, U>())
 reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, int mid_flush,
                      float* out_f32, double* out_f64, DevWorkspace ws, PeerCombine pc) {
     constexpr int ES = FmtInfo<F>::kBytes;
     constexpr int kTileBytes = 512;
     TCR_COMPLETE_EDGE(0);
+    // Programmatic dependent launch (TCR_CFG_PDL): this grid may have been
+    // scheduled while the previous kernel on the stream drained; wait for it
+    // to complete (and its writes -- x, the workspace -- to be visible)
+    // before touching memory, then let the next call's grid be scheduled.
+    // Both are no-ops for a plain launch.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int me = pc.rank;
     if (kPeer && gridDim.y > 1) {  // emulated peer group: slice y is rank y, reducing its shard
@@ -137,7 +150,7 @@ reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, i
 
 constexpr int kStreamWarps = 8;  // 256 threads per CTA
 
-int stream_grid(size_t n, const LaunchCfg& cfg) {
+int stream_grid(size_t n, const LaunchCfg& cfg, int resident_in) {
     const size_t tiles = n / kTileElems;  // (n in 2-byte element equivalents)
     const size_t per_cta = (size_t)kStreamWarps * cfg.unroll;  // tiles one CTA covers per iteration
     size_t g = (tiles + per_cta - 1) / per_cta;
@@ -145,7 +158,7 @@ int stream_grid(size_t n, const LaunchCfg& cfg) {
     // (measured best at 2^30).  Below 2^28 elements the launch is latency
     // bound and a second wave costs more than it hides: cap the grid at one
     // resident wave (the __launch_bounds__ minimum CTAs per SM).
-    const int resident = cfg.unroll <= 8 ? 4 : 2;
+    const int resident = resident_in > 0 ? resident_in : (cfg.unroll <= 8 ? 4 : 2);
     const int per_sm = (n < ((size_t)1 << 28) && cfg.blocks_per_sm > resident) ? resident
                                                                                : cfg.blocks_per_sm;
     const size_t gmax = (size_t)cfg.sms * per_sm;
@@ -165,9 +178,17 @@ static cudaError_t launch_stream_u(const uint8_t* x, size_t n, int fe, float* ou
     auto kernel = reduce_stream_kernel<kMma, F, U, kStreamWarps, kPeer>;
     const int mid = (U == 16 && 2 * cfg.chain < U) ? 1 : 0;
     if (!emulate) {
-        const int g = stream_grid(n * FmtInfo<F>::kBytes / 2, cfg);
-        kernel<<<g, kStreamWarps * 32, 0, stream>>>(x, n, fe, mid, out_f32, out_f64, ws, pc);
-        return cudaGetLastError();
+        const int g = stream_grid(n * FmtInfo<F>::kBytes / 2, cfg, stream_resident<F, U>());
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(g);
+        lc.blockDim = dim3(kStreamWarps * 32);
+        lc.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = (cfg.pdl && !kPeer) ? 1 : 0;  // the peer combine waits on other ranks
+        return cudaLaunchKernelEx(&lc, kernel, x, n, fe, mid, out_f32, out_f64, ws, pc);
     }
     // Emulated peer group: the ranks' last CTAs wait on one another, so all
     // P grid slices must be co-resident -- a cooperative launch guarantees it

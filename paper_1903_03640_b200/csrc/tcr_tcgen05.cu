@@ -272,8 +272,8 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
             auto tile = [&](const uint4& v) {
                 switch (prm.fmt) {
                     case 1: mma_rowsum_bf16(c, v); break;
-                    case 2: mma_rowsum_e4m3(c, v); break;
-                    case 3: mma_rowsum_e5m2(c, v); break;
+                    case 2: mma_rowsum_fp8_as_f16<kE4M3>(c, v); break;
+                    case 3: mma_rowsum_fp8_as_f16<kE5M2>(c, v); break;
                     default: mma_rowsum(c, v); break;
                 }
                 flush_rows(c, acc, lane);

@@ -2,7 +2,10 @@
 paths vs the warp-shuffle path.
   cold: a 512 MiB buffer is written between timed launches (outside the
         events; its dirty lines are written back during the timed kernel);
-        per-launch CUDA-event time, median of 200.
+        per-launch CUDA-event time, median of 200.  Every timed launch is
+        queued behind a 40 us spin kernel (torch.cuda._sleep), so the host's
+        launch cost is hidden (r02; r01's numbers included it); the launch
+        floor of the event pair is reported as "empty" (an empty torch op).
   cold_clean: the same with the 512 MiB buffer READ instead (L2 left full of
         clean lines: no write-back inside the timed kernel).
   warm: 100 back-to-back launches captured in a CUDA graph, replay time / 100
@@ -56,6 +59,7 @@ def cold_time(fn, clean):
         else:
             flush.fill_(i & 0xFF)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(80000)  # ~40 us at 1.9 GHz: the host enqueues fn() meanwhile
         a.record()
         fn()
         b.record()
@@ -65,12 +69,19 @@ def cold_time(fn, clean):
     return statistics.median(ts)
 
 
-for algo in ("mma_sync", "tcgen05", "shuffle"):
+pdl_modes = [1, 0] if hasattr(tcr, "TCR_CFG_PDL") else [None]
+empty = torch.empty(1, device="cuda")
+res["empty:cold_clean"] = {"us": cold_time(lambda: empty.zero_(), True)}
+print(f"empty op  cold_clean: {res['empty:cold_clean']['us']:7.2f} us  (event-pair launch floor)")
+for pdl, algo in [(p, a) for p in pdl_modes for a in ("mma_sync", "tcgen05", "shuffle")]:
+    if pdl is not None:
+        tcr.tcr_set_config(tcr.TCR_CFG_PDL, pdl)
+    tag = algo if pdl is None else f"{algo}/pdl{pdl}"
     fn = lambda: tcr.tcr_reduce_sum_algo(x, out_f32=out, algo=algo)  # noqa: E731
     for mode, us in (("cold", cold_time(fn, False)), ("cold_clean", cold_time(fn, True)),
                      ("warm", graph_time(lambda: tcr.tcr_reduce_sum_algo(x, out_f32=out, algo=algo)))):
-        res[f"{algo}:{mode}"] = {"us": us, "GB/s": 2 * n / (us * 1e-6) / 1e9, "Gelem/s": n / (us * 1e-6) / 1e9}
-        print(f"{algo:9s} {mode:10s}: {us:7.2f} us  {2*n/(us*1e-6)/1e9:8.1f} GB/s  {n/(us*1e-6)/1e9:8.1f} Gelem/s")
+        res[f"{tag}:{mode}"] = {"us": us, "GB/s": 2 * n / (us * 1e-6) / 1e9, "Gelem/s": n / (us * 1e-6) / 1e9}
+        print(f"{tag:14s} {mode:10s}: {us:7.2f} us  {2*n/(us*1e-6)/1e9:8.1f} GB/s  {n/(us*1e-6)/1e9:8.1f} Gelem/s")
 # torch.sum as a library reference point
 tfn = lambda: torch.sum(x, dtype=torch.float32)  # noqa: E731
 for mode, us in (("cold", cold_time(tfn, False)), ("cold_clean", cold_time(tfn, True)),

@@ -1,5 +1,6 @@
-"""NEXT-4: fp8 (E4M3 / E5M2) inputs through the MMA encoding (mma.sync
-m16n8k32 and tcgen05 kind::f8f6f4, B = fp8 ones) and the shuffle path, vs the
+"""NEXT-4: fp8 (E4M3 / E5M2) inputs through the MMA encoding (mma.sync: the
+exact binary16 conversion of each tile as two m16n8k16 against ones; tcgen05
+kind::f8f6f4, B = fp8 ones) and the shuffle path, vs the
 exact fp8 oracle; tolerance |g - R| <= 2^-20 * sum|x_i|; any byte alignment."""
 import numpy as np
 import pytest
