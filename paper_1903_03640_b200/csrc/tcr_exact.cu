@@ -8,7 +8,7 @@
 // binary64 subnormal f*2^-1032).  All such numbers are multiples of 2^-1032,
 // so binary64 additions of up to 8192 of them (|sum| < 2^-979, i.e. fewer
 // than 53 significant bits) are exact.  Each lane therefore adds scaled
-// binary64 values in two accumulators, flushes them every kFlushIter
+// binary64 values in two or four accumulators, flushes them every kFlushIter
 // iterations (<= 1024 elements per accumulator) into a signed 128-bit
 // integer in units of 2^-24, and the warp / CTA / grid levels add int128
 // exactly (the same last-CTA completion as the MMA kernels).  The result is
@@ -60,8 +60,8 @@ __device__ __forceinline__ uint32_t probe_word(uint32_t w, uint32_t probe) {
 // Rare path: count the non-finite halves of v and subtract the scaled
 // binary64 values they contributed (exactly: every partial sum stays a
 // multiple of 2^-1032 below 2^-979).
-__device__ __forceinline__ void fix_specials(const uint4& v, double& a0, double& a1,
-                                             uint32_t (&cnt)[3]) {
+template <int NA>
+__device__ __forceinline__ void fix_specials(const uint4& v, double (&a)[NA], uint32_t (&cnt)[3]) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     for (int k = 0; k < 4; ++k) {
         for (int h = 0; h < 2; ++h) {
@@ -70,52 +70,36 @@ __device__ __forceinline__ void fix_specials(const uint4& v, double& a0, double&
                 if (half & 0x3FFu) ++cnt[0];            // NaN
                 else if (half & 0x8000u) ++cnt[2];      // -inf
                 else ++cnt[1];                          // +inf
-                if (h == 0) a0 -= scaled_lo(w[k]);
-                else a1 -= scaled_hi(w[k]);
+                // the accumulator exact_vec added it to: word parity, half
+                if (h == 0) a[(2 * (k & 1)) % NA] -= scaled_lo(w[k]);
+                else a[(2 * (k & 1) + 1) % NA] -= scaled_hi(w[k]);
             }
         }
     }
 }
 
-__device__ __forceinline__ void exact_vec(const uint4& v, double& a0, double& a1,
-                                          uint32_t& probe) {
+// NA accumulators (2 or 4): word k's low / high half go to a[(2(k&1)) % NA]
+// / a[(2(k&1)+1) % NA]; with NA = 4 an iteration's adds form four independent
+// DADD chains (r02: two chains left the binary16 kernel FP64-latency-bound).
+template <int NA>
+__device__ __forceinline__ void exact_vec(const uint4& v, double (&a)[NA], uint32_t& probe) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         probe = probe_word(w[k], probe);
-        a0 += scaled_lo(w[k]);
-        a1 += scaled_hi(w[k]);
+        a[(2 * (k & 1)) % NA] += scaled_lo(w[k]);
+        a[(2 * (k & 1) + 1) % NA] += scaled_hi(w[k]);
     }
 }
 
 // fp8 (E4M3 / E5M2) -> binary16 is exact (every fp8 value is a binary16
 // value; cvt.rn.f16x2.{e4m3,e5m2}x2): 16 fp8 bytes become two vectors of 8
 // binary16 that go through the same exact accumulation (NEXT-3 x NEXT-4).
-template <int F>
-__device__ __forceinline__ void fp8_to_f16(const uint4& v, uint4& lo, uint4& hi) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    uint32_t o[8];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const uint16_t b0 = (uint16_t)(w[k] & 0xFFFFu), b1 = (uint16_t)(w[k] >> 16);
-        if constexpr (F == kE4M3) {
-            asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(o[2 * k]) : "h"(b0));
-            asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(o[2 * k + 1]) : "h"(b1));
-        } else {
-            asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(o[2 * k]) : "h"(b0));
-            asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(o[2 * k + 1]) : "h"(b1));
-        }
-    }
-    lo = make_uint4(o[0], o[1], o[2], o[3]);
-    hi = make_uint4(o[4], o[5], o[6], o[7]);
-}
-
 // One loaded 16-byte vector of format F into the accumulators.
-template <int F>
-__device__ __forceinline__ void exact_vec_f(const uint4& v, double& a0, double& a1,
-                                            uint32_t& probe) {
+template <int F, int NA>
+__device__ __forceinline__ void exact_vec_f(const uint4& v, double (&a)[NA], uint32_t& probe) {
     if constexpr (F == kF16) {
-        exact_vec(v, a0, a1, probe);
+        exact_vec<NA>(v, a, probe);
     } else {  // word by word: two binary16 pairs per 32-bit word, few live registers
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -126,24 +110,40 @@ __device__ __forceinline__ void exact_vec_f(const uint4& v, double& a0, double& 
                 uint32_t o;
                 if constexpr (F == kE4M3) asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(o) : "h"(b));
                 else asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(o) : "h"(b));
+                // converted word j = 2k + h: parity of j (= h) picks the pair,
+                // as fix_specials_f's word index in lo / hi does
                 probe = probe_word(o, probe);
-                a0 += scaled_lo(o);
-                a1 += scaled_hi(o);
+                a[(2 * h) % NA] += scaled_lo(o);
+                a[(2 * h + 1) % NA] += scaled_hi(o);
             }
         }
     }
 }
 
-template <int F>
-__device__ __forceinline__ void fix_specials_f(const uint4& v, double& a0, double& a1,
-                                               uint32_t (&cnt)[3]) {
+template <int F, int NA>
+__device__ __forceinline__ void fix_specials_f(const uint4& v, double (&a)[NA], uint32_t (&cnt)[3]) {
     if constexpr (F == kF16) {
-        fix_specials(v, a0, a1, cnt);
-    } else {
-        uint4 lo, hi;
-        fp8_to_f16<F>(v, lo, hi);
-        fix_specials(lo, a0, a1, cnt);
-        fix_specials(hi, a0, a1, cnt);
+        fix_specials<NA>(v, a, cnt);
+    } else {  // word by word, as exact_vec_f converts (few live registers)
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll 1
+        for (int j = 0; j < 8; ++j) {
+            const uint16_t b = (uint16_t)(w[j >> 1] >> (16 * (j & 1)));
+            uint32_t o;
+            if constexpr (F == kE4M3) asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(o) : "h"(b));
+            else asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(o) : "h"(b));
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t half = (o >> (16 * h)) & 0xFFFFu;
+                if ((half & 0x7C00u) == 0x7C00u) {
+                    if (half & 0x3FFu) ++cnt[0];
+                    else if (half & 0x8000u) ++cnt[2];
+                    else ++cnt[1];
+                    // converted word j went to the pair of parity j & 1
+                    if (h == 0) a[(2 * (j & 1)) % NA] -= scaled_lo(o);
+                    else a[(2 * (j & 1) + 1) % NA] -= scaled_hi(o);
+                }
+            }
+        }
     }
 }
 
@@ -275,8 +275,20 @@ reduce_exact_kernel(const uint8_t* __restrict__ x, size_t n, long long* out_acc,
     // <= 1024 binary16 per accumulator between flushes (an fp8 vector is 16 of them)
     constexpr int kFlush = kFlushIter * kExactUnroll / U / (ES == 1 ? 2 : 1);
 
-    double a0 = 0.0, a1 = 0.0;
+    // four accumulators at U = 8 (the default); two at U = 4, where 4 CTAs/SM
+    // leave 64 registers
+    constexpr int NA = U >= 8 ? 4 : 2;
     i128 acc = 0;
+    double a[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) a[i] = 0.0;
+    auto drain = [&]() {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            acc += (i128)to_units(a[i]);
+            a[i] = 0.0;
+        }
+    };
     uint32_t cnt[3] = {0u, 0u, 0u};
     uint32_t probe = 0u;
     int it = 0;
@@ -287,23 +299,22 @@ reduce_exact_kernel(const uint8_t* __restrict__ x, size_t n, long long* out_acc,
         for (int u = 0; u < U; ++u) v[u] = ldg_stream(base + (t + (size_t)u * W) * 32);
         __syncwarp();  // scheduling fence: all U loads issue before the first consumer
 #pragma unroll
-        for (int u = 0; u < U; ++u) exact_vec_f<F>(v[u], a0, a1, probe);
+        for (int u = 0; u < U; ++u) exact_vec_f<F, NA>(v[u], a, probe);
         if (probe & 0x7FFF7FFFu) {  // some half was inf or NaN (rare): reload and fix
 #pragma unroll 1
             for (int u = 0; u < U; ++u)
-                fix_specials_f<F>(ldg_stream(base + (t + (size_t)u * W) * 32), a0, a1, cnt);
+                fix_specials_f<F, NA>(ldg_stream(base + (t + (size_t)u * W) * 32), a, cnt);
             probe = 0u;
         }
         if (++it == kFlush) {
             it = 0;
-            acc += (i128)to_units(a0) + (i128)to_units(a1);
-            a0 = a1 = 0.0;
+            drain();
         }
     }
     auto one = [&](const uint4& v) {
         uint32_t p = 0u;
-        exact_vec_f<F>(v, a0, a1, p);
-        if (p & 0x7FFF7FFFu) fix_specials_f<F>(v, a0, a1, cnt);
+        exact_vec_f<F, NA>(v, a, p);
+        if (p & 0x7FFF7FFFu) fix_specials_f<F, NA>(v, a, cnt);
     };
     if (t < T) {  // fewer than U tiles left for this warp: one predicated batch (one latency)
         uint4 v[U];
@@ -319,7 +330,7 @@ reduce_exact_kernel(const uint8_t* __restrict__ x, size_t n, long long* out_acc,
         if (head) one(load_ragged_bytes(x, (int)head, lane));
         if (tail) one(load_ragged_bytes(xa + T * kTileBytes, tail, lane));
     }
-    acc += (i128)to_units(a0) + (i128)to_units(a1);
+    drain();
 
     // warp, CTA and grid levels: exact integer adds (order-free)
     __shared__ long long s_part[kExactWarps][5];

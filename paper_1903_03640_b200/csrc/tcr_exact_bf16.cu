@@ -9,8 +9,9 @@
 // exponent field), is a multiple of the window's unit and below 2^40 units,
 // so up to 2^13 of them add exactly in binary64.
 //   fast path  all halves of a warp's iteration lie in one window (or are
-//              zero): one binary64 accumulator for that window, flushed every
-//              64 iterations or when the window changes;
+//              zero): four binary64 accumulators for that window (no serial
+//              DADD chain), flushed every 64 iterations or when the window
+//              changes;
 //   slow path  mixed windows or inf/NaN in the iteration: each half is turned
 //              into an integer of its window's unit and added to a per-lane
 //              int64 slot of that window in shared memory.
@@ -30,13 +31,9 @@ typedef unsigned __int128 u128;
 
 constexpr int kXbWarps = 8;
 constexpr int kXbU = 4;
-constexpr int kXbFlushIter = 64;        // 64 iterations x 32 halves <= 2^13 per accumulator
+constexpr int kXbAcc = 4;               // independent binary64 accumulators per lane
+constexpr int kXbFlushIter = 64;        // 64 iterations x 32 halves = 2^11 adds per lane per flush (<= 2^13 exact)
 constexpr int kXbWords = 8 * 2 + 3;     // per CTA partial: 8 x int128 + 3 special counts
-
-__device__ __forceinline__ double placed(uint32_t h) {  // bf16 (low 16 bits) * 2^-896
-    const uint32_t hi = ((h & 0x7FFFu) << 13) | ((h & 0x8000u) << 16);
-    return __hiloint2double((int)hi, 0);
-}
 
 // Flushed window accumulator -> integer in the window's unit (exact; < 2^53).
 __device__ __forceinline__ long long win_units(double a, int k) {
@@ -193,12 +190,23 @@ reduce_exact_bf16_kernel(const uint16_t* __restrict__ x, size_t n, long long* ou
     const size_t w = (size_t)blockIdx.x * kXbWarps + warp;
     const uint4* base = reinterpret_cast<const uint4*>(xa) + lane;
 
-    double aw = 0.0;
+    // kXbAcc independent binary64 accumulators of the current window (the
+    // adds of an iteration are spread over them: no serial DADD chain)
+    double aw[kXbAcc];
+#pragma unroll
+    for (int a = 0; a < kXbAcc; ++a) aw[a] = 0.0;
     int wcur = -1;  // window of aw (warp-uniform)
     int it = 0;
     auto flush = [&]() {
-        if (wcur >= 0) s_I[wcur][tid] += win_units(aw, wcur);
-        aw = 0.0;
+        if (wcur >= 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int a = 0; a < kXbAcc; ++a) {
+                t += aw[a];  // exact: multiples of the window's unit, total < 2^53 units
+                aw[a] = 0.0;
+            }
+            s_I[wcur][tid] += win_units(t, wcur);
+        }
         it = 0;
     };
     auto slow = [&](const uint4& v) {
@@ -216,31 +224,34 @@ reduce_exact_bf16_kernel(const uint16_t* __restrict__ x, size_t n, long long* ou
             }
         }
     };
-    // an iteration's vectors: fast path if every nonzero finite half is in one window
+    // an iteration's vectors: fast path if every nonzero finite half is in one window.
+    // Per word m = the two 15-bit magnitudes; per half t = mag + 0x7FFF as a
+    // signed 16-bit value (no carry between halves): zero -> +32767, nonzero
+    // -> (mag - 1) - 32768, monotone in mag.  Then the warp's largest
+    // magnitude M fixes the window wc = M >> 12 (= biased exponent >> 5), M >=
+    // 0x7F80 flags inf / NaN, and "every nonzero half is in window wc" is
+    // min over halves of t >= (wc << 12) - 1 - 32768 (zeros pass).  Three
+    // SIMD-16x2 operations per word (r02; the r01 test with a per-half zero
+    // compare cost ~5 operations per element).
     auto process = [&](const uint4 (&v)[kXbU], int nv) {
-        // packed over the two halves of each word: window bits (exponent >> 5),
-        // their max, their min over nonzero halves, and an inf/NaN flag
-        uint32_t kmax = 0u, kmin = 0x00070007u, spec = 0u;
+        uint32_t vmax = 0u, vmin = 0x7FFF7FFFu;
 #pragma unroll
         for (int u = 0; u < kXbU; ++u) {
             if (u >= nv) break;
             const uint32_t ws4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const uint32_t wd = ws4[q];
-                spec |= ((wd & 0x7F807F80u) + 0x00800080u) & 0x80008000u;
-                const uint32_t kk = (wd >> 12) & 0x00070007u;
-                const uint32_t zero = __vcmpeq2(wd & 0x7FFF7FFFu, 0u);  // 0xFFFF per zero half
-                kmax = __vmaxu2(kmax, kk);
-                kmin = __vminu2(kmin, kk | (zero & 0x00070007u));
+                const uint32_t m = ws4[q] & 0x7FFF7FFFu;
+                vmax = __vmaxu2(vmax, m);
+                vmin = __vmins2(vmin, m + 0x7FFF7FFFu);
             }
         }
-        const uint32_t lmax = max(kmax & 0xFFFFu, kmax >> 16);
-        const uint32_t lmin = min(kmin & 0xFFFFu, kmin >> 16);
-        const uint32_t wc = __reduce_max_sync(0xffffffffu, lmax);
-        // every nonzero half of the warp is in window wc (<= wc by the max, >= by the min)
-        const bool own_ok = spec == 0u && lmin >= wc;
-        if (__all_sync(0xffffffffu, own_ok)) {
+        const uint32_t lmax = max(vmax & 0xFFFFu, vmax >> 16);
+        const int lmin = min((int)(short)(vmin & 0xFFFFu), (int)(short)(vmin >> 16));
+        const uint32_t M = __reduce_max_sync(0xffffffffu, lmax);
+        const uint32_t wc = M >> 12;
+        const bool own_ok = lmin >= (int)(wc << 12) - 1 - 32768;
+        if (M < 0x7F80u && __all_sync(0xffffffffu, own_ok)) {
             const int k = (int)wc;
             if (k != wcur) {
                 flush();
@@ -252,8 +263,12 @@ reduce_exact_bf16_kernel(const uint16_t* __restrict__ x, size_t n, long long* ou
                 const uint32_t ws4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    aw += placed(ws4[q] & 0xFFFFu);
-                    aw += placed(ws4[q] >> 16);
+                    // bf16 * 2^-896 as binary64 hi words: sign to bit 31, the
+                    // magnitude to bits 13..27 (arithmetic shift keeps the sign)
+                    const int hi1 = ((int)ws4[q] >> 3) & (int)0x8FFFE000u;
+                    const int hi0 = ((int)(ws4[q] << 16) >> 3) & (int)0x8FFFE000u;
+                    aw[(2 * q) % kXbAcc] += __hiloint2double(hi0, 0);
+                    aw[(2 * q + 1) % kXbAcc] += __hiloint2double(hi1, 0);
                 }
             }
             if (++it == kXbFlushIter) flush();

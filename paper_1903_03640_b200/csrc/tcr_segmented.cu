@@ -41,8 +41,14 @@ __device__ __forceinline__ void seg_piece(const uint4& v, double& acc, int lane)
     }
 }
 
+// Resident CTAs per SM of the union-stream kernel (__launch_bounds__): 4 for
+// CSR (64 registers); 3 for fixed-length batches, whose 64-bit segment
+// arithmetic needs the room (85 registers: zero spills, ptxas report).
+template <bool kBatched>
+constexpr int seg_resident() { return kBatched ? 3 : 4; }
+
 template <bool kMma, int F, bool kBatched, int U, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 4)
+__global__ void __launch_bounds__(WARPS * 32, seg_resident<kBatched>())
 reduce_segmented_kernel(const uint8_t* __restrict__ x, const int64_t* __restrict__ offsets,
                         size_t S, size_t L, int batch, float* __restrict__ out, DevWorkspace ws) {
     constexpr int kLogEpv = FmtInfo<F>::kBytes == 2 ? 3 : 4;  // log2(elements per vector)
@@ -250,8 +256,11 @@ static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, cons
         size_t b = L ? ((size_t)32768 / FmtInfo<F>::kBytes / L) : 255;
         if (b < kBatchSeg) b = kBatchSeg;
         if (b > 255) b = 255;
+        dim3 bgrid = grid;  // one resident wave at this kernel's occupancy
+        const unsigned bmax = (unsigned)(sms * seg_resident<true>());
+        if (bgrid.x > bmax) bgrid.x = bmax;
         reduce_segmented_kernel<kMma, F, true, kSegUnroll, kSegWarps>
-            <<<grid, block, 0, stream>>>(x, offsets, S, L, (int)b, out, ws);
+            <<<bgrid, block, 0, stream>>>(x, offsets, S, L, (int)b, out, ws);
     } else {
         reduce_segmented_kernel<kMma, F, false, kSegUnroll, kSegWarps>
             <<<grid, block, 0, stream>>>(x, offsets, S, L, (int)kBatchSeg, out, ws);

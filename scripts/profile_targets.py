@@ -1,6 +1,7 @@
 """Small driver for ncu captures: runs one named kernel a few times on the
 synthetic workload.  Usage: python scripts/profile_targets.py <target>
-targets: c3_mma c3_tcgen05 c3_shuffle c3_exact c5 rows256 fp8_tcgen05 bf16_mma"""
+targets: c3_mma c3_tcgen05 c3_shuffle c3_exact c5 rows256 fp8_tcgen05 bf16_mma
+         c2_mma c2_tcgen05 c2_shuffle (n = 2^24, BASELINE config 2)"""
 import sys
 
 import numpy as np
@@ -12,7 +13,11 @@ import tcr_inputs as gen  # noqa: E402
 
 t = sys.argv[1]
 out = torch.empty(1 << 20, dtype=torch.float32, device="cuda")
-if t.startswith("c3_"):
+if t.startswith("c2_"):
+    x = gen.generate_tensor(gen.SEED_C2, 0, 1 << 24, gen.UNIFORM_PM1)
+    for _ in range(5):
+        tcr.tcr_reduce_sum_algo(x, out_f32=out, algo={"mma": "mma_sync"}.get(t[3:], t[3:]))
+elif t.startswith("c3_"):
     x = gen.generate_tensor(gen.SEED_C3, 0, 1 << 30, gen.UNIFORM_PM1)
     for _ in range(3):
         if t == "c3_exact":

@@ -1,0 +1,10 @@
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; O=gpurun_out
+./scripts/tc05_borient > $O/r2_tc05_borient.txt 2>&1
+for t in c2_mma c2_shuffle c2_tcgen05; do
+  python scripts/profile_targets.py $t > /dev/null 2>&1 && \
+  timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum \
+     --clock-control none --cache-control all -k regex:reduce_ --csv python scripts/profile_targets.py $t > $O/r2_ncu_$t.csv 2>&1
+done
+python scripts/profile_targets.py c3_mma > /dev/null 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:reduce_stream_kernel -s 1 -c 1 -o $O/r2_prof_c3_mma -f python scripts/profile_targets.py c3_mma > $O/r2_ncu_c3_mma.log 2>&1
+P="python bench.py --e2e-steps 0 --no-cpu-baseline --steps 3 --warmup 3"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/r2_launches_default.csv $P > $O/r2_ncu_l.log 2>&1
