@@ -28,14 +28,14 @@ __device__ __forceinline__ unsigned long long now() {
 __global__ void __launch_bounds__(128, 1) rate(int borient, int N, int groups, unsigned long long* out,
                                                float* dcheck) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t* cbar = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* cbar = reinterpret_cast<uint64_t*>(smem);  // [2]: one per group parity
     uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 64);
     uint8_t* in = smem + 1024;
     uint8_t* ones = smem + 1024 + 65536;
     for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(in)[i] = 0x3C003C00u;
     for (int i = threadIdx.x; i < 8192 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(ones)[i] = 0x3C003C00u;
     fence_proxy_async_smem();
-    if (threadIdx.x == 0) { mbar_init(cbar, 1); fence_mbar_init(); }
+    if (threadIdx.x == 0) { mbar_init(&cbar[0], 1); mbar_init(&cbar[1], 1); fence_mbar_init(); }
     if (threadIdx.x < 32) tmem_alloc(tslot, 512);
     tc_fence_before(); __syncthreads(); tc_fence_after();
     const uint32_t tmem = *tslot;
@@ -45,19 +45,27 @@ __global__ void __launch_bounds__(128, 1) rate(int borient, int N, int groups, u
     if (threadIdx.x == 0) {
         const uint64_t onesd = smem_desc_kmajor(smem_addr(ones), 128, 256);
         const uint64_t in0 = smem_desc_kmajor(smem_addr(in), 128, 256);
-        uint32_t ph = 0;
+        // group g commits to cbar[g & 1]; before reusing a barrier, wait for
+        // its previous phase (group g - 2), so no barrier ever runs more than
+        // one phase ahead of its waiter (parity waits would otherwise alias)
+        uint32_t ph[2] = {0u, 0u};
         const unsigned long long t0 = now();
         for (int g = 0; g < groups; ++g) {
+            const int b = g & 1;
+            if (g >= 2) { mbar_wait(&cbar[b], ph[b]); ph[b] ^= 1u; }
             for (int k = 0; k < 4; ++k) {
                 const uint64_t idd = in0 + (uint64_t)((((g * 4 + k) % tiles) * in_bytes) >> 4);
                 const uint32_t d = tmem + (uint32_t)((k & 1) * N);  // two accumulators (N <= 256)
                 if (borient) mma_f16_ss(d, onesd, idd, idesc, (g | (k >> 1)) ? 1u : 0u);
                 else mma_f16_ss(d, idd, onesd, idesc, (g | (k >> 1)) ? 1u : 0u);
             }
-            mma_commit(cbar);
-            if (g >= 1) { mbar_wait(cbar, ph); ph ^= 1u; }  // at most two groups in flight
+            mma_commit(&cbar[b]);
         }
-        mbar_wait(cbar, ph);
+        for (int g = groups >= 2 ? groups - 2 : 0; g < groups; ++g) {
+            const int b = g & 1;
+            mbar_wait(&cbar[b], ph[b]);
+            ph[b] ^= 1u;
+        }
         const unsigned long long t1 = now();
         out[blockIdx.x] = t1 - t0;
     }

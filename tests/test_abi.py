@@ -165,3 +165,26 @@ def test_product_path_fails_loudly_without_the_library(tmp_path):
                        capture_output=True, text=True, env={**os.environ, "PYTHONPATH": str(tmp_path)})
     assert r.returncode != 0
     assert "ImportError" in r.stderr and "no fallback" in r.stderr
+
+
+def test_no_register_spills_in_any_kernel():
+    """Every kernel of libtcr.so compiles without register spills (ptxas -v
+    report written by the Makefile next to each object; r02)."""
+    import subprocess
+
+    csrc = os.path.join(ROOT, "paper_1903_03640_b200", "csrc")
+    subprocess.run(["make", "-s", "-C", csrc], check=True, capture_output=True)
+    objdir = os.path.join(ROOT, "build", "obj")
+    reports = [f for f in os.listdir(objdir) if f.endswith(".ptxas.txt")]
+    assert len(reports) >= 8
+    seen, bad = 0, []
+    for f in reports:
+        for blk in open(os.path.join(objdir, f)).read().split("Compiling entry function '")[1:]:
+            name = blk.split("'")[0]
+            m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", blk)
+            if m:
+                seen += 1
+                if int(m.group(1)) or int(m.group(2)):
+                    bad.append((f, name, m.group(0)))
+    assert seen >= 50, seen
+    assert not bad, bad[:5]
