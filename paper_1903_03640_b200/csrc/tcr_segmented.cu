@@ -225,6 +225,75 @@ reduce_rows_kernel(const uint8_t* __restrict__ x, size_t S, float* __restrict__ 
     }
 }
 
+// Fixed-length rows as MMA rows (r02): 16 consecutive segments fill the 16
+// rows of A, so the row sums of Eq. 9-10 (D = A x 1 + C) ARE per-segment
+// partial sums -- no second-level collapse per segment.  In the paper one
+// group of m^2 inputs fills A and D' = 1 x D collapses its rows;
+// here the rows belong to different segments and stay apart.  Each row takes
+// 16 elements of its segment per MMA; C is carried over the segment's MMAs
+// (bounded chain: flushed into fp64 every kRsChain MMAs, reading G9).
+// Fragment use (m16n8k16, lane 4g + t): a0 = A[g][2t..], a1 = A[g+8][2t..],
+// a2 = A[g][2t+8..], a3 = A[g+8][2t+8..].  Lane 4g + t loads 16 bytes
+// (8 values) of segment g and 16 of segment g + 8 at element 32p + 8t: values
+// 0-3 feed MMA 2p, 4-7 MMA 2p + 1, so every row of A gets 16 elements of its
+// own segment (a bijection of the segment's elements onto its A rows, reading
+// G1).  Lanes 4g..4g+3 read 64 contiguous bytes per segment per load round.
+// D: c0 = c1 = row g, c2 = c3 = row g + 8 in every lane of quad g.  Needs
+// L % 32 == 0 (whole MMA pairs) and a 16-byte aligned x; 16-bit formats.
+constexpr int kRsChain = 4;  // MMAs per fp32 chain before the fp64 flush (K = 4, reading G10)
+
+// P = MMA pairs in flight per lane (2 loads each): 4 from L = 128 (the whole
+// row span up to 2048 in rounds of 256 B per row), else the row's own pair
+// count -- no dead load slots for short rows (measured, scripts/ab_rows.py:
+// L = 64 at P = 4: 5.9 TB/s, at P = 2: 6.7 TB/s).
+constexpr int kRsCtasPerSm = 3;  // resident CTAs per SM (<= 85 registers: no spills at P <= 4)
+
+template <int F, int WARPS, int P>
+__global__ void __launch_bounds__(WARPS * 32, kRsCtasPerSm)
+reduce_rowseg_kernel(const uint8_t* __restrict__ x, size_t S, size_t L, float* __restrict__ out) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const size_t slabs = (S + 15) / 16;
+    const size_t W = (size_t)gridDim.x * WARPS;
+    const size_t pairs = L / 32;  // 32 elements (64 bytes) of a row per MMA pair
+    for (size_t sl = (size_t)blockIdx.x * WARPS + (threadIdx.x >> 5); sl < slabs; sl += W) {
+        const size_t r0 = sl * 16 + (size_t)g, r1 = r0 + 8;
+        const bool in0 = r0 < S, in1 = r1 < S;
+        const uint4* p0 = reinterpret_cast<const uint4*>(x + r0 * L * 2) + t;  // row r1 = p0 + L
+        double acc0 = 0.0, acc1 = 0.0;
+        float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+        for (size_t p = 0; p < pairs; p += P) {
+            uint4 lo[P], hi[P];
+#pragma unroll
+            for (int u = 0; u < P; ++u) {
+                const bool in = p + (size_t)u < pairs;
+                lo[u] = (in && in0) ? ldg_stream(p0 + (p + (size_t)u) * 4) : make_uint4(0u, 0u, 0u, 0u);
+                hi[u] = (in && in1) ? ldg_stream(p0 + L + (p + (size_t)u) * 4) : make_uint4(0u, 0u, 0u, 0u);
+            }
+            __syncwarp();  // scheduling fence: all loads issue before the first MMA
+#pragma unroll
+            for (int u = 0; u < P; ++u) {
+                mma_rowsum_f<F>(c, make_uint4(lo[u].x, hi[u].x, lo[u].y, hi[u].y));
+                mma_rowsum_f<F>(c, make_uint4(lo[u].z, hi[u].z, lo[u].w, hi[u].w));
+                if ((2 * u + 2) % kRsChain == 0 || u == P - 1) {  // <= kRsChain MMAs per chain (static)
+                    // every lane of quad g holds rows g / g + 8 (no branch)
+                    acc0 += (double)c[0];
+                    acc1 += (double)c[2];
+                    c[0] = c[1] = c[2] = c[3] = 0.f;
+                }
+            }
+        }
+        acc0 += (double)c[0];
+        acc1 += (double)c[2];
+        if (t == 0) {
+            if (in0) out[r0] = (float)acc0;
+            if (in1) out[r1] = (float)acc1;
+        }
+    }
+}
+
 constexpr int kSegWarps = 8;
 constexpr int kSegUnroll = 8;  // tiles per group (one round trip)
 constexpr int kSegCtasPerSm = 4;  // resident CTAs per SM at <= 64 registers (launch bounds)
@@ -232,8 +301,39 @@ constexpr int kSegCtasPerSm = 4;  // resident CTAs per SM at <= 64 registers (la
 template <bool kMma, int F>
 static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, const uint8_t* x,
                          const int64_t* offsets, size_t S, size_t L, float* out,
-                         const DevWorkspace& ws, cudaStream_t stream, int sms) {
+                         const DevWorkspace& ws, cudaStream_t stream, int sms, int pdl) {
     constexpr size_t kTileEl = 512 / FmtInfo<F>::kBytes;
+    if constexpr (kMma && FmtInfo<F>::kBytes == 2) {
+        // fixed-length rows of 32..2048 binary16 / bfloat16: rows as MMA rows,
+        // except L = 1024 / 2048, where the whole-tile rows kernel below
+        // measured faster (6.9 vs 6.5 TB/s; profiles/r02/batched_b2b.txt)
+        if (batched && ((uintptr_t)x & 15u) == 0 && L % 32 == 0 && L >= 32 && L <= 2048 &&
+            L != 4 * kTileEl && L != 8 * kTileEl) {
+            const size_t slabs = (S + 15) / 16;
+            const size_t pairs = L / 32;
+            size_t g = (slabs + kSegWarps - 1) / kSegWarps;
+            // P <= 2 needs <= 46 registers: 5 CTAs per SM fit (more loads in flight)
+            const size_t gmax = (size_t)sms * (pairs >= 4 ? kRsCtasPerSm : 5);
+            if (g > gmax) g = gmax;
+            if (g < 1) g = 1;
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3((unsigned)g);
+            lc.blockDim = block;
+            lc.stream = stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            lc.attrs = at;
+            lc.numAttrs = pdl ? 1 : 0;
+            if (pairs >= 4)
+                cudaLaunchKernelEx(&lc, reduce_rowseg_kernel<F, kSegWarps, 4>, x, S, L, out);
+            else if (pairs >= 2)
+                cudaLaunchKernelEx(&lc, reduce_rowseg_kernel<F, kSegWarps, 2>, x, S, L, out);
+            else
+                cudaLaunchKernelEx(&lc, reduce_rowseg_kernel<F, kSegWarps, 1>, x, S, L, out);
+            return;
+        }
+    }
     if (batched && ((uintptr_t)x & 15u) == 0 &&
         (L == kTileEl || L == 2 * kTileEl || L == 4 * kTileEl || L == 8 * kTileEl)) {
         const size_t rows_per_group = 8 * kTileEl / L;
@@ -270,12 +370,12 @@ static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, cons
 template <bool kMma>
 static void launch_seg_m(int fmt, bool batched, const dim3& grid, const dim3& block,
                          const uint8_t* x, const int64_t* offsets, size_t S, size_t L, float* out,
-                         const DevWorkspace& ws, cudaStream_t stream, int sms) {
+                         const DevWorkspace& ws, cudaStream_t stream, int sms, int pdl) {
     switch (fmt) {
-        case kBF16: launch_seg_t<kMma, kBF16>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms); break;
-        case kE4M3: launch_seg_t<kMma, kE4M3>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms); break;
-        case kE5M2: launch_seg_t<kMma, kE5M2>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms); break;
-        default: launch_seg_t<kMma, kF16>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms); break;
+        case kBF16: launch_seg_t<kMma, kBF16>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms, pdl); break;
+        case kE4M3: launch_seg_t<kMma, kE4M3>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms, pdl); break;
+        case kE5M2: launch_seg_t<kMma, kE5M2>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms, pdl); break;
+        default: launch_seg_t<kMma, kF16>(batched, grid, block, x, offsets, S, L, out, ws, stream, sms, pdl); break;
     }
 }
 
@@ -291,10 +391,10 @@ cudaError_t launch_reduce_segmented(bool mma, int fmt, bool batched, const void*
     const uint8_t* xb = static_cast<const uint8_t*>(x);
     if (mma)
         launch_seg_m<true>(fmt, batched, grid, block, xb, offsets, num_segments, segment_len, out, ws,
-                           stream, cfg.sms);
+                           stream, cfg.sms, cfg.pdl);
     else
         launch_seg_m<false>(fmt, batched, grid, block, xb, offsets, num_segments, segment_len, out, ws,
-                            stream, cfg.sms);
+                            stream, cfg.sms, cfg.pdl);
     return cudaGetLastError();
 }
 

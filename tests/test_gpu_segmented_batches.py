@@ -189,3 +189,33 @@ def test_full_size_c5_all_outputs(tcr):
             assert bad.size == 0, (algo, (bad[:8] + j0).tolist())
         del bits
     del x
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_batched_rows_as_mma_rows(tcr, dtype):
+    """Fixed-length rows with L % 32 == 0, L <= 2048 and a 16-byte aligned x
+    take the rows-as-MMA-rows kernel (16 segments fill the 16 rows of A, the
+    row sums of Eq. 10 are the segment sums): every row vs the oracle, ragged
+    last slab (S % 16 != 0), integer data bitwise, and the same rows through
+    a misaligned x (the union-stream kernel) agree within tolerance."""
+    import torch
+
+    for L, S in ((32, 100_003), (64, 40_001), (96, 33_333), (224, 20_000), (256, 65_541),
+                 (480, 9_999), (2048, 1_029)):
+        n = L * S
+        x, bits = _gen_device(dtype, 900 + L, n, gen.UNIFORM_PM1, xoff=0)
+        assert x.data_ptr() % 16 == 0
+        out = torch.full((S,), float("nan"), dtype=torch.float32, device="cuda")
+        tcr.tcr_reduce_sum_batched_ex(x, L, out, algo="mma_sync")
+        torch.cuda.synchronize()
+        g = out.cpu().numpy()
+        ok = _oracle_ok(dtype, bits, np.arange(S + 1, dtype=np.int64) * L, g)
+        assert ok.all(), (L, np.nonzero(~ok)[0][:8].tolist())
+        if dtype == "f16":
+            xi, bi = _gen_device(dtype, 77, n, gen.SMALLINT, xoff=0)
+            tcr.tcr_reduce_sum_batched_ex(xi, L, out, algo="mma_sync")
+            torch.cuda.synchronize()
+            ss = oracle.exact_segment_sums_fp16_array(bi, np.arange(S + 1, dtype=np.int64) * L,
+                                                      threads=THREADS)
+            want = ss.rec["t_lo"].view(np.int64).astype(np.float64) * 2.0 ** -24
+            assert np.array_equal(out.cpu().numpy().astype(np.float64), want), L
