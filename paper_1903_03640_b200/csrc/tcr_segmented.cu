@@ -11,6 +11,30 @@
 
 namespace tcr {
 
+// Programmatic dependent launch (TCR_CFG_PDL), as in the streaming kernels:
+// wait for the previous kernel on the stream (its writes -- x, offsets, the
+// scheduler counters it reset -- visible), then let the next one be
+// scheduled.  No-ops for a plain launch.
+__device__ __forceinline__ void pdl_wait_and_release() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_maybe_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t stream,
+                             int pdl, Args... args) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&lc, kernel, static_cast<KArgs>(args)...);
+}
+
 constexpr unsigned long long kBatchSeg = 8;  // segments per scheduler atomic (guided)
 
 // Reduce elements [s, e) of the 16-byte-aligned array xb (element indices
@@ -51,6 +75,7 @@ template <bool kMma, int F, bool kBatched, int U, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, seg_resident<kBatched>())
 reduce_segmented_kernel(const uint8_t* __restrict__ x, const int64_t* __restrict__ offsets,
                         size_t S, size_t L, int batch, float* __restrict__ out, DevWorkspace ws) {
+    pdl_wait_and_release();
     constexpr int kLogEpv = FmtInfo<F>::kBytes == 2 ? 3 : 4;  // log2(elements per vector)
     constexpr int64_t kEpv = (int64_t)1 << kLogEpv;
     constexpr int64_t kTileEl = 32 * kEpv;                     // elements per 512-byte tile
@@ -189,6 +214,7 @@ reduce_segmented_kernel(const uint8_t* __restrict__ x, const int64_t* __restrict
 template <bool kMma, int F, int T, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 4)
 reduce_rows_kernel(const uint8_t* __restrict__ x, size_t S, float* __restrict__ out) {
+    pdl_wait_and_release();
     constexpr int R = 8 / T;  // rows per group
     const int lane = threadIdx.x & 31;
     const uint4* xv = reinterpret_cast<const uint4*>(x) + lane;
@@ -251,8 +277,7 @@ constexpr int kRsCtasPerSm = 3;  // resident CTAs per SM (<= 85 registers: no sp
 template <int F, int WARPS, int P>
 __global__ void __launch_bounds__(WARPS * 32, kRsCtasPerSm)
 reduce_rowseg_kernel(const uint8_t* __restrict__ x, size_t S, size_t L, float* __restrict__ out) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" :::);
+    pdl_wait_and_release();
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const size_t slabs = (S + 15) / 16;
     const size_t W = (size_t)gridDim.x * WARPS;
@@ -316,21 +341,13 @@ static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, cons
             const size_t gmax = (size_t)sms * (pairs >= 4 ? kRsCtasPerSm : 5);
             if (g > gmax) g = gmax;
             if (g < 1) g = 1;
-            cudaLaunchConfig_t lc{};
-            lc.gridDim = dim3((unsigned)g);
-            lc.blockDim = block;
-            lc.stream = stream;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[0].val.programmaticStreamSerializationAllowed = 1;
-            lc.attrs = at;
-            lc.numAttrs = pdl ? 1 : 0;
+            const dim3 rg((unsigned)g);
             if (pairs >= 4)
-                cudaLaunchKernelEx(&lc, reduce_rowseg_kernel<F, kSegWarps, 4>, x, S, L, out);
+                launch_maybe_pdl(reduce_rowseg_kernel<F, kSegWarps, 4>, rg, block, stream, pdl, x, S, L, out);
             else if (pairs >= 2)
-                cudaLaunchKernelEx(&lc, reduce_rowseg_kernel<F, kSegWarps, 2>, x, S, L, out);
+                launch_maybe_pdl(reduce_rowseg_kernel<F, kSegWarps, 2>, rg, block, stream, pdl, x, S, L, out);
             else
-                cudaLaunchKernelEx(&lc, reduce_rowseg_kernel<F, kSegWarps, 1>, x, S, L, out);
+                launch_maybe_pdl(reduce_rowseg_kernel<F, kSegWarps, 1>, rg, block, stream, pdl, x, S, L, out);
             return;
         }
     }
@@ -344,10 +361,10 @@ static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, cons
         if (g < 1) g = 1;
         const dim3 rgrid((unsigned)g);
         switch (L / kTileEl) {
-            case 1: reduce_rows_kernel<kMma, F, 1, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
-            case 2: reduce_rows_kernel<kMma, F, 2, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
-            case 4: reduce_rows_kernel<kMma, F, 4, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
-            default: reduce_rows_kernel<kMma, F, 8, kSegWarps><<<rgrid, block, 0, stream>>>(x, S, out); break;
+            case 1: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 1, kSegWarps>, rgrid, block, stream, pdl, x, S, out); break;
+            case 2: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 2, kSegWarps>, rgrid, block, stream, pdl, x, S, out); break;
+            case 4: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 4, kSegWarps>, rgrid, block, stream, pdl, x, S, out); break;
+            default: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 8, kSegWarps>, rgrid, block, stream, pdl, x, S, out); break;
         }
         return;
     }
@@ -359,11 +376,11 @@ static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, cons
         dim3 bgrid = grid;  // one resident wave at this kernel's occupancy
         const unsigned bmax = (unsigned)(sms * seg_resident<true>());
         if (bgrid.x > bmax) bgrid.x = bmax;
-        reduce_segmented_kernel<kMma, F, true, kSegUnroll, kSegWarps>
-            <<<bgrid, block, 0, stream>>>(x, offsets, S, L, (int)b, out, ws);
+        launch_maybe_pdl(reduce_segmented_kernel<kMma, F, true, kSegUnroll, kSegWarps>, bgrid, block,
+                         stream, pdl, x, offsets, S, L, (int)b, out, ws);
     } else {
-        reduce_segmented_kernel<kMma, F, false, kSegUnroll, kSegWarps>
-            <<<grid, block, 0, stream>>>(x, offsets, S, L, (int)kBatchSeg, out, ws);
+        launch_maybe_pdl(reduce_segmented_kernel<kMma, F, false, kSegUnroll, kSegWarps>, grid, block,
+                         stream, pdl, x, offsets, S, L, (int)kBatchSeg, out, ws);
     }
 }
 
