@@ -69,6 +69,7 @@ reduce_bulk_kernel(const uint8_t* __restrict__ x, size_t n, int stages, uint32_t
         sm100::fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait_and_release();  // PDL: no global memory before the previous kernel completes
 
     double acc = 0.0;
     if (warp == kConsumers) {  // producer warp
@@ -180,8 +181,8 @@ static cudaError_t launch_bulk_t(const uint8_t* x, size_t n, float* out_f32, dou
     const int tiles_per_warp = (int)(stage_bytes / 512 / kConsumers);
     int fe = 2 * cfg.chain / (tiles_per_warp < 1 ? 1 : tiles_per_warp);
     if (fe < 1) fe = 1;
-    reduce_bulk_kernel<F><<<(unsigned)g, kBulkWarps * 32, smem, stream>>>(
-        x, n, stages, stage_bytes, fe, out_f32, out_f64, ws);
+    launch_maybe_pdl(reduce_bulk_kernel<F>, dim3((unsigned)g), dim3(kBulkWarps * 32), smem, stream, cfg.pdl,
+                     x, n, stages, stage_bytes, fe, out_f32, out_f64, ws);
     return cudaGetLastError();
 }
 

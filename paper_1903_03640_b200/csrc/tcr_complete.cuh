@@ -16,17 +16,6 @@
 
 namespace tcr {
 
-// Completion ticket: one acq_rel atomic at GPU scope.  Release orders the
-// CTA's partial (stored by the same thread just before) ahead of the ticket;
-// acquire makes every earlier CTA's partial visible to the last one.  One
-// atomic instead of __threadfence() + atomicAdd (measured ~0.6 us less on
-// the critical path, scripts/c2_trace.cu).
-__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* t) {
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
-    return old;
-}
-
 // Level 4 in the last CTA: the G CTA partials, all WARPS warps at once.
 // Thread i adds partials i, i + T, i + 2T, ... (T = 32 * WARPS) in index
 // order with every load issued before the first add (one L2 round trip),

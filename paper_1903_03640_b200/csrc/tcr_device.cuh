@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <cuda_fp16.h>
+#include <cuda_runtime.h>
 
 namespace tcr {
 
@@ -257,6 +258,52 @@ __device__ __forceinline__ uint4 load_ragged(const uint16_t* p, int cnt, int lan
         w[k] = lo | (hi << 16);
     }
     return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// ---------------------------------------------------------------------------
+// Launch plumbing shared by the kernels (r02)
+// ---------------------------------------------------------------------------
+
+// Programmatic dependent launch (TCR_CFG_PDL): a kernel launched with the
+// programmatic-serialisation attribute may be scheduled while the previous
+// kernel on the stream drains.  griddepcontrol.wait blocks until that kernel
+// has completed and its writes (x, the workspace's partials and counters) are
+// visible; launch_dependents lets the next kernel be scheduled early in turn.
+// Both are no-ops for a plain launch.  Call before touching global memory
+// (CTA-local set-up -- barriers, TMEM allocation, SMEM tables -- may precede).
+__device__ __forceinline__ void pdl_wait_and_release() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+// Completion ticket: one acq_rel atomic at GPU scope.  Release orders the
+// CTA's partial (stored by the same thread just before) ahead of the ticket;
+// acquire makes every earlier CTA's partial visible to the last one (then
+// __syncthreads() extends that to the whole CTA).  One atomic instead of
+// __threadfence() + atomicAdd (~0.6 us less on the critical path,
+// scripts/c2_trace.cu, profiles/r02/c2_trace_ab.txt).
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* t) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+    return old;
+}
+
+// Host: launch `kernel` with the programmatic-serialisation attribute when
+// pdl != 0 (cudaLaunchKernelEx; errors surface through cudaGetLastError).
+template <typename... KArgs, typename... Args>
+static inline void launch_maybe_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                    cudaStream_t stream, int pdl, Args... args) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&lc, kernel, static_cast<KArgs>(args)...);
 }
 
 }  // namespace tcr

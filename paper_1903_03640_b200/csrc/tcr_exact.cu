@@ -248,6 +248,7 @@ reduce_exact_kernel(const uint8_t* __restrict__ x, size_t n, long long* out_acc,
                     double* out_f64, DevWorkspace ws, PeerCombine pc) {
     constexpr int ES = FmtInfo<F>::kBytes;
     constexpr int kTileBytes = 512;
+    pdl_wait_and_release();  // PDL (plain-launch no-op): the previous kernel's writes visible
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int me = pc.rank;
     if (kPeer && gridDim.y > 1) {  // emulated peer group: slice y is rank y
@@ -366,12 +367,10 @@ reduce_exact_kernel(const uint8_t* __restrict__ x, size_t n, long long* out_acc,
             p[2] = c[0];
             p[3] = c[1];
             p[4] = c[2];
-            __threadfence();
-            s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+            s_last = (ticket_acq_rel(ws.ticket) == gridDim.x - 1) ? 1u : 0u;
         }
-        __syncwarp();
+        __syncwarp();  // lane 0's acquire, then the warp's loads below
         if (!__shfl_sync(0xffffffffu, s_last, 0)) return;
-        __threadfence();
         b = 0;
         c[0] = c[1] = c[2] = 0;
         for (int i = lane; i < (int)gridDim.x; i += 32) {
@@ -446,11 +445,11 @@ static cudaError_t launch_exact_f(const uint8_t* x, size_t n, long long* out_acc
     const int g = exact_grid(n * FmtInfo<F>::kBytes / 2, cfg, ws.capacity);
     const PeerCombine none{};
     if (cfg.exact_unroll == 8)
-        reduce_exact_kernel<8, false, F><<<g, kExactWarps * 32, 0, stream>>>(
-            x, n, out_acc, out_f32, out_f64, ws, none);
+        launch_maybe_pdl(reduce_exact_kernel<8, false, F>, dim3(g), dim3(kExactWarps * 32), 0, stream,
+                         cfg.pdl, x, n, out_acc, out_f32, out_f64, ws, none);
     else
-        reduce_exact_kernel<4, false, F><<<g, kExactWarps * 32, 0, stream>>>(
-            x, n, out_acc, out_f32, out_f64, ws, none);
+        launch_maybe_pdl(reduce_exact_kernel<4, false, F>, dim3(g), dim3(kExactWarps * 32), 0, stream,
+                         cfg.pdl, x, n, out_acc, out_f32, out_f64, ws, none);
     return cudaGetLastError();
 }
 

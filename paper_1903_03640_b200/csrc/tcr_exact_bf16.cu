@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(kXbWarps * 32, 3)
 reduce_exact_bf16_kernel(const uint16_t* __restrict__ x, size_t n, long long* out_acc,
                          float* out_f32, double* out_f64, DevWorkspace ws) {
     __shared__ long long s_I[8][kXbWarps * 32];
+    pdl_wait_and_release();  // PDL (plain-launch no-op): the previous kernel's writes visible
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
 #pragma unroll
     for (int k = 0; k < 8; ++k) s_I[k][tid] = 0;
@@ -342,12 +343,10 @@ reduce_exact_bf16_kernel(const uint16_t* __restrict__ x, size_t n, long long* ou
                 p[2 * k + 1] = (long long)(win[k] >> 64);
             }
             for (int c = 0; c < 3; ++c) p[16 + c] = c3[c];
-            __threadfence();
-            s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+            s_last = (ticket_acq_rel(ws.ticket) == gridDim.x - 1) ? 1u : 0u;
         }
-        __syncwarp();
+        __syncwarp();  // lane 0's acquire, then the warp's loads below
         if (!__shfl_sync(0xffffffffu, s_last, 0)) return;
-        __threadfence();
         for (int k = 0; k < 8; ++k) {
             i128 s = 0;
             for (int i = lane; i < (int)gridDim.x; i += 32) {
@@ -400,8 +399,8 @@ cudaError_t launch_reduce_exact_bf16(const uint16_t* x, size_t n, long long* out
     if (gmax > cap) gmax = cap;
     if (g > gmax) g = gmax;
     if (g < 1) g = 1;
-    reduce_exact_bf16_kernel<<<(unsigned)g, kXbWarps * 32, 0, stream>>>(x, n, out_acc, out_f32,
-                                                                         out_f64, ws);
+    launch_maybe_pdl(reduce_exact_bf16_kernel, dim3((unsigned)g), dim3(kXbWarps * 32), 0, stream, cfg.pdl,
+                     x, n, out_acc, out_f32, out_f64, ws);
     return cudaGetLastError();
 }
 

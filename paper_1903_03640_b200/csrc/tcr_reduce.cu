@@ -76,8 +76,7 @@ reduce_stream_kernel(const uint8_t* __restrict__ x, size_t n, int flush_every, i
     // to complete (and its writes -- x, the workspace -- to be visible)
     // before touching memory, then let the next call's grid be scheduled.
     // Both are no-ops for a plain launch.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" :::);
+    pdl_wait_and_release();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int me = pc.rank;
     if (kPeer && gridDim.y > 1) {  // emulated peer group: slice y is rank y, reducing its shard
@@ -179,16 +178,10 @@ static cudaError_t launch_stream_u(const uint8_t* x, size_t n, int fe, float* ou
     const int mid = (U == 16 && 2 * cfg.chain < U) ? 1 : 0;
     if (!emulate) {
         const int g = stream_grid(n * FmtInfo<F>::kBytes / 2, cfg, stream_resident<F, U>());
-        cudaLaunchConfig_t lc{};
-        lc.gridDim = dim3(g);
-        lc.blockDim = dim3(kStreamWarps * 32);
-        lc.stream = stream;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        lc.attrs = at;
-        lc.numAttrs = (cfg.pdl && !kPeer) ? 1 : 0;  // the peer combine waits on other ranks
-        return cudaLaunchKernelEx(&lc, kernel, x, n, fe, mid, out_f32, out_f64, ws, pc);
+        // (the peer variant waits on other ranks: plain launch)
+        launch_maybe_pdl(kernel, dim3(g), dim3(kStreamWarps * 32), 0, stream, (cfg.pdl && !kPeer) ? 1 : 0,
+                         x, n, fe, mid, out_f32, out_f64, ws, pc);
+        return cudaGetLastError();
     }
     // Emulated peer group: the ranks' last CTAs wait on one another, so all
     // P grid slices must be co-resident -- a cooperative launch guarantees it

@@ -11,30 +11,6 @@
 
 namespace tcr {
 
-// Programmatic dependent launch (TCR_CFG_PDL), as in the streaming kernels:
-// wait for the previous kernel on the stream (its writes -- x, offsets, the
-// scheduler counters it reset -- visible), then let the next one be
-// scheduled.  No-ops for a plain launch.
-__device__ __forceinline__ void pdl_wait_and_release() {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" :::);
-}
-
-template <typename... KArgs, typename... Args>
-static void launch_maybe_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t stream,
-                             int pdl, Args... args) {
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = grid;
-    lc.blockDim = block;
-    lc.stream = stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    lc.attrs = at;
-    lc.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&lc, kernel, static_cast<KArgs>(args)...);
-}
-
 constexpr unsigned long long kBatchSeg = 8;  // segments per scheduler atomic (guided)
 
 // Reduce elements [s, e) of the 16-byte-aligned array xb (element indices
@@ -343,11 +319,11 @@ static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, cons
             if (g < 1) g = 1;
             const dim3 rg((unsigned)g);
             if (pairs >= 4)
-                launch_maybe_pdl(reduce_rowseg_kernel<F, kSegWarps, 4>, rg, block, stream, pdl, x, S, L, out);
+                launch_maybe_pdl(reduce_rowseg_kernel<F, kSegWarps, 4>, rg, block, 0, stream, pdl, x, S, L, out);
             else if (pairs >= 2)
-                launch_maybe_pdl(reduce_rowseg_kernel<F, kSegWarps, 2>, rg, block, stream, pdl, x, S, L, out);
+                launch_maybe_pdl(reduce_rowseg_kernel<F, kSegWarps, 2>, rg, block, 0, stream, pdl, x, S, L, out);
             else
-                launch_maybe_pdl(reduce_rowseg_kernel<F, kSegWarps, 1>, rg, block, stream, pdl, x, S, L, out);
+                launch_maybe_pdl(reduce_rowseg_kernel<F, kSegWarps, 1>, rg, block, 0, stream, pdl, x, S, L, out);
             return;
         }
     }
@@ -361,10 +337,10 @@ static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, cons
         if (g < 1) g = 1;
         const dim3 rgrid((unsigned)g);
         switch (L / kTileEl) {
-            case 1: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 1, kSegWarps>, rgrid, block, stream, pdl, x, S, out); break;
-            case 2: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 2, kSegWarps>, rgrid, block, stream, pdl, x, S, out); break;
-            case 4: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 4, kSegWarps>, rgrid, block, stream, pdl, x, S, out); break;
-            default: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 8, kSegWarps>, rgrid, block, stream, pdl, x, S, out); break;
+            case 1: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 1, kSegWarps>, rgrid, block, 0, stream, pdl, x, S, out); break;
+            case 2: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 2, kSegWarps>, rgrid, block, 0, stream, pdl, x, S, out); break;
+            case 4: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 4, kSegWarps>, rgrid, block, 0, stream, pdl, x, S, out); break;
+            default: launch_maybe_pdl(reduce_rows_kernel<kMma, F, 8, kSegWarps>, rgrid, block, 0, stream, pdl, x, S, out); break;
         }
         return;
     }
@@ -376,10 +352,10 @@ static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, cons
         dim3 bgrid = grid;  // one resident wave at this kernel's occupancy
         const unsigned bmax = (unsigned)(sms * seg_resident<true>());
         if (bgrid.x > bmax) bgrid.x = bmax;
-        launch_maybe_pdl(reduce_segmented_kernel<kMma, F, true, kSegUnroll, kSegWarps>, bgrid, block,
+        launch_maybe_pdl(reduce_segmented_kernel<kMma, F, true, kSegUnroll, kSegWarps>, bgrid, block, 0,
                          stream, pdl, x, offsets, S, L, (int)b, out, ws);
     } else {
-        launch_maybe_pdl(reduce_segmented_kernel<kMma, F, false, kSegUnroll, kSegWarps>, grid, block,
+        launch_maybe_pdl(reduce_segmented_kernel<kMma, F, false, kSegUnroll, kSegWarps>, grid, block, 0,
                          stream, pdl, x, offsets, S, L, (int)kBatchSeg, out, ws);
     }
 }

@@ -156,6 +156,9 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     TC05_EDGE(1);
+    // PDL: the CTA-local set-up above (barriers, ones tile, TMEM) overlaps the
+    // previous kernel's tail; nothing global is touched before this wait
+    pdl_wait_and_release();
 
     double acc = 0.0;
     if (warp == 0) {
@@ -354,9 +357,11 @@ cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x16, size_t n, float*
     }
     const int g = tcgen05_grid(n * (fmt >= 2 ? 1u : 2u), cfg);
     if (fmt >= 2)
-        reduce_tcgen05_kernel<true><<<g, kTcWarps * 32, smem, stream>>>(x, n, prm, out_f32, out_f64, ws);
+        launch_maybe_pdl(reduce_tcgen05_kernel<true>, dim3(g), dim3(kTcWarps * 32), smem, stream, cfg.pdl,
+                         x, n, prm, out_f32, out_f64, ws);
     else
-        reduce_tcgen05_kernel<false><<<g, kTcWarps * 32, smem, stream>>>(x, n, prm, out_f32, out_f64, ws);
+        launch_maybe_pdl(reduce_tcgen05_kernel<false>, dim3(g), dim3(kTcWarps * 32), smem, stream, cfg.pdl,
+                         x, n, prm, out_f32, out_f64, ws);
     return cudaGetLastError();
 }
 

@@ -95,6 +95,9 @@ def test_config_validation():
     with pytest.raises(tcr.TcrError):
         tcr.tcr_set_config(tcr.TCR_CFG_TC05_STAGE_KB, 6)
     assert tcr.tcr_get_config(99) == -1
+    assert tcr.tcr_get_config(tcr.TCR_CFG_PDL) == 1  # programmatic dependent launch on by default
+    with pytest.raises(tcr.TcrError):
+        tcr.tcr_set_config(tcr.TCR_CFG_PDL, 2)
 
 
 def test_product_path_does_not_import_oracle():
