@@ -422,11 +422,14 @@ typedef enum {
     TCR_CFG_BULK_CTAS_PER_SM = 16, /* bulk kernel: CTAs per SM (clamped by SMEM) */
     TCR_CFG_PEER_TIMEOUT_MS = 17,  /* fused peer combine: bound on the wait for the
                                      peers' partials (default 10000 ms)          */
-    TCR_CFG_PDL = 18              /* 1 (default): the streaming kernels are launched with
-                                   * programmatic dependent launch -- a call's CTAs are
-                                   * scheduled while the previous kernel on the stream
-                                   * drains and wait (griddepcontrol.wait) for its
-                                   * completion before touching memory; 0: plain launch */
+    TCR_CFG_PDL = 18              /* 1 (default): the reduction kernels (streaming,
+                                   * tcgen05, bulk, exact, segmented / batched) are
+                                   * launched with programmatic dependent launch -- a
+                                   * call's CTAs are scheduled while the previous kernel
+                                   * on the stream drains and wait (griddepcontrol.wait)
+                                   * for its completion before touching global memory;
+                                   * results are bitwise identical either way (the fused
+                                   * peer kernels always launch plainly); 0: plain launch */
 } tcr_config_key;
 tcr_status tcr_set_config(tcr_config_key key, int value);
 int tcr_get_config(tcr_config_key key); /* -1 for an unknown key */

@@ -248,7 +248,9 @@ reduce_exact_kernel(const uint8_t* __restrict__ x, size_t n, long long* out_acc,
                     double* out_f64, DevWorkspace ws, PeerCombine pc) {
     constexpr int ES = FmtInfo<F>::kBytes;
     constexpr int kTileBytes = 512;
-    pdl_wait_and_release();  // PDL (plain-launch no-op): the previous kernel's writes visible
+    // PDL (plain-launch no-op): the previous kernel's writes visible.  The
+    // peer variant always launches plainly (it waits on other ranks).
+    if constexpr (!kPeer) pdl_wait_and_release();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int me = pc.rank;
     if (kPeer && gridDim.y > 1) {  // emulated peer group: slice y is rank y
@@ -367,10 +369,16 @@ reduce_exact_kernel(const uint8_t* __restrict__ x, size_t n, long long* out_acc,
             p[2] = c[0];
             p[3] = c[1];
             p[4] = c[2];
-            s_last = (ticket_acq_rel(ws.ticket) == gridDim.x - 1) ? 1u : 0u;
+            if constexpr (kPeer) {  // fence + relaxed ticket: no spill in the peer variant
+                __threadfence();
+                s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+            } else {
+                s_last = (ticket_acq_rel(ws.ticket) == gridDim.x - 1) ? 1u : 0u;
+            }
         }
         __syncwarp();  // lane 0's acquire, then the warp's loads below
         if (!__shfl_sync(0xffffffffu, s_last, 0)) return;
+        if constexpr (kPeer) __threadfence();
         b = 0;
         c[0] = c[1] = c[2] = 0;
         for (int i = lane; i < (int)gridDim.x; i += 32) {
