@@ -183,28 +183,44 @@ def cpu_oracle_leg(bits_sample, threads: int, want_sum: bool = False):
     return bits_sample.size / dt / 1e9, dt
 
 
+def c3c4_workload(world: int, n_total: int, dtype: str, weak: bool) -> str:
+    """config.workload of the flat reduction lines (both arms use it): C3 at
+    N = 1, C4 (sharded) at N > 1."""
+    lg = n_total.bit_length() - 1
+    lgs = f"2^{lg}" if n_total == 1 << lg else str(n_total)
+    if world == 1:
+        return f"c3: sum of n={lgs} {dtype} uniform[-1,1] on one GPU"
+    return (f"c4: sharded sum, n={lgs} {dtype} uniform[-1,1] over {world} GPUs "
+            f"({'weak: fixed per rank' if weak else 'strong: fixed global n'})")
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle on the box's host cores (tier rule: the
-    reference arm is the oracle).  Rank 0 only; other ranks exit without work."""
+    reference arm is the oracle), on the same workload as our arm's line for
+    this N: C3 (2^30) at N = 1, C4 (the whole 2^33 array, seed C4) at N > 1;
+    every step reduces all of it.  Rank 0 only; other ranks exit without
+    work."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     import numpy as np
 
     import tcr_inputs as gen
 
-    # the same workload as our arm's N = 1 line (C3: all 2^30 elements per
-    # step; --n-total overrides, e.g. for tests); generated on the host in
-    # parallel chunks (untimed)
+    # generated on the host in parallel chunks (untimed)
     from concurrent.futures import ThreadPoolExecutor
 
-    sample = args.n_total if args.n_total is not None else N_C3
+    weak = args.n_per_rank is not None
+    sample = (args.n_per_rank * world if weak else
+              args.n_total if args.n_total is not None else (N_C3 if world == 1 else N_C4))
+    seed = gen.SEED_C3 if world == 1 else gen.SEED_C4
     threads = _cpu_count()
     bits = np.empty(sample, dtype=np.uint16)
     step = 1 << 22
 
     def fill(lo):
-        bits[lo:lo + step] = gen.generate(gen.SEED_C3, lo, min(step, sample - lo), gen.UNIFORM_PM1)
+        bits[lo:lo + step] = gen.generate(seed, lo, min(step, sample - lo), gen.UNIFORM_PM1)
 
     with ThreadPoolExecutor(max_workers=threads) as ex:
         list(ex.map(fill, range(0, sample, step)))
@@ -216,13 +232,13 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gelem/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 and not weak else "weak",
         "vs_baseline": None, "dtype": "int128", "data": "synthetic",
-        "config": {"workload": ("c3: sum of n=2^30 f16 uniform[-1,1] on one GPU"
-                                if sample == N_C3 else f"c3 stream, n={sample}"),
+        "config": {"workload": c3c4_workload(world, sample, "f16", weak),
                    "sample_elems_per_step": sample, "n_total": sample},
         "cpu_baseline": {"value": value, "unit": "Gelem/s", "cores": threads, "kind": "oracle",
-                         "sample": f"all {sample} elements of the c3 workload per step, "
+                         "sample": f"all {sample} elements of the workload per step, "
                                    f"exact int128 oracle, {threads} threads", **_host_info()},
         "e2e": {"value": value, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -538,11 +554,7 @@ def main():
         elems_per_step = n
         job_elems_per_step = n_total
         job_bytes_per_step = x.element_size() * n_total
-        lg = n_total.bit_length() - 1
-        lgs = f"2^{lg}" if n_total == 1 << lg else str(n_total)
-        workload = (f"c3: sum of n={lgs} {args.dtype} uniform[-1,1] on one GPU" if world == 1 else
-                    f"c4: sharded sum, n={lgs} {args.dtype} uniform[-1,1] over {world} GPUs "
-                    f"({'weak: fixed per rank' if weak else 'strong: fixed global n'})")
+        workload = c3c4_workload(world, n_total, args.dtype, weak)
     else:
         from paper_1903_03640_b200.sharded import segment_shard
 
