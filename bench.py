@@ -731,9 +731,6 @@ def main():
     achieved = bytes_per_step / (kern_ms * 1e-3) / 1e9              # GB/s of the dominant kernel
     if args.algo != "default":
         algo_name = args.algo
-    elif args.dtype in ("e4m3", "e5m2") and peer is None:
-        # the library's DEFAULT for fp8: kind::f8f6f4 from 2^26 elements, mma.sync below
-        algo_name = "tcgen05" if n >= (1 << 26) else "mma_sync"
     else:
         algo_name = {1: "mma_sync", 2: "tcgen05", 3: "shuffle", 4: "bulk"}[
             tcr.tcr_get_config(tcr.TCR_CFG_DEFAULT_ALGO)]

@@ -94,12 +94,11 @@ typedef enum {
     TCR_DTYPE_F16 = 0,  /* IEEE-754 binary16 (the north star)                */
     TCR_DTYPE_BF16 = 1, /* bfloat16: the same MMA encoding with .bf16 / kind::f16-BF16
                            operands and B = bfloat16 ones                    */
-    TCR_DTYPE_E4M3 = 2, /* OCP fp8 E4M3FN (1 byte): tcgen05 kind::f8f6f4 (the
-                           default for fp8 from 2^26 elements, B = fp8 ones) or
-                           mma.sync: each 512-element tile is converted exactly
-                           to binary16 and reduced as two m16n8k16 against
-                           binary16 ones (what sm_100a runs for m16n8k32 .e4m3;
-                           the default below 2^26) */
+    TCR_DTYPE_E4M3 = 2, /* OCP fp8 E4M3FN (1 byte): mma.sync (the default): each
+                           512-element tile is converted exactly to binary16 and
+                           reduced as two m16n8k16 against binary16 ones (what
+                           sm_100a runs for m16n8k32 .e4m3); or tcgen05
+                           kind::f8f6f4 with B = fp8 ones */
     TCR_DTYPE_E5M2 = 3  /* OCP fp8 E5M2 (1 byte), as E4M3                     */
 } tcr_dtype;
 

@@ -202,13 +202,12 @@ tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_
         return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
     if (algo == TCR_ALGO_DEFAULT) {
         std::lock_guard<std::mutex> lk(g_cfg_mu);
-        // fp8: mma.sync .e4m3/.e5m2 is converted to fp16 HMMAs on sm_100a; the
-        // native fp8 tensor path is tcgen05 kind::f8f6f4, measured fastest at
-        // large n but latency-heavy below 64 MiB (per-CTA TMEM / barrier
-        // set-up), where mma.sync with the auto unroll wins
-        // (scripts/runs/fp8_small.py: 2^24 elements 5.1 vs 11.1 us)
-        algo = fmt >= 2 ? (n < ((size_t)1 << 26) ? TCR_ALGO_MMA_SYNC : TCR_ALGO_TCGEN05)
-                        : g_cfg.default_algo;
+        // every format takes TCR_CFG_DEFAULT_ALGO (mma.sync).  fp8 used to
+        // take tcgen05 kind::f8f6f4 from 2^26 elements; since fp8 tiles run as
+        // exact binary16 conversions + two m16n8k16 (r02) mma.sync is at least
+        // as fast at every size (2^28: 6.41 vs 6.01 TB/s, 2^31: 7.20 vs 7.18;
+        // profiles/r02/fp8_default.txt)
+        algo = g_cfg.default_algo;
     }
     if (algo < TCR_ALGO_MMA_SYNC || algo > TCR_ALGO_BULK_MMA)
         return fail(TCR_ERR_INVALID_VALUE, "unknown algo");
@@ -442,12 +441,8 @@ static tcr_status reduce_host_impl(const void* x, size_t n, int fmt, float* out,
             (e = cudaStreamWaitEvent(stream, ws->copied[b], 0)))
             return cuda_fail(e, "event ordering (copied)");
         const uint16_t* db = static_cast<const uint16_t*>(buf);
-        // the type's default algorithm (reduce_impl's rule): fp8 takes
-        // tcgen05 kind::f8f6f4 from 2^26 elements, mma.sync below; binary16
-        // / bfloat16 take TCR_CFG_DEFAULT_ALGO
-        const int a = fmt >= TCR_DTYPE_E4M3
-                          ? (cnt >= ((size_t)1 << 26) ? TCR_ALGO_TCGEN05 : TCR_ALGO_MMA_SYNC)
-                          : algo;
+        // the default algorithm (reduce_impl's rule: TCR_CFG_DEFAULT_ALGO)
+        const int a = algo;
         if (a == TCR_ALGO_TCGEN05)
             e = tcr::launch_reduce_tcgen05(fmt, db, cnt, nullptr, ws->chunk_partials + c, ws->dev,
                                            cfg, stream);
