@@ -392,6 +392,8 @@ def one_gpu_c4_time(args, rank, n_total, algo, dev, gen, torch, tcr):
     launches between CUDA events).  Other ranks return None."""
     if rank != 0:
         return None
+    if args.dtype != "f16":
+        return {"skipped": "binary16 (C4) only"}
     free, _ = torch.cuda.mem_get_info(dev)
     if 2 * n_total > free * 0.9:
         return {"skipped": f"needs {2 * n_total} B, {free} B free"}
