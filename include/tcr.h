@@ -409,7 +409,9 @@ typedef enum {
     TCR_CFG_TC05_SLOTS = 6,       /* tcgen05: independent TMEM accumulators per
                                      buffer (1, 2, 4, 8, 16)                    */
     TCR_CFG_TC05_CHAIN = 7,       /* tcgen05: MMAs carried per accumulator (K) */
-    TCR_CFG_TC05_CTAS_PER_SM = 8, /* tcgen05: CTAs per SM (1..4)              */
+    TCR_CFG_TC05_CTAS_PER_SM = 8, /* tcgen05: CTAs per SM (1..4); 0 (default) =
+                                   * auto: 1 from 256 MiB of input, else 3 with
+                                   * <= 2 stages each                          */
     TCR_CFG_TC05_PREFETCH = 9,    /* tcgen05: L2 prefetch distance in chunks (0 = off) */
     TCR_CFG_TC05_SPLIT = 10,      /* tcgen05: bulk copies per stage (1, 2, 4, 8) */
     TCR_CFG_TC05_INTERLEAVE = 11, /* tcgen05: 0 = each CTA streams a contiguous run

@@ -37,11 +37,13 @@ struct Config {
     int blocks_per_sm = 8;
     int unroll = 0;       // 0 = auto: 16 below 2^26 elements, 4 above
     int chain = 4;        // carried chain K (tiles per fp32 accumulator before a flush)
+    // tcgen05 (r02): 4 x 32 KiB stages, 4 accumulators with chain 2 = one
+    // round per stage (the tight issue loop), CTAs per SM by size (0 = auto)
     int tc05_stages = 4;
-    int tc05_stage_kb = 16;
+    int tc05_stage_kb = 32;
     int tc05_slots = 4;
-    int tc05_chain = 4;
-    int tc05_ctas = 3;
+    int tc05_chain = 2;
+    int tc05_ctas = 0;
     int tc05_prefetch = 0;
     int tc05_split = 1;
     int tc05_interleave = 0;
@@ -754,7 +756,7 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             g_cfg.tc05_chain = value;
             return TCR_OK;
         case TCR_CFG_TC05_CTAS_PER_SM:
-            if (value < 1 || value > 4) break;
+            if (value < 0 || value > 4) break;  // 0 = auto by input size
             g_cfg.tc05_ctas = value;
             return TCR_OK;
         case TCR_CFG_TC05_PREFETCH:

@@ -49,7 +49,7 @@ namespace tcr {
 // Diagnostic timeline of CTA 0 (scripts/tc05_trace.cu compiles this file with
 // -DTCR_TC05_TRACE): [0] producer issues chunk i, [1] MMA thread sees chunk i
 // full, [2] MMA thread committed chunk i, [3] epilogue sees round r full.
-__device__ unsigned long long g_tc05_trace[4][4096];
+__device__ unsigned long long g_tc05_trace[6][4096];  // [4] each MMA issued, [5] tempty seen
 __device__ __forceinline__ unsigned long long tc05_now() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -101,7 +101,15 @@ struct Tc05Params {
 // between neighbours), each accumulator carries `chain` tiles (bounded
 // truncation, reading G10), and the epilogue drains one buffer per round
 // while the tensor core fills the other.
-template <bool kF8>
+// KM > 0 (r02): one accumulator round per SMEM stage -- KM MMAs per stage
+// over 4 accumulators (chain KM / 4) -- and a tight, fully unrolled issue
+// loop: the issuing thread waits full[s] and tempty[buf] once per stage, issues
+// the KM MMAs with compile-time descriptor / TMEM offsets and commits twice.
+// The generic loop (KM = 0) spent ~190 ns of issuing-thread time per MMA on
+// its per-MMA bookkeeping (scripts/tc05_trace.cu: MMA issue gap, r02), against
+// ~37 ns for a bare issue loop (scripts/tc05_floor.cu) -- which is why r01
+// needed three CTAs (three issuers) per SM.
+template <bool kF8, int KM>
 __global__ void __launch_bounds__(kTcWarps * 32)
 reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, float* out_f32,
                       double* out_f64, DevWorkspace ws) {
@@ -187,6 +195,42 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
             }
         }
         __syncwarp();
+    } else if (KM > 0 && warp == 1) {
+        if (lane == 0 && nchunks > 0) {  // MMA issuer, one round per stage (tight loop)
+            const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
+            const uint64_t adesc0 = sm100::smem_desc_kmajor(sm100::smem_addr(ring), 128, 256);
+            const uint64_t stage_step = stage_bytes >> 4;
+            constexpr uint64_t kTileStep = kTileBytes >> 4;
+            int s = 0, buf = 0;
+            uint32_t ph = 0, use = 0;
+            for (int i = 0; i < nchunks; ++i) {
+                sm100::mbar_wait(&full[s], ph);
+                sm100::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);  // drained two rounds ago
+                TC05_TRACE(1, i);
+                sm100::tc_fence_after();
+                const uint64_t a = adesc0 + (uint64_t)s * stage_step;
+                const uint32_t d = tmem + (uint32_t)buf * (4u * kSlotCols);
+#pragma unroll
+                for (int k = 0; k < (KM > 0 ? KM : 1); ++k) {
+                    if constexpr (kF8)
+                        sm100::mma_f8_ss(d + (uint32_t)(k & 3) * kSlotCols, a + (uint64_t)k * kTileStep,
+                                         bdesc, prm.idesc, k >= 4 ? 1u : 0u);
+                    else
+                        sm100::mma_f16_ss(d + (uint32_t)(k & 3) * kSlotCols, a + (uint64_t)k * kTileStep,
+                                          bdesc, prm.idesc, k >= 4 ? 1u : 0u);
+                }
+                sm100::mma_commit(&tfull[buf]);  // this round's accumulators, once complete
+                sm100::mma_commit(&empty[s]);    // SMEM stage free once these MMAs complete
+                TC05_TRACE(2, i);
+                if (buf) ++use;
+                buf ^= 1;
+                if (++s == stages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+        __syncwarp();
     } else if (warp == 1) {
         if (lane == 0 && nchunks > 0) {  // MMA issuer
             const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
@@ -208,6 +252,7 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
                     if (pos == 0) {  // buffer drained by the epilogue two rounds ago?
                         sm100::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
                         sm100::tc_fence_after();
+                        TC05_TRACE(5, (int)((total_mma - left) / per_round));
                     }
                     const uint32_t d = tmem + (uint32_t)buf * buf_cols +
                                        ((uint32_t)pos & last_slot) * kSlotCols;
@@ -215,6 +260,7 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
                         sm100::mma_f8_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
                     else
                         sm100::mma_f16_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
+                    TC05_TRACE(4, (int)(total_mma - left));
                     --left;
                     if (++pos == per_round || left == 0) {
                         sm100::mma_commit(&tfull[buf]);
@@ -315,10 +361,30 @@ int tcgen05_grid(size_t nbytes, const LaunchCfg& cfg) {
     return g < 1 ? 1 : (int)g;
 }
 
+// TCR_CFG_TC05_CTAS_PER_SM = 0 (auto, the default since r02): one CTA (one
+// issuer) per SM with the configured ring from 256 MiB of input, where the
+// tight issue loop keeps up with HBM alone; below, three CTAs per SM with at
+// most two stages each, so that a short input is spread over three times as
+// many independent pipelines (profiles/r02/tc05_commit_sweep.txt: 2^24 warm
+// 7.5 -> 6.8 us).
+static LaunchCfg tc05_effective(size_t nbytes, const LaunchCfg& cfg) {
+    LaunchCfg c = cfg;
+    if (c.tc05_ctas == 0) {
+        if (nbytes >= ((size_t)256 << 20)) {
+            c.tc05_ctas = 1;
+        } else {
+            c.tc05_ctas = 3;
+            if (c.tc05_stages > 2) c.tc05_stages = 2;
+        }
+    }
+    return c;
+}
+
 cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x16, size_t n, float* out_f32,
-                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg_in,
                                   cudaStream_t stream) {
     const uint8_t* x = reinterpret_cast<const uint8_t*>(x16);
+    const LaunchCfg cfg = tc05_effective(n * (fmt >= 2 ? 1u : 2u), cfg_in);
     Tc05Params prm;
     prm.fmt = fmt;
     // kind::f16: a/b_format F16 = 0, BF16 = 1; kind::f8f6f4: E4M3 = 0, E5M2 = 1 (bits 7-9, 10-12)
@@ -347,21 +413,38 @@ cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x16, size_t n, float*
         static std::map<int, size_t> configured;
         std::lock_guard<std::mutex> lk(mu);
         if (smem > configured[dev]) {
-            if ((e = cudaFuncSetAttribute(reduce_tcgen05_kernel<false>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) ||
-                (e = cudaFuncSetAttribute(reduce_tcgen05_kernel<true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
-                return e;
+            const void* fns[8] = {(const void*)reduce_tcgen05_kernel<false, 0>,
+                                  (const void*)reduce_tcgen05_kernel<true, 0>,
+                                  (const void*)reduce_tcgen05_kernel<false, 4>,
+                                  (const void*)reduce_tcgen05_kernel<true, 4>,
+                                  (const void*)reduce_tcgen05_kernel<false, 8>,
+                                  (const void*)reduce_tcgen05_kernel<true, 8>,
+                                  (const void*)reduce_tcgen05_kernel<false, 16>,
+                                  (const void*)reduce_tcgen05_kernel<true, 16>};
+            for (const void* f : fns)
+                if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+                    return e;
             configured[dev] = smem;
         }
     }
     const int g = tcgen05_grid(n * (fmt >= 2 ? 1u : 2u), cfg);
-    if (fmt >= 2)
-        launch_maybe_pdl(reduce_tcgen05_kernel<true>, dim3(g), dim3(kTcWarps * 32), smem, stream, cfg.pdl,
-                         x, n, prm, out_f32, out_f64, ws);
-    else
-        launch_maybe_pdl(reduce_tcgen05_kernel<false>, dim3(g), dim3(kTcWarps * 32), smem, stream, cfg.pdl,
-                         x, n, prm, out_f32, out_f64, ws);
+    // one accumulator round per stage (4 slots, chain = MMAs per stage / 4):
+    // the tight issue loop, instantiated for 4, 8 and 16 MMAs per stage
+    const int kmma = (int)(prm.stage_bytes / kTileBytes);
+    const int km = (prm.slots == 4 && prm.slots * prm.chain == kmma &&
+                    (kmma == 4 || kmma == 8 || kmma == 16)) ? kmma : 0;
+    const dim3 grid(g), block(kTcWarps * 32);
+#define TCR_TC05_LAUNCH(F8, K)                                                                   \
+    launch_maybe_pdl(reduce_tcgen05_kernel<F8, K>, grid, block, smem, stream, cfg.pdl, x, n, prm, \
+                     out_f32, out_f64, ws)
+    const bool f8 = fmt >= 2;
+    switch (km) {
+        case 4: if (f8) TCR_TC05_LAUNCH(true, 4); else TCR_TC05_LAUNCH(false, 4); break;
+        case 8: if (f8) TCR_TC05_LAUNCH(true, 8); else TCR_TC05_LAUNCH(false, 8); break;
+        case 16: if (f8) TCR_TC05_LAUNCH(true, 16); else TCR_TC05_LAUNCH(false, 16); break;
+        default: if (f8) TCR_TC05_LAUNCH(true, 0); else TCR_TC05_LAUNCH(false, 0); break;
+    }
+#undef TCR_TC05_LAUNCH
     return cudaGetLastError();
 }
 

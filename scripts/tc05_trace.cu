@@ -49,7 +49,7 @@ int main(int argc, char** argv) {
     printf("cfg stages=%d kb=%d slots=%d chain=%d ctas=%d: %.1f us, %.1f GB/s\n", cfg.tc05_stages,
            cfg.tc05_stage_kb, cfg.tc05_slots, cfg.tc05_chain, cfg.tc05_ctas, ms * 1e3,
            n * 2 / (ms * 1e-3) / 1e9);
-    static unsigned long long tr[4][4096];
+    static unsigned long long tr[6][4096];
     cudaMemcpyFromSymbol(tr, tcr::g_tc05_trace, sizeof(tr));
     const int nch = (int)((n * 2 / (cfg.tc05_stage_kb * 1024)) / (cfg.sms * cfg.tc05_ctas));
     const int m = std::min(nch, 4096);
@@ -77,6 +77,13 @@ int main(int argc, char** argv) {
     printf("epilogue rounds (ns): ");
     for (int r = 0; r < 12; ++r) printf("%llu ", tr[3][r] - t0);
     printf("\nlast chunk committed at %llu ns\n", tr[2][m - 1] - t0);
+    printf("MMA issue times (ns from first issue), first 40: ");
+    for (int i = 0; i < 40; ++i) printf("%llu ", tr[4][i] - t0);
+    printf("\ntempty seen per round, first 12: ");
+    for (int r = 0; r < 12; ++r) printf("%llu ", tr[5][r] - t0);
+    std::vector<double> mg;
+    for (int i = 1; i < 4000; ++i) mg.push_back((double)(tr[4][i] - tr[4][i - 1]));
+    printf("\nMMA issue gap p10 %.0f p50 %.0f p90 %.0f ns\n", pct(mg, .1), pct(mg, .5), pct(mg, .9));
     // per-CTA phase edges of the last launch, relative to the earliest entry
     static unsigned long long ed[10][2048];
     cudaMemcpyFromSymbol(ed, tcr::g_tc05_edges, sizeof(ed));

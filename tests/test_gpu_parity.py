@@ -172,6 +172,7 @@ def test_config_knobs(tcr):
     bits = gen.generate(31, 0, (1 << 23) + 77, gen.UNIFORM_01)
     es = oracle.exact_sum_fp16(bits, threads=4)
     x = _dev(bits, 1)
+    saved = {k: tcr.tcr_get_config(k) for k in range(0, 19)}
     try:
         for unroll in (0, 4, 8, 16):
             for bps in (1, 2, 4, 8):
@@ -192,7 +193,10 @@ def test_config_knobs(tcr):
             assert oracle.within_tolerance(g, es), (stages, kb, g, es.f64())
         tc_knobs = [  # (stages, kb, slots, chain, ctas, prefetch, split)
             (8, 16, 1, 4, 1, 0, 1), (8, 16, 2, 1, 1, 0, 2), (8, 16, 16, 4, 1, 8, 4),
-            (6, 16, 8, 4, 2, 0, 1), (3, 64, 16, 2, 1, 4, 8), (4, 32, 4, 3, 2, 2, 1)]
+            (6, 16, 8, 4, 2, 0, 1), (3, 64, 16, 2, 1, 4, 8), (4, 32, 4, 3, 2, 2, 1),
+            # one accumulator round per stage (the tight issue loop, r02), incl. auto CTAs
+            (4, 32, 4, 2, 0, 0, 1), (4, 32, 4, 2, 1, 2, 2), (2, 64, 4, 4, 1, 0, 4),
+            (4, 16, 4, 1, 3, 0, 1), (2, 32, 4, 2, 3, 1, 1), (3, 64, 4, 4, 0, 0, 8)]
         for st, kb, sl, ch, ct, pf, sp in tc_knobs:
             for key, val in ((tcr.TCR_CFG_TC05_STAGES, st), (tcr.TCR_CFG_TC05_STAGE_KB, kb),
                              (tcr.TCR_CFG_TC05_SLOTS, sl), (tcr.TCR_CFG_TC05_CHAIN, ch),
@@ -214,16 +218,9 @@ def test_config_knobs(tcr):
             assert oracle.within_tolerance(g, es), (st, kb, ct, ch, g, es.f64())
             assert g == _reduce(tcr, x, "bulk")
     finally:
-        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 0)
-        tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 8)
-        tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
-        for key, val in ((tcr.TCR_CFG_BULK_STAGES, 6), (tcr.TCR_CFG_BULK_STAGE_KB, 16),
-                         (tcr.TCR_CFG_BULK_CTAS_PER_SM, 2), (tcr.TCR_CFG_CHAIN, 4),
-                         (tcr.TCR_CFG_TC05_STAGES, 4), (tcr.TCR_CFG_TC05_STAGE_KB, 16),
-                         (tcr.TCR_CFG_TC05_SLOTS, 4), (tcr.TCR_CFG_TC05_CHAIN, 4),
-                         (tcr.TCR_CFG_TC05_CTAS_PER_SM, 3), (tcr.TCR_CFG_TC05_PREFETCH, 0),
-                         (tcr.TCR_CFG_TC05_SPLIT, 1)):
-            tcr.tcr_set_config(key, val)
+        for key, val in saved.items():
+            if val >= 0:
+                tcr.tcr_set_config(key, val)
 
 
 def test_two_streams_concurrently(tcr):

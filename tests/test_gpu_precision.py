@@ -39,6 +39,8 @@ def test_precision_vs_chain_length():
     o64 = torch.empty(1, dtype=torch.float64, device="cuda")
     # few CTAs so that each carried chain really runs K tiles (at full
     # occupancy every warp sees only ~n/2^21 tiles)
+    saved = {k: tcr.tcr_get_config(k) for k in (tcr.TCR_CFG_BLOCKS_PER_SM, tcr.TCR_CFG_TC05_CTAS_PER_SM,
+                                                 tcr.TCR_CFG_CHAIN, tcr.TCR_CFG_UNROLL, tcr.TCR_CFG_TC05_CHAIN)}
     tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 1)
     tcr.tcr_set_config(tcr.TCR_CFG_TC05_CTAS_PER_SM, 1)
     try:
@@ -57,20 +59,19 @@ def test_precision_vs_chain_length():
                                  "err_f64_units": _err_units(float(o64.item()), es),
                                  "err_f32_units": _err_units(float(o32.item()), es)})
             tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
-            for K in (1, 4, 16, 64, 256):
+            # K = 2 with 4 slots and 32 KiB stages is the default (one round per
+            # stage, the tight issue loop); the others take the generic loop
+            for K in (1, 2, 4, 16, 64, 256):
                 tcr.tcr_set_config(tcr.TCR_CFG_TC05_CHAIN, K)
                 tcr.tcr_reduce_sum_algo(x, out_f32=o32, out_f64=o64, algo="tcgen05")
                 torch.cuda.synchronize()
                 rows.append({"dist": dname, "algo": "tcgen05", "K": K,
                              "err_f64_units": _err_units(float(o64.item()), es),
                              "err_f32_units": _err_units(float(o32.item()), es)})
-            tcr.tcr_set_config(tcr.TCR_CFG_TC05_CHAIN, 4)
+            tcr.tcr_set_config(tcr.TCR_CFG_TC05_CHAIN, saved[tcr.TCR_CFG_TC05_CHAIN])
     finally:
-        tcr.tcr_set_config(tcr.TCR_CFG_BLOCKS_PER_SM, 8)
-        tcr.tcr_set_config(tcr.TCR_CFG_TC05_CTAS_PER_SM, 3)
-        tcr.tcr_set_config(tcr.TCR_CFG_CHAIN, 4)
-        tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 0)
-        tcr.tcr_set_config(tcr.TCR_CFG_TC05_CHAIN, 4)
+        for k, v in saved.items():
+            tcr.tcr_set_config(k, v)
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/precision.json", "w") as f:
         json.dump({"n": n, "unit": "2^-24 * sum|x|", "rows": rows}, f, indent=1)
