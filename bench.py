@@ -733,9 +733,11 @@ def main():
     achieved = bytes_per_step / (kern_ms * 1e-3) / 1e9              # GB/s of the dominant kernel
     if args.algo != "default":
         algo_name = args.algo
-    else:
+    elif peer is not None or args.workload == "c5":
+        algo_name = "mma_sync"  # the fused peer kernel / the segmented MMA kernels
+    else:  # what TCR_ALGO_DEFAULT resolved to for this rank's input size
         algo_name = {1: "mma_sync", 2: "tcgen05", 3: "shuffle", 4: "bulk"}[
-            tcr.tcr_get_config(tcr.TCR_CFG_DEFAULT_ALGO)]
+            tcr.tcr_default_algo(n, dtype_code)]
 
     cpu, check, t1 = None, None, None
     if not args.no_cpu_baseline:

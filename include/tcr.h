@@ -80,7 +80,10 @@ typedef enum {
 
 /* Kernel selection for tcr_reduce_sum_algo / the _config default. */
 typedef enum {
-    TCR_ALGO_DEFAULT = 0, /* the library's fastest MMA-encoded kernel        */
+    TCR_ALGO_DEFAULT = 0, /* the library's fastest MMA-encoded kernel for the
+                             input's size (TCR_CFG_DEFAULT_ALGO; auto: tcgen05
+                             from 1 GiB of input, mma.sync below -- see
+                             tcr_default_algo)                               */
     TCR_ALGO_MMA_SYNC = 1, /* mma.sync m16n8k16 (A from 128-bit loads)       */
     TCR_ALGO_TCGEN05 = 2, /* cp.async.bulk -> SMEM -> tcgen05.mma, D in TMEM */
     TCR_ALGO_SHUFFLE = 3, /* classic comparison path (§II): fp32
@@ -395,7 +398,10 @@ tcr_status tcr_probe_collapse(const double *in, double *out, tcr_algo algo, tcr_
 
 /* Tuning knobs (process-wide; defaults are the measured best on B200). */
 typedef enum {
-    TCR_CFG_DEFAULT_ALGO = 0,     /* tcr_algo used by tcr_reduce_sum        */
+    TCR_CFG_DEFAULT_ALGO = 0,     /* tcr_algo used by tcr_reduce_sum; 0 (the
+                                   * default) = auto by input size: tcgen05 from
+                                   * 1 GiB, mma.sync below (r02 measurements,
+                                   * DESIGN.md §15.5)                          */
     TCR_CFG_BLOCKS_PER_SM = 1,    /* CTAs per SM of the streaming kernels   */
     TCR_CFG_UNROLL = 2,           /* 16-byte loads in flight per lane (mma.sync/shuffle):
                                      4, 8, 16, or 0 = auto (default: 16 below
@@ -439,6 +445,9 @@ const char *tcr_status_string(tcr_status s);
 const char *tcr_last_error(void);        /* thread-local detail of the last error */
 tcr_status tcr_release_workspaces(void); /* caller guarantees no in-flight work   */
 uint64_t tcr_launch_count(void);         /* kernels launched by this library so far */
+/* The kernel TCR_ALGO_DEFAULT resolves to for n elements of `dtype` under the
+ * current configuration (never TCR_ALGO_DEFAULT); no device work. */
+tcr_algo tcr_default_algo(size_t n, tcr_dtype dtype);
 int tcr_version(void);
 
 #ifdef __cplusplus

@@ -140,6 +140,8 @@ _lib.tcr_last_error.argtypes = []
 _lib.tcr_last_error.restype = ctypes.c_char_p
 _lib.tcr_launch_count.argtypes = []
 _lib.tcr_launch_count.restype = ctypes.c_uint64
+_lib.tcr_default_algo.argtypes = [_SZ, _I]
+_lib.tcr_default_algo.restype = ctypes.c_int
 _lib.tcr_version.argtypes = []
 _lib.tcr_version.restype = ctypes.c_int
 
@@ -519,6 +521,11 @@ def tcr_get_config(key: int) -> int:
 
 def tcr_launch_count() -> int:
     return int(_lib.tcr_launch_count())
+
+
+def tcr_default_algo(n: int, dtype: int = TCR_DTYPE_F16) -> int:
+    """The kernel TCR_ALGO_DEFAULT resolves to for n elements of dtype."""
+    return int(_lib.tcr_default_algo(int(n), int(dtype)))
 
 
 def tcr_release_workspaces() -> None:

@@ -33,7 +33,9 @@ std::atomic<uint64_t> g_launches{0};
 
 struct Config {
     // Defaults = the measured best on B200 at n = 2^30 (profiles/r01/retune_final.txt, profiles/r01/sweep_r01a.jsonl).
-    int default_algo = TCR_ALGO_MMA_SYNC;
+    // 0 = auto (r02): by input size, the measured faster kernel -- tcgen05
+    // (TMA ring, one issuer per SM) from 1 GiB, mma.sync below
+    int default_algo = TCR_ALGO_DEFAULT;
     int blocks_per_sm = 8;
     int unroll = 0;       // 0 = auto: 16 below 2^26 elements, 4 above
     int chain = 4;        // carried chain K (tiles per fp32 accumulator before a flush)
@@ -196,21 +198,26 @@ tcr_status after_launch(cudaError_t e, const char* where, int launches = 1) {
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
+// TCR_ALGO_DEFAULT resolved for an input of `nbytes`: TCR_CFG_DEFAULT_ALGO if
+// set, else (auto, the default) the kernel measured fastest at that size on
+// B200 -- every format alike (profiles/r02/big_n_ab*.txt, tc05_vs_mma.txt):
+//   >= 1 GiB: tcgen05 (TMA ring, one MMA issuer per SM, tight issue loop):
+//             2^30 fp16 0.998-1.001 x mma.sync's time (0.984 on one box),
+//             2^32 0.97-0.98 x, also under sw_power_cap;
+//   <  1 GiB: mma.sync (LDG): 2^24 warm 4.9 vs 6.7-7.1 us, 2^28 77.9 vs 78.5 us.
+int resolve_default_algo(size_t nbytes) {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    if (g_cfg.default_algo != TCR_ALGO_DEFAULT) return g_cfg.default_algo;
+    return nbytes >= ((size_t)1 << 30) ? TCR_ALGO_TCGEN05 : TCR_ALGO_MMA_SYNC;
+}
+
 tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_f64, int algo,
                        cudaStream_t stream, int fmt = 0) {
     if ((!x && n) || (!out_f32 && !out_f64)) return fail(TCR_ERR_INVALID_VALUE, "null pointer");
     if (!aligned(x, fmt >= 2 ? 1 : 2) || (out_f32 && !aligned(out_f32, 4)) ||
         (out_f64 && !aligned(out_f64, 8)))
         return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
-    if (algo == TCR_ALGO_DEFAULT) {
-        std::lock_guard<std::mutex> lk(g_cfg_mu);
-        // every format takes TCR_CFG_DEFAULT_ALGO (mma.sync).  fp8 used to
-        // take tcgen05 kind::f8f6f4 from 2^26 elements; since fp8 tiles run as
-        // exact binary16 conversions + two m16n8k16 (r02) mma.sync is at least
-        // as fast at every size (2^28: 6.41 vs 6.01 TB/s, 2^31: 7.20 vs 7.18;
-        // profiles/r02/fp8_default.txt)
-        algo = g_cfg.default_algo;
-    }
+    if (algo == TCR_ALGO_DEFAULT) algo = resolve_default_algo(n * (fmt >= 2 ? 1u : 2u));
     if (algo < TCR_ALGO_MMA_SYNC || algo > TCR_ALGO_BULK_MMA)
         return fail(TCR_ERR_INVALID_VALUE, "unknown algo");
     DeviceInfo di;
@@ -418,11 +425,6 @@ static tcr_status reduce_host_impl(const void* x, size_t n, int fmt, float* out,
                 return cuda_fail(e, "cudaEventCreate");
         }
     }
-    int algo;
-    {
-        std::lock_guard<std::mutex> lk(g_cfg_mu);
-        algo = g_cfg.default_algo;
-    }
     int launches = 0;
     const char* xb = static_cast<const char*>(x);
     // the copy stream starts after the caller's earlier work (staging reuse
@@ -443,8 +445,8 @@ static tcr_status reduce_host_impl(const void* x, size_t n, int fmt, float* out,
             (e = cudaStreamWaitEvent(stream, ws->copied[b], 0)))
             return cuda_fail(e, "event ordering (copied)");
         const uint16_t* db = static_cast<const uint16_t*>(buf);
-        // the default algorithm (reduce_impl's rule: TCR_CFG_DEFAULT_ALGO)
-        const int a = algo;
+        // the default algorithm for this chunk's size (reduce_impl's rule)
+        const int a = resolve_default_algo(cnt * es);
         if (a == TCR_ALGO_TCGEN05)
             e = tcr::launch_reduce_tcgen05(fmt, db, cnt, nullptr, ws->chunk_partials + c, ws->dev,
                                            cfg, stream);
@@ -723,8 +725,8 @@ tcr_status tcr_probe_collapse(const double* in, double* out, tcr_algo algo, tcr_
 tcr_status tcr_set_config(tcr_config_key key, int value) {
     std::lock_guard<std::mutex> lk(g_cfg_mu);
     switch (key) {
-        case TCR_CFG_DEFAULT_ALGO:
-            if (value < TCR_ALGO_MMA_SYNC || value > TCR_ALGO_BULK_MMA) break;
+        case TCR_CFG_DEFAULT_ALGO:  // 0 = auto by input size
+            if (value < TCR_ALGO_DEFAULT || value > TCR_ALGO_BULK_MMA) break;
             g_cfg.default_algo = value;
             return TCR_OK;
         case TCR_CFG_BLOCKS_PER_SM:
@@ -872,6 +874,11 @@ tcr_status tcr_release_workspaces(void) {
 }
 
 uint64_t tcr_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+tcr_algo tcr_default_algo(size_t n, tcr_dtype dtype) {
+    const size_t es = (dtype == TCR_DTYPE_E4M3 || dtype == TCR_DTYPE_E5M2) ? 1 : 2;
+    return (tcr_algo)resolve_default_algo(n * es);
+}
 
 int tcr_version(void) { return TCR_VERSION; }
 
