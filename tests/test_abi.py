@@ -191,3 +191,24 @@ def test_no_register_spills_in_any_kernel():
                     bad.append((f, name, m.group(0)))
     assert seen >= 50, seen
     assert not bad, bad[:5]
+
+
+def test_default_algo_resolution():
+    """TCR_ALGO_DEFAULT (auto) picks the kernel by input size: mma.sync below
+    1 GiB, tcgen05 from 1 GiB, for every format; an explicit
+    TCR_CFG_DEFAULT_ALGO overrides it.  Host logic only (no device work)."""
+    import paper_1903_03640_b200 as tcr
+
+    assert tcr.tcr_get_config(tcr.TCR_CFG_DEFAULT_ALGO) == tcr.TCR_ALGO_DEFAULT
+    f16, e4 = tcr.TCR_DTYPE_F16, tcr.TCR_DTYPE_E4M3
+    assert tcr.tcr_default_algo(1 << 16, f16) == tcr.TCR_ALGO_MMA_SYNC
+    assert tcr.tcr_default_algo((1 << 29) - 1, f16) == tcr.TCR_ALGO_MMA_SYNC
+    assert tcr.tcr_default_algo(1 << 29, f16) == tcr.TCR_ALGO_TCGEN05  # 1 GiB
+    assert tcr.tcr_default_algo(1 << 30, tcr.TCR_DTYPE_BF16) == tcr.TCR_ALGO_TCGEN05
+    assert tcr.tcr_default_algo((1 << 30) - 1, e4) == tcr.TCR_ALGO_MMA_SYNC
+    assert tcr.tcr_default_algo(1 << 30, e4) == tcr.TCR_ALGO_TCGEN05
+    try:
+        tcr.tcr_set_config(tcr.TCR_CFG_DEFAULT_ALGO, tcr.TCR_ALGO_SHUFFLE)
+        assert tcr.tcr_default_algo(1 << 31, f16) == tcr.TCR_ALGO_SHUFFLE
+    finally:
+        tcr.tcr_set_config(tcr.TCR_CFG_DEFAULT_ALGO, tcr.TCR_ALGO_DEFAULT)
