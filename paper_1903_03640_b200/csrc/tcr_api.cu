@@ -49,9 +49,13 @@ struct Config {
     int tc05_prefetch = 0;
     int tc05_split = 1;
     int tc05_interleave = 0;
-    int bulk_stages = 6;
-    int bulk_stage_kb = 16;
-    int bulk_ctas = 2;
+    // bulk (TMA -> SMEM -> mma.sync), r02: one CTA per SM with 4 x 32 KiB
+    // (8 tiles per consumer warp per stage = the K = 4 chain per accumulator);
+    // 2^30: 0.994-0.995 x mma.sync's time vs 1.07-1.09 x for r01's 6 x 16 KiB,
+    // 2 CTAs (profiles/r02/big_n_ab*.txt, bulk_sweep.txt)
+    int bulk_stages = 4;
+    int bulk_stage_kb = 32;
+    int bulk_ctas = 1;
     int exact_unroll = 8;
     int exact_bps = 3;
     int peer_timeout_ms = 10000;
