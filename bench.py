@@ -507,7 +507,7 @@ def main():
     peak, peak_src = _peaks()
     peer, combine_note = None, None
     peer_cfg = (args.workload == "c3" and args.dtype == "f16"
-                and args.algo in ("default", "mma_sync", "shuffle", "exact"))
+                and args.algo in ("default", "mma_sync", "tcgen05", "shuffle", "exact"))
     if args.combine == "peer":
         if not peer_cfg:
             raise SystemExit("--combine peer supports the f16 c3/c4 workload with mma_sync / "
@@ -531,7 +531,7 @@ def main():
             if ok.item() == 0 and peer is not None:
                 peer, combine_note = None, "peer setup failed on another rank; NCCL combine used"
         if peer is not None and not exact:
-            algo = tcr.ALGOS["mma_sync" if args.algo == "default" else args.algo]
+            algo = tcr.ALGOS[args.algo]  # "default": by shard size inside the library
 
     # ---------------- inputs (untimed), resident in HBM ----------------
     if args.workload == "c3":
@@ -733,8 +733,8 @@ def main():
     achieved = bytes_per_step / (kern_ms * 1e-3) / 1e9              # GB/s of the dominant kernel
     if args.algo != "default":
         algo_name = args.algo
-    elif peer is not None or args.workload == "c5":
-        algo_name = "mma_sync"  # the fused peer kernel / the segmented MMA kernels
+    elif args.workload == "c5":
+        algo_name = "mma_sync"  # the segmented MMA kernels
     else:  # what TCR_ALGO_DEFAULT resolved to for this rank's input size
         algo_name = {1: "mma_sync", 2: "tcgen05", 3: "shuffle", 4: "bulk"}[
             tcr.tcr_default_algo(n, dtype_code)]

@@ -304,7 +304,9 @@ tcr_status tcr_peer_ipc_close(void *peer_mailbox);
  * = the total over all nranks shards (binary64 sum of the ranks' fp64
  * partials in rank order; out_f32 its RNE rounding).  One kernel launch on
  * `stream`.
- *   algo:      TCR_ALGO_DEFAULT / MMA_SYNC (the north-star kernel) or SHUFFLE.
+ *   algo:      TCR_ALGO_DEFAULT (by the per-rank shard size, as tcr_reduce_sum:
+ *              tcgen05 from 1 GiB, else mma.sync), MMA_SYNC, TCGEN05 (r02: the
+ *              combine fused into the tcgen05 kernel's last CTA) or SHUFFLE.
  *   mailboxes: HOST array of nranks device pointers, indexed by rank.
  *   nranks:    1..TCR_MAX_PEERS; rank: this process's index.
  * Every rank of the group must make the same sequence of calls, each rank's

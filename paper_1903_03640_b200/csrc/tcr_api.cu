@@ -246,9 +246,14 @@ tcr_status peer_impl(const void* x, size_t n, int dtype, int algo, void* const* 
     static_assert(tcr::kMailboxBytes == TCR_PEER_MAILBOX_BYTES, "mailbox size");
     if (dtype < TCR_DTYPE_F16 || dtype > TCR_DTYPE_E5M2)
         return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
-    if (algo == TCR_ALGO_DEFAULT) algo = TCR_ALGO_MMA_SYNC;
-    if (algo != TCR_ALGO_MMA_SYNC && algo != TCR_ALGO_SHUFFLE)
-        return fail(TCR_ERR_INVALID_VALUE, "peer combine algo must be DEFAULT, MMA_SYNC or SHUFFLE");
+    if (algo == TCR_ALGO_DEFAULT) {  // by the per-rank shard size, as reduce_impl
+        const size_t es = dtype >= TCR_DTYPE_E4M3 ? 1 : 2;
+        algo = resolve_default_algo(n / (size_t)(emulate && nranks > 0 ? nranks : 1) * es);
+        if (algo == TCR_ALGO_BULK_MMA) algo = TCR_ALGO_MMA_SYNC;  // no fused bulk variant
+    }
+    if (algo != TCR_ALGO_MMA_SYNC && algo != TCR_ALGO_SHUFFLE && algo != TCR_ALGO_TCGEN05)
+        return fail(TCR_ERR_INVALID_VALUE,
+                    "peer combine algo must be DEFAULT, MMA_SYNC, TCGEN05 or SHUFFLE");
     if (nranks < 1 || nranks > tcr::kMaxPeers || rank < 0 || rank >= nranks)
         return fail(TCR_ERR_INVALID_VALUE, "nranks must be 1..TCR_MAX_PEERS and 0 <= rank < nranks");
     if (!mailboxes || (!x && n) || (!out_f32 && !out_f64 && !out_acc))
@@ -280,6 +285,11 @@ tcr_status peer_impl(const void* x, size_t n, int dtype, int algo, void* const* 
                                           reinterpret_cast<long long*>(out_acc), out_f32, out_f64,
                                           ws->dev, cfg, pc, emulate, stream),
             emulate ? "exact peer-emulated launch" : "exact peer launch");
+    if (algo == TCR_ALGO_TCGEN05)
+        return after_launch(tcr::launch_reduce_tcgen05_peer(dtype, static_cast<const uint16_t*>(x), n,
+                                                            out_f32, out_f64, ws->dev, cfg, pc, emulate,
+                                                            stream),
+                            emulate ? "tcgen05 peer-emulated launch" : "tcgen05 peer launch");
     return after_launch(tcr::launch_reduce_stream_peer(algo == TCR_ALGO_MMA_SYNC, dtype,
                                                        static_cast<const uint16_t*>(x), n, out_f32,
                                                        out_f64, ws->dev, cfg, pc, emulate, stream),

@@ -73,6 +73,11 @@ cudaError_t launch_reduce_stream_peer(bool mma, int fmt, const uint16_t* x, size
 cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x, size_t n, float* out_f32,
                                   double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                   cudaStream_t stream);
+// NEXT-2 on the tcgen05 kernel: the cross-GPU combine fused into its last CTA
+// (emulate: nranks grid slices in one cooperative launch)
+cudaError_t launch_reduce_tcgen05_peer(int fmt, const uint16_t* x, size_t n, float* out_f32,
+                                       double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                       const PeerCombine& pc, bool emulate, cudaStream_t stream);
 cudaError_t launch_reduce_segmented(bool mma, int fmt, bool batched, const void* x,
                                     const int64_t* offsets, size_t num_segments,
                                     size_t segment_len, float* out, const DevWorkspace& ws,

@@ -109,12 +109,26 @@ struct Tc05Params {
 // its per-MMA bookkeeping (scripts/tc05_trace.cu: MMA issue gap, r02), against
 // ~37 ns for a bare issue loop (scripts/tc05_floor.cu) -- which is why r01
 // needed three CTAs (three issuers) per SM.
-template <bool kF8, int KM>
+// kPeer: the NEXT-2 variant (the cross-GPU combine fused into the last CTA,
+// tcr_peer.cuh), as for the streaming kernel; grid.y slices = emulated ranks.
+template <bool kF8, int KM, bool kPeer = false>
 __global__ void __launch_bounds__(kTcWarps * 32)
 reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, float* out_f32,
-                      double* out_f64, DevWorkspace ws) {
+                      double* out_f64, DevWorkspace ws, PeerCombine pc) {
     extern __shared__ __align__(1024) uint8_t smem[];
     TC05_EDGE(0);
+    int me = pc.rank;
+    if (kPeer && gridDim.y > 1) {  // emulated peer group: slice y is rank y, reducing its shard
+        const size_t P = gridDim.y, r = blockIdx.y, es = prm.fmt >= 2 ? 1u : 2u;
+        const size_t lo = r * n / P, hi = (r + 1) * n / P;
+        x += lo * es;
+        n = hi - lo;
+        ws.partials += r * gridDim.x;
+        ws.ticket += r;
+        if (out_f32) out_f32 += r;
+        if (out_f64) out_f64 += r;
+        me = (int)r;
+    }
     const int stages = prm.stages;
     const uint32_t stage_bytes = prm.stage_bytes;
     const uint32_t buf_cols = (uint32_t)prm.slots * kSlotCols;
@@ -336,7 +350,7 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
     __syncthreads();
     TC05_EDGE(2);
     if (warp == 1) sm100::tmem_dealloc(tmem, tmem_cols);
-    complete_block_and_grid<true, kTcWarps>(acc, out_f32, out_f64, ws);
+    complete_block_and_grid<true, kTcWarps>(acc, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
     TC05_EDGE(3);
 }
 
@@ -380,11 +394,33 @@ static LaunchCfg tc05_effective(size_t nbytes, const LaunchCfg& cfg) {
     return c;
 }
 
-cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x16, size_t n, float* out_f32,
-                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg_in,
-                                  cudaStream_t stream) {
-    const uint8_t* x = reinterpret_cast<const uint8_t*>(x16);
-    const LaunchCfg cfg = tc05_effective(n * (fmt >= 2 ? 1u : 2u), cfg_in);
+using Tc05Kernel = void (*)(const uint8_t*, size_t, Tc05Params, float*, double*, DevWorkspace,
+                           PeerCombine);
+
+// The instantiation for (format, MMAs per stage): the tight issue loop for
+// KM = 4, 8, 16 (the peer variant: 8, the default, else the generic loop).
+template <bool kPeer>
+static Tc05Kernel tc05_kernel(bool f8, int km) {
+    if constexpr (kPeer) {
+        if (km == 8) return f8 ? reduce_tcgen05_kernel<true, 8, true> : reduce_tcgen05_kernel<false, 8, true>;
+        return f8 ? reduce_tcgen05_kernel<true, 0, true> : reduce_tcgen05_kernel<false, 0, true>;
+    } else {
+        switch (km) {
+            case 4: return f8 ? reduce_tcgen05_kernel<true, 4> : reduce_tcgen05_kernel<false, 4>;
+            case 8: return f8 ? reduce_tcgen05_kernel<true, 8> : reduce_tcgen05_kernel<false, 8>;
+            case 16: return f8 ? reduce_tcgen05_kernel<true, 16> : reduce_tcgen05_kernel<false, 16>;
+            default: return f8 ? reduce_tcgen05_kernel<true, 0> : reduce_tcgen05_kernel<false, 0>;
+        }
+    }
+}
+
+template <bool kPeer>
+static cudaError_t launch_tc05(int fmt, const uint8_t* x, size_t n, float* out_f32, double* out_f64,
+                               const DevWorkspace& ws, const LaunchCfg& cfg_in, const PeerCombine& pc,
+                               bool emulate, cudaStream_t stream) {
+    const size_t es = fmt >= 2 ? 1u : 2u;
+    const int P = emulate ? pc.nranks : 1;
+    const LaunchCfg cfg = tc05_effective(n / (size_t)P * es, cfg_in);  // by the per-rank bytes
     Tc05Params prm;
     prm.fmt = fmt;
     // kind::f16: a/b_format F16 = 0, BF16 = 1; kind::f8f6f4: E4M3 = 0, E5M2 = 1 (bits 7-9, 10-12)
@@ -404,48 +440,69 @@ cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x16, size_t n, float*
         return cudaErrorInvalidValue;
     const size_t smem = kHeaderBytes + (size_t)prm.stages * prm.stage_bytes;
     if (kHeaderBytes - 8 < 512 + (size_t)(2 * prm.stages + 4) * 8) return cudaErrorInvalidValue;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    {
-        // largest dynamic shared memory size configured so far, per device
-        static std::mutex mu;
-        static std::map<int, size_t> configured;
-        std::lock_guard<std::mutex> lk(mu);
-        if (smem > configured[dev]) {
-            const void* fns[8] = {(const void*)reduce_tcgen05_kernel<false, 0>,
-                                  (const void*)reduce_tcgen05_kernel<true, 0>,
-                                  (const void*)reduce_tcgen05_kernel<false, 4>,
-                                  (const void*)reduce_tcgen05_kernel<true, 4>,
-                                  (const void*)reduce_tcgen05_kernel<false, 8>,
-                                  (const void*)reduce_tcgen05_kernel<true, 8>,
-                                  (const void*)reduce_tcgen05_kernel<false, 16>,
-                                  (const void*)reduce_tcgen05_kernel<true, 16>};
-            for (const void* f : fns)
-                if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
-                    return e;
-            configured[dev] = smem;
-        }
-    }
-    const int g = tcgen05_grid(n * (fmt >= 2 ? 1u : 2u), cfg);
     // one accumulator round per stage (4 slots, chain = MMAs per stage / 4):
     // the tight issue loop, instantiated for 4, 8 and 16 MMAs per stage
     const int kmma = (int)(prm.stage_bytes / kTileBytes);
     const int km = (prm.slots == 4 && prm.slots * prm.chain == kmma &&
                     (kmma == 4 || kmma == 8 || kmma == 16)) ? kmma : 0;
-    const dim3 grid(g), block(kTcWarps * 32);
-#define TCR_TC05_LAUNCH(F8, K)                                                                   \
-    launch_maybe_pdl(reduce_tcgen05_kernel<F8, K>, grid, block, smem, stream, cfg.pdl, x, n, prm, \
-                     out_f32, out_f64, ws)
-    const bool f8 = fmt >= 2;
-    switch (km) {
-        case 4: if (f8) TCR_TC05_LAUNCH(true, 4); else TCR_TC05_LAUNCH(false, 4); break;
-        case 8: if (f8) TCR_TC05_LAUNCH(true, 8); else TCR_TC05_LAUNCH(false, 8); break;
-        case 16: if (f8) TCR_TC05_LAUNCH(true, 16); else TCR_TC05_LAUNCH(false, 16); break;
-        default: if (f8) TCR_TC05_LAUNCH(true, 0); else TCR_TC05_LAUNCH(false, 0); break;
+    const Tc05Kernel kernel = tc05_kernel<kPeer>(fmt >= 2, km);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    {
+        // largest dynamic shared memory size configured so far, per (device, kernel)
+        static std::mutex mu;
+        static std::map<std::pair<int, const void*>, size_t> configured;
+        std::lock_guard<std::mutex> lk(mu);
+        size_t& have = configured[{dev, (const void*)kernel}];
+        if (smem > have) {
+            if ((e = cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem)))
+                return e;
+            have = smem;
+        }
     }
-#undef TCR_TC05_LAUNCH
-    return cudaGetLastError();
+    int g = tcgen05_grid(n / (size_t)P * es, cfg);
+    const dim3 block(kTcWarps * 32);
+    if (!emulate) {
+        // the peer variant waits on other ranks: plain launch
+        launch_maybe_pdl(kernel, dim3(g), block, smem, stream, (cfg.pdl && !kPeer) ? 1 : 0, x, n, prm,
+                         out_f32, out_f64, ws, pc);
+        return cudaGetLastError();
+    }
+    // emulated peer group: the ranks' last CTAs wait on one another, so all P
+    // grid slices must be co-resident -- a cooperative launch guarantees it
+    int occ = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTcWarps * 32, smem)))
+        return e;
+    const int cap = occ * cfg.sms / P;
+    if (g > cap) g = cap;
+    if (g < 1) return cudaErrorCooperativeLaunchTooLarge;
+    const uint8_t* xa = x;
+    size_t na = n;
+    Tc05Params pa = prm;
+    float* o32 = out_f32;
+    double* o64 = out_f64;
+    DevWorkspace wsa = ws;
+    PeerCombine pca = pc;
+    void* args[] = {(void*)&xa, (void*)&na, (void*)&pa, (void*)&o32, (void*)&o64, (void*)&wsa,
+                    (void*)&pca};
+    return cudaLaunchCooperativeKernel((const void*)kernel, dim3(g, P), block, args, smem, stream);
+}
+
+cudaError_t launch_reduce_tcgen05(int fmt, const uint16_t* x16, size_t n, float* out_f32,
+                                  double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                  cudaStream_t stream) {
+    const PeerCombine none{};
+    return launch_tc05<false>(fmt, reinterpret_cast<const uint8_t*>(x16), n, out_f32, out_f64, ws, cfg,
+                              none, false, stream);
+}
+
+cudaError_t launch_reduce_tcgen05_peer(int fmt, const uint16_t* x16, size_t n, float* out_f32,
+                                       double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                       const PeerCombine& pc, bool emulate, cudaStream_t stream) {
+    return launch_tc05<true>(fmt, reinterpret_cast<const uint8_t*>(x16), n, out_f32, out_f64, ws, cfg,
+                             pc, emulate, stream);
 }
 
 // One tcgen05.mma (M=128, N=16, K=16) with A = a (row-major 128x16 fp16),

@@ -62,10 +62,12 @@ class PeerGroup:
                 self.mailboxes.append(p)
         self.calls = 0
 
-    def reduce_sum(self, x_local, out_f32=None, out_f64=None, algo="mma_sync", stream=None):
+    def reduce_sum(self, x_local, out_f32=None, out_f64=None, algo="default", stream=None):
         """Group total of every rank's shard into out_f32 / out_f64 (device,
         1 element each), replicated on all ranks.  Every rank must call it
-        the same number of times, in the same order, stream-ordered."""
+        the same number of times, in the same order, stream-ordered.  algo:
+        "default" (by shard size: tcgen05 from 1 GiB, else mma_sync),
+        "mma_sync", "tcgen05" or "shuffle"."""
         self.calls += 1
         self._lib.tcr_reduce_sum_peer(x_local, self.mailboxes, self.rank, out_f32=out_f32,
                                       out_f64=out_f64, algo=algo, stream=stream)

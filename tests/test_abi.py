@@ -64,7 +64,7 @@ def test_invalid_arguments_rejected_before_device():
     mb = [0x10000 + 0x1000 * r for r in range(9)]
     F16 = tcr.TCR_DTYPE_F16
     for args in ((mb[:9], 0, 1), (mb[:0], 0, 1), (mb[:2], 2, 1), (mb[:2], -1, 1),
-                 (mb[:2], 0, tcr.TCR_ALGO_TCGEN05), ([0x10000, 0], 0, 1), ([0x10008], 0, 1)):
+                 (mb[:2], 0, tcr.TCR_ALGO_BULK_MMA), ([0x10000, 0], 0, 1), ([0x10008], 0, 1)):
         with pytest.raises(tcr.TcrError) as e:
             tcr.tcr_reduce_sum_peer(0x1000, args[0], args[1], out_f32=0x2000, algo=args[2],
                                     dtype=F16, n=16, stream=0)

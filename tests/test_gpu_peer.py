@@ -55,15 +55,16 @@ def _shards(n, P):
     return [(n * r // P, n * (r + 1) // P) for r in range(P)]
 
 
-@pytest.mark.parametrize("algo", ["mma_sync", "shuffle"])
-@pytest.mark.parametrize("n", [0, 1, 4097, 1_000_003])
+@pytest.mark.parametrize("algo", ["mma_sync", "shuffle", "tcgen05"])
+@pytest.mark.parametrize("n", [0, 1, 4097, 1_000_003, (1 << 29) + 7])
 def test_single_rank_equals_f64_entry(tcr, mailboxes, algo, n):
     """nranks = 1: the fused kernel is the ordinary reduction plus 0.0 + v
     (compared at the peer variant's fixed unroll of 4, so both launches use
     the same grid and chain)."""
     import torch
 
-    x = _dev(gen.generate(3, 0, n, gen.UNIFORM_PM1))
+    x = (_dev(gen.generate(3, 0, n, gen.UNIFORM_PM1)) if n <= (1 << 24)
+         else gen.generate_tensor(3, 0, n, gen.UNIFORM_PM1))  # 1 GiB: the tcgen05 1-CTA/SM shape
     ref = torch.empty(1, dtype=torch.float64, device="cuda")
     tcr.tcr_set_config(tcr.TCR_CFG_UNROLL, 4)
     try:
@@ -81,7 +82,7 @@ def test_single_rank_equals_f64_entry(tcr, mailboxes, algo, n):
 
 
 @pytest.mark.parametrize("P", [2, 3, 4, 8])
-@pytest.mark.parametrize("algo", ["mma_sync", "shuffle"])
+@pytest.mark.parametrize("algo", ["mma_sync", "shuffle", "tcgen05"])
 def test_emulated_ranks(tcr, mailboxes, P, algo):
     import torch
 
@@ -119,20 +120,21 @@ def test_emulated_partials_are_the_ranks_shard_sums(tcr, mailboxes):
             assert o64.cpu().tolist() == [1.0] * P, pos
 
 
-def test_emulated_bf16_fp8(tcr, mailboxes):
+@pytest.mark.parametrize("algo", ["default", "tcgen05"])
+def test_emulated_bf16_fp8(tcr, mailboxes, algo):
     import torch
 
     P, n = 4, 500_003
     out = torch.empty(P, dtype=torch.float32, device="cuda")
     b = gen.generate_bf16(5, 0, n, gen.UNIFORM_PM1)
     xb = torch.from_numpy(b.view(np.int16)).cuda().view(torch.bfloat16)
-    tcr.tcr_reduce_sum_peer_emulated(xb, mailboxes[:P], out_f32=out)
+    tcr.tcr_reduce_sum_peer_emulated(xb, mailboxes[:P], out_f32=out, algo=algo)
     torch.cuda.synchronize()
     assert len(set(out.cpu().tolist())) == 1
     assert oracle.within_tolerance(out[0].item(), oracle.exact_sum_bf16(b))
     f8 = gen.generate_fp8(5, 0, n, gen.UNIFORM_PM1, gen.FP8_E4M3)
     x8 = torch.from_numpy(f8).cuda().view(torch.float8_e4m3fn)
-    tcr.tcr_reduce_sum_peer_emulated(x8, mailboxes[:P], out_f32=out)
+    tcr.tcr_reduce_sum_peer_emulated(x8, mailboxes[:P], out_f32=out, algo=algo)
     torch.cuda.synchronize()
     assert len(set(out.cpu().tolist())) == 1
     assert oracle.within_tolerance(out[0].item(), oracle.exact_sum_fp8(f8, gen.FP8_E4M3))
@@ -148,10 +150,15 @@ def test_emulated_c4_scale(tcr, mailboxes):
     x = gen.generate_tensor(gen.SEED_C4, 0, n, gen.ONES)
     o64 = torch.empty(P, dtype=torch.float64, device="cuda")
     o32 = torch.empty(P, dtype=torch.float32, device="cuda")
-    tcr.tcr_reduce_sum_peer_emulated(x, mailboxes[:P], out_f32=o32, out_f64=o64)
-    torch.cuda.synchronize()
-    assert o64.cpu().tolist() == [float(n)] * P
-    assert o32.cpu().tolist() == [float(n)] * P
+    # default: 2 GiB shards take the fused tcgen05 kernel (r02); then mma.sync
+    assert tcr.tcr_default_algo(n // P) == tcr.TCR_ALGO_TCGEN05
+    for algo in ("default", "mma_sync"):
+        o64.fill_(float("nan"))
+        o32.fill_(float("nan"))
+        tcr.tcr_reduce_sum_peer_emulated(x, mailboxes[:P], out_f32=o32, out_f64=o64, algo=algo)
+        torch.cuda.synchronize()
+        assert o64.cpu().tolist() == [float(n)] * P, algo
+        assert o32.cpu().tolist() == [float(n)] * P, algo
     del x
 
 
