@@ -152,6 +152,15 @@ def test_sass_fused_peer_kernel_has_mma_and_system_scope_peer_traffic():
         assert mnemonic in body, mnemonic
     plain = [f for f in funcs if f.startswith("_ZN3tcr20reduce_stream_kernelILb1ELi0ELi4ELi8ELb0E")]
     assert plain and "STRONG.SYS" not in plain[0]  # the plain kernel has no peer traffic
+    # r02: the same combine fused into the tcgen05 kernel (tight loop, KM = 8):
+    # UTCHMMA tiles from SMEM + the DMMA collapse + the system-scope push / poll
+    tpeer = [f for f in funcs if f.startswith("_ZN3tcr21reduce_tcgen05_kernelILb0ELi8ELb1E")]
+    assert tpeer, "fused tcgen05 peer kernel not found"
+    for mnemonic in ("UTCHMMA", "UBLKCP", "LDTM", "DMMA.8x8x4", "STG.E.128.STRONG.SYS",
+                     "LDG.E.128.STRONG.SYS"):
+        assert mnemonic in tpeer[0], mnemonic
+    tplain = [f for f in funcs if f.startswith("_ZN3tcr21reduce_tcgen05_kernelILb0ELi8ELb0E")]
+    assert tplain and "STRONG.SYS" not in tplain[0]
 
 
 def test_product_path_fails_loudly_without_the_library(tmp_path):
