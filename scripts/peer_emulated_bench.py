@@ -54,13 +54,19 @@ def main():
         x = gen.generate_tensor(gen.SEED_C3, 0, n, gen.UNIFORM_PM1)
         o = torch.empty(8, dtype=torch.float64, device="cuda")
         reps = 20 if logn >= 33 else 50
-        r = {"plain_us": timed(lambda: tcr.tcr_reduce_sum_ex(x, out_f64=o[:1], algo="mma_sync"),
-                               boxes, reps),
-             "peer_P1_us": timed(lambda: tcr.tcr_reduce_sum_peer(x, boxes[:1], 0, out_f64=o[:1]),
-                                 boxes, reps)}
-        for P in (1, 2, 4, 8):
-            r[f"emulated_P{P}_us"] = timed(
-                lambda: tcr.tcr_reduce_sum_peer_emulated(x, boxes[:P], out_f64=o[:P]), boxes, reps)
+        r = {}
+        # r02: both fused kernels (mma.sync, tcgen05) against their plain twins
+        for algo in ("mma_sync", "tcgen05"):
+            r[f"{algo}_plain_us"] = timed(
+                lambda: tcr.tcr_reduce_sum_ex(x, out_f64=o[:1], algo=algo), boxes, reps)
+            r[f"{algo}_peer_P1_us"] = timed(
+                lambda: tcr.tcr_reduce_sum_peer(x, boxes[:1], 0, out_f64=o[:1], algo=algo), boxes, reps)
+            for P in (1, 2, 4, 8):
+                r[f"{algo}_emulated_P{P}_us"] = timed(
+                    lambda: tcr.tcr_reduce_sum_peer_emulated(x, boxes[:P], out_f64=o[:P], algo=algo),
+                    boxes, reps)
+        r["plain_us"] = r["mma_sync_plain_us"]
+        r["emulated_P8_us"] = r["mma_sync_emulated_P8_us"]
         r["gbs_plain"] = 2 * n / (r["plain_us"] * 1e-6) / 1e9
         r["gbs_emulated_P8"] = 2 * n / (r["emulated_P8_us"] * 1e-6) / 1e9
         res[f"n=2^{logn}"] = r
