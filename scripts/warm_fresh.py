@@ -17,6 +17,7 @@ import paper_1903_03640_b200 as tcr  # noqa: E402
 import tcr_inputs as gen  # noqa: E402
 
 variant = sys.argv[1]
+algo = sys.argv[2] if len(sys.argv) > 2 else "default"
 torch.cuda.set_device(0)
 x = gen.generate_tensor(gen.SEED_C3, 0, 1 << 30, gen.UNIFORM_PM1)
 out = torch.empty(1, dtype=torch.float32, device="cuda")
@@ -37,17 +38,17 @@ elif variant == "e2e":
 elif variant == "self":
     with torch.cuda.stream(s):
         for _ in range(100):
-            tcr.tcr_reduce_sum_ex(x, out_f32=out, stream=s)
+            tcr.tcr_reduce_sum_ex(x, out_f32=out, algo=algo, stream=s)
 torch.cuda.synchronize()
 pre_ms = (time.perf_counter() - t0) * 1e3
 ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(60)]
 with torch.cuda.stream(s):
     for a, b in ev:
         a.record(s)
-        tcr.tcr_reduce_sum_ex(x, out_f32=out, stream=s)
+        tcr.tcr_reduce_sum_ex(x, out_f32=out, algo=algo, stream=s)
         b.record(s)
 torch.cuda.synchronize()
 d = [round(a.elapsed_time(b) * 1e3, 1) for a, b in ev]
-print(json.dumps({"variant": variant, "pre_ms": round(pre_ms, 1), "us": d,
+print(json.dumps({"variant": variant, "algo": algo, "pre_ms": round(pre_ms, 1), "us": d,
                   "mean_1_6": sum(d[1:6]) / 5, "mean_6_26": sum(d[6:26]) / 20,
                   "mean_26_60": sum(d[26:]) / 34}))
