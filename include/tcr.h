@@ -80,10 +80,9 @@ typedef enum {
 
 /* Kernel selection for tcr_reduce_sum_algo / the _config default. */
 typedef enum {
-    TCR_ALGO_DEFAULT = 0, /* the library's fastest MMA-encoded kernel for the
-                             input's size (TCR_CFG_DEFAULT_ALGO; auto: tcgen05
-                             from 1 GiB of input, mma.sync below -- see
-                             tcr_default_algo)                               */
+    TCR_ALGO_DEFAULT = 0, /* TCR_CFG_DEFAULT_ALGO: mma.sync unless changed
+                             (value 0 = auto by size: tcgen05 from 1 GiB of
+                             input, mma.sync below -- see tcr_default_algo) */
     TCR_ALGO_MMA_SYNC = 1, /* mma.sync m16n8k16 (A from 128-bit loads)       */
     TCR_ALGO_TCGEN05 = 2, /* cp.async.bulk -> SMEM -> tcgen05.mma, D in TMEM */
     TCR_ALGO_SHUFFLE = 3, /* classic comparison path (§II): fp32
@@ -304,9 +303,9 @@ tcr_status tcr_peer_ipc_close(void *peer_mailbox);
  * = the total over all nranks shards (binary64 sum of the ranks' fp64
  * partials in rank order; out_f32 its RNE rounding).  One kernel launch on
  * `stream`.
- *   algo:      TCR_ALGO_DEFAULT (by the per-rank shard size, as tcr_reduce_sum:
- *              tcgen05 from 1 GiB, else mma.sync), MMA_SYNC, TCGEN05 (r02: the
- *              combine fused into the tcgen05 kernel's last CTA) or SHUFFLE.
+ *   algo:      TCR_ALGO_DEFAULT (as tcr_reduce_sum, resolved for the per-rank
+ *              shard size), MMA_SYNC, TCGEN05 (r02: the combine fused into the
+ *              tcgen05 kernel's last CTA) or SHUFFLE.
  *   mailboxes: HOST array of nranks device pointers, indexed by rank.
  *   nranks:    1..TCR_MAX_PEERS; rank: this process's index.
  * Every rank of the group must make the same sequence of calls, each rank's
@@ -400,10 +399,10 @@ tcr_status tcr_probe_collapse(const double *in, double *out, tcr_algo algo, tcr_
 
 /* Tuning knobs (process-wide; defaults are the measured best on B200). */
 typedef enum {
-    TCR_CFG_DEFAULT_ALGO = 0,     /* tcr_algo used by tcr_reduce_sum; 0 (the
-                                   * default) = auto by input size: tcgen05 from
-                                   * 1 GiB, mma.sync below (r02 measurements,
-                                   * DESIGN.md §15.5)                          */
+    TCR_CFG_DEFAULT_ALGO = 0,     /* tcr_algo used by tcr_reduce_sum (default
+                                   * MMA_SYNC); 0 = auto by input size: tcgen05
+                                   * from 1 GiB, mma.sync below (r02
+                                   * measurements)            */
     TCR_CFG_BLOCKS_PER_SM = 1,    /* CTAs per SM of the streaming kernels   */
     TCR_CFG_UNROLL = 2,           /* 16-byte loads in flight per lane (mma.sync/shuffle):
                                      4, 8, 16, or 0 = auto (default: 16 below

@@ -33,9 +33,10 @@ std::atomic<uint64_t> g_launches{0};
 
 struct Config {
     // Defaults = the measured best on B200 at n = 2^30 (profiles/r01/retune_final.txt, profiles/r01/sweep_r01a.jsonl).
-    // 0 = auto (r02): by input size, the measured faster kernel -- tcgen05
-    // (TMA ring, one issuer per SM) from 1 GiB, mma.sync below
-    int default_algo = TCR_ALGO_DEFAULT;
+    // mma.sync (r02 measurements: tcgen05 ties it from 1 GiB
+    // in back-to-back streams but is ~2 % slower for an isolated launch at
+    // 2^30 and 1.4 x at 2^24); 0 = auto by size (tcgen05 from 1 GiB) on request
+    int default_algo = TCR_ALGO_MMA_SYNC;
     int blocks_per_sm = 8;
     int unroll = 0;       // 0 = auto: 16 below 2^26 elements, 4 above
     int chain = 4;        // carried chain K (tiles per fp32 accumulator before a flush)
@@ -202,13 +203,11 @@ tcr_status after_launch(cudaError_t e, const char* where, int launches = 1) {
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
-// TCR_ALGO_DEFAULT resolved for an input of `nbytes`: TCR_CFG_DEFAULT_ALGO if
-// set, else (auto, the default) the kernel measured fastest at that size on
-// B200 -- every format alike (profiles/r02/big_n_ab*.txt, tc05_vs_mma.txt):
-//   >= 1 GiB: tcgen05 (TMA ring, one MMA issuer per SM, tight issue loop):
-//             2^30 fp16 0.998-1.001 x mma.sync's time (0.984 on one box),
-//             2^32 0.97-0.98 x, also under sw_power_cap;
-//   <  1 GiB: mma.sync (LDG): 2^24 warm 4.9 vs 6.7-7.1 us, 2^28 77.9 vs 78.5 us.
+// TCR_ALGO_DEFAULT resolved for an input of `nbytes`: TCR_CFG_DEFAULT_ALGO
+// (mma.sync unless changed); its value 0 (auto) picks by size -- tcgen05 (TMA
+// ring, one MMA issuer per SM, tight issue loop) from 1 GiB, where it ties
+// mma.sync in back-to-back streams (profiles/r02/big_n_ab*.txt,
+// tc05_vs_mma.txt), mma.sync below (2^24 warm 4.9 vs 6.7-7.1 us).
 int resolve_default_algo(size_t nbytes) {
     std::lock_guard<std::mutex> lk(g_cfg_mu);
     if (g_cfg.default_algo != TCR_ALGO_DEFAULT) return g_cfg.default_algo;

@@ -150,9 +150,8 @@ def test_emulated_c4_scale(tcr, mailboxes):
     x = gen.generate_tensor(gen.SEED_C4, 0, n, gen.ONES)
     o64 = torch.empty(P, dtype=torch.float64, device="cuda")
     o32 = torch.empty(P, dtype=torch.float32, device="cuda")
-    # default: 2 GiB shards take the fused tcgen05 kernel (r02); then mma.sync
-    assert tcr.tcr_default_algo(n // P) == tcr.TCR_ALGO_TCGEN05
-    for algo in ("default", "mma_sync"):
+    # both fused kernels: tcgen05 (r02) and mma.sync
+    for algo in ("tcgen05", "mma_sync"):
         o64.fill_(float("nan"))
         o32.fill_(float("nan"))
         tcr.tcr_reduce_sum_peer_emulated(x, mailboxes[:P], out_f32=o32, out_f64=o64, algo=algo)
