@@ -158,8 +158,14 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
     const int per_round = prm.slots * prm.chain;
     const long long total_mma = (long long)nchunks * kmma;
 
-    for (int i = threadIdx.x; i < 128; i += blockDim.x) ones[i] = prm.one_bits;
-    sm100::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+    // The producer (thread 0) initialises the barriers and issues the first
+    // ring's worth of bulk copies right away (r02): their HBM latency then
+    // overlaps the rest of the set-up (ones tile, TMEM allocation, the CTA
+    // barrier) instead of following it.  It waits for the previous kernel
+    // (PDL) before touching x; the other threads do after the CTA barrier.
+    const uint64_t pol = sm100::policy_evict_first();
+    const uint32_t piece = stage_bytes / (uint32_t)prm.split;
+    const int pre = nchunks < stages ? nchunks : stages;  // chunks issued before the barrier
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             sm100::mbar_init(&full[s], 1);
@@ -170,7 +176,18 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
             sm100::mbar_init(&tempty[b], 4);
         }
         sm100::fence_mbar_init();
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        const uint8_t* src = xa + c_begin * (size_t)stage_bytes;
+        for (int i = 0; i < pre; ++i, src += chunk_step) {  // ring stage i, first phase: free
+            TC05_TRACE(0, i);
+            sm100::mbar_arrive_expect_tx(&full[i], stage_bytes);
+            uint8_t* dst = ring + (size_t)i * stage_bytes;
+            for (int q = 0; q < prm.split; ++q)
+                sm100::bulk_g2s(dst + (size_t)q * piece, src + (size_t)q * piece, piece, &full[i], pol);
+        }
     }
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) ones[i] = prm.one_bits;
+    sm100::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
     const uint32_t tmem_cols = 2u * buf_cols < 32u ? 32u : 2u * buf_cols;
     if (warp == 1) sm100::tmem_alloc(tmem_slot, tmem_cols);
     sm100::tc_fence_before();
@@ -184,15 +201,13 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
 
     double acc = 0.0;
     if (warp == 0) {
-        if (lane == 0 && nchunks > 0) {  // producer
-            const uint64_t pol = sm100::policy_evict_first();
-            const uint32_t piece = stage_bytes / (uint32_t)prm.split;
-            const uint8_t* src = xa + c_begin * (size_t)stage_bytes;
-            for (int i = 0; i < prm.prefetch && i < nchunks; ++i)
-                sm100::prefetch_l2(src + (size_t)i * chunk_step, stage_bytes);
-            int s = 0;
-            uint32_t ph = 0;
-            for (int i = 0; i < nchunks; ++i, src += chunk_step) {
+        if (lane == 0 && nchunks > pre) {  // producer: the chunks after the first ring
+            const uint8_t* src = xa + c_begin * (size_t)stage_bytes + (size_t)pre * chunk_step;
+            for (int i = pre; i < pre + prm.prefetch && i < nchunks; ++i)
+                sm100::prefetch_l2(src + (size_t)(i - pre) * chunk_step, stage_bytes);
+            int s = pre % stages;
+            uint32_t ph = pre / stages;  // pre <= stages: the first ring is one phase
+            for (int i = pre; i < nchunks; ++i, src += chunk_step) {
                 if (prm.prefetch && i + prm.prefetch < nchunks)
                     sm100::prefetch_l2(src + (size_t)prm.prefetch * chunk_step, stage_bytes);
                 sm100::mbar_wait(&empty[s], ph ^ 1u);
