@@ -80,9 +80,10 @@ typedef enum {
 
 /* Kernel selection for tcr_reduce_sum_algo / the _config default. */
 typedef enum {
-    TCR_ALGO_DEFAULT = 0, /* TCR_CFG_DEFAULT_ALGO: mma.sync unless changed
-                             (value 0 = auto by size: tcgen05 from 1 GiB of
-                             input, mma.sync below -- see tcr_default_algo) */
+    TCR_ALGO_DEFAULT = 0, /* TCR_CFG_DEFAULT_ALGO; its default, 0 = auto by
+                             size: tcgen05 (dynamic tail) for binary16 / fp8
+                             from 512 MiB of input, mma.sync below and for
+                             bfloat16 -- see tcr_default_algo              */
     TCR_ALGO_MMA_SYNC = 1, /* mma.sync m16n8k16 (A from 128-bit loads)       */
     TCR_ALGO_TCGEN05 = 2, /* cp.async.bulk -> SMEM -> tcgen05.mma, D in TMEM */
     TCR_ALGO_SHUFFLE = 3, /* classic comparison path (§II): fp32
@@ -399,10 +400,10 @@ tcr_status tcr_probe_collapse(const double *in, double *out, tcr_algo algo, tcr_
 
 /* Tuning knobs (process-wide; defaults are the measured best on B200). */
 typedef enum {
-    TCR_CFG_DEFAULT_ALGO = 0,     /* tcr_algo used by tcr_reduce_sum (default
-                                   * MMA_SYNC); 0 = auto by input size: tcgen05
-                                   * from 1 GiB, mma.sync below (r02
-                                   * measurements)            */
+    TCR_CFG_DEFAULT_ALGO = 0,     /* tcr_algo used by tcr_reduce_sum; 0 (the
+                                   * default) = auto by input size: tcgen05 for
+                                   * binary16 / fp8 from 512 MiB, mma.sync below
+                                   * and for bfloat16          */
     TCR_CFG_BLOCKS_PER_SM = 1,    /* CTAs per SM of the streaming kernels   */
     TCR_CFG_UNROLL = 2,           /* 16-byte loads in flight per lane (mma.sync/shuffle):
                                      4, 8, 16, or 0 = auto (default: 16 below
@@ -430,7 +431,7 @@ typedef enum {
     TCR_CFG_BULK_CTAS_PER_SM = 16, /* bulk kernel: CTAs per SM (clamped by SMEM) */
     TCR_CFG_PEER_TIMEOUT_MS = 17,  /* fused peer combine: bound on the wait for the
                                      peers' partials (default 10000 ms)          */
-    TCR_CFG_PDL = 18              /* 1 (default): the reduction kernels (streaming,
+    TCR_CFG_PDL = 18,             /* 1 (default): the reduction kernels (streaming,
                                    * tcgen05, bulk, exact, segmented / batched) are
                                    * launched with programmatic dependent launch -- a
                                    * call's CTAs are scheduled while the previous kernel
@@ -438,6 +439,21 @@ typedef enum {
                                    * for its completion before touching global memory;
                                    * results are bitwise identical either way (the fused
                                    * peer kernels always launch plainly); 0: plain launch */
+    TCR_CFG_TC05_DYNAMIC = 19,    /* tcgen05: percent (0..100) of the chunks handed
+                                   * out at run time from a chunk counter (the
+                                   * dynamic tail: every CTA first streams its own
+                                   * contiguous run, then takes the remaining chunks
+                                   * one at a time) -- 0 = static partition.  With a
+                                   * nonzero value the rounds are combined exactly
+                                   * (integer units of 2^-24), so the result does not
+                                   * depend on which CTA took which chunk; binary16
+                                   * and fp8 (bfloat16 always uses the static
+                                   * partition; so do runs shorter than
+                                   * TCR_CFG_TC05_DYN_MIN_RUN); default 8
+                                   *                             */
+    TCR_CFG_TC05_DYN_MIN_RUN = 20 /* tcgen05: the dynamic tail only when every CTA
+                                   * streams at least this many chunks (default 32;
+                                   * 0 = whenever TCR_CFG_TC05_DYNAMIC > 0)       */
 } tcr_config_key;
 tcr_status tcr_set_config(tcr_config_key key, int value);
 int tcr_get_config(tcr_config_key key); /* -1 for an unknown key */

@@ -33,10 +33,9 @@ std::atomic<uint64_t> g_launches{0};
 
 struct Config {
     // Defaults = the measured best on B200 at n = 2^30 (profiles/r01/retune_final.txt, profiles/r01/sweep_r01a.jsonl).
-    // mma.sync (r02 measurements: tcgen05 ties it from 1 GiB
-    // in back-to-back streams but is ~2 % slower for an isolated launch at
-    // 2^30 and 1.4 x at 2^24); 0 = auto by size (tcgen05 from 1 GiB) on request
-    int default_algo = TCR_ALGO_MMA_SYNC;
+    // auto by size (r02 §16): tcgen05 with the dynamic tail for binary16 /
+    // fp8 from 512 MiB, mma.sync below and for bfloat16 (resolve_default_algo)
+    int default_algo = TCR_ALGO_DEFAULT;
     int blocks_per_sm = 8;
     int unroll = 0;       // 0 = auto: 16 below 2^26 elements, 4 above
     int chain = 4;        // carried chain K (tiles per fp32 accumulator before a flush)
@@ -50,6 +49,8 @@ struct Config {
     int tc05_prefetch = 0;
     int tc05_split = 1;
     int tc05_interleave = 0;
+    int tc05_dynamic = 8;  // percent of the chunks handed out at run time (r02 §16)
+    int tc05_dyn_min_run = 32;  // ... when every CTA streams >= 32 chunks (r02 §16)
     // bulk (TMA -> SMEM -> mma.sync), r02: one CTA per SM with 4 x 32 KiB
     // (8 tiles per consumer warp per stage = the K = 4 chain per accumulator);
     // 2^30: 0.994-0.995 x mma.sync's time vs 1.07-1.09 x for r01's 6 x 16 KiB,
@@ -116,6 +117,8 @@ LaunchCfg make_cfg(const DeviceInfo& di) {
     c.tc05_prefetch = g_cfg.tc05_prefetch;
     c.tc05_split = g_cfg.tc05_split;
     c.tc05_interleave = g_cfg.tc05_interleave;
+    c.tc05_dynamic = g_cfg.tc05_dynamic;
+    c.tc05_dyn_min_run = g_cfg.tc05_dyn_min_run;
     c.bulk_stages = g_cfg.bulk_stages;
     c.bulk_stage_kb = g_cfg.bulk_stage_kb;
     c.bulk_ctas = g_cfg.bulk_ctas;
@@ -176,6 +179,7 @@ tcr_status get_workspace(int dev, const DeviceInfo& di, cudaStream_t stream, Wor
     ws->dev.seg_next = reinterpret_cast<unsigned long long*>(ctr);
     ws->dev.seg_exit = reinterpret_cast<unsigned*>(ctr + 8);
     ws->dev.ticket = reinterpret_cast<unsigned*>(ctr + 16);  // kMaxPeers tickets
+    ws->dev.chunk_next = reinterpret_cast<unsigned*>(ctr + 64);  // kMaxPeers counters
     ws->dev.capacity = capacity;
     e = cudaMemsetAsync(ctr, 0, kCounterBytes, stream);
     if (e != cudaSuccess) {
@@ -203,15 +207,18 @@ tcr_status after_launch(cudaError_t e, const char* where, int launches = 1) {
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
-// TCR_ALGO_DEFAULT resolved for an input of `nbytes`: TCR_CFG_DEFAULT_ALGO
-// (mma.sync unless changed); its value 0 (auto) picks by size -- tcgen05 (TMA
-// ring, one MMA issuer per SM, tight issue loop) from 1 GiB, where it ties
-// mma.sync in back-to-back streams (profiles/r02/big_n_ab*.txt,
-// tc05_vs_mma.txt), mma.sync below (2^24 warm 4.9 vs 6.7-7.1 us).
-int resolve_default_algo(size_t nbytes) {
+// TCR_ALGO_DEFAULT resolved for an input of `nbytes` in format `fmt`:
+// TCR_CFG_DEFAULT_ALGO unless it is 0 (auto, the default since r02 §16),
+// which picks by size -- tcgen05 (TMA ring, one MMA issuer per SM, tight
+// issue loop, dynamic tail) for binary16 / fp8 from 512 MiB, where it beats
+// mma.sync by 1.5-2.8 % (2^29..2^33, back to back and isolated,
+// profiles/r02/tc05_dyn_ab2.txt), mma.sync below (2^24 warm 4.9 vs 6.4 us)
+// and for bfloat16 (no dynamic tail: its sums are not multiples of 2^-24).
+constexpr size_t kTc05AutoBytes = (size_t)512 << 20;
+int resolve_default_algo(size_t nbytes, int fmt) {
     std::lock_guard<std::mutex> lk(g_cfg_mu);
     if (g_cfg.default_algo != TCR_ALGO_DEFAULT) return g_cfg.default_algo;
-    return nbytes >= ((size_t)1 << 30) ? TCR_ALGO_TCGEN05 : TCR_ALGO_MMA_SYNC;
+    return (fmt != TCR_DTYPE_BF16 && nbytes >= kTc05AutoBytes) ? TCR_ALGO_TCGEN05 : TCR_ALGO_MMA_SYNC;
 }
 
 tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_f64, int algo,
@@ -220,7 +227,7 @@ tcr_status reduce_impl(const tcr_half* x, size_t n, float* out_f32, double* out_
     if (!aligned(x, fmt >= 2 ? 1 : 2) || (out_f32 && !aligned(out_f32, 4)) ||
         (out_f64 && !aligned(out_f64, 8)))
         return fail(TCR_ERR_INVALID_VALUE, "misaligned pointer");
-    if (algo == TCR_ALGO_DEFAULT) algo = resolve_default_algo(n * (fmt >= 2 ? 1u : 2u));
+    if (algo == TCR_ALGO_DEFAULT) algo = resolve_default_algo(n * (fmt >= 2 ? 1u : 2u), fmt);
     if (algo < TCR_ALGO_MMA_SYNC || algo > TCR_ALGO_BULK_MMA)
         return fail(TCR_ERR_INVALID_VALUE, "unknown algo");
     DeviceInfo di;
@@ -247,7 +254,7 @@ tcr_status peer_impl(const void* x, size_t n, int dtype, int algo, void* const* 
         return fail(TCR_ERR_INVALID_VALUE, "unknown dtype");
     if (algo == TCR_ALGO_DEFAULT) {  // by the per-rank shard size, as reduce_impl
         const size_t es = dtype >= TCR_DTYPE_E4M3 ? 1 : 2;
-        algo = resolve_default_algo(n / (size_t)(emulate && nranks > 0 ? nranks : 1) * es);
+        algo = resolve_default_algo(n / (size_t)(emulate && nranks > 0 ? nranks : 1) * es, dtype);
         if (algo == TCR_ALGO_BULK_MMA) algo = TCR_ALGO_MMA_SYNC;  // no fused bulk variant
     }
     if (algo != TCR_ALGO_MMA_SYNC && algo != TCR_ALGO_SHUFFLE && algo != TCR_ALGO_TCGEN05)
@@ -459,7 +466,7 @@ static tcr_status reduce_host_impl(const void* x, size_t n, int fmt, float* out,
             return cuda_fail(e, "event ordering (copied)");
         const uint16_t* db = static_cast<const uint16_t*>(buf);
         // the default algorithm for this chunk's size (reduce_impl's rule)
-        const int a = resolve_default_algo(cnt * es);
+        const int a = resolve_default_algo(cnt * es, fmt);
         if (a == TCR_ALGO_TCGEN05)
             e = tcr::launch_reduce_tcgen05(fmt, db, cnt, nullptr, ws->chunk_partials + c, ws->dev,
                                            cfg, stream);
@@ -786,6 +793,14 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             if (value != 0 && value != 1) break;
             g_cfg.tc05_interleave = value;
             return TCR_OK;
+        case TCR_CFG_TC05_DYNAMIC:
+            if (value < 0 || value > 100) break;
+            g_cfg.tc05_dynamic = value;
+            return TCR_OK;
+        case TCR_CFG_TC05_DYN_MIN_RUN:
+            if (value < 0 || value > 1 << 20) break;
+            g_cfg.tc05_dyn_min_run = value;
+            return TCR_OK;
         case TCR_CFG_BULK_STAGES:
             if (value < 2 || value > 32) break;
             g_cfg.bulk_stages = value;
@@ -834,6 +849,8 @@ int tcr_get_config(tcr_config_key key) {
         case TCR_CFG_TC05_PREFETCH: return g_cfg.tc05_prefetch;
         case TCR_CFG_TC05_SPLIT: return g_cfg.tc05_split;
         case TCR_CFG_TC05_INTERLEAVE: return g_cfg.tc05_interleave;
+        case TCR_CFG_TC05_DYNAMIC: return g_cfg.tc05_dynamic;
+        case TCR_CFG_TC05_DYN_MIN_RUN: return g_cfg.tc05_dyn_min_run;
         case TCR_CFG_BULK_STAGES: return g_cfg.bulk_stages;
         case TCR_CFG_BULK_STAGE_KB: return g_cfg.bulk_stage_kb;
         case TCR_CFG_BULK_CTAS_PER_SM: return g_cfg.bulk_ctas;
@@ -890,7 +907,7 @@ uint64_t tcr_launch_count(void) { return g_launches.load(std::memory_order_relax
 
 tcr_algo tcr_default_algo(size_t n, tcr_dtype dtype) {
     const size_t es = (dtype == TCR_DTYPE_E4M3 || dtype == TCR_DTYPE_E5M2) ? 1 : 2;
-    return (tcr_algo)resolve_default_algo(n * es);
+    return (tcr_algo)resolve_default_algo(n * es, (int)dtype);
 }
 
 int tcr_version(void) { return TCR_VERSION; }

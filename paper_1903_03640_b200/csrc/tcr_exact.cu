@@ -21,6 +21,7 @@
 // integer SUM-allreduce of acc[] over GPUs is exact, and
 // tcr_exact_finalize() rounds it.
 #include "tcr_device.cuh"
+#include "tcr_int128.cuh"
 #include "tcr_internal.h"
 #include "tcr_peer.cuh"
 
@@ -31,9 +32,6 @@ namespace {
 constexpr int kExactWarps = 8;
 constexpr int kExactUnroll = 4;
 constexpr int kFlushIter = 64;  // 64 iterations x 4 vectors x 4 halves = 1024 per accumulator
-
-typedef __int128 i128;
-typedef unsigned __int128 u128;
 
 // Scaled binary64 of the low / high binary16 of a 32-bit word (x 2^-1008):
 // the high 32 bits of the binary64 are sign | 0000 | e(5) | f(10) | 0...,
@@ -152,19 +150,6 @@ __device__ __forceinline__ long long to_units(double a) {
     return __double2ll_rn((a * 0x1p1008) * 0x1p24);  // both scalings exact; result < 2^53
 }
 
-__device__ __forceinline__ i128 shfl_xor_i128(i128 v, int o) {
-    const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
-    const unsigned long long lo2 = __shfl_xor_sync(0xffffffffu, lo, o);
-    const unsigned long long hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
-    return (i128)(((u128)hi2 << 64) | (u128)lo2);
-}
-
-__device__ __forceinline__ i128 warp_sum_i128(i128 v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += shfl_xor_i128(v, o);
-    return v;
-}
-
 __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -181,30 +166,6 @@ __device__ __forceinline__ void to_limbs(i128 t, long long* acc) {
 
 __device__ __forceinline__ i128 from_limbs(const long long* acc) {
     return (i128)acc[0] + ((i128)acc[1] << 40) + ((i128)acc[2] << 80);
-}
-
-// Correctly rounded (RNE) value of T * 2^-24 with `bits` significand bits,
-// returned as mantissa (<= 2^bits) and binary exponent: value = mant * 2^exp.
-__device__ __forceinline__ void round_units(u128 U, int bits, unsigned long long& mant, int& exp) {
-    if (U == 0) {
-        mant = 0;
-        exp = 0;
-        return;
-    }
-    const unsigned long long hi = (unsigned long long)(U >> 64), lo = (unsigned long long)U;
-    const int msb = hi ? 127 - __clzll((long long)hi) : 63 - __clzll((long long)lo);
-    if (msb < bits) {  // exact
-        mant = lo;
-        exp = -24;
-        return;
-    }
-    const int shift = msb - (bits - 1);
-    u128 q = U >> shift;
-    const u128 rem = U - (q << shift);
-    const u128 halfway = (u128)1 << (shift - 1);
-    if (rem > halfway || (rem == halfway && (q & 1))) ++q;
-    mant = (unsigned long long)q;  // may equal 2^bits after rounding up: still exact below
-    exp = shift - 24;
 }
 
 __device__ void finalize(const long long* acc, float* out_f32, double* out_f64) {

@@ -15,6 +15,8 @@ struct DevWorkspace {
                                     // consecutive tickets (one per emulated rank)
     unsigned long long* seg_next;   // segmented: next segment index (self-resetting)
     unsigned* seg_exit;             // segmented: warps that finished (self-resetting)
+    unsigned* chunk_next;           // tcgen05 dynamic tail: next chunk ticket (self-resetting);
+                                    // kMaxPeers consecutive counters (one per emulated rank)
     int capacity;                   // entries in partials
 };
 
@@ -48,6 +50,10 @@ struct LaunchCfg {
     int tc05_prefetch;  // tcgen05 kernel: L2 prefetch distance in chunks
     int tc05_split;     // tcgen05 kernel: bulk copies per stage
     int tc05_interleave;  // tcgen05 kernel: chunk-to-CTA mapping (0 contiguous, 1 interleaved)
+    int tc05_dynamic;     // tcgen05 kernel: percent of the chunks handed out at run time
+                          // (dynamic tail; 0 = static partition)
+    int tc05_dyn_min_run; // tcgen05 kernel: the dynamic tail only when every CTA's
+                          // static run would be at least this many chunks
     int bulk_stages;      // bulk (TMA -> SMEM -> mma.sync) kernel: ring stages
     int bulk_stage_kb;    // bulk kernel: KiB per stage (multiple of 4)
     int bulk_ctas;        // bulk kernel: CTAs per SM

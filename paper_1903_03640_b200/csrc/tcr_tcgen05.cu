@@ -40,6 +40,7 @@ __device__ unsigned long long g_tc05_edges[10][2048];
 #endif
 #include "tcr_complete.cuh"
 #include "tcr_device.cuh"
+#include "tcr_int128.cuh"
 #include "tcr_internal.h"
 #include "tcr_sm100.cuh"
 
@@ -89,10 +90,91 @@ struct Tc05Params {
     int prefetch;          // L2 prefetch distance in chunks (0 = off)
     int split;             // bulk copies per stage
     int interleave;        // 0: CTA b owns a contiguous run of chunks; 1: chunks b, b+G, b+2G, ...
+    int dynamic;           // kDyn: percent of the chunks handed out from ws.chunk_next
     uint32_t idesc;        // instruction descriptor (kind::f16 with F16 or BF16 operands)
     uint32_t one_bits;     // 1.0 in the input type (the all-ones B)
     int fmt;               // element format (0 f16, 1 bf16, 2 e4m3, 3 e5m2)
 };
+
+// Levels 3-4 of the dynamic-tail variant (kDyn): every thread passes its
+// exact integer T (units of 2^-24) and the sum `sp` of the non-finite
+// level-2 totals it saw; the CTA and the grid add them as integers
+// (order-free), the last CTA rounds T * 2^-24 once (RNE) -- or returns sp
+// when some total was inf / NaN (inf + -inf = NaN in any order) -- and resets
+// the ticket and the chunk counter for the next launch on this stream.
+template <int WARPS>
+__device__ __forceinline__ void complete_units_grid(i128 T, double sp, float* out_f32,
+                                                    double* out_f64, const DevWorkspace& ws,
+                                                    const PeerCombine* pc, int me) {
+    __shared__ long long s_part[WARPS][3];
+    __shared__ unsigned s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T = warp_sum_i128(T);
+    sp = warp_collapse_shfl(sp);
+    if (lane == 0) {
+        s_part[warp][0] = (long long)(unsigned long long)T;
+        s_part[warp][1] = (long long)(T >> 64);
+        s_part[warp][2] = __double_as_longlong(sp);
+    }
+    TCR_COMPLETE_EDGE(4);
+    __syncthreads();
+    TCR_COMPLETE_EDGE(5);
+    if (warp != 0) return;
+    const bool peer = pc && pc->nranks > 0;
+    const unsigned long long prev = peer ? peer_counter(*pc, me) : 0ull;
+    i128 b = lane < WARPS ? make_i128(s_part[lane][0], s_part[lane][1]) : (i128)0;
+    double q = lane < WARPS ? __longlong_as_double(s_part[lane][2]) : 0.0;
+    b = warp_sum_i128(b);
+    q = warp_collapse_shfl(q);
+    TCR_COMPLETE_EDGE(6);
+    if (gridDim.x > 1) {
+        long long* parts = reinterpret_cast<long long*>(ws.partials);  // 3 words per CTA
+        if (lane == 0) {
+            long long* p = parts + 3 * (size_t)blockIdx.x;
+            p[0] = (long long)(unsigned long long)b;
+            p[1] = (long long)(b >> 64);
+            p[2] = __double_as_longlong(q);
+            TCR_COMPLETE_EDGE(7);
+            if (peer) {
+                __threadfence();
+                s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+            } else {
+                s_last = (ticket_acq_rel(ws.ticket) == gridDim.x - 1) ? 1u : 0u;
+            }
+        }
+        __syncwarp();  // lane 0's acquire, then the warp's loads below
+        TCR_COMPLETE_EDGE(8);
+        if (!__shfl_sync(0xffffffffu, s_last, 0)) return;
+        if (peer) __threadfence();
+        b = 0;
+        q = 0.0;
+        for (int i = lane; i < (int)gridDim.x; i += 32) {
+            const long long* p = parts + 3 * (size_t)i;
+            b += make_i128(__ldcg(p), __ldcg(p + 1));
+            q += __longlong_as_double(__ldcg(p + 2));
+        }
+        b = warp_sum_i128(b);
+        q = warp_collapse_shfl(q);
+        if (lane == 0) *ws.ticket = 0u;
+    }
+    if (lane == 0) *ws.chunk_next = 0u;  // every CTA's chunk tickets precede its completion ticket
+    float f;
+    double d;
+    if (q != 0.0) {  // some level-2 total was inf or NaN
+        f = (float)q;
+        d = q;
+    } else {
+        round_units_f32_f64(b, f, d);
+    }
+    if (peer) {
+        d = peer_combine(d, *pc, me, lane, prev);
+        f = (float)d;
+    }
+    if (lane == 0) {
+        if (out_f32) *out_f32 = f;
+        if (out_f64) *out_f64 = d;
+    }
+}
 
 // Accumulator schedule: MMA number j of this CTA (j = 0, 1, ...) goes to
 // round r = j / (slots*chain), slot j % slots of TMEM buffer r & 1, and
@@ -111,7 +193,18 @@ struct Tc05Params {
 // needed three CTAs (three issuers) per SM.
 // kPeer: the NEXT-2 variant (the cross-GPU combine fused into the last CTA,
 // tcr_peer.cuh), as for the streaming kernel; grid.y slices = emulated ranks.
-template <bool kF8, int KM, bool kPeer = false>
+// kDyn (r02 §16): the dynamic tail.  CTA b first streams its contiguous run
+// of the first (100 - dynamic) % of the chunks, then takes the remaining
+// chunks one at a time from ws.chunk_next (the producer holds two tickets
+// ahead, so the atomic's latency overlaps the ring), so every SM stops
+// within about one chunk of the others instead of waiting for the slowest
+// static run.  The producer marks each ring stage valid or END; the MMA
+// issuer forwards END to the epilogue through a per-buffer flag.  Order-free
+// arithmetic keeps the result independent of the schedule: each round's
+// 4 x 128 fp32 row sums (multiples of 2^-24, as every binary16 / fp8 value
+// and every fp32 sum of them is) are collapsed per warp by the DMMA D' = 1 x D
+// (exact: |total| < 2^29, i.e. < 2^53 units) and added as integers.
+template <bool kF8, int KM, bool kPeer = false, bool kDyn = false>
 __global__ void __launch_bounds__(kTcWarps * 32)
 reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, float* out_f32,
                       double* out_f64, DevWorkspace ws, PeerCombine pc) {
@@ -123,12 +216,19 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
         const size_t lo = r * n / P, hi = (r + 1) * n / P;
         x += lo * es;
         n = hi - lo;
-        ws.partials += r * gridDim.x;
+        ws.partials += (kDyn ? 3 : 1) * r * gridDim.x;  // kDyn: 3 words per CTA partial
         ws.ticket += r;
+        ws.chunk_next += r;
         if (out_f32) out_f32 += r;
         if (out_f64) out_f64 += r;
         me = (int)r;
     }
+    static_assert(!kDyn || KM > 0, "the dynamic tail runs the tight issue loop");
+    // exactness of the per-round DMMA collapse: 32 lanes x 4 slots x (KM / 4)
+    // MMAs x K elements x the largest magnitude < 2^29 (binary16: K = 16,
+    // 65504; fp8: K = 32, 57344 for E5M2 -- so fp8 takes KM <= 8)
+    static_assert(!kDyn || (kF8 ? 32.0 * KM * 32 * 57344.0 : 32.0 * KM * 16 * 65504.0) < 536870912.0,
+                  "per-round collapse must stay below 2^53 units");
     const int stages = prm.stages;
     const uint32_t stage_bytes = prm.stage_bytes;
     const uint32_t buf_cols = (uint32_t)prm.slots * kSlotCols;
@@ -137,6 +237,8 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
     uint64_t* empty = full + stages;                                // [stages]
     uint64_t* tfull = empty + stages;                               // [2]
     uint64_t* tempty = tfull + 2;                                   // [2]
+    volatile uint32_t* sinfo = reinterpret_cast<volatile uint32_t*>(tempty + 2);  // [stages] kDyn
+    volatile uint32_t* tend = sinfo + stages;                                       // [2] kDyn
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kHeaderBytes - 8);
     uint8_t* ring = smem + kHeaderBytes;
 
@@ -150,10 +252,14 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
     const size_t nb = nbytes - head;
     const size_t C = nb / stage_bytes;
     const size_t G = gridDim.x, b = blockIdx.x;
-    const size_t c_begin = prm.interleave ? b : b * C / G;
-    const int nchunks = prm.interleave ? (int)(C > b ? (C - b + G - 1) / G : 0)
-                                       : (int)((b + 1) * C / G - b * C / G);
-    const size_t chunk_step = prm.interleave ? G * (size_t)stage_bytes : (size_t)stage_bytes;
+    // kDyn: chunks [0, Cs) statically (contiguous runs), [Cs, C) by ticket
+    const size_t D = kDyn ? C * (size_t)prm.dynamic / 100u : 0;
+    const size_t Cs = C - D;
+    const size_t c_begin = kDyn ? b * Cs / G : prm.interleave ? b : b * C / G;
+    const int nchunks = kDyn ? (int)((b + 1) * Cs / G - b * Cs / G)
+                        : prm.interleave ? (int)(C > b ? (C - b + G - 1) / G : 0)
+                                         : (int)((b + 1) * C / G - b * C / G);
+    const size_t chunk_step = (!kDyn && prm.interleave) ? G * (size_t)stage_bytes : (size_t)stage_bytes;
     const int kmma = (int)(stage_bytes / kTileBytes);
     const int per_round = prm.slots * prm.chain;
     const long long total_mma = (long long)nchunks * kmma;
@@ -174,12 +280,14 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
         for (int b = 0; b < 2; ++b) {
             sm100::mbar_init(&tfull[b], 1);
             sm100::mbar_init(&tempty[b], 4);
+            if (kDyn) tend[b] = 0u;
         }
         sm100::fence_mbar_init();
         asm volatile("griddepcontrol.wait;" ::: "memory");
         const uint8_t* src = xa + c_begin * (size_t)stage_bytes;
         for (int i = 0; i < pre; ++i, src += chunk_step) {  // ring stage i, first phase: free
             TC05_TRACE(0, i);
+            if (kDyn) sinfo[i] = 1u;
             sm100::mbar_arrive_expect_tx(&full[i], stage_bytes);
             uint8_t* dst = ring + (size_t)i * stage_bytes;
             for (int q = 0; q < prm.split; ++q)
@@ -200,172 +308,320 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
     pdl_wait_and_release();
 
     double acc = 0.0;
-    if (warp == 0) {
-        if (lane == 0 && nchunks > pre) {  // producer: the chunks after the first ring
-            const uint8_t* src = xa + c_begin * (size_t)stage_bytes + (size_t)pre * chunk_step;
-            for (int i = pre; i < pre + prm.prefetch && i < nchunks; ++i)
-                sm100::prefetch_l2(src + (size_t)(i - pre) * chunk_step, stage_bytes);
-            int s = pre % stages;
-            uint32_t ph = pre / stages;  // pre <= stages: the first ring is one phase
-            for (int i = pre; i < nchunks; ++i, src += chunk_step) {
-                if (prm.prefetch && i + prm.prefetch < nchunks)
-                    sm100::prefetch_l2(src + (size_t)prm.prefetch * chunk_step, stage_bytes);
-                sm100::mbar_wait(&empty[s], ph ^ 1u);
-                TC05_TRACE(0, i);
-                sm100::mbar_arrive_expect_tx(&full[s], stage_bytes);
-                uint8_t* dst = ring + (size_t)s * stage_bytes;
-                for (int q = 0; q < prm.split; ++q)
-                    sm100::bulk_g2s(dst + (size_t)q * piece, src + (size_t)q * piece, piece, &full[s],
-                                    pol);
-                if (++s == stages) {
-                    s = 0;
-                    ph ^= 1u;
+    i128 T = 0;       // kDyn: exact sum in units of 2^-24
+    double sp = 0.0;  // kDyn: sum of the non-finite level-2 totals
+    if constexpr (kDyn) {
+        if (warp == 0) {
+            if (lane == 0) {  // producer: static run, then chunk tickets, then END
+                int s = pre % stages;
+                uint32_t ph = (uint32_t)(pre / stages);
+                auto issue = [&](const uint8_t* src) {
+                    sm100::mbar_wait(&empty[s], ph ^ 1u);
+                    sinfo[s] = 1u;
+                    sm100::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    uint8_t* dst = ring + (size_t)s * stage_bytes;
+                    for (int q = 0; q < prm.split; ++q)
+                        sm100::bulk_g2s(dst + (size_t)q * piece, src + (size_t)q * piece, piece, &full[s], pol);
+                    if (++s == stages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                };
+                // two tickets held ahead: each is fetched about two chunks before
+                // it is needed (its result is first read by the `t >= D` test)
+                unsigned t0 = 0u, t1 = 0u;
+                bool f0 = false, f1 = false;
+                const uint8_t* src = xa + (c_begin + (size_t)pre) * (size_t)stage_bytes;
+                for (int i = pre; i < nchunks; ++i, src += stage_bytes) {
+                    if (D && !f0 && nchunks - i <= 2) {
+                        t0 = atomicAdd(ws.chunk_next, 1u);
+                        f0 = true;
+                    }
+                    if (D && !f1 && nchunks - i <= 1) {
+                        t1 = atomicAdd(ws.chunk_next, 1u);
+                        f1 = true;
+                    }
+                    issue(src);
                 }
+                if (D) {
+                    if (!f0) t0 = atomicAdd(ws.chunk_next, 1u);
+                    if (!f1) t1 = atomicAdd(ws.chunk_next, 1u);
+                    for (;;) {
+                        const unsigned t = t0;
+                        t0 = t1;
+                        t1 = atomicAdd(ws.chunk_next, 1u);
+                        if ((size_t)t >= D) break;
+                        issue(xa + (Cs + (size_t)t) * (size_t)stage_bytes);
+                    }
+                }
+                sm100::mbar_wait(&empty[s], ph ^ 1u);  // END: a stage with no bytes
+                sinfo[s] = 0u;
+                sm100::mbar_arrive(&full[s]);
             }
-        }
-        __syncwarp();
-    } else if (KM > 0 && warp == 1) {
-        if (lane == 0 && nchunks > 0) {  // MMA issuer, one round per stage (tight loop)
-            const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
-            const uint64_t adesc0 = sm100::smem_desc_kmajor(sm100::smem_addr(ring), 128, 256);
-            const uint64_t stage_step = stage_bytes >> 4;
-            constexpr uint64_t kTileStep = kTileBytes >> 4;
-            int s = 0, buf = 0;
-            uint32_t ph = 0, use = 0;
-            for (int i = 0; i < nchunks; ++i) {
-                sm100::mbar_wait(&full[s], ph);
-                sm100::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);  // drained two rounds ago
-                TC05_TRACE(1, i);
-                sm100::tc_fence_after();
-                const uint64_t a = adesc0 + (uint64_t)s * stage_step;
-                const uint32_t d = tmem + (uint32_t)buf * (4u * kSlotCols);
-#pragma unroll
-                for (int k = 0; k < (KM > 0 ? KM : 1); ++k) {
-                    if constexpr (kF8)
-                        sm100::mma_f8_ss(d + (uint32_t)(k & 3) * kSlotCols, a + (uint64_t)k * kTileStep,
-                                         bdesc, prm.idesc, k >= 4 ? 1u : 0u);
-                    else
-                        sm100::mma_f16_ss(d + (uint32_t)(k & 3) * kSlotCols, a + (uint64_t)k * kTileStep,
-                                          bdesc, prm.idesc, k >= 4 ? 1u : 0u);
+            __syncwarp();
+        } else if (warp == 1) {
+            if (lane == 0) {  // MMA issuer: one round per valid stage, then END to the epilogue
+                const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
+                const uint64_t adesc0 = sm100::smem_desc_kmajor(sm100::smem_addr(ring), 128, 256);
+                const uint64_t stage_step = stage_bytes >> 4;
+                constexpr uint64_t kTileStep = kTileBytes >> 4;
+                int s = 0, buf = 0;
+                uint32_t ph = 0, use = 0;
+                for (;;) {
+                    sm100::mbar_wait(&full[s], ph);
+                    if (sinfo[s] == 0u) break;
+                    sm100::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);  // drained two rounds ago
+                    sm100::tc_fence_after();
+                    const uint64_t a = adesc0 + (uint64_t)s * stage_step;
+                    const uint32_t d = tmem + (uint32_t)buf * (4u * kSlotCols);
+    #pragma unroll
+                    for (int k = 0; k < (KM > 0 ? KM : 1); ++k) {
+                        if constexpr (kF8)
+                            sm100::mma_f8_ss(d + (uint32_t)(k & 3) * kSlotCols, a + (uint64_t)k * kTileStep,
+                                             bdesc, prm.idesc, k >= 4 ? 1u : 0u);
+                        else
+                            sm100::mma_f16_ss(d + (uint32_t)(k & 3) * kSlotCols, a + (uint64_t)k * kTileStep,
+                                              bdesc, prm.idesc, k >= 4 ? 1u : 0u);
+                    }
+                    sm100::mma_commit(&tfull[buf]);
+                    sm100::mma_commit(&empty[s]);
+                    if (buf) ++use;
+                    buf ^= 1;
+                    if (++s == stages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
                 }
-                sm100::mma_commit(&tfull[buf]);  // this round's accumulators, once complete
-                sm100::mma_commit(&empty[s]);    // SMEM stage free once these MMAs complete
-                TC05_TRACE(2, i);
+                sm100::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);  // that buffer's last round drained
+                tend[buf] = 1u;
+                sm100::mbar_arrive(&tfull[buf]);
+            }
+            __syncwarp();
+        } else {  // epilogue warps 2..5: one round per valid stage until END
+            const uint32_t quarter = (uint32_t)(warp & 3) * 32u;
+            int buf = 0;
+            uint32_t use = 0;
+            for (;;) {
+                sm100::mbar_wait(&tfull[buf], use & 1u);
+                if (tend[buf]) break;
+                sm100::tc_fence_after();
+                const uint32_t base = tmem + (quarter << 16) + (uint32_t)buf * (4u * kSlotCols);
+                uint32_t v[4];
+    #pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = sm100::tmem_ld_32x32b_x1(base + (uint32_t)q * kSlotCols);
+                sm100::tmem_wait_ld();
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(&tempty[buf]);
                 if (buf) ++use;
                 buf ^= 1;
-                if (++s == stages) {
-                    s = 0;
-                    ph ^= 1u;
+                // level 2: D' = 1 x D over the warp's 32 rows x 4 accumulators (exact)
+                const double w = ((double)__uint_as_float(v[0]) + (double)__uint_as_float(v[1])) +
+                                 ((double)__uint_as_float(v[2]) + (double)__uint_as_float(v[3]));
+                const double tot = warp_collapse<true>(w);
+                if (lane == 0) {
+                    if (isfinite(tot)) T += (i128)__double2ll_rn(tot * 0x1p24);
+                    else sp += tot;
                 }
+            }
+            if (blockIdx.x == gridDim.x - 1) {
+                // ragged work (< one chunk past the last full chunk, and the
+                // unaligned head): 512-byte mma.sync tiles, zero padded; a lane's
+                // rows stay below 2^27 (< 2^51 units): exact in binary64
+                const int e = warp - 2;
+                const uint8_t* xr = xa + C * (size_t)stage_bytes;
+                const size_t rem = nb - C * (size_t)stage_bytes;
+                const size_t Tr = rem / 512;
+                const int tail = (int)(rem - Tr * 512);
+                float c[4] = {0.f, 0.f, 0.f, 0.f};
+                double racc = 0.0;
+                const uint4* base = reinterpret_cast<const uint4*>(xr) + lane;
+                auto tile = [&](const uint4& v) {
+                    switch (prm.fmt) {
+                        case 2: mma_rowsum_fp8_as_f16<kE4M3>(c, v); break;
+                        case 3: mma_rowsum_fp8_as_f16<kE5M2>(c, v); break;
+                        default: mma_rowsum(c, v); break;
+                    }
+                    flush_rows(c, racc, lane);
+                };
+                for (size_t t = e; t < Tr; t += 4) tile(ldg_stream(base + t * 32));
+                if (e == 0 && head) tile(load_ragged_bytes(x, (int)head, lane));
+                if (e == 1 && tail) tile(load_ragged_bytes(xr + Tr * 512, tail, lane));
+                if (isfinite(racc)) T += (i128)__double2ll_rn(racc * 0x1p24);
+                else sp += racc;
             }
         }
-        __syncwarp();
-    } else if (warp == 1) {
-        if (lane == 0 && nchunks > 0) {  // MMA issuer
-            const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
-            const uint64_t adesc0 = sm100::smem_desc_kmajor(sm100::smem_addr(ring), 128, 256);
-            const uint64_t stage_step = stage_bytes >> 4, tile_step = kTileBytes >> 4;
-            const uint32_t last_slot = (uint32_t)prm.slots - 1;
-            int s = 0;
-            uint32_t ph = 0;
-            int pos = 0;          // MMA index within the current round
-            int buf = 0;          // TMEM buffer of the current round
-            uint32_t use = 0;     // how many times `buf` was filled before (parity)
-            long long left = total_mma;
-            for (int i = 0; i < nchunks; ++i) {
-                sm100::mbar_wait(&full[s], ph);
-                TC05_TRACE(1, i);
-                sm100::tc_fence_after();
-                uint64_t adesc = adesc0 + (uint64_t)s * stage_step;
-                for (int k = 0; k < kmma; ++k, adesc += tile_step) {
-                    if (pos == 0) {  // buffer drained by the epilogue two rounds ago?
-                        sm100::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
-                        sm100::tc_fence_after();
-                        TC05_TRACE(5, (int)((total_mma - left) / per_round));
-                    }
-                    const uint32_t d = tmem + (uint32_t)buf * buf_cols +
-                                       ((uint32_t)pos & last_slot) * kSlotCols;
-                    if constexpr (kF8)
-                        sm100::mma_f8_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
-                    else
-                        sm100::mma_f16_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
-                    TC05_TRACE(4, (int)(total_mma - left));
-                    --left;
-                    if (++pos == per_round || left == 0) {
-                        sm100::mma_commit(&tfull[buf]);
-                        pos = 0;
-                        if (buf) ++use;
-                        buf ^= 1;
+    } else {
+        if (warp == 0) {
+            if (lane == 0 && nchunks > pre) {  // producer: the chunks after the first ring
+                const uint8_t* src = xa + c_begin * (size_t)stage_bytes + (size_t)pre * chunk_step;
+                for (int i = pre; i < pre + prm.prefetch && i < nchunks; ++i)
+                    sm100::prefetch_l2(src + (size_t)(i - pre) * chunk_step, stage_bytes);
+                int s = pre % stages;
+                uint32_t ph = pre / stages;  // pre <= stages: the first ring is one phase
+                for (int i = pre; i < nchunks; ++i, src += chunk_step) {
+                    if (prm.prefetch && i + prm.prefetch < nchunks)
+                        sm100::prefetch_l2(src + (size_t)prm.prefetch * chunk_step, stage_bytes);
+                    sm100::mbar_wait(&empty[s], ph ^ 1u);
+                    TC05_TRACE(0, i);
+                    sm100::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    uint8_t* dst = ring + (size_t)s * stage_bytes;
+                    for (int q = 0; q < prm.split; ++q)
+                        sm100::bulk_g2s(dst + (size_t)q * piece, src + (size_t)q * piece, piece, &full[s],
+                                        pol);
+                    if (++s == stages) {
+                        s = 0;
+                        ph ^= 1u;
                     }
                 }
-                sm100::mma_commit(&empty[s]);  // SMEM stage free once these MMAs complete
-                TC05_TRACE(2, i);
-                if (++s == stages) {
-                    s = 0;
-                    ph ^= 1u;
-                }
             }
-        }
-        __syncwarp();
-    } else {  // epilogue warps 2..5: TMEM lane quarter (warp % 4)
-        const uint32_t quarter = (uint32_t)(warp & 3) * 32u;
-        const long long rounds = (total_mma + per_round - 1) / per_round;
-        long long left = total_mma;
-        int buf = 0;
-        uint32_t use = 0;
-        for (long long r = 0; r < rounds; ++r) {
-            const int valid = left < prm.slots ? (int)left : prm.slots;
-            left -= per_round;
-            sm100::mbar_wait(&tfull[buf], use & 1u);
-            if (lane == 0 && warp == 2) TC05_TRACE(3, (int)r);
-            sm100::tc_fence_after();
-            const uint32_t base = tmem + (quarter << 16) + (uint32_t)buf * buf_cols;
-            for (int s0 = 0; s0 < valid; s0 += 4) {
-                uint32_t v[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (s0 + q < valid)
-                        v[q] = sm100::tmem_ld_32x32b_x1(base + (uint32_t)(s0 + q) * kSlotCols);
-                sm100::tmem_wait_ld();
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (s0 + q < valid) acc += (double)__uint_as_float(v[q]);
-            }
-            sm100::tc_fence_before();
             __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(&tempty[buf]);
-            if (buf) ++use;
-            buf ^= 1;
-        }
-        if (blockIdx.x == gridDim.x - 1) {
-            // Ragged work (< one chunk past the last full chunk, and the
-            // unaligned head): 512-byte mma.sync tiles, zero padded.
-            const int e = warp - 2;
-            const uint8_t* xr = xa + C * (size_t)stage_bytes;
-            const size_t rem = nb - C * (size_t)stage_bytes;
-            const size_t Tr = rem / 512;
-            const int tail = (int)(rem - Tr * 512);
-            float c[4] = {0.f, 0.f, 0.f, 0.f};
-            const uint4* base = reinterpret_cast<const uint4*>(xr) + lane;
-            auto tile = [&](const uint4& v) {
-                switch (prm.fmt) {
-                    case 1: mma_rowsum_bf16(c, v); break;
-                    case 2: mma_rowsum_fp8_as_f16<kE4M3>(c, v); break;
-                    case 3: mma_rowsum_fp8_as_f16<kE5M2>(c, v); break;
-                    default: mma_rowsum(c, v); break;
+        } else if (KM > 0 && warp == 1) {
+            if (lane == 0 && nchunks > 0) {  // MMA issuer, one round per stage (tight loop)
+                const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
+                const uint64_t adesc0 = sm100::smem_desc_kmajor(sm100::smem_addr(ring), 128, 256);
+                const uint64_t stage_step = stage_bytes >> 4;
+                constexpr uint64_t kTileStep = kTileBytes >> 4;
+                int s = 0, buf = 0;
+                uint32_t ph = 0, use = 0;
+                for (int i = 0; i < nchunks; ++i) {
+                    sm100::mbar_wait(&full[s], ph);
+                    sm100::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);  // drained two rounds ago
+                    TC05_TRACE(1, i);
+                    sm100::tc_fence_after();
+                    const uint64_t a = adesc0 + (uint64_t)s * stage_step;
+                    const uint32_t d = tmem + (uint32_t)buf * (4u * kSlotCols);
+    #pragma unroll
+                    for (int k = 0; k < (KM > 0 ? KM : 1); ++k) {
+                        if constexpr (kF8)
+                            sm100::mma_f8_ss(d + (uint32_t)(k & 3) * kSlotCols, a + (uint64_t)k * kTileStep,
+                                             bdesc, prm.idesc, k >= 4 ? 1u : 0u);
+                        else
+                            sm100::mma_f16_ss(d + (uint32_t)(k & 3) * kSlotCols, a + (uint64_t)k * kTileStep,
+                                              bdesc, prm.idesc, k >= 4 ? 1u : 0u);
+                    }
+                    sm100::mma_commit(&tfull[buf]);  // this round's accumulators, once complete
+                    sm100::mma_commit(&empty[s]);    // SMEM stage free once these MMAs complete
+                    TC05_TRACE(2, i);
+                    if (buf) ++use;
+                    buf ^= 1;
+                    if (++s == stages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
                 }
-                flush_rows(c, acc, lane);
-            };
-            for (size_t t = e; t < Tr; t += 4) tile(ldg_stream(base + t * 32));
-            if (e == 0 && head) tile(load_ragged_bytes(x, (int)head, lane));
-            if (e == 1 && tail) tile(load_ragged_bytes(xr + Tr * 512, tail, lane));
+            }
+            __syncwarp();
+        } else if (warp == 1) {
+            if (lane == 0 && nchunks > 0) {  // MMA issuer
+                const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
+                const uint64_t adesc0 = sm100::smem_desc_kmajor(sm100::smem_addr(ring), 128, 256);
+                const uint64_t stage_step = stage_bytes >> 4, tile_step = kTileBytes >> 4;
+                const uint32_t last_slot = (uint32_t)prm.slots - 1;
+                int s = 0;
+                uint32_t ph = 0;
+                int pos = 0;          // MMA index within the current round
+                int buf = 0;          // TMEM buffer of the current round
+                uint32_t use = 0;     // how many times `buf` was filled before (parity)
+                long long left = total_mma;
+                for (int i = 0; i < nchunks; ++i) {
+                    sm100::mbar_wait(&full[s], ph);
+                    TC05_TRACE(1, i);
+                    sm100::tc_fence_after();
+                    uint64_t adesc = adesc0 + (uint64_t)s * stage_step;
+                    for (int k = 0; k < kmma; ++k, adesc += tile_step) {
+                        if (pos == 0) {  // buffer drained by the epilogue two rounds ago?
+                            sm100::mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
+                            sm100::tc_fence_after();
+                            TC05_TRACE(5, (int)((total_mma - left) / per_round));
+                        }
+                        const uint32_t d = tmem + (uint32_t)buf * buf_cols +
+                                           ((uint32_t)pos & last_slot) * kSlotCols;
+                        if constexpr (kF8)
+                            sm100::mma_f8_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
+                        else
+                            sm100::mma_f16_ss(d, adesc, bdesc, prm.idesc, pos >= prm.slots ? 1u : 0u);
+                        TC05_TRACE(4, (int)(total_mma - left));
+                        --left;
+                        if (++pos == per_round || left == 0) {
+                            sm100::mma_commit(&tfull[buf]);
+                            pos = 0;
+                            if (buf) ++use;
+                            buf ^= 1;
+                        }
+                    }
+                    sm100::mma_commit(&empty[s]);  // SMEM stage free once these MMAs complete
+                    TC05_TRACE(2, i);
+                    if (++s == stages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+            __syncwarp();
+        } else {  // epilogue warps 2..5: TMEM lane quarter (warp % 4)
+            const uint32_t quarter = (uint32_t)(warp & 3) * 32u;
+            const long long rounds = (total_mma + per_round - 1) / per_round;
+            long long left = total_mma;
+            int buf = 0;
+            uint32_t use = 0;
+            for (long long r = 0; r < rounds; ++r) {
+                const int valid = left < prm.slots ? (int)left : prm.slots;
+                left -= per_round;
+                sm100::mbar_wait(&tfull[buf], use & 1u);
+                if (lane == 0 && warp == 2) TC05_TRACE(3, (int)r);
+                sm100::tc_fence_after();
+                const uint32_t base = tmem + (quarter << 16) + (uint32_t)buf * buf_cols;
+                for (int s0 = 0; s0 < valid; s0 += 4) {
+                    uint32_t v[4];
+    #pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (s0 + q < valid)
+                            v[q] = sm100::tmem_ld_32x32b_x1(base + (uint32_t)(s0 + q) * kSlotCols);
+                    sm100::tmem_wait_ld();
+    #pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (s0 + q < valid) acc += (double)__uint_as_float(v[q]);
+                }
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(&tempty[buf]);
+                if (buf) ++use;
+                buf ^= 1;
+            }
+            if (blockIdx.x == gridDim.x - 1) {
+                // Ragged work (< one chunk past the last full chunk, and the
+                // unaligned head): 512-byte mma.sync tiles, zero padded.
+                const int e = warp - 2;
+                const uint8_t* xr = xa + C * (size_t)stage_bytes;
+                const size_t rem = nb - C * (size_t)stage_bytes;
+                const size_t Tr = rem / 512;
+                const int tail = (int)(rem - Tr * 512);
+                float c[4] = {0.f, 0.f, 0.f, 0.f};
+                const uint4* base = reinterpret_cast<const uint4*>(xr) + lane;
+                auto tile = [&](const uint4& v) {
+                    switch (prm.fmt) {
+                        case 1: mma_rowsum_bf16(c, v); break;
+                        case 2: mma_rowsum_fp8_as_f16<kE4M3>(c, v); break;
+                        case 3: mma_rowsum_fp8_as_f16<kE5M2>(c, v); break;
+                        default: mma_rowsum(c, v); break;
+                    }
+                    flush_rows(c, acc, lane);
+                };
+                for (size_t t = e; t < Tr; t += 4) tile(ldg_stream(base + t * 32));
+                if (e == 0 && head) tile(load_ragged_bytes(x, (int)head, lane));
+                if (e == 1 && tail) tile(load_ragged_bytes(xr + Tr * 512, tail, lane));
+            }
         }
     }
     sm100::tc_fence_before();
     __syncthreads();
     TC05_EDGE(2);
     if (warp == 1) sm100::tmem_dealloc(tmem, tmem_cols);
-    complete_block_and_grid<true, kTcWarps>(acc, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
+    if constexpr (kDyn)
+        complete_units_grid<kTcWarps>(T, sp, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
+    else
+        complete_block_and_grid<true, kTcWarps>(acc, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
     TC05_EDGE(3);
 }
 
@@ -414,12 +670,24 @@ using Tc05Kernel = void (*)(const uint8_t*, size_t, Tc05Params, float*, double*,
 
 // The instantiation for (format, MMAs per stage): the tight issue loop for
 // KM = 4, 8, 16 (the peer variant: 8, the default, else the generic loop).
+// dyn: the dynamic-tail variant (binary16 / fp8 with the tight loop; fp8 up
+// to 8 MMAs per stage, the exactness bound of the per-round collapse).
 template <bool kPeer>
-static Tc05Kernel tc05_kernel(bool f8, int km) {
+static Tc05Kernel tc05_kernel(bool f8, int km, bool dyn) {
     if constexpr (kPeer) {
+        if (km == 8 && dyn)
+            return f8 ? reduce_tcgen05_kernel<true, 8, true, true> : reduce_tcgen05_kernel<false, 8, true, true>;
         if (km == 8) return f8 ? reduce_tcgen05_kernel<true, 8, true> : reduce_tcgen05_kernel<false, 8, true>;
         return f8 ? reduce_tcgen05_kernel<true, 0, true> : reduce_tcgen05_kernel<false, 0, true>;
     } else {
+        if (dyn) {
+            switch (km) {
+                case 4: return f8 ? reduce_tcgen05_kernel<true, 4, false, true> : reduce_tcgen05_kernel<false, 4, false, true>;
+                case 8: return f8 ? reduce_tcgen05_kernel<true, 8, false, true> : reduce_tcgen05_kernel<false, 8, false, true>;
+                case 16: if (!f8) return reduce_tcgen05_kernel<false, 16, false, true>; break;
+                default: break;
+            }
+        }
         switch (km) {
             case 4: return f8 ? reduce_tcgen05_kernel<true, 4> : reduce_tcgen05_kernel<false, 4>;
             case 8: return f8 ? reduce_tcgen05_kernel<true, 8> : reduce_tcgen05_kernel<false, 8>;
@@ -450,17 +718,29 @@ static cudaError_t launch_tc05(int fmt, const uint8_t* x, size_t n, float* out_f
     prm.prefetch = cfg.tc05_prefetch;
     prm.split = cfg.tc05_split;
     prm.interleave = cfg.tc05_interleave;
+    prm.dynamic = cfg.tc05_dynamic;  // gated on the run length below
     if (prm.slots < 1 || prm.slots > 16 || (prm.slots & (prm.slots - 1)) || prm.chain < 1 ||
         prm.stage_bytes % kTileBytes || prm.stage_bytes % (16u * (uint32_t)prm.split))
         return cudaErrorInvalidValue;
     const size_t smem = kHeaderBytes + (size_t)prm.stages * prm.stage_bytes;
-    if (kHeaderBytes - 8 < 512 + (size_t)(2 * prm.stages + 4) * 8) return cudaErrorInvalidValue;
+    if (kHeaderBytes - 8 < 512 + (size_t)(2 * prm.stages + 4) * 8 + (size_t)(prm.stages + 2) * 4)
+        return cudaErrorInvalidValue;
     // one accumulator round per stage (4 slots, chain = MMAs per stage / 4):
     // the tight issue loop, instantiated for 4, 8 and 16 MMAs per stage
     const int kmma = (int)(prm.stage_bytes / kTileBytes);
     const int km = (prm.slots == 4 && prm.slots * prm.chain == kmma &&
                     (kmma == 4 || kmma == 8 || kmma == 16)) ? kmma : 0;
-    const Tc05Kernel kernel = tc05_kernel<kPeer>(fmt >= 2, km);
+    // the dynamic tail: binary16 / fp8 (bfloat16 sums are not multiples of
+    // 2^-24), the tight loop, fp8 up to 8 MMAs per stage, dynamic > 0, and
+    // runs of at least cfg.tc05_dyn_min_run chunks per CTA (default 32:
+    // shorter inputs lose more to the ticket latency than the tail costs,
+    // 2^24 6.4 -> 9.4 us, profiles/r02/tc05_dyn_ab1.txt)
+    const size_t chunks = n / (size_t)P * es / prm.stage_bytes;
+    const bool dyn = prm.dynamic > 0 && fmt != 1 && km > 0 && (fmt < 2 || km <= 8) &&
+                     (!kPeer || km == 8) &&
+                     chunks >= (size_t)cfg.tc05_dyn_min_run * (size_t)tcgen05_grid(n / (size_t)P * es, cfg);
+    if (!dyn) prm.dynamic = 0;
+    const Tc05Kernel kernel = tc05_kernel<kPeer>(fmt >= 2, km, dyn);
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;

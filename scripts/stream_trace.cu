@@ -40,7 +40,7 @@ int main(int argc, char** argv) {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     float ms = 0;
-    for (int r = 0; r < 5; ++r) {
+    for (int r = 0, R_ = getenv("TRACE_REPS") ? atoi(getenv("TRACE_REPS")) : 5; r < R_; ++r) {
         cudaEventRecord(a);
         cudaError_t e = tcr::launch_reduce_stream(true, 0, x, n, out, nullptr, ws, cfg, 0);
         cudaEventRecord(b);
@@ -74,6 +74,9 @@ int main(int argc, char** argv) {
            "p100 %.0f | completion p50 %.0f p100 %.0f | last exit %.0f ns\n",
            (int)(63 - __builtin_clzll(n)), G, ms * 1e3, pct(ent, .5), pct(ent, 1), pct(done, 0),
            pct(done, .5), pct(done, 1), pct(fin, .5), pct(fin, 1), (double)(eend - e0));
+    printf("  data done deciles (ns):");
+    for (int q = 0; q <= 10; ++q) printf(" %.0f", pct(done, q / 10.0));
+    printf("\n");
     const int ks[7] = {2, 4, 5, 6, 7, 8, 3};
     printf("  completion step p50 / p100 (ns):");
     for (int i = 0; i + 1 < 7; ++i) {

@@ -21,6 +21,7 @@ int main(int argc, char** argv) {
     cfg.tc05_prefetch = 0;
     cfg.tc05_split = 1;
     cfg.tc05_interleave = 0;
+    cfg.tc05_dynamic = getenv("TRACE_DYN") ? atoi(getenv("TRACE_DYN")) : 0;
     const size_t n = argc > 6 ? ((size_t)1 << atoi(argv[6])) : ((size_t)1 << 30);
     uint16_t* x;
     cudaMalloc(&x, n * 2);
@@ -29,6 +30,8 @@ int main(int argc, char** argv) {
     cudaMalloc(&ws.partials, 8 * 4096);
     cudaMalloc(&ws.ticket, 64);
     cudaMemset(ws.ticket, 0, 64);
+    cudaMalloc(&ws.chunk_next, 64);
+    cudaMemset(ws.chunk_next, 0, 64);
     ws.capacity = 4096;
     float* out;
     cudaMalloc(&out, 4);
@@ -36,7 +39,7 @@ int main(int argc, char** argv) {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     float ms = 0;
-    for (int r = 0; r < 5; ++r) {
+    for (int r = 0, R_ = getenv("TRACE_REPS") ? atoi(getenv("TRACE_REPS")) : 5; r < R_; ++r) {
         cudaEventRecord(a);
         cudaError_t e = tcr::launch_reduce_tcgen05(0, x, n, out, nullptr, ws, cfg, 0);
         cudaEventRecord(b);
@@ -46,8 +49,8 @@ int main(int argc, char** argv) {
         }
         cudaEventElapsedTime(&ms, a, b);
     }
-    printf("cfg stages=%d kb=%d slots=%d chain=%d ctas=%d: %.1f us, %.1f GB/s\n", cfg.tc05_stages,
-           cfg.tc05_stage_kb, cfg.tc05_slots, cfg.tc05_chain, cfg.tc05_ctas, ms * 1e3,
+    printf("cfg stages=%d kb=%d slots=%d chain=%d ctas=%d dyn=%d: %.1f us, %.1f GB/s\n", cfg.tc05_stages,
+           cfg.tc05_stage_kb, cfg.tc05_slots, cfg.tc05_chain, cfg.tc05_ctas, cfg.tc05_dynamic, ms * 1e3,
            n * 2 / (ms * 1e-3) / 1e9);
     static unsigned long long tr[6][4096];
     cudaMemcpyFromSymbol(tr, tcr::g_tc05_trace, sizeof(tr));
@@ -104,6 +107,9 @@ int main(int argc, char** argv) {
            "p50 %.0f p100 %.0f | completion p50 %.0f p100 %.0f | last exit %.0f ns\n",
            G, pct(ent, 0), pct(ent, 0.5), pct(ent, 1), pct(setup, 0.5), pct(setup, 1), pct(data, 0),
            pct(data, 0.5), pct(data, 1), pct(fin, 0.5), pct(fin, 1), (double)(eend - e0));
+    printf("data done deciles (ns):");
+    for (int q = 0; q <= 10; ++q) printf(" %.0f", pct(data, q / 10.0));
+    printf("\n");
     // completion steps: 2 data done -> 4 warp collapse -> 5 syncthreads -> 6 CTA collapse
     // -> 7 partial stored + threadfence -> 8 ticket returned -> 3 exit
     const int ks[7] = {2, 4, 5, 6, 7, 8, 3};

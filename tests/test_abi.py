@@ -203,24 +203,30 @@ def test_no_register_spills_in_any_kernel():
 
 
 def test_default_algo_resolution():
-    """TCR_ALGO_DEFAULT resolves to TCR_CFG_DEFAULT_ALGO (mma.sync by default);
-    its auto value 0 picks by input size (mma.sync below 1 GiB, tcgen05 from
-    1 GiB) for every format.  Host logic only (no device work)."""
+    """TCR_ALGO_DEFAULT resolves to TCR_CFG_DEFAULT_ALGO; its default, 0 = auto,
+    picks by input size and format (r02 §16): tcgen05 (dynamic tail) for
+    binary16 and fp8 from 512 MiB, mma.sync below and for bfloat16 at every
+    size.  Host logic only (no device work)."""
     import paper_1903_03640_b200 as tcr
 
-    assert tcr.tcr_get_config(tcr.TCR_CFG_DEFAULT_ALGO) == tcr.TCR_ALGO_MMA_SYNC
-    f16, e4 = tcr.TCR_DTYPE_F16, tcr.TCR_DTYPE_E4M3
-    for n in (1 << 16, 1 << 29, 1 << 33):
-        assert tcr.tcr_default_algo(n, f16) == tcr.TCR_ALGO_MMA_SYNC
+    assert tcr.tcr_get_config(tcr.TCR_CFG_DEFAULT_ALGO) == tcr.TCR_ALGO_DEFAULT
+    assert tcr.tcr_get_config(tcr.TCR_CFG_TC05_DYNAMIC) == 8
+    assert tcr.tcr_get_config(tcr.TCR_CFG_TC05_DYN_MIN_RUN) == 32
+    f16, bf16, e4, e5 = tcr.TCR_DTYPE_F16, tcr.TCR_DTYPE_BF16, tcr.TCR_DTYPE_E4M3, tcr.TCR_DTYPE_E5M2
+    assert tcr.tcr_default_algo(1 << 16, f16) == tcr.TCR_ALGO_MMA_SYNC
+    assert tcr.tcr_default_algo((1 << 28) - 1, f16) == tcr.TCR_ALGO_MMA_SYNC
+    assert tcr.tcr_default_algo(1 << 28, f16) == tcr.TCR_ALGO_TCGEN05  # 512 MiB
+    assert tcr.tcr_default_algo(1 << 30, f16) == tcr.TCR_ALGO_TCGEN05  # C3
+    for n in (1 << 16, 1 << 30, 1 << 33):
+        assert tcr.tcr_default_algo(n, bf16) == tcr.TCR_ALGO_MMA_SYNC
+    for fmt in (e4, e5):
+        assert tcr.tcr_default_algo((1 << 29) - 1, fmt) == tcr.TCR_ALGO_MMA_SYNC
+        assert tcr.tcr_default_algo(1 << 29, fmt) == tcr.TCR_ALGO_TCGEN05
     try:
-        tcr.tcr_set_config(tcr.TCR_CFG_DEFAULT_ALGO, tcr.TCR_ALGO_DEFAULT)  # auto by size
-        assert tcr.tcr_default_algo(1 << 16, f16) == tcr.TCR_ALGO_MMA_SYNC
-        assert tcr.tcr_default_algo((1 << 29) - 1, f16) == tcr.TCR_ALGO_MMA_SYNC
-        assert tcr.tcr_default_algo(1 << 29, f16) == tcr.TCR_ALGO_TCGEN05  # 1 GiB
-        assert tcr.tcr_default_algo(1 << 30, tcr.TCR_DTYPE_BF16) == tcr.TCR_ALGO_TCGEN05
-        assert tcr.tcr_default_algo((1 << 30) - 1, e4) == tcr.TCR_ALGO_MMA_SYNC
-        assert tcr.tcr_default_algo(1 << 30, e4) == tcr.TCR_ALGO_TCGEN05
+        tcr.tcr_set_config(tcr.TCR_CFG_DEFAULT_ALGO, tcr.TCR_ALGO_MMA_SYNC)
+        for n in (1 << 16, 1 << 29, 1 << 33):
+            assert tcr.tcr_default_algo(n, f16) == tcr.TCR_ALGO_MMA_SYNC
         tcr.tcr_set_config(tcr.TCR_CFG_DEFAULT_ALGO, tcr.TCR_ALGO_SHUFFLE)
         assert tcr.tcr_default_algo(1 << 31, f16) == tcr.TCR_ALGO_SHUFFLE
     finally:
-        tcr.tcr_set_config(tcr.TCR_CFG_DEFAULT_ALGO, tcr.TCR_ALGO_MMA_SYNC)
+        tcr.tcr_set_config(tcr.TCR_CFG_DEFAULT_ALGO, tcr.TCR_ALGO_DEFAULT)
