@@ -765,7 +765,10 @@ def main():
                            ("tc05_stage_kb", tcr.TCR_CFG_TC05_STAGE_KB), ("tc05_slots", tcr.TCR_CFG_TC05_SLOTS),
                            ("tc05_chain", tcr.TCR_CFG_TC05_CHAIN), ("tc05_ctas", tcr.TCR_CFG_TC05_CTAS_PER_SM),
                            ("tc05_prefetch", tcr.TCR_CFG_TC05_PREFETCH), ("tc05_split", tcr.TCR_CFG_TC05_SPLIT),
-                           ("tc05_interleave", tcr.TCR_CFG_TC05_INTERLEAVE))},
+                           ("tc05_interleave", tcr.TCR_CFG_TC05_INTERLEAVE),
+                           ("tc05_dynamic", tcr.TCR_CFG_TC05_DYNAMIC),
+                           ("tc05_dyn_min_run", tcr.TCR_CFG_TC05_DYN_MIN_RUN),
+                           ("default_algo", tcr.TCR_CFG_DEFAULT_ALGO))},
                        "n_total": job_elems_per_step, "l2": "inputs larger than L2 (no flush needed)",
                        "combine": ("fused in-kernel NVLink mailbox combine (peer.py)" if peer
                                    else "NCCL allreduce of fp64 partials") if world > 1 or peer

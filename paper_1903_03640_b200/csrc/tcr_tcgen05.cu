@@ -109,6 +109,7 @@ __device__ __forceinline__ void complete_units_grid(i128 T, double sp, float* ou
     __shared__ long long s_part[WARPS][3];
     __shared__ unsigned s_last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    TCR_COMPLETE_EDGE(9);
     T = warp_sum_i128(T);
     sp = warp_collapse_shfl(sp);
     if (lane == 0) {
