@@ -96,41 +96,44 @@ struct Tc05Params {
     int fmt;               // element format (0 f16, 1 bf16, 2 e4m3, 3 e5m2)
 };
 
-// Levels 3-4 of the dynamic-tail variant (kDyn): every thread passes its
-// exact integer T (units of 2^-24) and the sum `sp` of the non-finite
-// level-2 totals it saw; the CTA and the grid add them as integers
-// (order-free), the last CTA rounds T * 2^-24 once (RNE) -- or returns sp
-// when some total was inf / NaN (inf + -inf = NaN in any order) -- and resets
-// the ticket and the chunk counter for the next launch on this stream.
+// Levels 3-4 of the dynamic-tail variant (kDyn).  Only lane 0 of each
+// epilogue warp holds a value (its exact integer T in units of 2^-24 and the
+// sum `sp` of the non-finite level-2 totals it saw; the last CTA's ragged
+// work is folded into its warp's lane 0 before the call) and has written it
+// to s_part[warp] before the CTA barrier that ends the roles.  Thread 0 adds
+// the CTA's entries, stores the 3-word CTA partial and takes the ticket; the
+// last CTA then loads all G partials at once (one per thread: one L2 round
+// trip), adds them as integers (order-free), rounds T * 2^-24 once (RNE) --
+// or returns sp when some total was inf / NaN (inf + -inf = NaN in any
+// order) -- and resets the ticket and the chunk counter for the next launch
+// on this stream.
+struct UnitsPart {
+    long long lo, hi, sp;  // T = hi:lo, sp as binary64 bits
+};
+
 template <int WARPS>
-__device__ __forceinline__ void complete_units_grid(i128 T, double sp, float* out_f32,
+__device__ __forceinline__ void complete_units_grid(const UnitsPart* s_part, float* out_f32,
                                                     double* out_f64, const DevWorkspace& ws,
                                                     const PeerCombine* pc, int me) {
-    __shared__ long long s_part[WARPS][3];
+    constexpr int kThreads = WARPS * 32;
+    __shared__ UnitsPart s_red[WARPS];
     __shared__ unsigned s_last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    TCR_COMPLETE_EDGE(9);
-    T = warp_sum_i128(T);
-    sp = warp_collapse_shfl(sp);
-    if (lane == 0) {
-        s_part[warp][0] = (long long)(unsigned long long)T;
-        s_part[warp][1] = (long long)(T >> 64);
-        s_part[warp][2] = __double_as_longlong(sp);
-    }
-    TCR_COMPLETE_EDGE(4);
-    __syncthreads();
-    TCR_COMPLETE_EDGE(5);
-    if (warp != 0) return;
     const bool peer = pc && pc->nranks > 0;
-    const unsigned long long prev = peer ? peer_counter(*pc, me) : 0ull;
-    i128 b = lane < WARPS ? make_i128(s_part[lane][0], s_part[lane][1]) : (i128)0;
-    double q = lane < WARPS ? __longlong_as_double(s_part[lane][2]) : 0.0;
-    b = warp_sum_i128(b);
-    q = warp_collapse_shfl(q);
-    TCR_COMPLETE_EDGE(6);
-    if (gridDim.x > 1) {
-        long long* parts = reinterpret_cast<long long*>(ws.partials);  // 3 words per CTA
-        if (lane == 0) {
+    const unsigned long long prev = (peer && warp == 0) ? peer_counter(*pc, me) : 0ull;
+    long long* parts = reinterpret_cast<long long*>(ws.partials);  // 3 words per CTA
+    TCR_COMPLETE_EDGE(4);
+    TCR_COMPLETE_EDGE(5);
+    if (threadIdx.x == 0) {
+        i128 b = 0;
+        double q = 0.0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) {
+            b += make_i128(s_part[w].lo, s_part[w].hi);
+            q += __longlong_as_double(s_part[w].sp);
+        }
+        TCR_COMPLETE_EDGE(6);
+        if (gridDim.x > 1) {
             long long* p = parts + 3 * (size_t)blockIdx.x;
             p[0] = (long long)(unsigned long long)b;
             p[1] = (long long)(b >> 64);
@@ -142,23 +145,43 @@ __device__ __forceinline__ void complete_units_grid(i128 T, double sp, float* ou
             } else {
                 s_last = (ticket_acq_rel(ws.ticket) == gridDim.x - 1) ? 1u : 0u;
             }
+        } else {
+            s_last = 1u;
+            s_red[0] = UnitsPart{(long long)(unsigned long long)b, (long long)(b >> 64),
+                                 __double_as_longlong(q)};
         }
-        __syncwarp();  // lane 0's acquire, then the warp's loads below
-        TCR_COMPLETE_EDGE(8);
-        if (!__shfl_sync(0xffffffffu, s_last, 0)) return;
+    }
+    TCR_COMPLETE_EDGE(8);
+    __syncthreads();  // thread 0's acquire, then CTA-wide: every partial visible
+    TCR_COMPLETE_EDGE(9);
+    if (!s_last) return;
+    if (gridDim.x > 1) {
         if (peer) __threadfence();
-        b = 0;
-        q = 0.0;
-        for (int i = lane; i < (int)gridDim.x; i += 32) {
+        i128 b = 0;
+        double q = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += kThreads) {
             const long long* p = parts + 3 * (size_t)i;
             b += make_i128(__ldcg(p), __ldcg(p + 1));
             q += __longlong_as_double(__ldcg(p + 2));
         }
         b = warp_sum_i128(b);
         q = warp_collapse_shfl(q);
-        if (lane == 0) *ws.ticket = 0u;
+        if (lane == 0) s_red[warp] = UnitsPart{(long long)(unsigned long long)b, (long long)(b >> 64),
+                                                __double_as_longlong(q)};
+        __syncthreads();
     }
-    if (lane == 0) *ws.chunk_next = 0u;  // every CTA's chunk tickets precede its completion ticket
+    if (warp != 0) return;
+    i128 b = 0;  // warp 0, every lane the same sums (peer_combine needs the warp)
+    double q = 0.0;
+    const int nred = gridDim.x > 1 ? WARPS : 1;
+    for (int w = 0; w < nred; ++w) {
+        b += make_i128(s_red[w].lo, s_red[w].hi);
+        q += __longlong_as_double(s_red[w].sp);
+    }
+    if (lane == 0) {
+        if (gridDim.x > 1) *ws.ticket = 0u;
+        *ws.chunk_next = 0u;  // every CTA's chunk tickets precede its completion ticket
+    }
     float f;
     double d;
     if (q != 0.0) {  // some level-2 total was inf or NaN
@@ -448,8 +471,21 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
                 for (size_t t = e; t < Tr; t += 4) tile(ldg_stream(base + t * 32));
                 if (e == 0 && head) tile(load_ragged_bytes(x, (int)head, lane));
                 if (e == 1 && tail) tile(load_ragged_bytes(xr + Tr * 512, tail, lane));
-                if (isfinite(racc)) T += (i128)__double2ll_rn(racc * 0x1p24);
-                else sp += racc;
+                // into lane 0 (every lane's rows: exact integers below 2^51; the
+                // warp's sum below 2^56)
+                long long u = 0;
+                double spl = 0.0;
+                if (isfinite(racc)) u = __double2ll_rn(racc * 0x1p24);
+                else spl = racc;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    u += __shfl_xor_sync(0xffffffffu, u, o);
+                    spl += __shfl_xor_sync(0xffffffffu, spl, o);
+                }
+                if (lane == 0) {
+                    T += (i128)u;
+                    sp += spl;
+                }
             }
         }
     } else {
@@ -615,12 +651,16 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
             }
         }
     }
+    __shared__ UnitsPart s_units[kTcWarps];  // kDyn: lane 0 of every warp (zero for warps 0, 1)
+    if (kDyn && lane == 0)
+        s_units[warp] = UnitsPart{(long long)(unsigned long long)T, (long long)(T >> 64),
+                                  __double_as_longlong(sp)};
     sm100::tc_fence_before();
     __syncthreads();
     TC05_EDGE(2);
     if (warp == 1) sm100::tmem_dealloc(tmem, tmem_cols);
     if constexpr (kDyn)
-        complete_units_grid<kTcWarps>(T, sp, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
+        complete_units_grid<kTcWarps>(s_units, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
     else
         complete_block_and_grid<true, kTcWarps>(acc, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
     TC05_EDGE(3);
