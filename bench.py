@@ -652,7 +652,8 @@ def main():
         host.copy_(x.view(torch.uint8).reshape(-1))
         res_t = torch.empty(1, dtype=torch.float32, device=dev)
         hs = torch.cuda.Stream(dev)
-        tcr.tcr_reduce_sum_host_ex(host, dtype_code, n=n, stream=hs.cuda_stream)  # warm-up
+        for _ in range(3):  # warm-up (a fresh box's first call ran at 85 % of the PCIe rate)
+            tcr.tcr_reduce_sum_host_ex(host, dtype_code, n=n, stream=hs.cuda_stream)
         if world > 1:
             dist.barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
