@@ -24,7 +24,8 @@ for lg in range(10, 33, 2):
     x = gen.generate_tensor(gen.SEED_C2, 0, n, gen.UNIFORM_PM1)
     reps = 100 if lg <= 26 else 10
     t = {}
-    for name, fn in (("mma_sync", lambda: tcr.tcr_reduce_sum_algo(x, out_f32=out, algo="mma_sync")),
+    for name, fn in (("default", lambda: tcr.tcr_reduce_sum_algo(x, out_f32=out, algo="default")),
+                     ("mma_sync", lambda: tcr.tcr_reduce_sum_algo(x, out_f32=out, algo="mma_sync")),
                      ("tcgen05", lambda: tcr.tcr_reduce_sum_algo(x, out_f32=out, algo="tcgen05")),
                      ("shuffle", lambda: tcr.tcr_reduce_sum_algo(x, out_f32=out, algo="shuffle")),
                      ("torch.sum", lambda: torch.sum(x, dtype=torch.float32)),

@@ -83,6 +83,21 @@ for lg in sizes:
         m, mi = statistics.median(res[name]), statistics.median(iso[name])
         print(f"  {name:12s} {m:9.2f} us {es * n / m / 1e3:6.0f} GB/s {m / base:.3f}x mma | "
               f"{mi:9.2f} us {es * n / mi / 1e3:6.0f} GB/s {mi / ibase:.3f}x mma", flush=True)
+    if os.environ.get("SUSTAIN"):  # blocks of 200 launches (~60 ms at 2^30), 4 interleaved rounds
+        import pynvml  # noqa: E402
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(0)
+        sus = {name: [] for name, _, _ in arms}
+        for r in range(4):
+            for name, algo, dyn in arms:
+                setup(dyn)
+                t = b2b(x, algo, 200)
+                sus[name].append((t, pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+        print("  sustained (blocks of 200, us per launch @ SM MHz after the block):")
+        for name, _, _ in arms:
+            print(f"    {name:12s} " + "  ".join(f"{t:8.2f}@{c}" for t, c in sus[name]) +
+                  f"   median {statistics.median(t for t, _ in sus[name]):.2f}", flush=True)
     if lg <= 26:
         g = {}
         for name, algo, dyn in arms:
