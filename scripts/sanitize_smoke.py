@@ -23,6 +23,16 @@ for n in (0, 1, 7, 300, 4096 + 3, (1 << 20) + 77):
         for algo in ("mma_sync", "tcgen05", "shuffle"):
             tcr.tcr_reduce_sum_algo(xh, out_f32=o32, out_f64=o64, algo=algo)
 torch.cuda.synchronize()
+# the tcgen05 dynamic tail at small sizes (forced on: its default gate is >= 32 chunks per CTA)
+tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYN_MIN_RUN, 0)
+for dyn in (8, 100):
+    tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYNAMIC, dyn)
+    for n in (5, 16384 * 3 + 7, (1 << 21) + 9):
+        xh = torch.from_numpy(gen.generate(3, 0, n, gen.UNIFORM_PM1).view(np.int16)).to(dev).view(torch.float16)
+        tcr.tcr_reduce_sum_algo(xh, out_f32=o32, out_f64=o64, algo="tcgen05")
+tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYNAMIC, 8)
+tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYN_MIN_RUN, 32)
+torch.cuda.synchronize()
 n = 100_000
 bits = gen.generate(2, 0, n, gen.WIDE)
 x = torch.from_numpy(bits.view(np.int16)).to(dev).view(torch.float16)
