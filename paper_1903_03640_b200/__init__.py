@@ -68,6 +68,8 @@ TCR_CFG_PEER_TIMEOUT_MS = 17
 TCR_CFG_PDL = 18
 TCR_CFG_TC05_DYNAMIC = 19
 TCR_CFG_TC05_DYN_MIN_RUN = 20
+TCR_CFG_ROWS_TC05 = 21
+TCR_CFG_ROWS_TC05_STAGES = 22
 
 TCR_EXACT_ACC_WORDS = 6
 TCR_EXACT_BF16_ACC_WORDS = 27

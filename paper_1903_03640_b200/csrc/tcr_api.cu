@@ -51,6 +51,8 @@ struct Config {
     int tc05_interleave = 0;
     int tc05_dynamic = 8;  // percent of the chunks handed out at run time (r02 §16)
     int tc05_dyn_min_run = 32;  // ... when every CTA streams >= 32 chunks (r02 §16)
+    int rows_tc05 = 1;          // batched rows on tcgen05 where applicable (r02 §17)
+    int rows_tc05_stages = 8;
     // bulk (TMA -> SMEM -> mma.sync), r02: one CTA per SM with 4 x 32 KiB
     // (8 tiles per consumer warp per stage = the K = 4 chain per accumulator);
     // 2^30: 0.994-0.995 x mma.sync's time vs 1.07-1.09 x for r01's 6 x 16 KiB,
@@ -119,6 +121,8 @@ LaunchCfg make_cfg(const DeviceInfo& di) {
     c.tc05_interleave = g_cfg.tc05_interleave;
     c.tc05_dynamic = g_cfg.tc05_dynamic;
     c.tc05_dyn_min_run = g_cfg.tc05_dyn_min_run;
+    c.rows_tc05 = g_cfg.rows_tc05;
+    c.rows_tc05_stages = g_cfg.rows_tc05_stages;
     c.bulk_stages = g_cfg.bulk_stages;
     c.bulk_stage_kb = g_cfg.bulk_stage_kb;
     c.bulk_ctas = g_cfg.bulk_ctas;
@@ -801,6 +805,14 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             if (value < 0 || value > 1 << 20) break;
             g_cfg.tc05_dyn_min_run = value;
             return TCR_OK;
+        case TCR_CFG_ROWS_TC05:
+            if (value != 0 && value != 1) break;
+            g_cfg.rows_tc05 = value;
+            return TCR_OK;
+        case TCR_CFG_ROWS_TC05_STAGES:
+            if (value < 2 || value > 13) break;
+            g_cfg.rows_tc05_stages = value;
+            return TCR_OK;
         case TCR_CFG_BULK_STAGES:
             if (value < 2 || value > 32) break;
             g_cfg.bulk_stages = value;
@@ -851,6 +863,8 @@ int tcr_get_config(tcr_config_key key) {
         case TCR_CFG_TC05_INTERLEAVE: return g_cfg.tc05_interleave;
         case TCR_CFG_TC05_DYNAMIC: return g_cfg.tc05_dynamic;
         case TCR_CFG_TC05_DYN_MIN_RUN: return g_cfg.tc05_dyn_min_run;
+        case TCR_CFG_ROWS_TC05: return g_cfg.rows_tc05;
+        case TCR_CFG_ROWS_TC05_STAGES: return g_cfg.rows_tc05_stages;
         case TCR_CFG_BULK_STAGES: return g_cfg.bulk_stages;
         case TCR_CFG_BULK_STAGE_KB: return g_cfg.bulk_stage_kb;
         case TCR_CFG_BULK_CTAS_PER_SM: return g_cfg.bulk_ctas;

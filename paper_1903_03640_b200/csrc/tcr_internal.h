@@ -54,6 +54,8 @@ struct LaunchCfg {
                           // (dynamic tail; 0 = static partition)
     int tc05_dyn_min_run; // tcgen05 kernel: the dynamic tail only when every CTA's
                           // static run would be at least this many chunks
+    int rows_tc05;        // batched: 1 = fixed-length rows on tcgen05 (128 segments per MMA)
+    int rows_tc05_stages; // batched tcgen05 kernel: SMEM ring stages of 16 KiB
     int bulk_stages;      // bulk (TMA -> SMEM -> mma.sync) kernel: ring stages
     int bulk_stage_kb;    // bulk kernel: KiB per stage (multiple of 4)
     int bulk_ctas;        // bulk kernel: CTAs per SM
@@ -128,6 +130,11 @@ cudaError_t launch_probe_mma(int algo, const uint16_t* a, const float* c, float*
 // Grid size of the streaming kernels for n elements (shared by the API's
 // workspace sizing and the launchers).
 int stream_grid(size_t n, const LaunchCfg& cfg, int resident = 0);
+// Batched fixed-length rows on tcgen05 (tcr_rows_tc05.cu): 128 segments as
+// the 128 rows of A, TMA tensor copies with 128-byte swizzle.
+bool rows_tc05_supported(int fmt, const void* x, size_t S, size_t L);
+cudaError_t launch_reduce_rows_tc05(int fmt, const void* x, size_t S, size_t L, float* out,
+                                    const LaunchCfg& cfg, cudaStream_t stream);
 int tcgen05_grid(size_t nbytes, const LaunchCfg& cfg);
 
 }  // namespace tcr

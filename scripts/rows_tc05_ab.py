@@ -1,0 +1,46 @@
+"""r02 §17: batched fixed-length rows, tcgen05 (128 segments per MMA, TMA
+tensor copies) vs the mma.sync kernels, 1 GiB of binary16 per L (S = 2^29 / L),
+back to back: 3 warm-up then 30 launches between one event pair, median of 5
+interleaved rounds; GB/s = (2 S L + 4 S) / t."""
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_1903_03640_b200 as tcr  # noqa: E402
+import tcr_inputs as gen  # noqa: E402
+
+Ls = [int(a) for a in sys.argv[1:]] or [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 16384]
+s = torch.cuda.Stream()
+
+
+def run(x, L, out, k=30):
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            tcr.tcr_reduce_sum_batched_ex(x, L, out, algo="mma_sync", stream=s)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(k):
+            tcr.tcr_reduce_sum_batched_ex(x, L, out, algo="mma_sync", stream=s)
+        b.record(s)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1e3 / k
+
+
+for L in Ls:
+    S = (1 << 29) // L
+    x = gen.generate_tensor(gen.SEED_C5, 0, L * S, gen.UNIFORM_PM1)
+    out = torch.empty(S, dtype=torch.float32, device="cuda")
+    res = {0: [], 1: []}
+    for r in range(5):
+        for on in (0, 1):
+            tcr.tcr_set_config(tcr.TCR_CFG_ROWS_TC05, on)
+            res[on].append(run(x, L, out))
+    tcr.tcr_set_config(tcr.TCR_CFG_ROWS_TC05, 1)
+    m0, m1 = statistics.median(res[0]), statistics.median(res[1])
+    gb = lambda us: (2 * S * L + 4 * S) / (us * 1e-6) / 1e9  # noqa: E731
+    print(f"L={L:6d} S={S:9d}  mma.sync {m0:8.1f} us {gb(m0):7.1f} GB/s | tcgen05 rows {m1:8.1f} us "
+          f"{gb(m1):7.1f} GB/s  ratio {m1 / m0:.3f}", flush=True)
+    del x, out
+    torch.cuda.empty_cache()

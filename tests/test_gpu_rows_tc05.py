@@ -1,0 +1,184 @@
+"""Batched fixed-length segments on tcgen05 (TCR_CFG_ROWS_TC05, r02, DESIGN.md
+§17): 128 segments are the 128 rows of A, loaded by TMA tensor copies with a
+128-byte swizzle; row r of D = A x 1 is segment r's partial sum (Eq. 9-10,
+P:171-195), the tensor map's zero fill pads the last box and block (G5).
+
+Checked against the exact oracle element by element (every out[j] within
+2^-20 * sum|x| of segment j, bit-exact indexing on integer data), at segment
+lengths that are and are not multiples of the 64-element box, segment counts
+that are and are not multiples of 128, binary16 and bfloat16, and bitwise
+against a second launch.  Expected values come only from oracle/."""
+import contextlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import tcr_inputs as gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tcr():
+    import torch
+
+    torch.cuda.set_device(0)
+    import paper_1903_03640_b200 as m
+
+    return m
+
+
+@contextlib.contextmanager
+def _rows(tcr, on, stages=None):
+    saved = (tcr.tcr_get_config(tcr.TCR_CFG_ROWS_TC05), tcr.tcr_get_config(tcr.TCR_CFG_ROWS_TC05_STAGES))
+    try:
+        tcr.tcr_set_config(tcr.TCR_CFG_ROWS_TC05, 1 if on else 0)
+        if stages:
+            tcr.tcr_set_config(tcr.TCR_CFG_ROWS_TC05_STAGES, stages)
+        yield
+    finally:
+        tcr.tcr_set_config(tcr.TCR_CFG_ROWS_TC05, saved[0])
+        tcr.tcr_set_config(tcr.TCR_CFG_ROWS_TC05_STAGES, saved[1])
+
+
+def _batched(tcr, x, L, S):
+    import torch
+
+    out = torch.full((S,), float("nan"), dtype=torch.float32, device="cuda")
+    tcr.tcr_reduce_sum_batched_ex(x, L, out, algo="mma_sync")
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _check(got, bits, L, S, fmt="f16"):
+    off = np.arange(S + 1, dtype=np.int64) * L
+    if fmt == "f16":
+        ss = oracle.exact_segment_sums_fp16_array(bits, off, threads=os.cpu_count() or 4)
+        ok = oracle.within_tolerance_segments(got, ss)
+        assert ok.all(), (L, S, np.flatnonzero(~ok)[:10])
+    else:
+        ref = oracle.exact_segment_sums_bf16(bits, off)
+        bad = [j for j in range(S) if not oracle.within_tolerance(float(got[j]), ref[j])]
+        assert not bad, (L, S, bad[:10])
+
+
+def _min_segments(tcr):
+    import torch
+
+    return 128 * torch.cuda.get_device_properties(0).multi_processor_count
+
+
+# (L, extra rows past 128 x SMs): L multiples of 8, below / at / above the box,
+# not multiples of 64; S not a multiple of 128
+CASES = [(8, 0), (16, 5), (24, 127), (32, 1), (40, 77), (64, 0), (72, 3), (128, 129), (200, 11),
+         (256, 64), (512, 7), (1000, 1), (1024, 0), (2048, 33), (4104, 2)]
+
+
+@pytest.mark.parametrize("L,extra", CASES)
+def test_against_oracle_f16(tcr, L, extra):
+    import torch
+
+    S = _min_segments(tcr) + extra
+    bits = gen.generate(700 + L, 0, L * S, gen.UNIFORM_PM1)
+    buf = torch.empty(L * S + 64, dtype=torch.int16, device="cuda")
+    x = buf[8:8 + L * S]  # 16-byte aligned, not 256-byte aligned
+    x.copy_(torch.from_numpy(bits.view(np.int16)))
+    x = x.view(torch.float16)
+    with _rows(tcr, True):
+        got = _batched(tcr, x, L, S)
+        again = _batched(tcr, x, L, S)
+    assert np.array_equal(got.view(np.uint32), again.view(np.uint32))
+    _check(got, bits, L, S)
+    with _rows(tcr, False):  # the mma.sync kernels on the same input: within tolerance too
+        _check(_batched(tcr, x, L, S), bits, L, S)
+
+
+@pytest.mark.parametrize("L", [8, 64, 96, 512])
+def test_integer_data_bitwise(tcr, L):
+    """SMALLINT rows: every partial is an exact integer, so out[j] equals the
+    exact segment sum bit for bit -- a row read from the wrong segment, a box
+    dropped or a K slice counted twice cannot pass."""
+    import torch
+
+    S = _min_segments(tcr) + 45
+    bits = gen.generate(4 + L, 0, L * S, gen.SMALLINT)
+    x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.float16)
+    with _rows(tcr, True):
+        got = _batched(tcr, x, L, S)
+    off = np.arange(S + 1, dtype=np.int64) * L
+    ss = oracle.exact_segment_sums_fp16_array(bits, off, threads=os.cpu_count() or 4)
+    want = np.array([ss[j].f32() for j in range(S)], dtype=np.float32)
+    assert np.array_equal(got, want), np.flatnonzero(got != want)[:10]
+
+
+def test_one_hot_positions(tcr):
+    """A single 1.0 at every position class of a box (K slice, 16-byte chunk
+    within the 128-byte swizzled row, row within the 8-row atom, atom): only
+    its segment reads 1.0."""
+    import torch
+
+    L, S = 192, _min_segments(tcr) + 3
+    rng = np.random.default_rng(5)
+    for _ in range(4):
+        pos = rng.choice(L * S, size=256, replace=False)
+        bits = np.zeros(L * S, dtype=np.uint16)
+        bits[pos] = 0x3C00
+        x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.float16)
+        with _rows(tcr, True):
+            got = _batched(tcr, x, L, S)
+        want = np.bincount(pos // L, minlength=S).astype(np.float32)
+        assert np.array_equal(got, want), np.flatnonzero(got != want)[:10]
+
+
+def test_bfloat16(tcr):
+    import torch
+
+    for L in (64, 136):
+        S = _min_segments(tcr) + 9
+        bits = gen.generate_bf16(31, 0, L * S, gen.UNIFORM_PM1)
+        x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
+        with _rows(tcr, True):
+            got = _batched(tcr, x, L, S)
+        _check(got, bits, L, S, fmt="bf16")
+
+
+@pytest.mark.parametrize("stages", [2, 4, 13])
+def test_ring_depths(tcr, stages):
+    import torch
+
+    L, S = 320, _min_segments(tcr) * 3 + 17
+    bits = gen.generate(9, 0, L * S, gen.WIDE)
+    x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.float16)
+    with _rows(tcr, True, stages=stages):
+        got = _batched(tcr, x, L, S)
+    _check(got, bits, L, S)
+
+
+def test_not_applicable_falls_back(tcr):
+    """Odd lengths, misaligned x, too few segments: the mma.sync kernels run
+    (the result is still right)."""
+    import torch
+
+    for L, S, off in ((100, _min_segments(tcr) + 1, 0), (64, _min_segments(tcr), 1), (64, 1000, 0)):
+        bits = gen.generate(3, 0, L * S, gen.UNIFORM_PM1)
+        buf = torch.empty(L * S + 16, dtype=torch.int16, device="cuda")
+        x = buf[off:off + L * S]
+        x.copy_(torch.from_numpy(bits.view(np.int16)))
+        with _rows(tcr, True):
+            got = _batched(tcr, x.view(torch.float16), L, S)
+        _check(got, bits, L, S)
+
+
+def test_full_size_c5_volume(tcr):
+    """2^29 elements (1 GiB) as 2^21 rows of 256, the volume of BASELINE's C5
+    workload in fixed-length form; every output vs the oracle."""
+    import torch
+
+    L, S = 256, 1 << 21
+    x = gen.generate_tensor(gen.SEED_C5, 0, L * S, gen.UNIFORM_PM1)
+    with _rows(tcr, True):
+        got = _batched(tcr, x, L, S)
+    bits = x.view(torch.int16).cpu().numpy().view(np.uint16)
+    _check(got, bits, L, S)
