@@ -457,12 +457,12 @@ typedef enum {
     TCR_CFG_ROWS_TC05 = 21,       /* batched (MMA): 1 (default) = fixed-length rows
                                    * on tcgen05 where applicable -- binary16 /
                                    * bfloat16, x 16-byte aligned, segment_len a
-                                   * multiple of 8, at least 128 x SMs segments:
+                                   * multiple of 8, at least 256 x SMs segments:
                                    * 128 segments are the 128 rows of A, loaded by
                                    * TMA tensor copies; 0 = the
                                    * mma.sync kernels                             */
-    TCR_CFG_ROWS_TC05_STAGES = 22 /* that kernel's SMEM ring stages of 16 KiB
-                                   * (2..13, default 8)                          */
+    TCR_CFG_ROWS_TC05_STAGES = 22 /* that kernel's SMEM ring stages of 32 KiB
+                                   * (2..6, default 4)                           */
 } tcr_config_key;
 tcr_status tcr_set_config(tcr_config_key key, int value);
 int tcr_get_config(tcr_config_key key); /* -1 for an unknown key */

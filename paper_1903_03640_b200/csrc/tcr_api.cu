@@ -52,7 +52,7 @@ struct Config {
     int tc05_dynamic = 8;  // percent of the chunks handed out at run time (r02 §16)
     int tc05_dyn_min_run = 32;  // ... when every CTA streams >= 32 chunks (r02 §16)
     int rows_tc05 = 1;          // batched rows on tcgen05 where applicable (r02 §17)
-    int rows_tc05_stages = 8;
+    int rows_tc05_stages = 4;
     // bulk (TMA -> SMEM -> mma.sync), r02: one CTA per SM with 4 x 32 KiB
     // (8 tiles per consumer warp per stage = the K = 4 chain per accumulator);
     // 2^30: 0.994-0.995 x mma.sync's time vs 1.07-1.09 x for r01's 6 x 16 KiB,
@@ -810,7 +810,7 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             g_cfg.rows_tc05 = value;
             return TCR_OK;
         case TCR_CFG_ROWS_TC05_STAGES:
-            if (value < 2 || value > 13) break;
+            if (value < 2 || value > 6) break;
             g_cfg.rows_tc05_stages = value;
             return TCR_OK;
         case TCR_CFG_BULK_STAGES:

@@ -134,7 +134,7 @@ int stream_grid(size_t n, const LaunchCfg& cfg, int resident = 0);
 // the 128 rows of A, TMA tensor copies with 128-byte swizzle.
 bool rows_tc05_supported(int fmt, const void* x, size_t S, size_t L);
 cudaError_t launch_reduce_rows_tc05(int fmt, const void* x, size_t S, size_t L, float* out,
-                                    const LaunchCfg& cfg, cudaStream_t stream);
+                                    const DevWorkspace& ws, const LaunchCfg& cfg, cudaStream_t stream);
 int tcgen05_grid(size_t nbytes, const LaunchCfg& cfg);
 
 }  // namespace tcr

@@ -1,11 +1,11 @@
 // tcr_rows_tc05.cu -- fixed-length segments (tcr_reduce_sum_batched) on the
 // 5th-generation tensor cores, 128 segments per MMA as the 128 rows of A:
 //
-//   HBM --(TMA tensor copy: 2-D map {L, S}, box {64 elements, 128 rows},
-//   128-byte swizzle)--> 16 KiB SMEM stage in the canonical K-major SW128
-//   layout --(4 x tcgen05.mma M128 N16 K16, the K slices at +32 B, B = ones)
-//   --> one fp32 TMEM accumulator per box --(tcgen05.ld, one row per
-//   thread)--> binary64 per segment --> out[j].
+//   HBM --(TMA tensor copy: 2-D map {L, S}, box {64 elements, 256 rows},
+//   128-byte swizzle)--> 32 KiB SMEM stage in the canonical K-major SW128
+//   layout --(2 x 4 tcgen05.mma M128 N16 K16: the box's two 128-row halves,
+//   the K slices at +32 B, B = ones)--> two fp32 TMEM accumulators per box
+//   --(tcgen05.ld, two rows per thread)--> binary64 per segment --> out[j].
 //
 // Paper mapping (arXiv 1903.03640): D = A x 1 (Eq. 9-10) with row
 // r of A holding 64 elements of segment r: "the m row sums" are the segment
@@ -22,8 +22,10 @@
 //
 // Warp roles (192 threads): warp 0 lane 0 producer (TMA), warp 1 lane 0 MMA
 // issuer (warp 1 allocates TMEM), warps 2-5 epilogue (TMEM lane quarter
-// warp % 4: rows 32 (warp % 4) .. + 31).  Row blocks are dealt to CTAs in
-// grid-stride order; every role walks the same (block, box) sequence.
+// warp % 4: rows 32 (warp % 4) .. + 31 of both halves).  256-row boxes (32
+// KiB, 8 MMAs) rather than 128-row ones: the issuing thread's per-box
+// bookkeeping (two barrier waits, a commit pair, the block hand-off) was the
+// limit at 16 KiB per box.
 #include <cuda.h>
 
 #include <map>
@@ -39,11 +41,12 @@ namespace {
 
 constexpr int kRtWarps = 6;
 constexpr int kRtBoxK = 64;                      // elements of a segment per box (128 B)
-constexpr int kRtRows = 128;                     // segments per box = M
-constexpr uint32_t kRtStageBytes = kRtBoxK * 2 * kRtRows;  // 16 KiB
+constexpr int kRtRows = 256;                     // segments per box = 2 x M
+constexpr uint32_t kRtHalfBytes = kRtBoxK * 2 * 128;       // one M = 128 half: 16 KiB
+constexpr uint32_t kRtStageBytes = 2 * kRtHalfBytes;       // 32 KiB
 constexpr uint32_t kRtHeader = 1024;             // ones tile + barriers + TMEM address
-constexpr int kRtAcc = 4;                        // TMEM accumulators (16 columns each)
-constexpr uint32_t kRtSlotCols = 16;
+constexpr int kRtAcc = 4;                        // TMEM accumulator pairs (2 x 16 columns each)
+constexpr uint32_t kRtSlotCols = 32;
 
 // K-major, 128-byte-swizzle UMMA descriptor of a 128 x 64 (16-bit) SMEM tile
 // written by a SWIZZLE_128B TMA box: 8-row atoms of 1024 B (SBO), rows of
@@ -75,10 +78,19 @@ struct RtParams {
     int stages;      // SMEM ring stages
     uint32_t idesc;  // kind::f16 instruction descriptor (F16 or BF16 operands)
     uint32_t one_bits;
+    long long dyn;   // row blocks handed out by ticket at the end (the dynamic tail)
 };
 
+// Row blocks [0, Bs) are dealt in grid-stride order, the last `dyn` blocks
+// one at a time from ws.chunk_next
+// (two tickets held ahead), as the flat kernel's dynamic tail (§16): every
+// block is reduced by one CTA in box order, so the schedule cannot change a
+// bit.  The producer writes each stage's block index (-1 = END) next to the
+// stage; the MMA issuer forwards it per accumulator with a plain arrive on
+// tinf[a] (release), which the epilogue waits on before reading it.
 __global__ void __launch_bounds__(kRtWarps * 32)
-reduce_rows_tc05_kernel(const __grid_constant__ CUtensorMap map, RtParams prm, float* __restrict__ out) {
+reduce_rows_tc05_kernel(const __grid_constant__ CUtensorMap map, RtParams prm, float* __restrict__ out,
+                        DevWorkspace ws) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int stages = prm.stages;
     uint32_t* ones = reinterpret_cast<uint32_t*>(smem);        // 512 B of ones (B operand)
@@ -86,14 +98,20 @@ reduce_rows_tc05_kernel(const __grid_constant__ CUtensorMap map, RtParams prm, f
     uint64_t* empty = full + stages;                           // [stages]
     uint64_t* tfull = empty + stages;                          // [kRtAcc]
     uint64_t* tempty = tfull + kRtAcc;                         // [kRtAcc]
+    uint64_t* tinf = tempty + kRtAcc;                          // [kRtAcc]
+    volatile int* sinfo = reinterpret_cast<volatile int*>(tinf + kRtAcc);  // [stages]
+    volatile int* tinfo = sinfo + stages;                                  // [kRtAcc]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kRtHeader - 8);
     uint8_t* ring = smem + kRtHeader;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    const size_t blocks = (prm.S + kRtRows - 1) / kRtRows;
-    const size_t G = gridDim.x, b0 = blockIdx.x;
-    const long long my_blocks = b0 < blocks ? (long long)((blocks - b0 + G - 1) / G) : 0;
-    const long long boxes = my_blocks * prm.nk;
+    const long long blocks = (long long)((prm.S + kRtRows - 1) / kRtRows);
+    const long long Bs = blocks - prm.dyn;
+    const long long G = gridDim.x, b = blockIdx.x;
+    // static part in grid-stride order (CTA b: blocks b, b + G, ... < Bs): at
+    // any moment the grid reads neighbouring blocks (contiguous runs per CTA
+    // measured ~10 % slower, profiles/r02/rows_tc05_ab2.txt)
+    const long long n_static = b < Bs ? (Bs - b + G - 1) / G : 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -103,57 +121,97 @@ reduce_rows_tc05_kernel(const __grid_constant__ CUtensorMap map, RtParams prm, f
         for (int a = 0; a < kRtAcc; ++a) {
             sm100::mbar_init(&tfull[a], 1);
             sm100::mbar_init(&tempty[a], 4);
+            sm100::mbar_init(&tinf[a], 1);
         }
         sm100::fence_mbar_init();
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
     }
     for (int i = threadIdx.x; i < 128; i += blockDim.x) ones[i] = prm.one_bits;
     sm100::fence_proxy_async_smem();
-    constexpr uint32_t kCols = kRtAcc * kRtSlotCols;  // 64 columns
+    constexpr uint32_t kCols = kRtAcc * kRtSlotCols;  // 128 columns
     if (warp == 1) sm100::tmem_alloc(tmem_slot, kCols);
     sm100::tc_fence_before();
     __syncthreads();
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    pdl_wait_and_release();  // the previous kernel's writes (x, out) visible
+    pdl_wait_and_release();  // the previous kernel's writes (x, out, counters) visible
 
     if (warp == 0) {
-        if (lane == 0) {  // producer: one TMA box per (row block, K box)
+        if (lane == 0) {  // producer: nk TMA boxes per row block, then END
             int s = 0;
             uint32_t ph = 0;
-            for (long long j = 0; j < boxes; ++j) {
-                const long long u = (long long)b0 + (j / prm.nk) * (long long)G;
-                const int k = (int)(j % prm.nk);
-                sm100::mbar_wait(&empty[s], ph ^ 1u);
-                sm100::mbar_arrive_expect_tx(&full[s], kRtStageBytes);
-                tma_load_2d(ring + (size_t)s * kRtStageBytes, &map, k * kRtBoxK, (int)(u * kRtRows), &full[s]);
-                if (++s == stages) {
-                    s = 0;
-                    ph ^= 1u;
+            auto block_boxes = [&](long long u) {
+                for (int k = 0; k < prm.nk; ++k) {
+                    sm100::mbar_wait(&empty[s], ph ^ 1u);
+                    sinfo[s] = (int)u;
+                    sm100::mbar_arrive_expect_tx(&full[s], kRtStageBytes);
+                    tma_load_2d(ring + (size_t)s * kRtStageBytes, &map, k * kRtBoxK, (int)(u * kRtRows),
+                                &full[s]);
+                    if (++s == stages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            };
+            unsigned t0 = 0u, t1 = 0u;
+            bool f0 = false, f1 = false;
+            for (long long i = 0; i < n_static; ++i) {
+                if (prm.dyn && !f0 && n_static - i <= 2) {
+                    t0 = atomicAdd(ws.chunk_next, 1u);
+                    f0 = true;
+                }
+                if (prm.dyn && !f1 && n_static - i <= 1) {
+                    t1 = atomicAdd(ws.chunk_next, 1u);
+                    f1 = true;
+                }
+                block_boxes(b + i * G);
+            }
+            if (prm.dyn) {
+                if (!f0) t0 = atomicAdd(ws.chunk_next, 1u);
+                if (!f1) t1 = atomicAdd(ws.chunk_next, 1u);
+                for (;;) {
+                    const unsigned t = t0;
+                    t0 = t1;
+                    t1 = atomicAdd(ws.chunk_next, 1u);
+                    if ((long long)t >= prm.dyn) break;
+                    block_boxes(Bs + (long long)t);
                 }
             }
+            sm100::mbar_wait(&empty[s], ph ^ 1u);  // END: a stage with no bytes
+            sinfo[s] = -1;
+            sm100::mbar_arrive(&full[s]);
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer: 4 MMAs per box into accumulator j % kRtAcc
+        if (lane == 0) {  // MMA issuer: 2 x 4 MMAs per box into accumulator pair j % kRtAcc
             const uint64_t bdesc = sm100::smem_desc_kmajor(sm100::smem_addr(ones), 128, 256);
             const uint64_t adesc0 = smem_desc_sw128(sm100::smem_addr(ring));
             constexpr uint64_t kStageStep = kRtStageBytes >> 4;
             int s = 0;
             uint32_t ph = 0;
-            for (long long j = 0; j < boxes; ++j) {
+            for (long long j = 0;; ++j) {
                 const int a = (int)(j % kRtAcc);
                 const uint32_t use = (uint32_t)(j / kRtAcc);
                 sm100::mbar_wait(&full[s], ph);
+                const int u = sinfo[s];
                 sm100::mbar_wait(&tempty[a], (use & 1u) ^ 1u);  // drained kRtAcc boxes ago
+                tinfo[a] = u;
+                if (u < 0) {
+                    sm100::mbar_arrive(&tinf[a]);
+                    break;
+                }
                 sm100::tc_fence_after();
                 const uint64_t ad = adesc0 + (uint64_t)s * kStageStep;
                 const uint32_t d = tmem + (uint32_t)a * kRtSlotCols;
 #pragma unroll
-                for (int q = 0; q < kRtBoxK / 16; ++q)  // K slice q: +32 B = +2 in the descriptor
-                    sm100::mma_f16_ss(d, ad + (uint64_t)(2 * q), bdesc, prm.idesc, q > 0 ? 1u : 0u);
+                for (int h = 0; h < 2; ++h)  // rows 128 h .. 128 h + 127 of the box: +16 KiB
+#pragma unroll
+                    for (int q = 0; q < kRtBoxK / 16; ++q)  // K slice q: +32 B = +2 in the descriptor
+                        sm100::mma_f16_ss(d + 16u * (uint32_t)h, ad + (uint64_t)(h * (kRtHalfBytes >> 4) + 2 * q),
+                                          bdesc, prm.idesc, q > 0 ? 1u : 0u);
                 sm100::mma_commit(&tfull[a]);
                 sm100::mma_commit(&empty[s]);
+                sm100::mbar_arrive(&tinf[a]);
                 if (++s == stages) {
                     s = 0;
                     ph ^= 1u;
@@ -163,30 +221,44 @@ reduce_rows_tc05_kernel(const __grid_constant__ CUtensorMap map, RtParams prm, f
         __syncwarp();
     } else {  // epilogue: row r = 32 (warp % 4) + lane of every box
         const uint32_t quarter = (uint32_t)(warp & 3) * 32u;
-        const int row = (int)quarter + lane;
-        double acc = 0.0;
-        for (long long j = 0; j < boxes; ++j) {
+        const int row = (int)quarter + lane;  // and row + 128 (the box's second M half)
+        double acc = 0.0, acc2 = 0.0;
+        int k = 0;
+        for (long long j = 0;; ++j) {
             const int a = (int)(j % kRtAcc);
             const uint32_t use = (uint32_t)(j / kRtAcc);
+            sm100::mbar_wait(&tinf[a], use & 1u);
+            const int u = tinfo[a];
+            if (u < 0) break;
             sm100::mbar_wait(&tfull[a], use & 1u);
             sm100::tc_fence_after();
-            const uint32_t v = sm100::tmem_ld_32x32b_x1(tmem + (quarter << 16) + (uint32_t)a * kRtSlotCols);
+            const uint32_t taddr = tmem + (quarter << 16) + (uint32_t)a * kRtSlotCols;
+            const uint32_t v = sm100::tmem_ld_32x32b_x1(taddr);
+            const uint32_t v2 = sm100::tmem_ld_32x32b_x1(taddr + 16u);
             sm100::tmem_wait_ld();
             sm100::tc_fence_before();
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(&tempty[a]);
             acc += (double)__uint_as_float(v);
-            if ((int)(j % prm.nk) == prm.nk - 1) {  // the row block's last box: segment done
-                const size_t u = b0 + (size_t)(j / prm.nk) * G;
-                const size_t seg = u * kRtRows + (size_t)row;
+            acc2 += (double)__uint_as_float(v2);
+            if (++k == prm.nk) {  // the row block's last box: its segments are done
+                const size_t seg = (size_t)u * kRtRows + (size_t)row;
                 if (seg < prm.S) out[seg] = (float)acc;
-                acc = 0.0;
+                if (seg + 128 < prm.S) out[seg + 128] = (float)acc2;
+                acc = acc2 = 0.0;
+                k = 0;
             }
         }
     }
     sm100::tc_fence_before();
     __syncthreads();
     if (warp == 1) sm100::tmem_dealloc(tmem, kCols);
+    // the last CTA resets the block counter (every CTA's tickets precede its
+    // completion ticket in thread 0's program order)
+    if (prm.dyn && threadIdx.x == 0 && ticket_acq_rel(ws.ticket) == gridDim.x - 1) {
+        *ws.chunk_next = 0u;
+        *ws.ticket = 0u;
+    }
 }
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -217,7 +289,7 @@ bool rows_tc05_supported(int fmt, const void* x, size_t S, size_t L) {
 }
 
 cudaError_t launch_reduce_rows_tc05(int fmt, const void* x, size_t S, size_t L, float* out,
-                                    const LaunchCfg& cfg, cudaStream_t stream) {
+                                    const DevWorkspace& ws, const LaunchCfg& cfg, cudaStream_t stream) {
     EncodeTiled enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
     CUtensorMap map;
@@ -236,7 +308,8 @@ cudaError_t launch_reduce_rows_tc05(int fmt, const void* x, size_t S, size_t L, 
     const uint32_t ab = fmt == kBF16 ? ((1u << 7) | (1u << 10)) : 0u;
     prm.idesc = sm100::idesc_f16_f32(128, 16) | ab;
     prm.one_bits = fmt == kBF16 ? 0x3F803F80u : 0x3C003C00u;
-    if (prm.stages < 2 || kRtHeader - 8 < 512 + (size_t)(2 * prm.stages + 2 * kRtAcc) * 8)
+    if (prm.stages < 2 ||
+        kRtHeader - 8 < 512 + (size_t)(2 * prm.stages + 3 * kRtAcc) * 8 + (size_t)(prm.stages + kRtAcc) * 4)
         return cudaErrorInvalidValue;
     const size_t smem = kRtHeader + (size_t)prm.stages * kRtStageBytes;
     int dev = 0;
@@ -257,8 +330,11 @@ cudaError_t launch_reduce_rows_tc05(int fmt, const void* x, size_t S, size_t L, 
     const size_t blocks = (S + kRtRows - 1) / kRtRows;
     size_t g = (size_t)cfg.sms;
     if (g > blocks) g = blocks;
+    // the dynamic tail (TCR_CFG_TC05_DYNAMIC percent of the row blocks) when
+    // every CTA has a run of at least 8 blocks
+    prm.dyn = (blocks >= 8 * g) ? (long long)(blocks * (size_t)cfg.tc05_dynamic / 100u) : 0;
     launch_maybe_pdl(reduce_rows_tc05_kernel, dim3((unsigned)g), dim3(kRtWarps * 32), smem, stream, cfg.pdl,
-                     map, prm, out);
+                     map, prm, out, ws);
     return cudaGetLastError();
 }
 

@@ -377,10 +377,10 @@ cudaError_t launch_reduce_segmented(bool mma, int fmt, bool batched, const void*
                                     size_t segment_len, float* out, const DevWorkspace& ws,
                                     const LaunchCfg& cfg, cudaStream_t stream) {
     // fixed-length rows on tcgen05 (tcr_rows_tc05.cu) when every SM gets a
-    // block of 128 segments
-    if (mma && batched && cfg.rows_tc05 && num_segments >= (size_t)128 * (size_t)cfg.sms &&
+    // block of 256 segments
+    if (mma && batched && cfg.rows_tc05 && num_segments >= (size_t)256 * (size_t)cfg.sms &&
         rows_tc05_supported(fmt, x, num_segments, segment_len))
-        return launch_reduce_rows_tc05(fmt, x, num_segments, segment_len, out, cfg, stream);
+        return launch_reduce_rows_tc05(fmt, x, num_segments, segment_len, out, ws, cfg, stream);
     size_t g = (num_segments + kSegWarps - 1) / kSegWarps;
     const size_t gmax = (size_t)cfg.sms * kSegCtasPerSm;
     if (g > gmax) g = gmax;

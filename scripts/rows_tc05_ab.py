@@ -13,6 +13,10 @@ import tcr_inputs as gen  # noqa: E402
 
 Ls = [int(a) for a in sys.argv[1:]] or [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 16384]
 s = torch.cuda.Stream()
+DYNS = [int(v) for v in __import__("os").environ.get("DYNS", "0 8").split()]
+if __import__("os").environ.get("STAGES"):
+    tcr.tcr_set_config(tcr.TCR_CFG_ROWS_TC05_STAGES, int(__import__("os").environ["STAGES"]))
+print("rows_tc05 stages", tcr.tcr_get_config(tcr.TCR_CFG_ROWS_TC05_STAGES), flush=True)
 
 
 def run(x, L, out, k=30):
@@ -32,15 +36,21 @@ for L in Ls:
     S = (1 << 29) // L
     x = gen.generate_tensor(gen.SEED_C5, 0, L * S, gen.UNIFORM_PM1)
     out = torch.empty(S, dtype=torch.float32, device="cuda")
-    res = {0: [], 1: []}
+    arms = [(0, 8)] + [(1, d) for d in DYNS]  # (rows_tc05, dynamic %)
+    res = {a: [] for a in arms}
     for r in range(5):
-        for on in (0, 1):
+        for on, d in arms:
             tcr.tcr_set_config(tcr.TCR_CFG_ROWS_TC05, on)
-            res[on].append(run(x, L, out))
+            tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYNAMIC, d)
+            res[(on, d)].append(run(x, L, out))
     tcr.tcr_set_config(tcr.TCR_CFG_ROWS_TC05, 1)
-    m0, m1 = statistics.median(res[0]), statistics.median(res[1])
+    tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYNAMIC, 8)
     gb = lambda us: (2 * S * L + 4 * S) / (us * 1e-6) / 1e9  # noqa: E731
-    print(f"L={L:6d} S={S:9d}  mma.sync {m0:8.1f} us {gb(m0):7.1f} GB/s | tcgen05 rows {m1:8.1f} us "
-          f"{gb(m1):7.1f} GB/s  ratio {m1 / m0:.3f}", flush=True)
+    m0 = statistics.median(res[(0, 8)])
+    line = f"L={L:6d} S={S:9d}  mma.sync {m0:8.1f} us {gb(m0):7.1f} GB/s"
+    for on, d in arms[1:]:
+        m = statistics.median(res[(on, d)])
+        line += f" | tc05 dyn{d} {m:8.1f} us {gb(m):7.1f} GB/s {m / m0:.3f}"
+    print(line, flush=True)
     del x, out
     torch.cuda.empty_cache()
