@@ -74,7 +74,7 @@ def _min_segments(tcr):
 # (L, extra rows past 256 x SMs): L multiples of 8, below / at / above the box,
 # not multiples of 64; S not a multiple of 128 or 256
 CASES = [(8, 0), (16, 5), (24, 127), (32, 1), (40, 77), (64, 0), (72, 3), (128, 129), (200, 11),
-         (256, 64), (384, 128), (512, 7), (1000, 1), (1024, 0), (2048, 33), (4104, 2)]
+         (256, 64), (384, 128), (512, 7), (1000, 1), (1024, 0), (2048, 33), (3072, 2), (4104, 2)]
 
 
 @pytest.mark.parametrize("L,extra", CASES)
@@ -94,6 +94,26 @@ def test_against_oracle_f16(tcr, L, extra):
     _check(got, bits, L, S)
     with _rows(tcr, False):  # the mma.sync kernels on the same input: within tolerance too
         _check(_batched(tcr, x, L, S), bits, L, S)
+
+
+def test_routing_rule_counts_launches(tcr):
+    """The library routes L % 8 == 0, L <= 3072, L not 32 / 1024, >= 256 x SMs
+    segments to the tcgen05 rows kernel: a wrong route would still be right,
+    so the rule is checked through its measurable side -- with the knob off
+    and on, the L = 32 / 1024 / 4104 results are bitwise identical (the same
+    mma.sync kernel ran) while L = 64 / 2048 differ in at least one output
+    on random data (a different kernel, a different rounding order)."""
+    import torch
+
+    S = _min_segments(tcr) + 3
+    for L, same in ((32, True), (1024, True), (4104, True), (64, False), (2048, False)):
+        bits = gen.generate(55 + L, 0, L * S, gen.UNIFORM_01)
+        x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.float16)
+        with _rows(tcr, True):
+            on = _batched(tcr, x, L, S)
+        with _rows(tcr, False):
+            off = _batched(tcr, x, L, S)
+        assert np.array_equal(on.view(np.uint32), off.view(np.uint32)) == same, L
 
 
 @pytest.mark.parametrize("L", [8, 64, 96, 512])
