@@ -163,6 +163,34 @@ def test_sass_fused_peer_kernel_has_mma_and_system_scope_peer_traffic():
     assert tplain and "STRONG.SYS" not in tplain[0]
 
 
+def test_sass_dynamic_tail_and_rows_kernels():
+    """r02 §16-§17 in SASS: the default large-n kernel (tcgen05 with the
+    dynamic tail) carries the bulk copies into SMEM (UBLKCP), the tensor-core
+    tiles (UTCHMMA), the TMEM reads (LDTM), the per-round D' = 1 x D DMMA
+    collapse and the chunk-ticket atomics; the batched rows kernel loads its
+    boxes with 2-D TMA tensor copies (UTMALDG.2D) and reduces them with
+    UTCHMMA."""
+    import re
+    import shutil
+    import subprocess
+
+    import paper_1903_03640_b200 as tcr
+
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run(["cuobjdump", "-sass", tcr.LIB_PATH], capture_output=True,
+                          text=True, check=True).stdout
+    funcs = re.split(r"\n\s+Function : ", sass)[1:]
+    dyn = [f for f in funcs if f.startswith("_ZN3tcr21reduce_tcgen05_kernelILb0ELi8ELb0ELb1E")]
+    assert dyn, "dynamic-tail tcgen05 kernel not found"
+    for mnemonic in ("UBLKCP", "UTCHMMA", "LDTM", "DMMA.8x8x4", "ATOMG"):
+        assert mnemonic in dyn[0], mnemonic
+    rows = [f for f in funcs if "reduce_rows_tc05_kernel" in f.split("\n", 1)[0]]
+    assert rows, "tcgen05 rows kernel not found"
+    for mnemonic in ("UTMALDG.2D", "UTCHMMA", "LDTM"):
+        assert mnemonic in rows[0], mnemonic
+
+
 def test_product_path_fails_loudly_without_the_library(tmp_path):
     """No fallback: a copy of the package without libtcr.so refuses to import."""
     import shutil
