@@ -174,6 +174,13 @@ tcr_status tcr_reduce_sum_segmented_ex(const void *x, tcr_dtype dtype, const int
 /*
  * tcr_reduce_sum_batched -- num_segments contiguous segments of segment_len
  * elements each: out[j] = R(x[j*segment_len .. (j+1)*segment_len)).
+ * Same accuracy contract per segment as tcr_reduce_sum; bitwise
+ * deterministic.  Kernel choice (internal, TCR_CFG_ROWS_TC05): binary16 /
+ * bfloat16 rows with x 16-byte aligned, segment_len % 8 == 0, segment_len <=
+ * 3072 (not 32 or 1024) and at least 256 x SMs segments run on tcgen05 with
+ * 256 segments per TMA tensor box, each segment a row of A (Eq. 9-10);
+ * otherwise the mma.sync kernels (16 segments as the 16 rows of A for
+ * segment_len % 32 == 0 up to 2048, whole-tile rows, or the union stream).
  */
 tcr_status tcr_reduce_sum_batched(const tcr_half *x, size_t num_segments, size_t segment_len,
                                   float *out, tcr_stream stream);
