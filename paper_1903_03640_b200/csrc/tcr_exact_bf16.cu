@@ -19,15 +19,14 @@
 // Levels 2-4 add the per-window totals as int128 (order-free); the last CTA
 // assembles T = 2 I_0 + sum_k I_k 2^(32k) in units of 2^-134 in a 384-bit
 // integer and rounds it once (RNE) to binary32 / binary64.
+#include "tcr_bigint.cuh"
 #include "tcr_device.cuh"
+#include "tcr_int128.cuh"
 #include "tcr_internal.h"
 
 namespace tcr {
 
 namespace {
-
-typedef __int128 i128;
-typedef unsigned __int128 u128;
 
 constexpr int kXbWarps = 8;
 constexpr int kXbU = 4;
@@ -57,76 +56,6 @@ __device__ __forceinline__ long long half_units(uint32_t h, int& k) {
     return (h & 0x8000u) ? -v : v;
 }
 
-__device__ __forceinline__ i128 shfl_xor_i128(i128 v, int o) {
-    const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
-    const unsigned long long lo2 = __shfl_xor_sync(0xffffffffu, lo, o);
-    const unsigned long long hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
-    return (i128)(((u128)hi2 << 64) | (u128)lo2);
-}
-
-__device__ __forceinline__ i128 warp_sum_i128(i128 v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += shfl_xor_i128(v, o);
-    return v;
-}
-
-// 384-bit two's complement accumulator: limbs l[0] (least significant) .. l[5].
-struct Big384 {
-    unsigned long long l[6];
-};
-
-__device__ void big_add_shifted(Big384& B, i128 v, int shift) {  // B += v * 2^shift (mod 2^384)
-    const unsigned long long ext = v < 0 ? ~0ull : 0ull;
-    unsigned long long e[7];  // v sign-extended to 448 bits
-    e[0] = (unsigned long long)v;
-    e[1] = (unsigned long long)(v >> 64);
-    for (int i = 2; i < 7; ++i) e[i] = ext;
-    const int q = shift >> 6, r = shift & 63;
-    unsigned long long carry = 0;
-    for (int i = 0; i < 6; ++i) {
-        const int j = i - q;
-        unsigned long long w = 0;
-        if (j >= 0) w = r ? (e[j] << r) : e[j];
-        if (r && j - 1 >= 0) w |= e[j - 1] >> (64 - r);
-        const unsigned long long a0 = B.l[i];
-        const unsigned long long s1 = a0 + w;
-        const unsigned long long c1 = s1 < a0 ? 1ull : 0ull;
-        const unsigned long long s2 = s1 + carry;
-        const unsigned long long c2 = s2 < s1 ? 1ull : 0ull;
-        B.l[i] = s2;
-        carry = c1 | c2;
-    }
-}
-
-// RNE of the non-negative 384-bit M (units 2^-134) to `bits` significant bits:
-// value = mant * 2^(exp - 134).
-__device__ void big_round(const Big384& M, int bits, unsigned long long& mant, int& exp) {
-    int top = -1;
-    for (int i = 5; i >= 0 && top < 0; --i)
-        if (M.l[i]) top = i * 64 + 63 - __clzll((long long)M.l[i]);
-    if (top < 0) {
-        mant = 0;
-        exp = 0;
-        return;
-    }
-    auto bit = [&](int p) -> unsigned long long { return (M.l[p >> 6] >> (p & 63)) & 1ull; };
-    if (top < bits) {  // fits: exact
-        unsigned long long m = 0;
-        for (int p = top; p >= 0; --p) m = (m << 1) | bit(p);
-        mant = m;
-        exp = 0;
-        return;
-    }
-    const int shift = top - (bits - 1);
-    unsigned long long q = 0;
-    for (int p = top; p >= shift; --p) q = (q << 1) | bit(p);
-    const unsigned long long half = bit(shift - 1);
-    bool sticky = false;
-    for (int p = shift - 2; p >= 0 && !sticky; --p) sticky = bit(p) != 0;
-    if (half && (sticky || (q & 1ull))) ++q;  // may reach 2^bits: still exact below
-    mant = q;
-    exp = shift;
-}
 
 // RNE binary32 / binary64 of T = 2 I_0 + sum_k I_k 2^(32k) (units 2^-134), or
 // the IEEE special value when inf / NaN inputs were counted.

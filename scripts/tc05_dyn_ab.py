@@ -62,7 +62,7 @@ for lg in sizes:
         x = gen.generate_tensor_fp8(gen.SEED_C3, 0, n, gen.UNIFORM_PM1,
                                     gen.FP8_E4M3 if dtype == "e4m3" else gen.FP8_E5M2)
     else:
-        x = gen.generate_tensor(gen.SEED_C3, 0, n, gen.UNIFORM_PM1)
+        x = gen.generate_tensor(gen.SEED_C3, 0, n, gen.UNIFORM_PM1, bf16=(dtype == "bf16"))
     for name, algo, dyn in arms:  # warm every path over this buffer
         setup(dyn)
         b2b(x, algo, 30)

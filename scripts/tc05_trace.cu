@@ -41,7 +41,7 @@ int main(int argc, char** argv) {
     float ms = 0;
     for (int r = 0, R_ = getenv("TRACE_REPS") ? atoi(getenv("TRACE_REPS")) : 5; r < R_; ++r) {
         cudaEventRecord(a);
-        cudaError_t e = tcr::launch_reduce_tcgen05(0, x, n, out, nullptr, ws, cfg, 0);
+        cudaError_t e = tcr::launch_reduce_tcgen05(getenv("TRACE_FMT") ? atoi(getenv("TRACE_FMT")) : 0, x, n, out, nullptr, ws, cfg, 0);
         cudaEventRecord(b);
         if (e || (e = cudaDeviceSynchronize())) {
             printf("error %s\n", cudaGetErrorString(e));
