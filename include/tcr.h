@@ -177,8 +177,8 @@ tcr_status tcr_reduce_sum_segmented_ex(const void *x, tcr_dtype dtype, const int
  * Same accuracy contract per segment as tcr_reduce_sum; bitwise
  * deterministic.  Kernel choice (internal, TCR_CFG_ROWS_TC05): binary16 /
  * bfloat16 rows with x 16-byte aligned, segment_len % 8 == 0, segment_len <=
- * 3072 (not 32 or 1024) and at least 256 x SMs segments run on tcgen05 with
- * 256 segments per TMA tensor box, each segment a row of A (Eq. 9-10);
+ * 3072 (not 1024) and at least 256 x SMs segments run on tcgen05 with 256
+ * segments per TMA tensor box, each segment a row of A (Eq. 9-10);
  * otherwise the mma.sync kernels (16 segments as the 16 rows of A for
  * segment_len % 32 == 0 up to 2048, whole-tile rows, or the union stream).
  */
@@ -464,7 +464,8 @@ typedef enum {
     TCR_CFG_ROWS_TC05 = 21,       /* batched (MMA): 1 (default) = fixed-length rows
                                    * on tcgen05 where applicable -- binary16 /
                                    * bfloat16, x 16-byte aligned, segment_len a
-                                   * multiple of 8, at least 256 x SMs segments:
+                                   * multiple of 8 up to 3072 (not 1024), at
+                                   * least 256 x SMs segments:
                                    * 128 segments are the 128 rows of A, loaded by
                                    * TMA tensor copies; 0 = the
                                    * mma.sync kernels                             */

@@ -377,14 +377,15 @@ cudaError_t launch_reduce_segmented(bool mma, int fmt, bool batched, const void*
                                     size_t segment_len, float* out, const DevWorkspace& ws,
                                     const LaunchCfg& cfg, cudaStream_t stream) {
     // fixed-length rows on tcgen05 (tcr_rows_tc05.cu) when every SM gets a
-    // block of 256 segments and L <= 3072, except L = 32 and L = 1024, where
-    // the mma.sync rows kernels measured faster (1 GiB inputs,
-    // profiles/r02/rows_tc05_sweep.txt: tcgen05 0.93-0.98 x their time for L
-    // = 64..768, 2048, 3072; 0.06-0.13 x for L = 8..56 other than 32, which
-    // had no specialised kernel; 1.21 x at 32, 1.03 x at 1024, 1.04 x at 4096)
+    // block of 256 segments and L <= 3072, except L = 1024, where the
+    // whole-tile mma.sync rows kernel measured faster (1 GiB inputs,
+    // profiles/r02/rows_tc05_sweep.txt, rows_tc05_sweep2.txt: tcgen05 0.89-
+    // 0.98 x the mma.sync kernels' time for L = 32..768, 2048, 3072; 0.03-
+    // 0.13 x for L = 8..56 other than 32, which had no specialised kernel;
+    // 1.03 x at 1024, 1.04 x at 4096)
     const size_t L = segment_len;
     if (mma && batched && cfg.rows_tc05 && num_segments >= (size_t)256 * (size_t)cfg.sms &&
-        L <= 3072 && L != 32 && L != 1024 && rows_tc05_supported(fmt, x, num_segments, L))
+        L <= 3072 && L != 1024 && rows_tc05_supported(fmt, x, num_segments, L))
         return launch_reduce_rows_tc05(fmt, x, num_segments, segment_len, out, ws, cfg, stream);
     size_t g = (num_segments + kSegWarps - 1) / kSegWarps;
     const size_t gmax = (size_t)cfg.sms * kSegCtasPerSm;

@@ -73,7 +73,8 @@ def _min_segments(tcr):
 
 # (L, extra rows past 256 x SMs): L multiples of 8, below / at / above the box,
 # not multiples of 64; S not a multiple of 128 or 256
-CASES = [(8, 0), (16, 5), (24, 127), (32, 1), (40, 77), (64, 0), (72, 3), (128, 129), (200, 11),
+CASES = [(8, 0), (8, 1000), (16, 5), (16, 1024 * 3 + 1), (24, 127), (32, 1), (32, 513), (40, 77), (64, 0),
+         (72, 3), (128, 129), (200, 11),
          (256, 64), (384, 128), (512, 7), (1000, 1), (1024, 0), (2048, 33), (3072, 2), (4104, 2)]
 
 
@@ -97,16 +98,16 @@ def test_against_oracle_f16(tcr, L, extra):
 
 
 def test_routing_rule_counts_launches(tcr):
-    """The library routes L % 8 == 0, L <= 3072, L not 32 / 1024, >= 256 x SMs
+    """The library routes L % 8 == 0, L <= 3072, L != 1024, >= 256 x SMs
     segments to the tcgen05 rows kernel: a wrong route would still be right,
     so the rule is checked through its measurable side -- with the knob off
-    and on, the L = 32 / 1024 / 4104 results are bitwise identical (the same
-    mma.sync kernel ran) while L = 64 / 2048 differ in at least one output
-    on random data (a different kernel, a different rounding order)."""
+    and on, the L = 1024 / 4104 results are bitwise identical (the same
+    mma.sync kernel ran) while L = 32 / 64 / 2048 differ in at least one
+    output on random data (a different kernel, a different rounding order)."""
     import torch
 
     S = _min_segments(tcr) + 3
-    for L, same in ((32, True), (1024, True), (4104, True), (64, False), (2048, False)):
+    for L, same in ((1024, True), (4104, True), (32, False), (64, False), (2048, False)):
         bits = gen.generate(55 + L, 0, L * S, gen.UNIFORM_01)
         x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.float16)
         with _rows(tcr, True):
@@ -116,7 +117,7 @@ def test_routing_rule_counts_launches(tcr):
         assert np.array_equal(on.view(np.uint32), off.view(np.uint32)) == same, L
 
 
-@pytest.mark.parametrize("L", [8, 64, 96, 512])
+@pytest.mark.parametrize("L", [8, 16, 24, 32, 64, 96, 512])
 def test_integer_data_bitwise(tcr, L):
     """SMALLINT rows: every partial is an exact integer, so out[j] equals the
     exact segment sum bit for bit -- a row read from the wrong segment, a box
@@ -134,13 +135,14 @@ def test_integer_data_bitwise(tcr, L):
     assert np.array_equal(got, want), np.flatnonzero(got != want)[:10]
 
 
-def test_one_hot_positions(tcr):
+@pytest.mark.parametrize("L", [8, 16, 32, 192])
+def test_one_hot_positions(tcr, L):
     """A single 1.0 at every position class of a box (K slice, 16-byte chunk
-    within the 128-byte swizzled row, row within the 8-row atom, atom): only
-    its segment reads 1.0."""
+    within the 32 / 64 / 128-byte swizzled row, row within the 8-row atom,
+    atom, box of the stage): only its segment reads 1.0."""
     import torch
 
-    L, S = 192, _min_segments(tcr) + 3
+    S = 4 * _min_segments(tcr) + 3
     rng = np.random.default_rng(5)
     for _ in range(4):
         pos = rng.choice(L * S, size=256, replace=False)
@@ -205,7 +207,7 @@ def test_full_size_c5_volume(tcr):
     _check(got, bits, L, S)
 
 
-@pytest.mark.parametrize("L", [64, 200])
+@pytest.mark.parametrize("L", [16, 32, 64, 200])
 def test_dynamic_tail_schedule_invariance(tcr, L):
     """The last TCR_CFG_TC05_DYNAMIC % of the row blocks are handed out at run
     time; each block is still reduced by one CTA in box order, so every
