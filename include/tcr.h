@@ -175,10 +175,11 @@ tcr_status tcr_reduce_sum_segmented_ex(const void *x, tcr_dtype dtype, const int
  * tcr_reduce_sum_batched -- num_segments contiguous segments of segment_len
  * elements each: out[j] = R(x[j*segment_len .. (j+1)*segment_len)).
  * Same accuracy contract per segment as tcr_reduce_sum; bitwise
- * deterministic.  Kernel choice (internal, TCR_CFG_ROWS_TC05): binary16 /
- * bfloat16 rows with x 16-byte aligned, segment_len % 8 == 0, segment_len <=
- * 3072 (not 1024) and at least 256 x SMs segments run on tcgen05 with 256
- * segments per TMA tensor box, each segment a row of A (Eq. 9-10);
+ * deterministic.  Kernel choice (internal, TCR_CFG_ROWS_TC05): rows of any
+ * format with x 16-byte aligned, a row pitch that is a multiple of 16 bytes
+ * and at most 6144 bytes (not binary16 / bfloat16 segment_len 1024) and at
+ * least 256 x SMs segments run on tcgen05 with 256 segments per TMA tensor
+ * box, each segment a row of A (Eq. 9-10);
  * otherwise the mma.sync kernels (16 segments as the 16 rows of A for
  * segment_len % 32 == 0 up to 2048, whole-tile rows, or the union stream).
  */
@@ -462,10 +463,10 @@ typedef enum {
                                    * streams at least this many chunks (default 32;
                                    * 0 = whenever TCR_CFG_TC05_DYNAMIC > 0)       */
     TCR_CFG_ROWS_TC05 = 21,       /* batched (MMA): 1 (default) = fixed-length rows
-                                   * on tcgen05 where applicable -- binary16 /
-                                   * bfloat16, x 16-byte aligned, segment_len a
-                                   * multiple of 8 up to 3072 (not 1024), at
-                                   * least 256 x SMs segments:
+                                   * on tcgen05 where applicable -- any format,
+                                   * x 16-byte aligned, row pitch a multiple of
+                                   * 16 bytes up to 6144 (not 16-bit L = 1024),
+                                   * at least 256 x SMs segments:
                                    * 128 segments are the 128 rows of A, loaded by
                                    * TMA tensor copies; 0 = the
                                    * mma.sync kernels                             */

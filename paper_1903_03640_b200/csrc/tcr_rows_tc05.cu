@@ -109,7 +109,9 @@ struct RtParams {
 // each stage's unit index (-1 = END) next to the stage; the MMA issuer
 // forwards it per accumulator buffer with a plain arrive on tinf[a]
 // (release), which the epilogue waits on before reading it.
-template <int BW>
+// kF8: fp8 E4M3 / E5M2 rows (kind::f8f6f4, K = 32 one-byte elements per
+// slice): the same byte geometry, BW counting 2-byte units.
+template <int BW, bool kF8>
 __global__ void __launch_bounds__(kRtWarps * 32)
 reduce_rows_tc05_kernel(const __grid_constant__ CUtensorMap map, RtParams prm, float* __restrict__ out,
                         DevWorkspace ws) {
@@ -172,7 +174,7 @@ reduce_rows_tc05_kernel(const __grid_constant__ CUtensorMap map, RtParams prm, f
                     sm100::mbar_arrive_expect_tx(&full[s], kRtStageBytes);
                     for (int bx = 0; bx < kNB; ++bx)
                         tma_load_2d(ring + (size_t)s * kRtStageBytes + (size_t)bx * Geo::kBoxBytes, &map,
-                                    k * BW, (int)((u * kNB + bx) * kRtRows), &full[s]);
+                                    k * BW * (kF8 ? 2 : 1), (int)((u * kNB + bx) * kRtRows), &full[s]);
                     if (++s == stages) {
                         s = 0;
                         ph ^= 1u;
@@ -234,11 +236,14 @@ reduce_rows_tc05_kernel(const __grid_constant__ CUtensorMap map, RtParams prm, f
 #pragma unroll
                     for (int h = 0; h < 2; ++h)  // rows 128 h .. 128 h + 127 of the box
 #pragma unroll
-                        for (int q = 0; q < Geo::kSlices; ++q)  // K slice q: +32 B = +2 in the descriptor
-                            sm100::mma_f16_ss(d + 16u * (uint32_t)(2 * bx + h),
-                                              ad + (uint64_t)((bx * Geo::kBoxBytes + h * Geo::kHalfBytes) >> 4) +
-                                                  (uint64_t)(2 * q),
-                                              bdesc, prm.idesc, q > 0 ? 1u : 0u);
+                        for (int q = 0; q < Geo::kSlices; ++q) {  // K slice q: +32 B = +2 in the descriptor
+                            const uint64_t aq = ad + (uint64_t)((bx * Geo::kBoxBytes + h * Geo::kHalfBytes) >> 4) +
+                                                (uint64_t)(2 * q);
+                            if constexpr (kF8)
+                                sm100::mma_f8_ss(d + 16u * (uint32_t)(2 * bx + h), aq, bdesc, prm.idesc, q > 0 ? 1u : 0u);
+                            else
+                                sm100::mma_f16_ss(d + 16u * (uint32_t)(2 * bx + h), aq, bdesc, prm.idesc, q > 0 ? 1u : 0u);
+                        }
                 sm100::mma_commit(&tfull[a]);
                 sm100::mma_commit(&empty[s]);
                 sm100::mbar_arrive(&tinf[a]);
@@ -316,41 +321,47 @@ EncodeTiled encode_fn() {
 
 }  // namespace
 
-// Applicability (checked by the caller): binary16 / bfloat16, x 16-byte
-// aligned, L % 8 == 0 (the tensor map's row pitch must be a multiple of 16
-// bytes), 8 <= L, S >= 1; rows and L below 2^31.
+// Applicability (checked by the caller): any element format, x 16-byte
+// aligned, the row pitch L * element bytes a multiple of 16 (the tensor
+// map's), S >= 1; rows and L below 2^31.
 bool rows_tc05_supported(int fmt, const void* x, size_t S, size_t L) {
-    return (fmt == kF16 || fmt == kBF16) && ((uintptr_t)x & 15u) == 0 && L % 8 == 0 && L >= 8 &&
+    const size_t lb = L * ((fmt == kE4M3 || fmt == kE5M2) ? 1 : 2);
+    return fmt >= kF16 && fmt <= kE5M2 && ((uintptr_t)x & 15u) == 0 && lb % 16 == 0 && lb >= 16 &&
            L < ((size_t)1 << 31) && S >= 1 && S < ((size_t)1 << 31) && encode_fn() != nullptr;
 }
 
-template <int BW>
+template <int BW, bool kF8>
 static cudaError_t launch_rows_bw(EncodeTiled enc, int fmt, const void* x, size_t S, size_t L, float* out,
                                   const DevWorkspace& ws, const LaunchCfg& cfg, cudaStream_t stream) {
     using Geo = RtGeom<BW>;
+    constexpr size_t es = kF8 ? 1 : 2;  // element bytes
+    constexpr int kBoxEl = BW * 2 / (int)es;  // elements per box row
     CUtensorMap map;
     const cuuint64_t dims[2] = {(cuuint64_t)L, (cuuint64_t)S};
-    const cuuint64_t strides[1] = {(cuuint64_t)L * 2u};
-    const cuuint32_t box[2] = {(cuuint32_t)BW, (cuuint32_t)kRtRows};
+    const cuuint64_t strides[1] = {(cuuint64_t)(L * es)};
+    const cuuint32_t box[2] = {(cuuint32_t)kBoxEl, (cuuint32_t)kRtRows};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUtensorMapSwizzle sw = BW == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
                                 : BW == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(x), dims, strides, box, estr,
+    if (enc(&map, kF8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(x),
+            dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     RtParams prm;
     prm.S = S;
-    prm.nk = (int)((L + BW - 1) / BW);
+    prm.nk = (int)((L + kBoxEl - 1) / kBoxEl);
     prm.stages = cfg.rows_tc05_stages;
-    const uint32_t ab = fmt == kBF16 ? ((1u << 7) | (1u << 10)) : 0u;
+    // kind::f16: a/b format F16 = 0, BF16 = 1; kind::f8f6f4: E4M3 = 0, E5M2 = 1
+    const uint32_t ab = (fmt == kBF16 || fmt == kE5M2) ? ((1u << 7) | (1u << 10)) : 0u;
     prm.idesc = sm100::idesc_f16_f32(128, 16) | ab;
-    prm.one_bits = fmt == kBF16 ? 0x3F803F80u : 0x3C003C00u;
+    prm.one_bits = fmt == kBF16 ? 0x3F803F80u : fmt == kE4M3 ? 0x38383838u : fmt == kE5M2 ? 0x3C3C3C3Cu
+                                                                                         : 0x3C003C00u;
     if (prm.stages < 2 ||
         kRtHeader - 8 < 512 + (size_t)(2 * prm.stages + 3 * kRtAcc) * 8 + (size_t)(prm.stages + kRtAcc) * 4)
         return cudaErrorInvalidValue;
     const size_t smem = kRtHeader + (size_t)prm.stages * kRtStageBytes;
-    auto kernel = reduce_rows_tc05_kernel<BW>;
+    auto kernel = reduce_rows_tc05_kernel<BW, kF8>;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -376,14 +387,22 @@ static cudaError_t launch_rows_bw(EncodeTiled enc, int fmt, const void* x, size_
     return cudaGetLastError();
 }
 
-// Box width by segment length: 16 (L <= 16), 32 (L <= 32), else 64.
+// Box width by segment bytes: 32 B (<= 32), 64 B (<= 64), else 128 B.
+template <bool kF8>
+static cudaError_t launch_rows_fmt(EncodeTiled enc, int fmt, const void* x, size_t S, size_t L, float* out,
+                                   const DevWorkspace& ws, const LaunchCfg& cfg, cudaStream_t stream) {
+    const size_t lb = L * (kF8 ? 1 : 2);
+    if (lb <= 32) return launch_rows_bw<16, kF8>(enc, fmt, x, S, L, out, ws, cfg, stream);
+    if (lb <= 64) return launch_rows_bw<32, kF8>(enc, fmt, x, S, L, out, ws, cfg, stream);
+    return launch_rows_bw<64, kF8>(enc, fmt, x, S, L, out, ws, cfg, stream);
+}
+
 cudaError_t launch_reduce_rows_tc05(int fmt, const void* x, size_t S, size_t L, float* out,
                                     const DevWorkspace& ws, const LaunchCfg& cfg, cudaStream_t stream) {
     EncodeTiled enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
-    if (L <= 16) return launch_rows_bw<16>(enc, fmt, x, S, L, out, ws, cfg, stream);
-    if (L <= 32) return launch_rows_bw<32>(enc, fmt, x, S, L, out, ws, cfg, stream);
-    return launch_rows_bw<64>(enc, fmt, x, S, L, out, ws, cfg, stream);
+    if (fmt == kE4M3 || fmt == kE5M2) return launch_rows_fmt<true>(enc, fmt, x, S, L, out, ws, cfg, stream);
+    return launch_rows_fmt<false>(enc, fmt, x, S, L, out, ws, cfg, stream);
 }
 
 }  // namespace tcr

@@ -385,7 +385,8 @@ cudaError_t launch_reduce_segmented(bool mma, int fmt, bool batched, const void*
     // 1.03 x at 1024, 1.04 x at 4096)
     const size_t L = segment_len;
     if (mma && batched && cfg.rows_tc05 && num_segments >= (size_t)256 * (size_t)cfg.sms &&
-        L <= 3072 && L != 1024 && rows_tc05_supported(fmt, x, num_segments, L))
+        L * ((fmt == kE4M3 || fmt == kE5M2) ? 1 : 2) <= 6144 && !(fmt <= kBF16 && L == 1024) &&
+        rows_tc05_supported(fmt, x, num_segments, L))
         return launch_reduce_rows_tc05(fmt, x, num_segments, segment_len, out, ws, cfg, stream);
     size_t g = (num_segments + kSegWarps - 1) / kSegWarps;
     const size_t gmax = (size_t)cfg.sms * kSegCtasPerSm;

@@ -32,9 +32,15 @@ def run(x, L, out, k=30):
     return a.elapsed_time(b) * 1e3 / k
 
 
+dt = __import__("os").environ.get("DTYPE", "f16")
+es = 1 if dt in ("e4m3", "e5m2") else 2
 for L in Ls:
-    S = (1 << 29) // L
-    x = gen.generate_tensor(gen.SEED_C5, 0, L * S, gen.UNIFORM_PM1)
+    S = (1 << 30) // es // L
+    if es == 1:
+        x = gen.generate_tensor_fp8(gen.SEED_C5, 0, L * S, gen.UNIFORM_PM1,
+                                    gen.FP8_E4M3 if dt == "e4m3" else gen.FP8_E5M2)
+    else:
+        x = gen.generate_tensor(gen.SEED_C5, 0, L * S, gen.UNIFORM_PM1, bf16=(dt == "bf16"))
     out = torch.empty(S, dtype=torch.float32, device="cuda")
     arms = [(0, 8)] + [(1, d) for d in DYNS]  # (rows_tc05, dynamic %)
     res = {a: [] for a in arms}
@@ -45,7 +51,7 @@ for L in Ls:
             res[(on, d)].append(run(x, L, out))
     tcr.tcr_set_config(tcr.TCR_CFG_ROWS_TC05, 1)
     tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYNAMIC, 8)
-    gb = lambda us: (2 * S * L + 4 * S) / (us * 1e-6) / 1e9  # noqa: E731
+    gb = lambda us: (es * S * L + 4 * S) / (us * 1e-6) / 1e9  # noqa: E731
     m0 = statistics.median(res[(0, 8)])
     line = f"L={L:6d} S={S:9d}  mma.sync {m0:8.1f} us {gb(m0):7.1f} GB/s"
     for on, d in arms[1:]:

@@ -233,3 +233,27 @@ def test_dynamic_tail_schedule_invariance(tcr, L):
         for o in outs:
             assert np.array_equal(o.view(np.uint32), ref.view(np.uint32)), d
     _check(ref, bits, L, S)
+
+
+@pytest.mark.parametrize("fmt", [oracle.FP8_E4M3, oracle.FP8_E5M2])
+def test_fp8_against_oracle(tcr, fmt):
+    """fp8 rows on tcgen05 (kind::f8f6f4, 32 one-byte elements per K slice,
+    the same 32 / 64 / 128-byte swizzled boxes): every output within the
+    tolerance of the exact fp8 oracle, bitwise on a second launch."""
+    import torch
+
+    for L, extra in ((16, 3), (48, 1000), (64, 0), (128, 77), (400, 5), (1024, 1), (4096, 2), (8192, 1)):
+        S = _min_segments(tcr) + extra
+        bits = gen.generate_fp8(600 + L, 0, L * S, gen.WIDE, fmt)
+        buf = torch.empty(L * S + 64, dtype=torch.uint8, device="cuda")
+        x = buf[16:16 + L * S]
+        x.copy_(torch.from_numpy(bits))
+        x = x.view(torch.float8_e4m3fn if fmt == oracle.FP8_E4M3 else torch.float8_e5m2)
+        with _rows(tcr, True):
+            got = _batched(tcr, x, L, S)
+            again = _batched(tcr, x, L, S)
+        assert np.array_equal(got.view(np.uint32), again.view(np.uint32)), L
+        off = np.arange(S + 1, dtype=np.int64) * L
+        ss = oracle.exact_segment_sums_fp8_array(bits, off, fmt, threads=os.cpu_count() or 4)
+        ok = oracle.within_tolerance_segments(got, ss)
+        assert ok.all(), (fmt, L, np.flatnonzero(~ok)[:10])
