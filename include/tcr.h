@@ -470,8 +470,14 @@ typedef enum {
                                    * 128 segments are the 128 rows of A, loaded by
                                    * TMA tensor copies; 0 = the
                                    * mma.sync kernels                             */
-    TCR_CFG_ROWS_TC05_STAGES = 22 /* that kernel's SMEM ring stages of 32 KiB
+    TCR_CFG_ROWS_TC05_STAGES = 22, /* that kernel's SMEM ring stages of 32 KiB
                                    * (2..6, default 4)                           */
+    TCR_CFG_EXACT_BULK = 23       /* exact (binary16 / fp8): 1 (default) = from 512
+                                   * MiB the TMA-fed kernel with the dynamic tail
+                                   * (cp.async.bulk ring, 8 consumer warps, chunk
+                                   * tickets per TCR_CFG_TC05_DYNAMIC; DESIGN.md
+                                   * §18); 2 = that kernel at every size; 0 = the
+                                   * LDG kernel at every size                     */
 } tcr_config_key;
 tcr_status tcr_set_config(tcr_config_key key, int value);
 int tcr_get_config(tcr_config_key key); /* -1 for an unknown key */

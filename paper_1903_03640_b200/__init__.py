@@ -70,6 +70,7 @@ TCR_CFG_TC05_DYNAMIC = 19
 TCR_CFG_TC05_DYN_MIN_RUN = 20
 TCR_CFG_ROWS_TC05 = 21
 TCR_CFG_ROWS_TC05_STAGES = 22
+TCR_CFG_EXACT_BULK = 23
 
 TCR_EXACT_ACC_WORDS = 6
 TCR_EXACT_BF16_ACC_WORDS = 27

@@ -52,6 +52,7 @@ struct Config {
     int tc05_dynamic = 8;  // percent of the chunks handed out at run time (r02 §16)
     int tc05_dyn_min_run = 32;  // ... when every CTA streams >= 32 chunks (r02 §16)
     int rows_tc05 = 1;          // batched rows on tcgen05 where applicable (r02 §17)
+    int exact_bulk = 1;         // exact: TMA-fed + dynamic tail from 512 MiB (r02 §18)
     int rows_tc05_stages = 4;
     // bulk (TMA -> SMEM -> mma.sync), r02: one CTA per SM with 4 x 32 KiB
     // (8 tiles per consumer warp per stage = the K = 4 chain per accumulator);
@@ -122,6 +123,7 @@ LaunchCfg make_cfg(const DeviceInfo& di) {
     c.tc05_dynamic = g_cfg.tc05_dynamic;
     c.tc05_dyn_min_run = g_cfg.tc05_dyn_min_run;
     c.rows_tc05 = g_cfg.rows_tc05;
+    c.exact_bulk = g_cfg.exact_bulk;
     c.rows_tc05_stages = g_cfg.rows_tc05_stages;
     c.bulk_stages = g_cfg.bulk_stages;
     c.bulk_stage_kb = g_cfg.bulk_stage_kb;
@@ -805,6 +807,10 @@ tcr_status tcr_set_config(tcr_config_key key, int value) {
             if (value < 0 || value > 1 << 20) break;
             g_cfg.tc05_dyn_min_run = value;
             return TCR_OK;
+        case TCR_CFG_EXACT_BULK:
+            if (value < 0 || value > 2) break;
+            g_cfg.exact_bulk = value;
+            return TCR_OK;
         case TCR_CFG_ROWS_TC05:
             if (value != 0 && value != 1) break;
             g_cfg.rows_tc05 = value;
@@ -864,6 +870,7 @@ int tcr_get_config(tcr_config_key key) {
         case TCR_CFG_TC05_DYNAMIC: return g_cfg.tc05_dynamic;
         case TCR_CFG_TC05_DYN_MIN_RUN: return g_cfg.tc05_dyn_min_run;
         case TCR_CFG_ROWS_TC05: return g_cfg.rows_tc05;
+        case TCR_CFG_EXACT_BULK: return g_cfg.exact_bulk;
         case TCR_CFG_ROWS_TC05_STAGES: return g_cfg.rows_tc05_stages;
         case TCR_CFG_BULK_STAGES: return g_cfg.bulk_stages;
         case TCR_CFG_BULK_STAGE_KB: return g_cfg.bulk_stage_kb;

@@ -24,6 +24,10 @@
 #include "tcr_int128.cuh"
 #include "tcr_internal.h"
 #include "tcr_peer.cuh"
+#include "tcr_sm100.cuh"
+
+#include <map>
+#include <mutex>
 
 namespace tcr {
 
@@ -200,6 +204,111 @@ __device__ void finalize(const long long* acc, float* out_f32, double* out_f64) 
     if (out_f64) *out_f64 = d;
 }
 
+// Levels 2-4 of the exact kernels: warp, CTA and grid as exact integer adds
+// (order-free), then the fused peer combine of the limbs (kPeer) or the
+// final rounding.  Every thread calls it with its lane's int128 and special
+// counts; WARPS warps per CTA; chunk_next (if not null) is reset by the last
+// CTA (the bulk kernel's dynamic tail).
+template <int WARPS, bool kPeer>
+__device__ __forceinline__ void exact_complete(i128 acc, uint32_t (&cnt)[3], long long* out_acc,
+                                               float* out_f32, double* out_f64, const DevWorkspace& ws,
+                                               const PeerCombine& pc, int me, unsigned* chunk_next) {
+    constexpr int kExactWarps = WARPS;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // warp, CTA and grid levels: exact integer adds (order-free)
+    __shared__ long long s_part[kExactWarps][5];
+    __shared__ unsigned s_last;
+    acc = warp_sum_i128(acc);
+    for (int k = 0; k < 3; ++k) cnt[k] = warp_sum_u32(cnt[k]);
+    if (lane == 0) {
+        s_part[warp][0] = (long long)(unsigned long long)acc;
+        s_part[warp][1] = (long long)(acc >> 64);
+        for (int k = 0; k < 3; ++k) s_part[warp][2 + k] = cnt[k];
+    }
+    __syncthreads();
+    if (warp != 0) return;
+    const unsigned long long prev = kPeer ? peer_counter(pc, me) : 0ull;
+    i128 b = 0;
+    long long c[3] = {0, 0, 0};
+    if (lane < kExactWarps) {
+        b = (i128)(((u128)(unsigned long long)s_part[lane][1] << 64) |
+                   (u128)(unsigned long long)s_part[lane][0]);
+        for (int k = 0; k < 3; ++k) c[k] = s_part[lane][2 + k];
+    }
+    b = warp_sum_i128(b);
+    for (int k = 0; k < 3; ++k)
+        for (int o = 16; o > 0; o >>= 1) c[k] += __shfl_xor_sync(0xffffffffu, c[k], o);
+    long long res[6];
+    if (gridDim.x > 1) {
+        // CTA partial: 5 int64 words per CTA in the workspace (reinterpreted doubles)
+        long long* parts = reinterpret_cast<long long*>(ws.partials);
+        if (lane == 0) {
+            long long* p = parts + 5 * (size_t)blockIdx.x;
+            p[0] = (long long)(unsigned long long)b;
+            p[1] = (long long)(b >> 64);
+            p[2] = c[0];
+            p[3] = c[1];
+            p[4] = c[2];
+            if constexpr (kPeer) {  // fence + relaxed ticket: no spill in the peer variant
+                __threadfence();
+                s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+            } else {
+                s_last = (ticket_acq_rel(ws.ticket) == gridDim.x - 1) ? 1u : 0u;
+            }
+        }
+        __syncwarp();  // lane 0's acquire, then the warp's loads below
+        if (!__shfl_sync(0xffffffffu, s_last, 0)) return;
+        if constexpr (kPeer) __threadfence();
+        b = 0;
+        c[0] = c[1] = c[2] = 0;
+        for (int i = lane; i < (int)gridDim.x; i += 32) {
+            const long long* p = parts + 5 * (size_t)i;
+            b += (i128)(((u128)(unsigned long long)__ldcg(p + 1) << 64) |
+                        (u128)(unsigned long long)__ldcg(p));
+            c[0] += __ldcg(p + 2);
+            c[1] += __ldcg(p + 3);
+            c[2] += __ldcg(p + 4);
+        }
+        b = warp_sum_i128(b);
+        for (int k = 0; k < 3; ++k)
+            for (int o = 16; o > 0; o >>= 1) c[k] += __shfl_xor_sync(0xffffffffu, c[k], o);
+        if (lane == 0) {
+            *ws.ticket = 0u;
+            if (chunk_next) *chunk_next = 0u;
+        }
+    } else if (lane == 0 && chunk_next) {
+        *chunk_next = 0u;
+    }
+    if constexpr (kPeer) {
+        // every lane computes the limbs (b, c are warp-uniform after the sums)
+        to_limbs(b, res);
+        res[3] = c[0];
+        res[4] = c[1];
+        res[5] = c[2];
+        const bool ok = peer_combine_exact(res, pc, me, lane, prev);
+        if (lane == 0) {
+            if (out_acc)
+                for (int k = 0; k < 6; ++k) out_acc[k] = res[k];
+            if (ok) {
+                finalize(res, out_f32, out_f64);
+            } else {
+                if (out_f32) *out_f32 = __int_as_float(0x7FC00000);
+                if (out_f64) *out_f64 = __longlong_as_double(0x7FF8000000000000ll);
+            }
+        }
+        return;
+    }
+    if (lane == 0) {
+        to_limbs(b, res);
+        res[3] = c[0];
+        res[4] = c[1];
+        res[5] = c[2];
+        if (out_acc)
+            for (int k = 0; k < 6; ++k) out_acc[k] = res[k];
+        finalize(res, out_f32, out_f64);
+    }
+}
+
 // kPeer: the NEXT-2 x NEXT-3 variant -- the last CTA combines the limbs
 // with the peers' over NVLink mailboxes (tcr_peer.cuh); grid.y slices =
 // emulated ranks, as in reduce_stream_kernel.
@@ -296,93 +405,185 @@ reduce_exact_kernel(const uint8_t* __restrict__ x, size_t n, long long* out_acc,
     }
     drain();
 
-    // warp, CTA and grid levels: exact integer adds (order-free)
-    __shared__ long long s_part[kExactWarps][5];
-    __shared__ unsigned s_last;
-    acc = warp_sum_i128(acc);
-    for (int k = 0; k < 3; ++k) cnt[k] = warp_sum_u32(cnt[k]);
-    if (lane == 0) {
-        s_part[warp][0] = (long long)(unsigned long long)acc;
-        s_part[warp][1] = (long long)(acc >> 64);
-        for (int k = 0; k < 3; ++k) s_part[warp][2 + k] = cnt[k];
+    exact_complete<kExactWarps, kPeer>(acc, cnt, out_acc, out_f32, out_f64, ws, pc, me, nullptr);
+}
+
+// TMA-fed exact reduction with a dynamic tail (r02 §18; binary16 / fp8, the
+// default exact kernel from 512 MiB): a producer lane streams 32 KiB chunks
+// into a 4-stage SMEM ring with cp.async.bulk -- CTA b its contiguous run of
+// the first 92 % of the chunks, then chunks by ticket (ws.chunk_next, two
+// tickets held ahead) -- and 8 consumer warps apply the same exact per-vector
+// accumulation as reduce_exact_kernel to the stage (warp w: 512-byte tiles w,
+// w + 8, ...).  Integer levels 2-4 are order-free, so which CTA took which
+// chunk cannot change a bit.  Bytes in flight are bounded by SMEM (128 KiB
+// per SM), not by registers, and the tail does not wait for the slowest SM.
+constexpr int kXbConsumers = 8;
+constexpr int kXbThreads = (kXbConsumers + 1) * 32;
+constexpr uint32_t kXbStageBytes = 32768;
+constexpr uint32_t kXbHeader = 1024;
+
+__device__ __forceinline__ uint4 lds128x(const void* p) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(sm100::smem_addr(p)));
+    return r;
+}
+
+template <int F>
+__global__ void __launch_bounds__(kXbThreads, 1)
+reduce_exact_bulk_kernel(const uint8_t* __restrict__ x, size_t n, int stages, int dyn_pct,
+                         long long* out_acc, float* out_f32, double* out_f64, DevWorkspace ws) {
+    constexpr int ES = FmtInfo<F>::kBytes;
+    constexpr int kTileBytes = 512;
+    constexpr int NA = 4;
+    constexpr int kTilesPerWarp = (int)(kXbStageBytes / kTileBytes) / kXbConsumers;  // 8 per stage
+    // <= 1024 binary16 per accumulator between flushes: a tile gives each of
+    // the 4 accumulators 2 (binary16) or 4 (fp8 as binary16) values per lane
+    constexpr int kFlushStages = (ES == 1 ? 256 : 512) / (2 * kTilesPerWarp);
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + stages;
+    volatile uint32_t* sinfo = reinterpret_cast<volatile uint32_t*>(empty + stages);  // [stages]
+    uint8_t* ring = smem + kXbHeader;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    const size_t nbytes = n * ES;
+    size_t head = (16u - ((uintptr_t)x & 15u)) & 15u;
+    if (head > nbytes) head = nbytes;
+    const uint8_t* xa = x + head;
+    const size_t nb = nbytes - head;
+    const size_t C = nb / kXbStageBytes;
+    const size_t D = C * (size_t)dyn_pct / 100u;
+    const size_t Cs = C - D;
+    const size_t G = gridDim.x, b = blockIdx.x;
+    const size_t c_begin = b * Cs / G;
+    const long long nstatic = (long long)((b + 1) * Cs / G - c_begin);
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < stages; ++st) {
+            sm100::mbar_init(&full[st], 1);
+            sm100::mbar_init(&empty[st], kXbConsumers);
+        }
+        sm100::fence_mbar_init();
     }
     __syncthreads();
-    if (warp != 0) return;
-    const unsigned long long prev = kPeer ? peer_counter(pc, me) : 0ull;
-    i128 b = 0;
-    long long c[3] = {0, 0, 0};
-    if (lane < kExactWarps) {
-        b = (i128)(((u128)(unsigned long long)s_part[lane][1] << 64) |
-                   (u128)(unsigned long long)s_part[lane][0]);
-        for (int k = 0; k < 3; ++k) c[k] = s_part[lane][2 + k];
-    }
-    b = warp_sum_i128(b);
-    for (int k = 0; k < 3; ++k)
-        for (int o = 16; o > 0; o >>= 1) c[k] += __shfl_xor_sync(0xffffffffu, c[k], o);
-    long long res[6];
-    if (gridDim.x > 1) {
-        // CTA partial: 5 int64 words per CTA in the workspace (reinterpreted doubles)
-        long long* parts = reinterpret_cast<long long*>(ws.partials);
+    pdl_wait_and_release();  // PDL: no global memory before the previous kernel completes
+
+    i128 acc = 0;
+    uint32_t cnt[3] = {0u, 0u, 0u};
+    if (warp == kXbConsumers) {  // producer lane: static run, tickets, END
         if (lane == 0) {
-            long long* p = parts + 5 * (size_t)blockIdx.x;
-            p[0] = (long long)(unsigned long long)b;
-            p[1] = (long long)(b >> 64);
-            p[2] = c[0];
-            p[3] = c[1];
-            p[4] = c[2];
-            if constexpr (kPeer) {  // fence + relaxed ticket: no spill in the peer variant
-                __threadfence();
-                s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
-            } else {
-                s_last = (ticket_acq_rel(ws.ticket) == gridDim.x - 1) ? 1u : 0u;
+            const uint64_t pol = sm100::policy_evict_first();
+            int st = 0;
+            uint32_t ph = 0;
+            auto issue = [&](size_t c) {
+                sm100::mbar_wait(&empty[st], ph ^ 1u);
+                sinfo[st] = 1u;
+                sm100::mbar_arrive_expect_tx(&full[st], kXbStageBytes);
+                sm100::bulk_g2s(ring + (size_t)st * kXbStageBytes, xa + c * (size_t)kXbStageBytes,
+                                kXbStageBytes, &full[st], pol);
+                if (++st == stages) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            };
+            unsigned t0 = 0u, t1 = 0u;
+            bool f0 = false, f1 = false;
+            for (long long i = 0; i < nstatic; ++i) {
+                if (D && !f0 && nstatic - i <= 2) {
+                    t0 = atomicAdd(ws.chunk_next, 1u);
+                    f0 = true;
+                }
+                if (D && !f1 && nstatic - i <= 1) {
+                    t1 = atomicAdd(ws.chunk_next, 1u);
+                    f1 = true;
+                }
+                issue(c_begin + (size_t)i);
+            }
+            if (D) {
+                if (!f0) t0 = atomicAdd(ws.chunk_next, 1u);
+                if (!f1) t1 = atomicAdd(ws.chunk_next, 1u);
+                for (;;) {
+                    const unsigned t = t0;
+                    t0 = t1;
+                    t1 = atomicAdd(ws.chunk_next, 1u);
+                    if ((size_t)t >= D) break;
+                    issue(Cs + (size_t)t);
+                }
+            }
+            sm100::mbar_wait(&empty[st], ph ^ 1u);  // END: a stage with no bytes
+            sinfo[st] = 0u;
+            sm100::mbar_arrive(&full[st]);
+        }
+        __syncwarp();
+    } else {  // consumer warps
+        double a[NA];
+#pragma unroll
+        for (int i = 0; i < NA; ++i) a[i] = 0.0;
+        auto drain = [&]() {
+#pragma unroll
+            for (int i = 0; i < NA; ++i) {
+                acc += (i128)to_units(a[i]);
+                a[i] = 0.0;
+            }
+        };
+        int st = 0, it = 0;
+        uint32_t ph = 0;
+        for (;;) {
+            sm100::mbar_wait(&full[st], ph);
+            if (sinfo[st] == 0u) break;
+            const uint8_t* stage = ring + (size_t)st * kXbStageBytes + lane * 16;
+            uint4 v[kTilesPerWarp];
+#pragma unroll
+            for (int k = 0; k < kTilesPerWarp; ++k) v[k] = lds128x(stage + (size_t)(warp + k * kXbConsumers) * kTileBytes);
+            uint32_t probe = 0u;
+#pragma unroll
+            for (int k = 0; k < kTilesPerWarp; ++k) exact_vec_f<F, NA>(v[k], a, probe);
+            if (probe & 0x7FFF7FFFu) {  // some half was inf or NaN (rare): fix from SMEM
+#pragma unroll 1
+                for (int k = 0; k < kTilesPerWarp; ++k)
+                    fix_specials_f<F, NA>(lds128x(stage + (size_t)(warp + k * kXbConsumers) * kTileBytes), a, cnt);
+            }
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&empty[st]);  // stage consumed by this warp
+            if (++it == kFlushStages) {
+                it = 0;
+                drain();
+            }
+            if (++st == stages) {
+                st = 0;
+                ph ^= 1u;
             }
         }
-        __syncwarp();  // lane 0's acquire, then the warp's loads below
-        if (!__shfl_sync(0xffffffffu, s_last, 0)) return;
-        if constexpr (kPeer) __threadfence();
-        b = 0;
-        c[0] = c[1] = c[2] = 0;
-        for (int i = lane; i < (int)gridDim.x; i += 32) {
-            const long long* p = parts + 5 * (size_t)i;
-            b += (i128)(((u128)(unsigned long long)__ldcg(p + 1) << 64) |
-                        (u128)(unsigned long long)__ldcg(p));
-            c[0] += __ldcg(p + 2);
-            c[1] += __ldcg(p + 3);
-            c[2] += __ldcg(p + 4);
-        }
-        b = warp_sum_i128(b);
-        for (int k = 0; k < 3; ++k)
-            for (int o = 16; o > 0; o >>= 1) c[k] += __shfl_xor_sync(0xffffffffu, c[k], o);
-        if (lane == 0) *ws.ticket = 0u;
-    }
-    if constexpr (kPeer) {
-        // every lane computes the limbs (b, c are warp-uniform after the sums)
-        to_limbs(b, res);
-        res[3] = c[0];
-        res[4] = c[1];
-        res[5] = c[2];
-        const bool ok = peer_combine_exact(res, pc, me, lane, prev);
-        if (lane == 0) {
-            if (out_acc)
-                for (int k = 0; k < 6; ++k) out_acc[k] = res[k];
-            if (ok) {
-                finalize(res, out_f32, out_f64);
-            } else {
-                if (out_f32) *out_f32 = __int_as_float(0x7FC00000);
-                if (out_f64) *out_f64 = __longlong_as_double(0x7FF8000000000000ll);
+        auto one = [&](const uint4& v) {
+            uint32_t p = 0u;
+            exact_vec_f<F, NA>(v, a, p);
+            if (p & 0x7FFF7FFFu) fix_specials_f<F, NA>(v, a, cnt);
+        };
+        if (blockIdx.x == gridDim.x - 1) {  // ragged work past the last chunk, and the head
+            const uint8_t* xr = xa + C * (size_t)kXbStageBytes;
+            const size_t rem = nb - C * (size_t)kXbStageBytes;
+            const size_t Tr = rem / kTileBytes;
+            const int tail = (int)(rem - Tr * kTileBytes);
+            const uint4* base = reinterpret_cast<const uint4*>(xr) + lane;
+            drain();
+            int k = 0;
+            for (size_t t = warp; t < Tr; t += kXbConsumers) {
+                one(ldg_stream(base + t * 32));
+                if (++k == 32) {  // <= 1024 values per accumulator between flushes
+                    k = 0;
+                    drain();
+                }
             }
+            if (warp == 0 && head) one(load_ragged_bytes(x, (int)head, lane));
+            if (warp == 1 && tail) one(load_ragged_bytes(xr + Tr * kTileBytes, tail, lane));
         }
-        return;
+        drain();
     }
-    if (lane == 0) {
-        to_limbs(b, res);
-        res[3] = c[0];
-        res[4] = c[1];
-        res[5] = c[2];
-        if (out_acc)
-            for (int k = 0; k < 6; ++k) out_acc[k] = res[k];
-        finalize(res, out_f32, out_f64);
-    }
+    const PeerCombine none{};
+    exact_complete<kXbConsumers + 1, false>(acc, cnt, out_acc, out_f32, out_f64, ws, none, 0,
+                                            D ? ws.chunk_next : nullptr);
 }
 
 __global__ void exact_finalize_kernel(const long long* acc, float* out_f32, double* out_f64) {
@@ -407,9 +608,44 @@ int exact_grid(size_t n, const LaunchCfg& cfg, int capacity_words) {
 }
 
 template <int F>
+static cudaError_t launch_exact_bulk(const uint8_t* x, size_t n, long long* out_acc, float* out_f32,
+                                     double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                     cudaStream_t stream) {
+    constexpr int kStages = 4;
+    const size_t smem = kXbHeader + (size_t)kStages * kXbStageBytes;
+    auto kernel = reduce_exact_bulk_kernel<F>;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    {
+        static std::mutex mu;
+        static std::map<int, size_t> configured;
+        std::lock_guard<std::mutex> lk(mu);
+        if (smem > configured[dev]) {
+            if ((e = cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem)))
+                return e;
+            configured[dev] = smem;
+        }
+    }
+    const size_t C = n * FmtInfo<F>::kBytes / kXbStageBytes;
+    size_t g = (size_t)cfg.sms;
+    if (g > C) g = C;
+    if (g < 1) g = 1;
+    // the dynamic tail when every CTA streams >= TCR_CFG_TC05_DYN_MIN_RUN chunks
+    const int dyn = (C >= (size_t)cfg.tc05_dyn_min_run * g) ? cfg.tc05_dynamic : 0;
+    launch_maybe_pdl(kernel, dim3((unsigned)g), dim3(kXbThreads), smem, stream, cfg.pdl, x, n, kStages, dyn,
+                     out_acc, out_f32, out_f64, ws);
+    return cudaGetLastError();
+}
+
+template <int F>
 static cudaError_t launch_exact_f(const uint8_t* x, size_t n, long long* out_acc, float* out_f32,
                                   double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                   cudaStream_t stream) {
+    // TMA-fed with the dynamic tail from 512 MiB (r02 §18), else the LDG kernel
+    if (cfg.exact_bulk == 2 || (cfg.exact_bulk == 1 && n * FmtInfo<F>::kBytes >= ((size_t)512 << 20)))
+        return launch_exact_bulk<F>(x, n, out_acc, out_f32, out_f64, ws, cfg, stream);
     // grid from the input bytes (in 2-byte element equivalents)
     const int g = exact_grid(n * FmtInfo<F>::kBytes / 2, cfg, ws.capacity);
     const PeerCombine none{};

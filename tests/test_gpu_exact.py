@@ -127,3 +127,31 @@ def test_exact_sharded_is_independent_of_P(tcr, P):
     t = tot.cpu().tolist()
     assert exact_limbs_to_int(t) == es.T
     assert float(o32.item()) == es.f32() and float(o64.item()) == es.f64()
+
+
+@pytest.mark.parametrize("n", [1, 9, 16384 * 2 + 7, (1 << 20) + 5, 3 * (1 << 21) + 4099, (1 << 27) + 16384 * 3 + 11])
+def test_exact_bulk_kernel_bitwise(tcr, n):
+    """The TMA-fed exact kernel with the dynamic tail (TCR_CFG_EXACT_BULK = 2
+    forces it at every size; r02 §18) equals the oracle bit for bit, for
+    static and dynamic chunk schedules, aligned and misaligned, with specials
+    in static runs, dynamic chunks and the ragged end."""
+    keys = (tcr.TCR_CFG_EXACT_BULK, tcr.TCR_CFG_TC05_DYNAMIC, tcr.TCR_CFG_TC05_DYN_MIN_RUN)
+    saved = [tcr.tcr_get_config(k) for k in keys]
+    try:
+        tcr.tcr_set_config(tcr.TCR_CFG_EXACT_BULK, 2)
+        tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYN_MIN_RUN, 0)
+        for dist in (gen.UNIFORM_PM1, gen.WIDE):
+            bits = gen.generate(8800 + dist, 0, n, dist)
+            es = oracle.exact_sum_fp16(bits, threads=os.cpu_count() or 4)
+            for d in (0, 8, 100):
+                tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYNAMIC, d)
+                for off in (0, 3):
+                    _check(tcr, *_exact(tcr, _dev(bits, off)), es)
+        if n > 100:
+            for pos in (0, n // 2, n - 3):
+                b2 = gen.generate(5, 0, n, gen.UNIFORM_PM1)
+                b2[pos] = 0x7C00
+                _check(tcr, *_exact(tcr, _dev(b2, 1)), oracle.exact_sum_fp16(b2))
+    finally:
+        for k, v in zip(keys, saved):
+            tcr.tcr_set_config(k, v)
