@@ -472,8 +472,8 @@ typedef enum {
                                    * mma.sync kernels                             */
     TCR_CFG_ROWS_TC05_STAGES = 22, /* that kernel's SMEM ring stages of 32 KiB
                                    * (2..6, default 4)                           */
-    TCR_CFG_EXACT_BULK = 23       /* exact (binary16 / fp8): 1 (default) = from 512
-                                   * MiB the TMA-fed kernel with the dynamic tail
+    TCR_CFG_EXACT_BULK = 23       /* exact: 1 (default) = binary16 from 128 MiB on
+                                   * the TMA-fed kernel with the dynamic tail
                                    * (cp.async.bulk ring, 8 consumer warps, chunk
                                    * tickets per TCR_CFG_TC05_DYNAMIC; DESIGN.md
                                    * §18); 2 = that kernel at every size; 0 = the

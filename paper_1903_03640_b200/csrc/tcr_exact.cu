@@ -643,8 +643,12 @@ template <int F>
 static cudaError_t launch_exact_f(const uint8_t* x, size_t n, long long* out_acc, float* out_f32,
                                   double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
                                   cudaStream_t stream) {
-    // TMA-fed with the dynamic tail from 512 MiB (r02 §18), else the LDG kernel
-    if (cfg.exact_bulk == 2 || (cfg.exact_bulk == 1 && n * FmtInfo<F>::kBytes >= ((size_t)512 << 20)))
+    // binary16: TMA-fed with the dynamic tail from 128 MiB (r02 §18: 0.90-0.94 x
+    // the LDG kernel's time from 2^26 to 2^32); fp8, ALU-bound by its
+    // conversions, keeps the LDG kernel's 24 warps per SM (1.05 x at 2^31 on
+    // 8 consumer warps, profiles/r02/exact_bulk_ab2.txt)
+    if (cfg.exact_bulk == 2 ||
+        (cfg.exact_bulk == 1 && F == kF16 && n * FmtInfo<F>::kBytes >= ((size_t)128 << 20)))
         return launch_exact_bulk<F>(x, n, out_acc, out_f32, out_f64, ws, cfg, stream);
     // grid from the input bytes (in 2-byte element equivalents)
     const int g = exact_grid(n * FmtInfo<F>::kBytes / 2, cfg, ws.capacity);

@@ -54,7 +54,7 @@ struct LaunchCfg {
                           // (dynamic tail; 0 = static partition)
     int tc05_dyn_min_run; // tcgen05 kernel: the dynamic tail only when every CTA's
                           // static run would be at least this many chunks
-    int exact_bulk;       // exact: 1 = TMA-fed kernel with the dynamic tail from 512 MiB (2: always)
+    int exact_bulk;       // exact: 1 = TMA-fed kernel + dynamic tail, binary16 from 128 MiB (2: always)
     int rows_tc05;        // batched: 1 = fixed-length rows on tcgen05 (128 segments per MMA)
     int rows_tc05_stages; // batched tcgen05 kernel: SMEM ring stages of 16 KiB
     int bulk_stages;      // bulk (TMA -> SMEM -> mma.sync) kernel: ring stages
