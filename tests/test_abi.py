@@ -230,6 +230,33 @@ def test_no_register_spills_in_any_kernel():
     assert not bad, bad[:5]
 
 
+def test_round2_knobs_defaults_and_ranges():
+    """r02 §16-§18 knobs: defaults, accepted ranges, rejected values restore
+    nothing.  Host logic only (no device work)."""
+    import paper_1903_03640_b200 as tcr
+
+    cases = [  # (key, default, accepted, rejected)
+        (tcr.TCR_CFG_TC05_DYNAMIC, 8, (0, 100), (-1, 101)),
+        (tcr.TCR_CFG_TC05_DYN_MIN_RUN, 32, (0, 1 << 20), (-1, (1 << 20) + 1)),
+        (tcr.TCR_CFG_ROWS_TC05, 1, (0, 1), (2, -1)),
+        (tcr.TCR_CFG_ROWS_TC05_STAGES, 4, (2, 6), (1, 7)),
+        (tcr.TCR_CFG_EXACT_BULK, 1, (0, 2), (3, -1)),
+    ]
+    for key, default, ok, bad in cases:
+        assert tcr.tcr_get_config(key) == default, key
+        try:
+            for v in ok:
+                tcr.tcr_set_config(key, v)
+                assert tcr.tcr_get_config(key) == v
+            tcr.tcr_set_config(key, default)
+            for v in bad:
+                with pytest.raises(tcr.TcrError):
+                    tcr.tcr_set_config(key, v)
+                assert tcr.tcr_get_config(key) == default
+        finally:
+            tcr.tcr_set_config(key, default)
+
+
 def test_default_algo_resolution():
     """TCR_ALGO_DEFAULT resolves to TCR_CFG_DEFAULT_ALGO; its default, 0 = auto,
     picks by input size and format (r02 §16): tcgen05 (dynamic tail) for
