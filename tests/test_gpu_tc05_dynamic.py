@@ -318,3 +318,26 @@ def test_fused_peer_combine_emulated(tcr, P):
         torch.cuda.synchronize()
         for b in boxes:
             tcr.tcr_peer_mailbox_free(b)
+
+
+def test_e4m3_default_path_is_exact(tcr):
+    """fp8 E4M3 values are multiples of 2^-9 below 448: a row of the default
+    stage (2 MMAs x 32 elements = 64 values) sums to < 2^24 units of 2^-9, so
+    every binary32 row sum is exact, the per-round D' = 1 x D collapse is
+    exact and the integer combine is exact -- the default large-n E4M3 path
+    returns RNE(R(X)) bit for bit (binary32 and binary64), for any schedule."""
+    import torch
+
+    n = (1 << 29) + 32768 * 3 + 17  # >= 512 MiB: the tcgen05 dynamic-tail default
+    assert tcr.tcr_default_algo(n, tcr.TCR_DTYPE_E4M3) == tcr.TCR_ALGO_TCGEN05
+    for dist in (gen.UNIFORM_PM1, gen.WIDE):
+        x = gen.generate_tensor_fp8(90 + dist, 0, n, dist, gen.FP8_E4M3)
+        bits = x.view(torch.uint8).cpu().numpy()
+        es = oracle.exact_sum_fp8(bits, oracle.FP8_E4M3)
+        o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+        o64 = torch.empty(1, dtype=torch.float64, device="cuda")
+        for d in (8, 100):
+            with _cfg(tcr, tc05_dynamic=d, tc05_dyn_min_run=32):
+                tcr.tcr_reduce_sum_ex(x, out_f32=o32, out_f64=o64)
+                torch.cuda.synchronize()
+            assert o32.item() == es.f32() and o64.item() == es.f64(), (dist, d, o64.item(), es.f64())
