@@ -341,3 +341,23 @@ def test_e4m3_default_path_is_exact(tcr):
                 tcr.tcr_reduce_sum_ex(x, out_f32=o32, out_f64=o64)
                 torch.cuda.synchronize()
             assert o32.item() == es.f32() and o64.item() == es.f64(), (dist, d, o64.item(), es.f64())
+
+
+def test_e4m3_exact_adversarial_rows(tcr):
+    """The sharpest case for the claim above: every element 448 (the E4M3
+    maximum) except one smallest subnormal 2^-9 per 4 KiB -- the rows holding
+    it sum 63 x 448 + 2^-9, which needs all 24 bits of a binary32.  The
+    binary64 result resolves the 2^-9 terms (~2^38 total, ulp 2^-15)."""
+    import torch
+
+    n = 1 << 29
+    bits = np.full(n, 0x7E, dtype=np.uint8)  # 448
+    bits[::4096] = 0x01                      # 2^-9
+    bits[2048::4096] = 0xFE                  # -448: keeps the total's ulp small enough
+    es = oracle.exact_sum_fp8(bits, oracle.FP8_E4M3)
+    x = torch.from_numpy(bits).cuda().view(torch.float8_e4m3fn)
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    o64 = torch.empty(1, dtype=torch.float64, device="cuda")
+    tcr.tcr_reduce_sum_ex(x, out_f32=o32, out_f64=o64)
+    torch.cuda.synchronize()
+    assert o64.item() == es.f64() and o32.item() == es.f32(), (o64.item(), es.f64())
