@@ -473,7 +473,9 @@ typedef enum {
     TCR_CFG_ROWS_TC05_STAGES = 22, /* that kernel's SMEM ring stages of 32 KiB
                                    * (2..6, default 4)                           */
     TCR_CFG_EXACT_BULK = 23       /* exact: 1 (default) = binary16 from 128 MiB on
-                                   * the TMA-fed kernel with the dynamic tail
+                                   * the TMA-fed kernel with the dynamic tail, fp8
+                                   * E4M3 from 64 MiB on the tcgen05 dynamic-tail
+                                   * kernel (its rows are exact; + a NaN count)
                                    * (cp.async.bulk ring, 8 consumer warps, chunk
                                    * tickets per TCR_CFG_TC05_DYNAMIC; DESIGN.md
                                    * §18); 2 = that kernel at every size; 0 = the

@@ -543,6 +543,14 @@ tcr_status tcr_reduce_sum_exact_ex(const void* x, size_t n, tcr_dtype dtype, int
                                                           reinterpret_cast<long long*>(acc), out_f32,
                                                           out_f64, ws->dev, cfg, (cudaStream_t)stream),
                             "exact bf16 kernel launch");
+    if (dtype == TCR_DTYPE_E4M3 && tcr::exact_e4m3_tc05_applies(n, cfg)) {
+        int launches = 1;
+        const cudaError_t e = tcr::launch_exact_e4m3_tc05(static_cast<const uint8_t*>(x), n,
+                                                          reinterpret_cast<long long*>(acc), out_f32,
+                                                          out_f64, ws->dev, cfg, (cudaStream_t)stream,
+                                                          &launches);
+        return after_launch(e, "exact E4M3 (tcgen05) launch", launches);
+    }
     return after_launch(tcr::launch_reduce_exact((int)dtype, x, n, reinterpret_cast<long long*>(acc),
                                                  out_f32, out_f64, ws->dev, cfg, (cudaStream_t)stream),
                         "exact kernel launch");

@@ -113,6 +113,13 @@ cudaError_t launch_reduce_exact_peer(const uint16_t* x, size_t n, long long* out
                                      cudaStream_t stream);
 cudaError_t launch_exact_finalize(const long long* acc, float* out_f32, double* out_f64,
                                   cudaStream_t stream);
+// Exact fp8 E4M3 on the tcgen05 dynamic-tail kernel (r02 §16: its rows of 64
+// E4M3 values are exact in binary32) + a NaN count when needed; *launches =
+// the kernels enqueued (1, or 2 with out_acc).
+bool exact_e4m3_tc05_applies(size_t n, const LaunchCfg& cfg);
+cudaError_t launch_exact_e4m3_tc05(const uint8_t* x, size_t n, long long* out_acc, float* out_f32,
+                                   double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                   cudaStream_t stream, int* launches);
 // The paper's algorithm literally (study mode, tcr_paper.cu): fp16 MMAs, fp16
 // partials in `scratch` (paper_scratch_elems(n) binary16), one launch per level.
 size_t paper_scratch_elems(size_t n);

@@ -94,6 +94,7 @@ struct Tc05Params {
     uint32_t idesc;        // instruction descriptor (kind::f16 with F16 or BF16 operands)
     uint32_t one_bits;     // 1.0 in the input type (the all-ones B)
     int fmt;               // element format (0 f16, 1 bf16, 2 e4m3, 3 e5m2)
+    long long* out_acc;    // kDyn, exact E4M3 entry: the 6-word exact state (else null)
 };
 
 // Levels 3-4 of the dynamic-tail variant (kDyn).  Only lane 0 of each
@@ -111,10 +112,15 @@ struct UnitsPart {
     long long lo, hi, sp;  // T = hi:lo, sp as binary64 bits
 };
 
+// out_acc (the exact E4M3 entry, r02 §16): the exact state {l0, l1, l2,
+// n_nan, n_pinf, n_ninf} of T with l0, l1 in [0, 2^40); when a level-2 total
+// was NaN the limbs are 0 and acc[4] = -1 asks rows_nan_fixup_kernel for the
+// NaN count (E4M3 has no infinities).
 template <int WARPS>
 __device__ __forceinline__ void complete_units_grid(const UnitsPart* s_part, float* out_f32,
                                                     double* out_f64, const DevWorkspace& ws,
-                                                    const PeerCombine* pc, int me) {
+                                                    const PeerCombine* pc, int me,
+                                                    long long* out_acc = nullptr) {
     constexpr int kThreads = WARPS * 32;
     __shared__ UnitsPart s_red[WARPS];
     __shared__ unsigned s_last;
@@ -197,6 +203,16 @@ __device__ __forceinline__ void complete_units_grid(const UnitsPart* s_part, flo
     if (lane == 0) {
         if (out_f32) *out_f32 = f;
         if (out_f64) *out_f64 = d;
+        if (out_acc) {
+            const bool spc = q != 0.0;
+            const u128 m40 = ((u128)1 << 40) - 1;
+            out_acc[0] = spc ? 0 : (long long)((u128)b & m40);
+            out_acc[1] = spc ? 0 : (long long)(((u128)b >> 40) & m40);
+            out_acc[2] = spc ? 0 : (long long)(b >> 80);
+            out_acc[3] = 0;
+            out_acc[4] = spc ? -1 : 0;
+            out_acc[5] = 0;
+        }
     }
 }
 
@@ -660,7 +676,7 @@ reduce_tcgen05_kernel(const uint8_t* __restrict__ x, size_t n, Tc05Params prm, f
     TC05_EDGE(2);
     if (warp == 1) sm100::tmem_dealloc(tmem, tmem_cols);
     if constexpr (kDyn)
-        complete_units_grid<kTcWarps>(s_units, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
+        complete_units_grid<kTcWarps>(s_units, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me, prm.out_acc);
     else
         complete_block_and_grid<true, kTcWarps>(acc, out_f32, out_f64, ws, kPeer ? &pc : nullptr, me);
     TC05_EDGE(3);
@@ -738,15 +754,32 @@ static Tc05Kernel tc05_kernel(bool f8, int km, bool dyn) {
     }
 }
 
+// exact: the exact E4M3 entry -- the default ring (4 x 32 KiB, 4
+// accumulators x chain 2: rows of 64 values, exact in binary32) and the
+// integer combine (the dynamic-tail instantiation, with or without a tail);
+// out_acc (may be null) receives the exact state.
 template <bool kPeer>
 static cudaError_t launch_tc05(int fmt, const uint8_t* x, size_t n, float* out_f32, double* out_f64,
                                const DevWorkspace& ws, const LaunchCfg& cfg_in, const PeerCombine& pc,
-                               bool emulate, cudaStream_t stream) {
+                               bool emulate, cudaStream_t stream, bool exact = false,
+                               long long* out_acc = nullptr) {
     const size_t es = fmt >= 2 ? 1u : 2u;
     const int P = emulate ? pc.nranks : 1;
-    const LaunchCfg cfg = tc05_effective(n / (size_t)P * es, cfg_in);  // by the per-rank bytes
+    LaunchCfg cfg0 = cfg_in;
+    if (exact) {
+        cfg0.tc05_stages = 4;
+        cfg0.tc05_stage_kb = 32;
+        cfg0.tc05_slots = 4;
+        cfg0.tc05_chain = 2;
+        cfg0.tc05_ctas = 0;
+        cfg0.tc05_prefetch = 0;
+        cfg0.tc05_split = 1;
+        cfg0.tc05_interleave = 0;
+    }
+    const LaunchCfg cfg = tc05_effective(n / (size_t)P * es, cfg0);  // by the per-rank bytes
     Tc05Params prm;
     prm.fmt = fmt;
+    prm.out_acc = out_acc;  // (exact only)
     // kind::f16: a/b_format F16 = 0, BF16 = 1; kind::f8f6f4: E4M3 = 0, E5M2 = 1 (bits 7-9, 10-12)
     const uint32_t ab = (fmt == 1 || fmt == 3) ? ((1u << 7) | (1u << 10)) : 0u;
     prm.idesc = kIdesc | ab;
@@ -781,7 +814,9 @@ static cudaError_t launch_tc05(int fmt, const uint8_t* x, size_t n, float* out_f
                      (!kPeer || km == 8) &&
                      chunks >= (size_t)cfg.tc05_dyn_min_run * (size_t)tcgen05_grid(n / (size_t)P * es, cfg);
     if (!dyn) prm.dynamic = 0;
-    const Tc05Kernel kernel = tc05_kernel<kPeer>(fmt >= 2, km, dyn);
+    if (exact && (fmt != 2 || km != 8 || kPeer)) return cudaErrorInvalidValue;
+    const bool dyn_inst = dyn || exact;  // exact: the integer combine even without a tail
+    const Tc05Kernel kernel = tc05_kernel<kPeer>(fmt >= 2, km, dyn_inst);
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -839,6 +874,45 @@ cudaError_t launch_reduce_tcgen05_peer(int fmt, const uint16_t* x16, size_t n, f
                                        const PeerCombine& pc, bool emulate, cudaStream_t stream) {
     return launch_tc05<true>(fmt, reinterpret_cast<const uint8_t*>(x16), n, out_f32, out_f64, ws, cfg,
                              pc, emulate, stream);
+}
+
+// NaN count for the exact E4M3 entry (runs after the reduction on the same
+// stream): nothing to do unless the reduction marked acc[4] = -1 (a level-2
+// total was NaN); then every CTA counts its share of the NaN bytes (0x7F /
+// 0xFF) into acc[3] and the last CTA (ticket) clears the marker.
+__global__ void e4m3_nan_count_kernel(const uint8_t* __restrict__ x, size_t n, long long* acc,
+                                      DevWorkspace ws) {
+    if (__ldcg(acc + 4) != -1) return;
+    unsigned long long c = 0;
+    const size_t T = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T)
+        c += ((__ldg(x + i) & 0x7Fu) == 0x7Fu) ? 1u : 0u;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    __shared__ unsigned s_last;
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(acc + 3), c);
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (ticket_acq_rel(ws.ticket) == gridDim.x - 1) ? 1u : 0u;
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        acc[4] = 0;
+        *ws.ticket = 0u;
+    }
+}
+
+bool exact_e4m3_tc05_applies(size_t n, const LaunchCfg& cfg) {
+    return cfg.exact_bulk != 0 && n >= ((size_t)64 << 20);
+}
+
+cudaError_t launch_exact_e4m3_tc05(const uint8_t* x, size_t n, long long* out_acc, float* out_f32,
+                                   double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                   cudaStream_t stream, int* launches) {
+    const PeerCombine none{};
+    cudaError_t e = launch_tc05<false>(2, x, n, out_f32, out_f64, ws, cfg, none, false, stream, true, out_acc);
+    *launches = 1;
+    if (e != cudaSuccess || !out_acc) return e;
+    e4m3_nan_count_kernel<<<cfg.sms * 2, 256, 0, stream>>>(x, n, out_acc, ws);
+    *launches = 2;
+    return cudaGetLastError();
 }
 
 // One tcgen05.mma (M=128, N=16, K=16) with A = a (row-major 128x16 fp16),

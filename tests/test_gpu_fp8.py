@@ -223,3 +223,46 @@ def test_exact_bf16_acc_state_is_mergeable(tcr):
     tcr.tcr_exact_finalize_ex(tot, tcr.TCR_DTYPE_BF16, out_f32=o32, out_f64=o64)
     torch.cuda.synchronize()
     assert float(o32.item()) == es.f32() and float(o64.item()) == es.f64()
+
+
+def test_fp8_e4m3_exact_on_tcgen05(tcr):
+    """The exact E4M3 entry from 64 MiB runs the tcgen05 dynamic-tail kernel
+    (rows of 64 E4M3 values are exact in binary32, r02 §16) plus a NaN count:
+    limbs, special counts and RNE outputs bitwise equal to the oracle, with
+    and without NaNs (counted exactly), misaligned, static or dynamic tail,
+    and equal to the LDG exact kernel's state (TCR_CFG_EXACT_BULK = 0)."""
+    import torch
+
+    fmt = oracle.FP8_E4M3
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    o64 = torch.empty(1, dtype=torch.float64, device="cuda")
+    acc = torch.empty(6, dtype=torch.int64, device="cuda")
+    keys = (tcr.TCR_CFG_EXACT_BULK, tcr.TCR_CFG_TC05_DYN_MIN_RUN)
+    saved = [tcr.tcr_get_config(k) for k in keys]
+    try:
+        for n in ((64 << 20) + 5, (1 << 29) + 32768 * 3 + 11):
+            for dist in (gen.UNIFORM_PM1, gen.WIDE):
+                bits = gen.generate_fp8(70 + dist, 0, n, dist, fmt)
+                es = oracle.exact_sum_fp8(bits, fmt)
+                for eb, mr in ((1, 32), (1, 0), (0, 32)):
+                    tcr.tcr_set_config(tcr.TCR_CFG_EXACT_BULK, eb)
+                    tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYN_MIN_RUN, mr)
+                    acc.fill_(-7)
+                    tcr.tcr_reduce_sum_exact_ex(_dev(bits, 3, fmt), acc=acc, out_f32=o32, out_f64=o64)
+                    torch.cuda.synchronize()
+                    a = acc.cpu().tolist()
+                    assert exact_limbs_to_int(a) * oracle.UNIT == es.value, (n, dist, eb, mr)
+                    assert a[3:] == [0, 0, 0] and 0 <= a[0] < (1 << 40) and 0 <= a[1] < (1 << 40)
+                    assert float(o32.item()) == es.f32() and float(o64.item()) == es.f64(), (n, dist, eb)
+        bits = gen.generate_fp8(7, 0, (64 << 20) + 3, gen.UNIFORM_PM1, fmt)
+        bits[[5, len(bits) // 2, len(bits) - 2]] = [0x7F, 0xFF, 0x7F]  # three NaNs
+        tcr.tcr_set_config(tcr.TCR_CFG_EXACT_BULK, 1)
+        for _ in range(2):  # the marker and the ticket reset between launches
+            tcr.tcr_reduce_sum_exact_ex(_dev(bits, 0, fmt), acc=acc, out_f32=o32)
+            torch.cuda.synchronize()
+            a = acc.cpu().tolist()
+            assert a[3:] == [3, 0, 0], a
+            assert o32.item() != o32.item()
+    finally:
+        for k, v in zip(keys, saved):
+            tcr.tcr_set_config(k, v)
