@@ -243,6 +243,11 @@ tcr_status tcr_reduce_sum_exact(const tcr_half *x, size_t n, int64_t *acc, float
  * Python binding checks the length).  tcr_exact_finalize_ex must be called
  * with the same dtype as the reduction that wrote acc.
  * Bitwise equal to the exact oracle of the type.
+ * Kernels (TCR_CFG_EXACT_BULK): binary16 from 128 MiB on the TMA-fed exact
+ * kernel; fp8 E4M3 from 64 MiB on the tcgen05 reduction itself (its rows of
+ * 64 E4M3 values are exact in binary32, the combine is integer), followed,
+ * when acc is given, by a second kernel that counts NaN bytes only if a NaN
+ * went by -- so this entry may enqueue two kernels.
  */
 #define TCR_EXACT_ACC_WORDS 6
 #define TCR_EXACT_BF16_ACC_WORDS 27
