@@ -623,9 +623,9 @@ def main():
                 peer.reduce_sum_exact(x, out_f32=out32, stream=stream)
             elif peer is not None:  # reduction + cross-GPU combine in ONE launch
                 peer.reduce_sum(x, out_f32=out32, algo=algo, stream=stream)
-            elif exact:
-                tcr.tcr_reduce_sum_exact_ex(x, acc=exact_state, out_f32=out32 if world == 1 else None,
-                                            stream=stream)
+            elif exact:  # N = 1: the rounded result only (one kernel); N > 1: the mergeable state
+                tcr.tcr_reduce_sum_exact_ex(x, acc=exact_state if world > 1 else None,
+                                            out_f32=out32 if world == 1 else None, stream=stream)
             elif world == 1:
                 tcr.tcr_reduce_sum_ex(x, out_f32=out32, algo=algo, stream=stream)
             else:
