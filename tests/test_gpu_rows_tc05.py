@@ -257,3 +257,54 @@ def test_fp8_against_oracle(tcr, fmt):
         ss = oracle.exact_segment_sums_fp8_array(bits, off, fmt, threads=os.cpu_count() or 4)
         ok = oracle.within_tolerance_segments(got, ss)
         assert ok.all(), (fmt, L, np.flatnonzero(~ok)[:10])
+
+
+def test_random_fuzz(tcr):
+    """24 random problems: L a random multiple of 8 (16-bit) or 16 (fp8) up to
+    the routing limit, S random above 256 x SMs, random format, distribution
+    and 16-byte-aligned offset; every output vs the exact oracle of its
+    format, and bitwise equal to a repeat launch."""
+    import torch
+
+    rng = np.random.default_rng(2026)
+    fmts = ["f16", "bf16", "e4m3", "e5m2"]
+    for it in range(24):
+        fmt = fmts[it % 4]
+        es = 1 if fmt in ("e4m3", "e5m2") else 2
+        L = int(rng.integers(1, 6144 // es // (16 // es) + 1)) * (16 // es) if es == 1 else \
+            int(rng.integers(1, 3072 // 8 + 1)) * 8
+        if es == 2 and L == 1024:
+            L = 1016
+        S = _min_segments(tcr) + int(rng.integers(0, 4000))
+        while L * S > (40 << 20):
+            L = max(16 // es, (L // 2) // (16 // es) * (16 // es))
+        dist = int(rng.choice([gen.UNIFORM_PM1, gen.WIDE, gen.UNIFORM_01]))
+        off = 16 * int(rng.integers(0, 4))
+        if fmt == "f16":
+            bits = gen.generate(it, 0, L * S, dist)
+        elif fmt == "bf16":
+            bits = gen.generate_bf16(it, 0, L * S, dist)
+        else:
+            bits = gen.generate_fp8(it, 0, L * S, dist, oracle.FP8_E4M3 if fmt == "e4m3" else oracle.FP8_E5M2)
+        buf = torch.empty(L * S * es + 64, dtype=torch.uint8, device="cuda")
+        xb = buf[off:off + L * S * es]
+        xb.copy_(torch.from_numpy(bits.view(np.uint8)))
+        x = xb.view({"f16": torch.float16, "bf16": torch.bfloat16, "e4m3": torch.float8_e4m3fn,
+                     "e5m2": torch.float8_e5m2}[fmt])
+        with _rows(tcr, True):
+            got = _batched(tcr, x, L, S)
+            again = _batched(tcr, x, L, S)
+        assert np.array_equal(got.view(np.uint32), again.view(np.uint32)), (it, fmt, L, S)
+        offs = np.arange(S + 1, dtype=np.int64) * L
+        if fmt == "f16":
+            ok = oracle.within_tolerance_segments(got, oracle.exact_segment_sums_fp16_array(bits, offs, threads=os.cpu_count() or 4))
+            assert ok.all(), (it, fmt, L, S, np.flatnonzero(~ok)[:5])
+        elif fmt == "bf16":
+            idx = rng.choice(S, size=min(S, 400), replace=False)
+            for j in idx:
+                es_j = oracle.exact_sum_bf16(bits[j * L:(j + 1) * L])
+                assert oracle.within_tolerance(float(got[j]), es_j), (it, fmt, L, S, j)
+        else:
+            f8 = oracle.FP8_E4M3 if fmt == "e4m3" else oracle.FP8_E5M2
+            ok = oracle.within_tolerance_segments(got, oracle.exact_segment_sums_fp8_array(bits, offs, f8, threads=os.cpu_count() or 4))
+            assert ok.all(), (it, fmt, L, S, np.flatnonzero(~ok)[:5])

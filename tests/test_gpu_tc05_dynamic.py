@@ -361,3 +361,40 @@ def test_e4m3_exact_adversarial_rows(tcr):
     tcr.tcr_reduce_sum_ex(x, out_f32=o32, out_f64=o64)
     torch.cuda.synchronize()
     assert o64.item() == es.f64() and o32.item() == es.f32(), (o64.item(), es.f64())
+
+
+def test_random_fuzz_flat(tcr):
+    """30 random flat problems on the dynamic-tail kernel (binary16 and fp8):
+    random size up to 2^25, byte offset, distribution, dynamic fraction and
+    ring shape (4 / 8 / 16 MMAs per stage) -- within tolerance of the exact
+    oracle and bitwise equal across two dynamic fractions."""
+    import torch
+
+    rng = np.random.default_rng(1903)
+    shapes = [(4, 16, 4, 1), (4, 32, 4, 2), (3, 64, 4, 4)]
+    for it in range(30):
+        f8 = it % 3 == 2
+        n = int(rng.integers(1, 1 << 25))
+        dist = int(rng.choice([gen.UNIFORM_PM1, gen.WIDE, gen.UNIFORM_01, gen.ALTERNATING]))
+        st, kb, sl, ch = shapes[int(rng.integers(0, 3 if not f8 else 2))]
+        d1, d2 = (int(v) for v in rng.choice([1, 8, 25, 60, 100], size=2, replace=False))
+        if f8:
+            fmt = oracle.FP8_E4M3 if it % 2 else oracle.FP8_E5M2
+            bits = gen.generate_fp8(it, 0, n, dist, fmt)
+            es = oracle.exact_sum_fp8(bits, fmt)
+            off = int(rng.integers(0, 16))
+            buf = torch.empty(n + 32, dtype=torch.uint8, device="cuda")
+            x = buf[off:off + n]
+            x.copy_(torch.from_numpy(bits))
+            x = x.view(torch.float8_e4m3fn if fmt == oracle.FP8_E4M3 else torch.float8_e5m2)
+        else:
+            bits = gen.generate(it, 0, n, dist)
+            es = oracle.exact_sum_fp16(bits, threads=os.cpu_count() or 4)
+            x = _dev16(bits, int(rng.integers(0, 8)))
+        with _cfg(tcr, tc05_stages=st, tc05_stage_kb=kb, tc05_slots=sl, tc05_chain=ch):
+            with _cfg(tcr, tc05_dynamic=d1):
+                g1 = _sum(tcr, x)
+            with _cfg(tcr, tc05_dynamic=d2):
+                g2 = _sum(tcr, x)
+        assert oracle.within_tolerance(g1, es), (it, n, f8, dist, g1, es.f64())
+        assert _bits32(g1) == _bits32(g2), (it, n, f8, d1, d2, g1, g2)
