@@ -705,15 +705,29 @@ int tcgen05_grid(size_t nbytes, const LaunchCfg& cfg) {
 
 // TCR_CFG_TC05_CTAS_PER_SM = 0 (auto, the default since r02): one CTA (one
 // issuer) per SM with the configured ring from 256 MiB of input, where the
-// tight issue loop keeps up with HBM alone; below, three CTAs per SM with at
-// most two stages each, so that a short input is spread over three times as
-// many independent pipelines (profiles/r02/tc05_commit_sweep.txt: 2^24 warm
-// 7.5 -> 6.8 us).
+// tight issue loop keeps up with HBM alone; below, several CTAs per SM with
+// short rings, so that a short input is spread over more independent
+// pipelines.  With the library's default ring (4 x 32 KiB, 4 accumulators x
+// chain 2) the shape below 256 MiB follows the measured best per size
+// (profiles/r02/tc05_small_sweep3.txt, warm CUDA graphs, time / mma.sync's):
+// 16 MiB and 64 MiB 3 x 32 KiB at 2 CTAs (1.21, 1.12), 32 MiB 2 x 16 KiB at
+// 3 CTAs (1.22), otherwise 2 x 32 KiB at 3 CTAs (1.07-1.25).
 static LaunchCfg tc05_effective(size_t nbytes, const LaunchCfg& cfg) {
     LaunchCfg c = cfg;
     if (c.tc05_ctas == 0) {
+        const bool default_ring = c.tc05_stages == 4 && c.tc05_stage_kb == 32 && c.tc05_slots == 4 &&
+                                  c.tc05_chain == 2;
+        const size_t mib = nbytes >> 20;
         if (nbytes >= ((size_t)256 << 20)) {
             c.tc05_ctas = 1;
+        } else if (default_ring && ((mib >= 12 && mib < 24) || (mib >= 48 && mib < 96))) {
+            c.tc05_ctas = 2;
+            c.tc05_stages = 3;
+        } else if (default_ring && mib >= 24 && mib < 48) {
+            c.tc05_ctas = 3;
+            c.tc05_stages = 2;
+            c.tc05_stage_kb = 16;
+            c.tc05_chain = 1;
         } else {
             c.tc05_ctas = 3;
             if (c.tc05_stages > 2) c.tc05_stages = 2;
@@ -814,7 +828,7 @@ static cudaError_t launch_tc05(int fmt, const uint8_t* x, size_t n, float* out_f
                      (!kPeer || km == 8) &&
                      chunks >= (size_t)cfg.tc05_dyn_min_run * (size_t)tcgen05_grid(n / (size_t)P * es, cfg);
     if (!dyn) prm.dynamic = 0;
-    if (exact && (fmt != 2 || km != 8 || kPeer)) return cudaErrorInvalidValue;
+    if (exact && (fmt != 2 || (km != 8 && km != 4) || kPeer)) return cudaErrorInvalidValue;  // chain <= 2
     const bool dyn_inst = dyn || exact;  // exact: the integer combine even without a tail
     const Tc05Kernel kernel = tc05_kernel<kPeer>(fmt >= 2, km, dyn_inst);
     int dev = 0;

@@ -19,7 +19,7 @@ saved = [tcr.tcr_get_config(k) for k in keys]
 cfgs = [(2, 32, 4, 2, 3), (2, 16, 4, 1, 4), (3, 16, 4, 1, 4), (4, 16, 4, 1, 3), (3, 32, 4, 2, 2),
         (2, 16, 4, 1, 3), (6, 16, 4, 1, 2), (4, 32, 4, 2, 1)]
 out = torch.empty(1, dtype=torch.float32, device="cuda")
-for lg in (20, 22, 24, 26):
+for lg in [int(a) for a in sys.argv[1:]] or (20, 22, 24, 26):
     x = gen.generate_tensor(gen.SEED_C2, 0, 1 << lg, gen.UNIFORM_PM1)
     m = statistics.median(graph_time(lambda: tcr.tcr_reduce_sum_algo(x, out_f32=out, algo="mma_sync"))
                           for _ in range(3))
