@@ -327,7 +327,8 @@ EncodeTiled encode_fn() {
 bool rows_tc05_supported(int fmt, const void* x, size_t S, size_t L) {
     const size_t lb = L * ((fmt == kE4M3 || fmt == kE5M2) ? 1 : 2);
     return fmt >= kF16 && fmt <= kE5M2 && ((uintptr_t)x & 15u) == 0 && lb % 16 == 0 && lb >= 16 &&
-           L < ((size_t)1 << 31) && S >= 1 && S < ((size_t)1 << 31) && encode_fn() != nullptr;
+           L < ((size_t)1 << 31) && S >= 1 && S < ((size_t)1 << 31) - 4096 &&  // box rows fit int32
+           encode_fn() != nullptr;
 }
 
 template <int BW, bool kF8>
