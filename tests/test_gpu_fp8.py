@@ -266,3 +266,38 @@ def test_fp8_e4m3_exact_on_tcgen05(tcr):
     finally:
         for k, v in zip(keys, saved):
             tcr.tcr_set_config(k, v)
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+def test_fp8_exact_bulk_kernel_forced(tcr, fmt):
+    """TCR_CFG_EXACT_BULK = 2 forces the TMA-fed exact kernel for fp8 too (below
+    the 64 MiB E4M3 tcgen05 threshold): bitwise equal to the oracle, with the
+    dynamic tail on at every size, misaligned, with a special value."""
+    import torch
+
+    o32 = torch.empty(1, dtype=torch.float32, device="cuda")
+    o64 = torch.empty(1, dtype=torch.float64, device="cuda")
+    acc = torch.empty(6, dtype=torch.int64, device="cuda")
+    keys = (tcr.TCR_CFG_EXACT_BULK, tcr.TCR_CFG_TC05_DYN_MIN_RUN)
+    saved = [tcr.tcr_get_config(k) for k in keys]
+    try:
+        tcr.tcr_set_config(tcr.TCR_CFG_EXACT_BULK, 2)
+        tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYN_MIN_RUN, 0)
+        for n in (1, 32768 * 3 + 9, (1 << 24) + 77):
+            bits = gen.generate_fp8(n, 0, n, gen.WIDE, fmt)
+            es = oracle.exact_sum_fp8(bits, fmt)
+            tcr.tcr_reduce_sum_exact_ex(_dev(bits, 5, fmt), acc=acc, out_f32=o32, out_f64=o64)
+            torch.cuda.synchronize()
+            assert exact_limbs_to_int(acc) * oracle.UNIT == es.value, (fmt, n)
+            assert float(o32.item()) == es.f32() and float(o64.item()) == es.f64(), (fmt, n)
+        bits = gen.generate_fp8(3, 0, 200_000, gen.UNIFORM_PM1, fmt)
+        bits[100_000] = 0x7F  # NaN in both formats
+        es = oracle.exact_sum_fp8(bits, fmt)
+        tcr.tcr_reduce_sum_exact_ex(_dev(bits, 0, fmt), acc=acc, out_f32=o32)
+        torch.cuda.synchronize()
+        a = acc.cpu().tolist()
+        assert (a[3], a[4], a[5]) == (es.n_nan, es.n_pinf, es.n_ninf), (fmt, a)
+        assert o32.item() != o32.item()
+    finally:
+        for k, v in zip(keys, saved):
+            tcr.tcr_set_config(k, v)
