@@ -11,7 +11,16 @@
 
 namespace tcr {
 
-constexpr unsigned long long kBatchSeg = 8;  // segments per scheduler atomic (guided)
+#ifndef TCR_SEG_BATCH
+#define TCR_SEG_BATCH 8
+#endif
+#ifndef TCR_SEG_UNROLL
+#define TCR_SEG_UNROLL 8
+#endif
+#ifndef TCR_SEG_CTAS
+#define TCR_SEG_CTAS 4
+#endif
+constexpr unsigned long long kBatchSeg = TCR_SEG_BATCH;  // segments per scheduler atomic (guided)
 
 // Reduce elements [s, e) of the 16-byte-aligned array xb (element indices
 // relative to xb).  Returns the lane's fp64 share; the sum over lanes is the
@@ -45,7 +54,7 @@ __device__ __forceinline__ void seg_piece(const uint4& v, double& acc, int lane)
 // CSR (64 registers); 3 for fixed-length batches, whose 64-bit segment
 // arithmetic needs the room (85 registers: zero spills, ptxas report).
 template <bool kBatched>
-constexpr int seg_resident() { return kBatched ? 3 : 4; }
+constexpr int seg_resident() { return kBatched ? 3 : TCR_SEG_CTAS; }
 
 template <bool kMma, int F, bool kBatched, int U, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, seg_resident<kBatched>())
@@ -296,8 +305,8 @@ reduce_rowseg_kernel(const uint8_t* __restrict__ x, size_t S, size_t L, float* _
 }
 
 constexpr int kSegWarps = 8;
-constexpr int kSegUnroll = 8;  // tiles per group (one round trip)
-constexpr int kSegCtasPerSm = 4;  // resident CTAs per SM at <= 64 registers (launch bounds)
+constexpr int kSegUnroll = TCR_SEG_UNROLL;  // tiles per group (one round trip)
+constexpr int kSegCtasPerSm = TCR_SEG_CTAS;  // resident CTAs per SM (launch bounds: 64 registers at 4)
 
 template <bool kMma, int F>
 static void launch_seg_t(bool batched, const dim3& grid, const dim3& block, const uint8_t* x,
