@@ -430,10 +430,13 @@ __device__ __forceinline__ uint4 lds128x(const void* p) {
     return r;
 }
 
-template <int F>
+// kPeer: the NEXT-2 x NEXT-3 variant (the limb combine with the peers fused
+// into the last CTA); grid.y slices = emulated ranks, as reduce_exact_kernel.
+template <int F, bool kPeer = false>
 __global__ void __launch_bounds__(kXbThreads, 1)
 reduce_exact_bulk_kernel(const uint8_t* __restrict__ x, size_t n, int stages, int dyn_pct,
-                         long long* out_acc, float* out_f32, double* out_f64, DevWorkspace ws) {
+                         long long* out_acc, float* out_f32, double* out_f64, DevWorkspace ws,
+                         PeerCombine pc) {
     constexpr int ES = FmtInfo<F>::kBytes;
     constexpr int kTileBytes = 512;
     constexpr int NA = 4;
@@ -447,6 +450,20 @@ reduce_exact_bulk_kernel(const uint8_t* __restrict__ x, size_t n, int stages, in
     volatile uint32_t* sinfo = reinterpret_cast<volatile uint32_t*>(empty + stages);  // [stages]
     uint8_t* ring = smem + kXbHeader;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int me = pc.rank;
+    if (kPeer && gridDim.y > 1) {  // emulated peer group: slice y is rank y, reducing its shard
+        const size_t P = gridDim.y, r = blockIdx.y;
+        const size_t lo = r * n / P, hi = (r + 1) * n / P;
+        x += lo * ES;
+        n = hi - lo;
+        ws.partials += 5 * r * gridDim.x;  // 5 int64 words per CTA
+        ws.ticket += r;
+        ws.chunk_next += r;
+        if (out_acc) out_acc += 6 * r;
+        if (out_f32) out_f32 += r;
+        if (out_f64) out_f64 += r;
+        me = (int)r;
+    }
 
     const size_t nbytes = n * ES;
     size_t head = (16u - ((uintptr_t)x & 15u)) & 15u;
@@ -468,7 +485,7 @@ reduce_exact_bulk_kernel(const uint8_t* __restrict__ x, size_t n, int stages, in
         sm100::fence_mbar_init();
     }
     __syncthreads();
-    pdl_wait_and_release();  // PDL: no global memory before the previous kernel completes
+    if constexpr (!kPeer) pdl_wait_and_release();  // PDL: no global memory before the previous kernel completes
 
     i128 acc = 0;
     uint32_t cnt[3] = {0u, 0u, 0u};
@@ -581,8 +598,7 @@ reduce_exact_bulk_kernel(const uint8_t* __restrict__ x, size_t n, int stages, in
         }
         drain();
     }
-    const PeerCombine none{};
-    exact_complete<kXbConsumers + 1, false>(acc, cnt, out_acc, out_f32, out_f64, ws, none, 0,
+    exact_complete<kXbConsumers + 1, kPeer>(acc, cnt, out_acc, out_f32, out_f64, ws, pc, me,
                                             D ? ws.chunk_next : nullptr);
 }
 
@@ -634,8 +650,9 @@ static cudaError_t launch_exact_bulk(const uint8_t* x, size_t n, long long* out_
     if (g < 1) g = 1;
     // the dynamic tail when every CTA streams >= TCR_CFG_TC05_DYN_MIN_RUN chunks
     const int dyn = (C >= (size_t)cfg.tc05_dyn_min_run * g) ? cfg.tc05_dynamic : 0;
+    const PeerCombine none{};
     launch_maybe_pdl(kernel, dim3((unsigned)g), dim3(kXbThreads), smem, stream, cfg.pdl, x, n, kStages, dyn,
-                     out_acc, out_f32, out_f64, ws);
+                     out_acc, out_f32, out_f64, ws, none);
     return cudaGetLastError();
 }
 
@@ -674,10 +691,72 @@ cudaError_t launch_reduce_exact(int fmt, const void* x, size_t n, long long* out
     }
 }
 
+// The TMA-fed exact kernel fused with the peer limb combine (binary16): a
+// plain launch per real rank; emulated ranks in one cooperative launch
+// (grid.y = ranks; one CTA per SM, so at most SMs / P CTAs per rank).
+static cudaError_t launch_exact_bulk_peer(const uint8_t* x, size_t n, long long* out_acc, float* out_f32,
+                                          double* out_f64, const DevWorkspace& ws, const LaunchCfg& cfg,
+                                          const PeerCombine& pc, bool emulate, cudaStream_t stream) {
+    constexpr int kStages = 4;
+    const size_t smem = kXbHeader + (size_t)kStages * kXbStageBytes;
+    auto kernel = reduce_exact_bulk_kernel<kF16, true>;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    {
+        static std::mutex mu;
+        static std::map<int, size_t> configured;
+        std::lock_guard<std::mutex> lk(mu);
+        if (smem > configured[dev]) {
+            if ((e = cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem)))
+                return e;
+            configured[dev] = smem;
+        }
+    }
+    const int P = emulate ? pc.nranks : 1;
+    const size_t C = n / (size_t)P * 2u / kXbStageBytes;
+    size_t g = (size_t)cfg.sms / (size_t)P;
+    if (g > C) g = C;
+    if (g < 1) g = 1;
+    const int dyn = (C >= (size_t)cfg.tc05_dyn_min_run * g) ? cfg.tc05_dynamic : 0;
+    int stages = kStages;
+    if (!emulate) {
+        kernel<<<(unsigned)g, kXbThreads, smem, stream>>>(x, n, stages, dyn, out_acc, out_f32, out_f64, ws, pc);
+        return cudaGetLastError();
+    }
+    int occ = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kXbThreads, smem))) return e;
+    const size_t cap = (size_t)occ * (size_t)cfg.sms / (size_t)P;
+    if (g > cap) g = cap;
+    if (g < 1) return cudaErrorCooperativeLaunchTooLarge;
+    const uint8_t* xa = x;
+    size_t na = n;
+    long long* acc = out_acc;
+    float* o32 = out_f32;
+    double* o64 = out_f64;
+    DevWorkspace wsa = ws;
+    PeerCombine pca = pc;
+    int dp = dyn;
+    void* args[] = {(void*)&xa, (void*)&na, (void*)&stages, (void*)&dp, (void*)&acc, (void*)&o32,
+                    (void*)&o64, (void*)&wsa, (void*)&pca};
+    return cudaLaunchCooperativeKernel((const void*)kernel, dim3((unsigned)g, (unsigned)P), dim3(kXbThreads),
+                                       args, smem, stream);
+}
+
 cudaError_t launch_reduce_exact_peer(const uint16_t* x, size_t n, long long* out_acc,
                                      float* out_f32, double* out_f64, const DevWorkspace& ws,
                                      const LaunchCfg& cfg, const PeerCombine& pc, bool emulate,
                                      cudaStream_t stream) {
+    const int P0 = emulate ? pc.nranks : 1;
+    const size_t shard_bytes = n / (size_t)(P0 > 0 ? P0 : 1) * 2u;
+    // real ranks: the TMA-fed kernel from 128 MiB per rank (1 rank at 2^30: 300.9 vs 319.7 us);
+    // emulated ranks share one GPU's SMs (one CTA per SM, SMs / P per rank), where the LDG
+    // kernel's three CTAs per SM do better (8 x 2^30: 2553 vs 2800 us,
+    // profiles/r02/exact_peer_ab.txt) -- forced with TCR_CFG_EXACT_BULK = 2
+    if (cfg.exact_bulk == 2 || (cfg.exact_bulk == 1 && !emulate && shard_bytes >= ((size_t)128 << 20)))
+        return launch_exact_bulk_peer(reinterpret_cast<const uint8_t*>(x), n, out_acc, out_f32, out_f64, ws,
+                                      cfg, pc, emulate, stream);
     auto kernel = reduce_exact_kernel<8, true, kF16>;  // the peer variant: binary16, unroll 8
     LaunchCfg c8 = cfg;
     c8.exact_unroll = 8;

@@ -349,3 +349,37 @@ def test_exact_specials_in_one_shard(tcr, mailboxes):
         torch.cuda.synchronize()
         for g in o32.cpu().tolist():
             assert (math.isnan(g) if math.isnan(expect) else g == expect), (special, g)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_exact_bulk_peer_emulated_bitwise(tcr, mailboxes, P):
+    """The TMA-fed exact kernel fused with the limb combine (TCR_CFG_EXACT_BULK
+    = 2 forces it below its 128 MiB-per-rank threshold; r02 §18): bitwise
+    equal to the oracle on every rank, static and dynamic tails, and equal to
+    the LDG peer kernel's limbs."""
+    import torch
+
+    keys = (tcr.TCR_CFG_EXACT_BULK, tcr.TCR_CFG_TC05_DYN_MIN_RUN)
+    saved = [tcr.tcr_get_config(k) for k in keys]
+    acc = torch.empty(6 * P, dtype=torch.int64, device="cuda")
+    o32 = torch.empty(P, dtype=torch.float32, device="cuda")
+    o64 = torch.empty(P, dtype=torch.float64, device="cuda")
+    try:
+        for seed, n, dist in ((1, 3_000_017, gen.WIDE), (3, (1 << 24) + 9, gen.UNIFORM_01), (4, 5, gen.SMALLINT)):
+            bits = gen.generate(seed, 0, n, dist)
+            es = oracle.exact_sum_fp16(bits)
+            for eb, mr in ((2, 32), (2, 0), (0, 32)):
+                tcr.tcr_set_config(tcr.TCR_CFG_EXACT_BULK, eb)
+                tcr.tcr_set_config(tcr.TCR_CFG_TC05_DYN_MIN_RUN, mr)
+                tcr.tcr_reduce_sum_exact_peer_emulated(_dev(bits), mailboxes[:P], acc=acc, out_f32=o32,
+                                                       out_f64=o64)
+                torch.cuda.synchronize()
+                assert o32.cpu().tolist() == [es.f32()] * P, (seed, P, eb, mr)
+                assert o64.cpu().tolist() == [es.f64()] * P, (seed, P, eb, mr)
+                for r in range(P):
+                    assert exact_limbs_to_int(acc[6 * r:6 * r + 6]) == es.T, (seed, P, eb, mr, r)
+        for b in mailboxes[:P]:
+            assert not tcr.tcr_peer_mailbox_error(b)
+    finally:
+        for k, v in zip(keys, saved):
+            tcr.tcr_set_config(k, v)
