@@ -281,7 +281,11 @@ tcr_status tcr_round_f64_to_f32(const double *in, float *out, tcr_stream stream)
  * rank gets the bitwise identical result (D' replicated, Eq. 12) from ONE
  * launch, with no host synchronisation.  Each mailbox counts its rank's
  * combines on the device (the epoch that tags the partials), so the launch
- * can be captured in a CUDA graph and replayed.
+ * can be captured in a CUDA graph and replayed.  A mailbox therefore belongs
+ * to ONE group: every rank of the group must have made the same number of
+ * combines on it (using a mailbox in two groups, e.g. alone and then in a
+ * group of 8, desynchronises the epochs and the waits run into
+ * TCR_CFG_PEER_TIMEOUT_MS, returning NaN with the error word set).
  *
  * Group setup (once): each rank tcr_peer_mailbox_alloc()s its mailbox,
  * exports it with tcr_peer_ipc_handle(), the handles are exchanged out of
